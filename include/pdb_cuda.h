@@ -1,0 +1,188 @@
+/*
+ * pdb_cuda.h -- C-ABI of the B200-native patch featurization + threshold
+ * similarity join (libpdb_cuda.so).
+ *
+ * Plain C: pointers, sizes, status codes.  No torch / CUDA types in the
+ * signatures (streams travel as `void*` = cudaStream_t).  Every call is
+ * synchronous with respect to the caller unless it ends in `_dev`, never
+ * throws, is re-entrant (per-call stream and workspace, no global mutable
+ * state beyond a per-device context initialised once), and returns a
+ * PDB_* status code; the message of the last failure on the calling thread
+ * is available from pdb_last_error().  There is no CPU fallback: without a
+ * usable sm_100 device every compute entry point returns PDB_ERR_NO_DEVICE.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference's proj/ directory).
+ */
+#ifndef PDB_CUDA_H
+#define PDB_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------------------
+ * Status codes.  Codes 1-5 map 1:1 onto the reference exception types
+ * (include/patchdb/core.hpp:22-47) so a C++ or Python shim can re-raise them:
+ *   PDB_ERR_CONFIG             ConfigError            (tau < 0, bins < 2, tile < 1)
+ *   PDB_ERR_SHAPE              ShapeError             (empty vectors, non-pixel input)
+ *   PDB_ERR_MIXED_DIMENSION    MixedDimensionError
+ *   PDB_ERR_DIMENSION_MISMATCH DimensionMismatchError
+ *   PDB_ERR_DUPLICATE_ID       DuplicatePatchIdError
+ */
+enum {
+    PDB_OK = 0,
+    PDB_ERR_CONFIG = 1,
+    PDB_ERR_SHAPE = 2,
+    PDB_ERR_MIXED_DIMENSION = 3,
+    PDB_ERR_DIMENSION_MISMATCH = 4,
+    PDB_ERR_DUPLICATE_ID = 5,
+    PDB_ERR_CAPACITY = 6,         /* caller-provided device buffer too small */
+    PDB_ERR_INVALID_ARGUMENT = 7, /* null pointer, negative size, bad flags */
+    PDB_ERR_CUDA = 10,            /* CUDA runtime / driver failure */
+    PDB_ERR_OUT_OF_MEMORY = 11,
+    PDB_ERR_NO_DEVICE = 12        /* no sm_100 device: the product has no CPU path */
+};
+
+/* Message of the last failure on this thread ("" if none). */
+const char* pdb_last_error(void);
+const char* pdb_status_name(int status);
+/* Library version, (major << 16) | (minor << 8) | patch. */
+int pdb_version(void);
+/* Number of usable sm_100 devices (0 when none). */
+int pdb_device_count(void);
+
+/* ---------------------------------------------------------------------------
+ * K1 -- colour histograms.
+ *
+ * mode PDB_HIST_PER_CHANNEL: the reference color_histogram transformer,
+ *   out[c*B + bin], each channel slice normalised to 1, D = 3B
+ *   (src/etl.cpp:330-354).  Any B >= 2.
+ * mode PDB_HIST_JOINT: joint RGB histogram (BASELINE config 2; restated, not
+ *   in the reference), out[(br*B + bg)*B + bb], L1 mass 1, D = B^3,
+ *   2 <= B <= 16.
+ * Binning is the reference's bin = min((uint32)(v*B/256.0f), B-1) and
+ * normalisation its IEEE float count / (float)(h*w), so features are
+ * bit-identical to the reference. */
+#define PDB_HIST_PER_CHANNEL 0
+#define PDB_HIST_JOINT 1
+
+/* Feature dimension D for (bins, mode), or -1 if the pair is invalid. */
+int pdb_hist_dim(int32_t bins, int32_t mode);
+
+/* generate(tiles) -> transform(color_histogram) fused over uint8 frames.
+ * Replaces generate() src/etl.cpp:264-298 (floor grid ntx = W/tile_w,
+ * nty = H/tile_h, partial edges dropped, tiles row by row with tx fastest),
+ * the make_patch float crop src/core.cpp:88-93 (fused away) and
+ * apply_transformer src/etl.cpp:330-354.
+ * frames: [n_frames, height, width, 3] row-major HWC interleaved RGB
+ *         (Frame, include/patchdb/core.hpp:66-80).
+ * out:    [n_frames * nty * ntx, D] fp32, caller-allocated.
+ * Host pointers; the call copies in, runs K1 and copies out. */
+int pdb_featurize_tiles(const uint8_t* frames, int64_t n_frames, int32_t height,
+                        int32_t width, int32_t tile_h, int32_t tile_w, int32_t bins,
+                        int32_t mode, float* out);
+
+/* Same on device pointers, enqueued on `stream` (cudaStream_t, NULL = legacy
+ * default stream); returns after enqueueing. */
+int pdb_featurize_tiles_dev(const uint8_t* d_frames, int64_t n_frames, int32_t height,
+                            int32_t width, int32_t tile_h, int32_t tile_w, int32_t bins,
+                            int32_t mode, float* d_out, void* stream);
+
+/* apply_transformer(color_histogram) over float pixel patches
+ * [n, h, w, 3] (src/etl.cpp:330-354; pixel values as produced by make_patch,
+ * i.e. integral 0..255; values >= 256 clamp to the top bin as in the
+ * reference, negative / NaN values -- undefined behaviour in the reference --
+ * land in bin 0).  Host pointers. */
+int pdb_color_histogram_f32(const float* patches, int64_t n, int32_t h, int32_t w,
+                            int32_t bins, int32_t mode, float* out);
+int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, int32_t w,
+                                int32_t bins, int32_t mode, float* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K2 + K3 -- threshold similarity join.
+ *
+ * Emits every (i, j) with euclidean(L_i, R_j) <= tau, where euclidean is the
+ * reference's sequential, unfused fp64 chain (src/index.cpp:69-76) and tau
+ * a double (src/planfile.cpp:228-229).  The pair SET is bit-identical to the
+ * reference's brute-force contract (tests/oracles.hpp:77-85, equal to
+ * sim_join_pairs, src/query.cpp:1094-1104); `dist` is that fp64 distance
+ * rounded to fp32.
+ *
+ * Flags:
+ *   PDB_JOIN_SELF    L and R are the same relation; emit only i < j
+ *                    (BASELINE's "(i<j, dist)" view; R/nR are ignored).
+ *   PDB_JOIN_SORTED  pairs ascend by (left, right) -- the reference's
+ *                    emission order when the build side is R (probe order,
+ *                    ascending build id).  Without it the order is
+ *                    unspecified.
+ * Sharding (multi-GPU, one process per GPU): with shard_count > 1 this call
+ * only scans the 128-row blocks b of L with b % shard_count == shard_index
+ * (indices stay global), so the shards partition the pair set. */
+#define PDB_JOIN_SELF 1u
+#define PDB_JOIN_SORTED 2u
+
+typedef struct pdb_join_opts {
+    uint32_t flags;
+    int32_t shard_index;
+    int32_t shard_count;  /* 0 or 1: no sharding */
+    int32_t reserved0;
+    void* stream;         /* cudaStream_t for the _dev variants */
+} pdb_join_opts;
+
+/* Host-side result of pdb_sim_join; free with pdb_pairs_free. */
+typedef struct pdb_pairs {
+    int64_t count;
+    int32_t* left;   /* row index into L */
+    int32_t* right;  /* row index into R (into L for PDB_JOIN_SELF) */
+    float* dist;
+} pdb_pairs;
+
+/* Per-call counters (optional out-parameter of the _dev variant). */
+typedef struct pdb_join_stats {
+    int64_t candidates;      /* pairs passing the tensor-core screen */
+    int64_t pairs;           /* pairs passing the exact fp64 re-check */
+    int64_t tiles;           /* 128x256 screen tiles executed */
+    int64_t candidate_capacity;
+} pdb_join_stats;
+
+/* Host pointers: L [nL, d] and R [nR, d] fp32 row-major. */
+int pdb_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int32_t d,
+                 double tau, const pdb_join_opts* opts, pdb_pairs* out);
+void pdb_pairs_free(pdb_pairs* p);
+
+/* Device-resident result.  pdb_sim_join_dev (re)allocates the three arrays
+ * on the device when `capacity` is smaller than needed, so a caller can keep
+ * one pdb_dev_pairs across calls; free with pdb_dev_pairs_free. */
+typedef struct pdb_dev_pairs {
+    int64_t count;
+    int64_t capacity;
+    int32_t* left;
+    int32_t* right;
+    float* dist;
+} pdb_dev_pairs;
+
+int pdb_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR, int32_t d,
+                     double tau, const pdb_join_opts* opts, pdb_dev_pairs* out,
+                     pdb_join_stats* stats);
+void pdb_dev_pairs_free(pdb_dev_pairs* p);
+
+/* The q1 pipeline in one call (src/bench.cpp:695-730 shape: featurize
+ * tiles, then self-join the features): host frames in, host pairs out
+ * (PDB_JOIN_SELF semantics).  `features` (host, [tiles, D]) is optional. */
+int pdb_featurize_join(const uint8_t* frames, int64_t n_frames, int32_t height, int32_t width,
+                       int32_t tile_h, int32_t tile_w, int32_t bins, int32_t mode,
+                       double tau, const pdb_join_opts* opts, float* features,
+                       pdb_pairs* out);
+
+/* Pinned host memory helpers (the e2e path copies from pinned buffers). */
+void* pdb_host_alloc(int64_t bytes);
+void pdb_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDB_CUDA_H */

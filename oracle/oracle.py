@@ -1,0 +1,191 @@
+"""ctypes bindings of the CPU checkers (TEST / BASELINE INFRASTRUCTURE ONLY).
+
+* ``port()``  -- oracle/libpdb_oracle.so, the C restatement in pdb_oracle.c
+* ``ref()``   -- oracle/_ref/libpdb_ref.so, the reference sources themselves
+                 (None where they were never built)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs import this module.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_PATH = os.path.join(HERE, "libpdb_oracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libpdb_ref.so")
+
+_port = None
+_ref = None
+
+
+class OrcPairs(C.Structure):
+    _fields_ = [("count", C.c_int64), ("left", C.POINTER(C.c_int32)),
+                ("right", C.POINTER(C.c_int32)), ("dist", C.POINTER(C.c_double))]
+
+
+def _p(a):
+    return a.ctypes.data
+
+
+def port():
+    global _port
+    if _port is None:
+        L = C.CDLL(PORT_PATH)
+        i64, i32, f64, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
+        L.orc_featurize_tiles.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, vp]
+        L.orc_color_histogram_f32.argtypes = [vp, i64, i32, i32, i32, i32, vp]
+        L.orc_euclidean.argtypes = [vp, vp, i64]
+        L.orc_euclidean.restype = f64
+        L.orc_sim_join.argtypes = [vp, i64, vp, i64, i64, f64, i32, i64, i64, i32,
+                                   C.POINTER(OrcPairs)]
+        L.orc_pairs_free.argtypes = [C.POINTER(OrcPairs)]
+        L.orc_pairs_free.restype = None
+        L.orc_sim_join_count.argtypes = [vp, i64, vp, i64, i64, f64, i32, i64, i64]
+        L.orc_sim_join_count.restype = i64
+        L.orc_hist_dim.argtypes = [C.c_int, C.c_int]
+        _port = L
+    return _port
+
+
+def ref():
+    """The reference compiled from its own sources, or None if not built."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_PATH):
+            return None
+        L = C.CDLL(REF_PATH)
+        i64, i32, f64, vp = C.c_int64, C.c_int32, C.c_double, C.c_void_p
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_featurize_tiles.argtypes = [vp, i64, i32, i32, i32, i32, i32, vp, i32]
+        L.ref_color_histogram_f32.argtypes = [vp, i64, i32, i32, i32, vp]
+        L.ref_euclidean.argtypes = [vp, vp, i64]
+        L.ref_euclidean.restype = f64
+        L.ref_sim_join.argtypes = [vp, i64, vp, i64, i32, f64, i32, C.POINTER(i64),
+                                   C.POINTER(C.POINTER(i32)), C.POINTER(C.POINTER(i32)),
+                                   C.POINTER(C.c_uint64)]
+        L.ref_free.argtypes = [vp]
+        L.ref_free.restype = None
+        L.ref_join_probe_timed.argtypes = [vp, i64, vp, i64, i32, f64, i32, i64, i64, i32,
+                                           C.POINTER(f64), C.POINTER(f64)]
+        L.ref_join_probe_timed.restype = i64
+        _ref = L
+    return _ref
+
+
+# ---- restatement (port) ------------------------------------------------------
+
+def featurize_tiles(frames: np.ndarray, th: int, tw: int, bins: int, mode: int) -> np.ndarray:
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    F, H, W = frames.shape[:3]
+    D = port().orc_hist_dim(bins, mode)
+    out = np.empty((F * (H // th) * (W // tw), max(D, 1)), dtype=np.float32)
+    rc = port().orc_featurize_tiles(_p(frames), F, H, W, th, tw, bins, mode, _p(out))
+    if rc:
+        raise RuntimeError(f"oracle featurize failed: {rc}")
+    return out
+
+
+def color_histogram(px: np.ndarray, bins: int, mode: int) -> np.ndarray:
+    px = np.ascontiguousarray(px, dtype=np.float32)
+    n, h, w = px.shape[:3]
+    D = port().orc_hist_dim(bins, mode)
+    out = np.empty((n, max(D, 1)), dtype=np.float32)
+    rc = port().orc_color_histogram_f32(_p(px), n, h, w, bins, mode, _p(out))
+    if rc:
+        raise RuntimeError(f"oracle histogram failed: {rc}")
+    return out
+
+
+def euclidean(a: np.ndarray, b: np.ndarray) -> float:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    return port().orc_euclidean(_p(a), _p(b), a.shape[0])
+
+
+def sim_join(L: np.ndarray, R, tau: float, self_join: bool = False, rows=(0, -1),
+             threads: int | None = None):
+    """Brute-force pairs sorted by (i, j): (left int32, right int32, dist f64)."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = L if self_join else np.ascontiguousarray(R, dtype=np.float32)
+    out = OrcPairs()
+    th = threads or max(1, os.cpu_count() or 1)
+    rc = port().orc_sim_join(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
+                             int(self_join), rows[0], rows[1], th, C.byref(out))
+    if rc:
+        raise RuntimeError(f"oracle join failed: {rc}")
+    n = out.count
+    try:
+        if n:
+            res = (np.ctypeslib.as_array(out.left, (n,)).copy(),
+                   np.ctypeslib.as_array(out.right, (n,)).copy(),
+                   np.ctypeslib.as_array(out.dist, (n,)).copy())
+        else:
+            res = (np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0, np.float64))
+    finally:
+        port().orc_pairs_free(C.byref(out))
+    return res
+
+
+# ---- the reference itself ------------------------------------------------------
+
+def ref_featurize_tiles(frames: np.ndarray, th: int, tw: int, bins: int, threads: int = 1):
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    F, H, W = frames.shape[:3]
+    out = np.empty((F * (H // th) * (W // tw), 3 * bins), dtype=np.float32)
+    rc = ref().ref_featurize_tiles(_p(frames), F, H, W, th, tw, bins, _p(out), threads)
+    if rc:
+        raise RuntimeError(f"reference featurize failed: {rc} {ref().ref_last_error()}")
+    return out
+
+
+def ref_color_histogram(px: np.ndarray, bins: int) -> np.ndarray:
+    px = np.ascontiguousarray(px, dtype=np.float32)
+    n, h, w = px.shape[:3]
+    out = np.empty((n, 3 * bins), dtype=np.float32)
+    rc = ref().ref_color_histogram_f32(_p(px), n, h, w, bins, _p(out))
+    if rc:
+        return rc
+    return out
+
+
+def ref_sim_join(L: np.ndarray, R: np.ndarray, tau: float, side: int = 0):
+    """sim_join_pairs positions in reference emission order + probe count,
+    or an int error code (1 ConfigError, 2 ShapeError, 3 MixedDimension ...)."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = np.ascontiguousarray(R, dtype=np.float32)
+    n = C.c_int64()
+    a = C.POINTER(C.c_int32)()
+    b = C.POINTER(C.c_int32)()
+    pr = C.c_uint64()
+    d = L.shape[1] if L.shape[0] else R.shape[1]
+    rc = ref().ref_sim_join(_p(L), L.shape[0], _p(R), R.shape[0], d, float(tau), side,
+                            C.byref(n), C.byref(a), C.byref(b), C.byref(pr))
+    if rc:
+        return rc
+    k = n.value
+    li = np.ctypeslib.as_array(a, (max(k, 1),))[:k].copy()
+    ri = np.ctypeslib.as_array(b, (max(k, 1),))[:k].copy()
+    ref().ref_free(C.cast(a, C.c_void_p))
+    ref().ref_free(C.cast(b, C.c_void_p))
+    return li, ri, pr.value
+
+
+def ref_euclidean(a, b) -> float:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    return ref().ref_euclidean(_p(a), _p(b), a.shape[0])
+
+
+def ref_join_probe_timed(L, R, tau, self_join, p0, p1, threads):
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = L if self_join else np.ascontiguousarray(R, dtype=np.float32)
+    b = C.c_double()
+    p = C.c_double()
+    n = ref().ref_join_probe_timed(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
+                                   int(self_join), p0, p1, threads, C.byref(b), C.byref(p))
+    return n, b.value, p.value

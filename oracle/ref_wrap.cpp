@@ -1,0 +1,255 @@
+// ref_wrap.cpp -- extern "C" entry points over the UNMODIFIED reference
+// sources, compiled where they lie under $PATCHDB_REF (default
+// /root/reference/proj) by oracle/Makefile into oracle/_ref/libpdb_ref.so.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY: used by tests (to pin the C
+// restatement and to mint tests/golden fixtures) and by bench.py's
+// cpu_baseline / --impl reference legs.  Never linked by the product.
+//
+// The reference functions are called through their public API exactly as
+// a reference user would:
+//   transform(generate(VectorStream<Frame>, tiles), color_histogram)
+//       include/patchdb/etl.hpp:66-69, src/etl.cpp:252-373
+//   apply_transformer                       src/etl.cpp:330-354
+//   sim_join_pairs                          src/query.cpp:1094-1104
+//   build_balltree + balltree_within        src/index.cpp:700-842
+//   euclidean                               src/index.cpp:69-76
+// The library is built with -fvisibility=hidden so the reference's
+// `patchdb` symbols never clash with anything else in the process.
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "patchdb/core.hpp"
+#include "patchdb/etl.hpp"
+#include "patchdb/index.hpp"
+#include "patchdb/query.hpp"
+
+#define REF_API extern "C" __attribute__((visibility("default")))
+
+using namespace patchdb;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Error codes mirror include/pdb_cuda.h so tests compare behaviour 1:1.
+int code_of(const std::exception& e) {
+    if (dynamic_cast<const ConfigError*>(&e)) return 1;
+    if (dynamic_cast<const ShapeError*>(&e)) return 2;
+    if (dynamic_cast<const MixedDimensionError*>(&e)) return 3;
+    if (dynamic_cast<const DimensionMismatchError*>(&e)) return 4;
+    if (dynamic_cast<const DuplicatePatchIdError*>(&e)) return 5;
+    return 99;
+}
+
+std::vector<Frame> make_frames(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
+                               int64_t first_no) {
+    std::vector<Frame> out(static_cast<size_t>(n));
+    size_t fb = static_cast<size_t>(H) * W * 3;
+    for (int64_t f = 0; f < n; f++) {
+        Frame& fr = out[static_cast<size_t>(f)];
+        fr.video_id = "v";
+        fr.frame_no = static_cast<uint64_t>(first_no + f);
+        fr.width = static_cast<uint32_t>(W);
+        fr.height = static_cast<uint32_t>(H);
+        fr.channels = 3;
+        fr.pixels.assign(frames + f * fb, frames + (f + 1) * fb);
+    }
+    return out;
+}
+
+std::vector<Patch> make_vecs(const float* X, int64_t n, int32_t d, uint64_t first_id) {
+    std::vector<Patch> out(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; i++) {
+        Patch& p = out[static_cast<size_t>(i)];
+        p.patch_id = first_id + static_cast<uint64_t>(i);
+        p.data.assign(X + i * d, X + (i + 1) * d);
+        p.shape = {static_cast<uint32_t>(d)};
+    }
+    return out;
+}
+
+// Featurize a frame range through the reference stream stages.
+int64_t featurize_range(const uint8_t* frames, int64_t f0, int64_t f1, int32_t H,
+                        int32_t W, int32_t th, int32_t tw, int32_t bins, float* out,
+                        int64_t out_row0) {
+    GeneratorSpec g;
+    g.kind = GeneratorKind::tiles;
+    g.tile_w = static_cast<uint32_t>(tw);
+    g.tile_h = static_cast<uint32_t>(th);
+    TransformerSpec t;
+    t.kind = TransformerKind::color_histogram;
+    t.bins = static_cast<uint32_t>(bins);
+    size_t fb = static_cast<size_t>(H) * W * 3;
+    auto stream = transform(
+        generate(std::make_unique<VectorStream<Frame>>(
+                     make_frames(frames + f0 * fb, f1 - f0, H, W, f0)),
+                 g),
+        t);
+    int64_t row = out_row0;
+    const size_t D = 3u * static_cast<size_t>(bins);
+    while (auto p = stream->next()) {
+        std::memcpy(out + row * D, p->data.data(), D * sizeof(float));
+        row++;
+    }
+    return row - out_row0;
+}
+
+}  // namespace
+
+REF_API const char* ref_last_error() { return g_err.c_str(); }
+
+// Per-channel colour histograms of the tiles of uint8 frames [F,H,W,3].
+// Frames are sharded across `threads` host threads (each shard is an
+// independent reference stream; the reference itself is single-threaded).
+REF_API int ref_featurize_tiles(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
+                                int32_t th, int32_t tw, int32_t bins, float* out,
+                                int32_t threads) {
+    try {
+        if (threads <= 1 || n < 2) {
+            featurize_range(frames, 0, n, H, W, th, tw, bins, out, 0);
+            return 0;
+        }
+        int64_t per_frame = static_cast<int64_t>(W / tw) * (H / th);
+        std::vector<std::thread> pool;
+        std::atomic<int> rc{0};
+        for (int32_t k = 0; k < threads; k++) {
+            int64_t f0 = n * k / threads, f1 = n * (k + 1) / threads;
+            if (f1 <= f0) continue;
+            pool.emplace_back([&, f0, f1] {
+                try {
+                    featurize_range(frames, f0, f1, H, W, th, tw, bins, out, f0 * per_frame);
+                } catch (const std::exception& e) {
+                    rc = code_of(e);
+                }
+            });
+        }
+        for (auto& t : pool) t.join();
+        return rc;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// apply_transformer(color_histogram) on float pixel patches [n,h,w,3].
+REF_API int ref_color_histogram_f32(const float* px, int64_t n, int32_t h, int32_t w,
+                                    int32_t bins, float* out) {
+    try {
+        TransformerSpec t;
+        t.kind = TransformerKind::color_histogram;
+        t.bins = static_cast<uint32_t>(bins);
+        size_t pix = static_cast<size_t>(h) * w * 3;
+        for (int64_t i = 0; i < n; i++) {
+            Patch p;
+            p.patch_id = static_cast<uint64_t>(i + 1);
+            p.shape = {static_cast<uint32_t>(h), static_cast<uint32_t>(w), 3u};
+            p.data.assign(px + i * pix, px + (i + 1) * pix);
+            Patch q = apply_transformer(p, t);
+            std::memcpy(out + i * q.data.size(), q.data.data(), q.data.size() * sizeof(float));
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+REF_API double ref_euclidean(const float* a, const float* b, int64_t d) {
+    return euclidean(a, b, static_cast<size_t>(d));
+}
+
+// sim_join_pairs(left, right, tau, side): left ids 1..nL, right ids
+// 2^32+1..; returns positions (left index, right index) in the reference's
+// emission order.  Caller frees with ref_free.  side: 0 automatic, 1 left,
+// 2 right (query.hpp:84).
+REF_API int ref_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int32_t d,
+                         double tau, int32_t side, int64_t* out_count, int32_t** out_left,
+                         int32_t** out_right, uint64_t* out_probes) {
+    try {
+        auto left = make_vecs(L, nL, d, 1);
+        auto right = make_vecs(R, nR, d, (1ull << 32) + 1);
+        uint64_t probes = 0;
+        auto pairs = sim_join_pairs(left, right, tau, static_cast<BuildSide>(side), &probes);
+        int64_t n = static_cast<int64_t>(pairs.size());
+        int32_t* a = static_cast<int32_t*>(std::malloc(std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        int32_t* b = static_cast<int32_t*>(std::malloc(std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        for (int64_t k = 0; k < n; k++) {
+            a[k] = static_cast<int32_t>(pairs[k].first.patch_id - 1);
+            b[k] = static_cast<int32_t>(pairs[k].second.patch_id - ((1ull << 32) + 1));
+        }
+        *out_count = n;
+        *out_left = a;
+        *out_right = b;
+        if (out_probes) *out_probes = probes;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+REF_API void ref_free(void* p) { std::free(p); }
+
+// Timed CPU baseline of the reference join: the reference's own build
+// (build_balltree over the build side) and probe (balltree_within) with the
+// probe loop of src/query.cpp:516-526 spread over `threads` host threads
+// (BallTreeIndex is immutable after build).  Probes rows
+// [p0, p1) of L against all of R.  self_join counts only j > i.  Returns
+// the number of matched pairs; *build_s / *probe_s receive wall seconds.
+REF_API int64_t ref_join_probe_timed(const float* L, int64_t nL, const float* R,
+                                     int64_t nR, int32_t d, double tau, int32_t self_join,
+                                     int64_t p0, int64_t p1, int32_t threads,
+                                     double* build_s, double* probe_s) {
+    try {
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::pair<std::vector<float>, uint64_t>> pts;
+        pts.reserve(static_cast<size_t>(nR));
+        for (int64_t j = 0; j < nR; j++)
+            pts.emplace_back(std::vector<float>(R + j * d, R + (j + 1) * d),
+                             static_cast<uint64_t>(j));
+        BallTreeIndex tree = build_balltree(pts);
+        auto t1 = std::chrono::steady_clock::now();
+        if (p1 > nL) p1 = nL;
+        std::atomic<int64_t> total{0};
+        std::atomic<int64_t> next{p0};
+        std::vector<std::thread> pool;
+        for (int32_t k = 0; k < std::max(threads, 1); k++)
+            pool.emplace_back([&] {
+                int64_t local = 0;
+                for (;;) {
+                    int64_t i0 = next.fetch_add(64);
+                    if (i0 >= p1) break;
+                    int64_t i1 = std::min(i0 + 64, p1);
+                    for (int64_t i = i0; i < i1; i++) {
+                        std::vector<float> q(L + i * d, L + (i + 1) * d);
+                        auto ids = balltree_within(tree, q, tau);
+                        if (self_join) {
+                            for (uint64_t id : ids)
+                                if (static_cast<int64_t>(id) > i) local++;
+                        } else {
+                            local += static_cast<int64_t>(ids.size());
+                        }
+                    }
+                }
+                total += local;
+            });
+        for (auto& t : pool) t.join();
+        auto t2 = std::chrono::steady_clock::now();
+        if (build_s) *build_s = std::chrono::duration<double>(t1 - t0).count();
+        if (probe_s) *probe_s = std::chrono::duration<double>(t2 - t1).count();
+        return total;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}

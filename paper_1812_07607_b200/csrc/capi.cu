@@ -1,0 +1,423 @@
+// capi.cu -- the extern "C" boundary of libpdb_cuda.so (include/pdb_cuda.h):
+// argument validation with the reference's error taxonomy, the per-device
+// context, stream-ordered scratch memory, host<->device staging.
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pdb_internal.cuh"
+
+#define PDB_API extern "C" __attribute__((visibility("default")))
+
+namespace pdb {
+
+namespace {
+thread_local std::string g_last_error;
+std::mutex g_ctx_mu;
+DeviceCtx g_ctx[64];
+bool g_ctx_ok[64] = {};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
+
+void fail(int status, const std::string& msg) { throw Failure{status, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    const int st = e == cudaErrorMemoryAllocation ? PDB_ERR_OUT_OF_MEMORY : PDB_ERR_CUDA;
+    fail(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+const DeviceCtx& device_ctx() {
+    int dev = 0;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        fail(PDB_ERR_NO_DEVICE, "no CUDA device visible (libpdb_cuda has no CPU path)");
+    }
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) fail(PDB_ERR_NO_DEVICE, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (g_ctx_ok[dev]) return g_ctx[dev];
+    DeviceCtx c;
+    c.device = dev;
+    cudaDeviceProp prop;
+    PDB_CUDA(cudaGetDeviceProperties(&prop, dev));
+    c.sm_count = prop.multiProcessorCount;
+    c.cc_major = prop.major;
+    c.cc_minor = prop.minor;
+    c.smem_optin = prop.sharedMemPerBlockOptin;
+    if (prop.major != 10)
+        fail(PDB_ERR_NO_DEVICE, std::string("device '") + prop.name +
+                                    "' is not sm_100 (Blackwell); this build targets sm_100a only");
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    PDB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+        fail(PDB_ERR_CUDA, "driver entry point cuTensorMapEncodeTiled unavailable");
+    c.encode_tiled = fn;
+    // Keep freed scratch in the stream-ordered pool between calls.
+    cudaMemPool_t pool;
+    PDB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    PDB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_ctx[dev] = c;
+    g_ctx_ok[dev] = true;
+    return g_ctx[dev];
+}
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(PDB_ERR_OUT_OF_MEMORY, "device allocation of " + std::to_string(bytes) +
+                                        " bytes failed: " + cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+}  // namespace pdb
+
+using namespace pdb;
+
+namespace {
+
+// Runs `body`, converting Failure / CUDA errors into status codes.
+template <class F>
+int guarded(F&& body) {
+    clear_error();
+    try {
+        body();
+        return PDB_OK;
+    } catch (const Failure& f) {
+        set_error(f.msg);
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return PDB_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        set_error("unexpected exception");
+        return PDB_ERR_CUDA;
+    }
+}
+
+cudaStream_t stream_of(void* s) { return s ? static_cast<cudaStream_t>(s) : cudaStreamPerThread; }
+
+void check_featurize_args(const void* frames, int64_t n, int32_t H, int32_t W, int32_t th,
+                          int32_t tw, int32_t bins, int32_t mode, const void* out) {
+    // Reference order: TransformerSpec::validate (bins, src/etl.cpp:64-67) and
+    // GeneratorSpec::validate (tile sizes, src/etl.cpp:47-50) -> ConfigError.
+    if (mode != PDB_HIST_PER_CHANNEL && mode != PDB_HIST_JOINT)
+        fail(PDB_ERR_INVALID_ARGUMENT, "histogram mode must be 0 (per-channel) or 1 (joint)");
+    if (bins < 2) fail(PDB_ERR_CONFIG, "color_histogram needs at least 2 bins per channel");
+    if (hist_dim(bins, mode) < 0)
+        fail(PDB_ERR_CONFIG, "joint colour histogram supports 2..16 bins per channel");
+    if (tw < 1 || th < 1) fail(PDB_ERR_CONFIG, "tiles generator needs tile_w and tile_h >= 1");
+    if (n < 0 || H < 0 || W < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative frame count or size");
+    if (n > 0 && (!frames || !out)) fail(PDB_ERR_INVALID_ARGUMENT, "null frames/out pointer");
+}
+
+int64_t n_tiles_of(int64_t n, int32_t H, int32_t W, int32_t th, int32_t tw) {
+    return n * static_cast<int64_t>(W / tw) * static_cast<int64_t>(H / th);
+}
+
+void check_join_args(const void* L, int64_t nL, const void* R, int64_t nR, int32_t d, double tau,
+                     const pdb_join_opts* o) {
+    // run_sim_join order: tau (src/query.cpp:488), then dims (467-499).
+    if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
+    if (nL < 0 || nR < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative row count");
+    if (nL > INT32_MAX || nR > INT32_MAX)
+        fail(PDB_ERR_INVALID_ARGUMENT, "row counts above 2^31-1 are not supported");
+    const bool self = o && (o->flags & PDB_JOIN_SELF);
+    if ((nL > 0 || (!self && nR > 0)) && d < 1)
+        fail(PDB_ERR_SHAPE, "similarity join needs non-empty patch data");
+    if (nL > 0 && !L) fail(PDB_ERR_INVALID_ARGUMENT, "null L");
+    if (!self && nR > 0 && !R) fail(PDB_ERR_INVALID_ARGUMENT, "null R");
+    if (o && (o->flags & ~(PDB_JOIN_SELF | PDB_JOIN_SORTED)))
+        fail(PDB_ERR_INVALID_ARGUMENT, "unknown join flags");
+    if (o && o->shard_count > 1 && (o->shard_index < 0 || o->shard_index >= o->shard_count))
+        fail(PDB_ERR_INVALID_ARGUMENT, "shard_index out of range");
+}
+
+void pairs_to_host(const pdb_dev_pairs& dp, pdb_pairs* out, cudaStream_t s) {
+    out->count = dp.count;
+    const size_t n = static_cast<size_t>(std::max<int64_t>(dp.count, 1));
+    out->left = static_cast<int32_t*>(std::malloc(n * sizeof(int32_t)));
+    out->right = static_cast<int32_t*>(std::malloc(n * sizeof(int32_t)));
+    out->dist = static_cast<float*>(std::malloc(n * sizeof(float)));
+    if (!out->left || !out->right || !out->dist) {
+        pdb_pairs_free(out);
+        fail(PDB_ERR_OUT_OF_MEMORY, "host allocation for pairs failed");
+    }
+    if (dp.count > 0) {
+        PDB_CUDA(cudaMemcpyAsync(out->left, dp.left, dp.count * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaMemcpyAsync(out->right, dp.right, dp.count * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaMemcpyAsync(out->dist, dp.dist, dp.count * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    PDB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+PDB_API const char* pdb_last_error(void) { return g_last_error.c_str(); }
+
+PDB_API const char* pdb_status_name(int status) {
+    switch (status) {
+        case PDB_OK: return "ok";
+        case PDB_ERR_CONFIG: return "ConfigError";
+        case PDB_ERR_SHAPE: return "ShapeError";
+        case PDB_ERR_MIXED_DIMENSION: return "MixedDimensionError";
+        case PDB_ERR_DIMENSION_MISMATCH: return "DimensionMismatchError";
+        case PDB_ERR_DUPLICATE_ID: return "DuplicatePatchIdError";
+        case PDB_ERR_CAPACITY: return "CapacityError";
+        case PDB_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+        case PDB_ERR_CUDA: return "CudaError";
+        case PDB_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+        case PDB_ERR_NO_DEVICE: return "NoDevice";
+    }
+    return "unknown";
+}
+
+PDB_API int pdb_version(void) { return (0 << 16) | (1 << 8) | 0; }
+
+PDB_API int pdb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int ok = 0;
+    for (int i = 0; i < n; i++) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ok++;
+    }
+    return ok;
+}
+
+PDB_API int pdb_hist_dim(int32_t bins, int32_t mode) { return hist_dim(bins, mode); }
+
+PDB_API int pdb_featurize_tiles_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W,
+                                    int32_t th, int32_t tw, int32_t bins, int32_t mode,
+                                    float* d_out, void* stream) {
+    return guarded([&] {
+        check_featurize_args(d_frames, n, H, W, th, tw, bins, mode, d_out);
+        device_ctx();
+        launch_featurize_tiles(d_frames, n, H, W, th, tw, bins, mode, d_out, stream_of(stream));
+    });
+}
+
+PDB_API int pdb_featurize_tiles(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
+                                int32_t th, int32_t tw, int32_t bins, int32_t mode, float* out) {
+    return guarded([&] {
+        check_featurize_args(frames, n, H, W, th, tw, bins, mode, out);
+        device_ctx();
+        const int64_t nt = n_tiles_of(n, H, W, th, tw);
+        const int D = hist_dim(bins, mode);
+        if (nt == 0) return;
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t fbytes = static_cast<size_t>(n) * H * W * 3;
+        DevBuf<uint8_t> dF(fbytes, s);
+        DevBuf<float> dO(static_cast<size_t>(nt) * D, s);
+        PDB_CUDA(cudaMemcpyAsync(dF.p, frames, fbytes, cudaMemcpyHostToDevice, s));
+        launch_featurize_tiles(dF.p, n, H, W, th, tw, bins, mode, dO.p, s);
+        PDB_CUDA(cudaMemcpyAsync(out, dO.p, static_cast<size_t>(nt) * D * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+static void check_f32_args(const void* px, int64_t n, int32_t h, int32_t w, int32_t bins,
+                           int32_t mode, const void* out) {
+    if (mode != PDB_HIST_PER_CHANNEL && mode != PDB_HIST_JOINT)
+        fail(PDB_ERR_INVALID_ARGUMENT, "histogram mode must be 0 (per-channel) or 1 (joint)");
+    if (bins < 2) fail(PDB_ERR_CONFIG, "color_histogram needs at least 2 bins per channel");
+    if (hist_dim(bins, mode) < 0)
+        fail(PDB_ERR_CONFIG, "joint colour histogram supports 2..16 bins per channel");
+    // apply_transformer: input must be pixel shaped [h,w,3] (src/etl.cpp:332-334).
+    if (h < 1 || w < 1) fail(PDB_ERR_SHAPE, "transformer input must be pixel shaped [h,w,3]");
+    if (n < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative patch count");
+    if (n > 0 && (!px || !out)) fail(PDB_ERR_INVALID_ARGUMENT, "null pointer");
+}
+
+PDB_API int pdb_color_histogram_f32_dev(const float* d_px, int64_t n, int32_t h, int32_t w,
+                                        int32_t bins, int32_t mode, float* d_out, void* stream) {
+    return guarded([&] {
+        check_f32_args(d_px, n, h, w, bins, mode, d_out);
+        device_ctx();
+        launch_hist_f32(d_px, n, h, w, bins, mode, d_out, stream_of(stream));
+    });
+}
+
+PDB_API int pdb_color_histogram_f32(const float* px, int64_t n, int32_t h, int32_t w,
+                                    int32_t bins, int32_t mode, float* out) {
+    return guarded([&] {
+        check_f32_args(px, n, h, w, bins, mode, out);
+        device_ctx();
+        if (n == 0) return;
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t in_n = static_cast<size_t>(n) * h * w * 3;
+        const size_t D = static_cast<size_t>(hist_dim(bins, mode));
+        DevBuf<float> dI(in_n, s), dO(static_cast<size_t>(n) * D, s);
+        PDB_CUDA(cudaMemcpyAsync(dI.p, px, in_n * sizeof(float), cudaMemcpyHostToDevice, s));
+        launch_hist_f32(dI.p, n, h, w, bins, mode, dO.p, s);
+        PDB_CUDA(cudaMemcpyAsync(out, dO.p, static_cast<size_t>(n) * D * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+PDB_API int pdb_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
+                             int32_t d, double tau, const pdb_join_opts* opts, pdb_dev_pairs* out,
+                             pdb_join_stats* stats) {
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_join_args(d_L, nL, d_R, nR, d, tau, opts);
+        device_ctx();
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        o.stream = stream_of(o.stream);
+        run_sim_join_dev(d_L, nL, d_R, nR, d, tau, o, out, stats);
+    });
+}
+
+PDB_API void pdb_dev_pairs_free(pdb_dev_pairs* p) {
+    if (!p) return;
+    cudaFree(p->left);
+    cudaFree(p->right);
+    cudaFree(p->dist);
+    p->left = p->right = nullptr;
+    p->dist = nullptr;
+    p->count = p->capacity = 0;
+}
+
+PDB_API int pdb_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int32_t d,
+                         double tau, const pdb_join_opts* opts, pdb_pairs* out) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_join_args(L, nL, R, nR, d, tau, opts);
+        device_ctx();
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        cudaStream_t s = cudaStreamPerThread;
+        o.stream = s;
+        const bool self = (o.flags & PDB_JOIN_SELF) != 0;
+        DevBuf<float> dL(static_cast<size_t>(nL) * std::max(d, 1), s), dR;
+        if (nL > 0)
+            PDB_CUDA(cudaMemcpyAsync(dL.p, L, static_cast<size_t>(nL) * d * sizeof(float),
+                                     cudaMemcpyHostToDevice, s));
+        if (!self && nR > 0) {
+            dR.reset(static_cast<size_t>(nR) * d, s);
+            PDB_CUDA(cudaMemcpyAsync(dR.p, R, static_cast<size_t>(nR) * d * sizeof(float),
+                                     cudaMemcpyHostToDevice, s));
+        }
+        pdb_dev_pairs dp{};
+        try {
+            run_sim_join_dev(dL.p, nL, self ? dL.p : dR.p, self ? nL : nR, d, tau, o, &dp, nullptr);
+            pairs_to_host(dp, out, s);
+        } catch (...) {
+            pdb_dev_pairs_free(&dp);
+            throw;
+        }
+        pdb_dev_pairs_free(&dp);
+    });
+}
+
+PDB_API void pdb_pairs_free(pdb_pairs* p) {
+    if (!p) return;
+    std::free(p->left);
+    std::free(p->right);
+    std::free(p->dist);
+    p->left = p->right = nullptr;
+    p->dist = nullptr;
+    p->count = 0;
+}
+
+PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
+                               int32_t th, int32_t tw, int32_t bins, int32_t mode, double tau,
+                               const pdb_join_opts* opts, float* features, pdb_pairs* out) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_featurize_args(frames, n, H, W, th, tw, bins, mode, frames);
+        if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
+        device_ctx();
+        const int64_t nt = n_tiles_of(n, H, W, th, tw);
+        const int D = hist_dim(bins, mode);
+        if (nt > INT32_MAX) fail(PDB_ERR_INVALID_ARGUMENT, "too many tiles");
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t fb = static_cast<size_t>(H) * W * 3;
+        DevBuf<uint8_t> dF(static_cast<size_t>(n) * fb, s);
+        DevBuf<float> dX(static_cast<size_t>(std::max<int64_t>(nt, 1)) * D, s);
+        // Copy frames in chunks on a second stream so K1 on chunk k overlaps
+        // the H2D copy of chunk k+1.
+        cudaStream_t cs;
+        PDB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 64));
+        std::vector<cudaEvent_t> evs;
+        const int64_t tpf = static_cast<int64_t>(W / tw) * (H / th);
+        try {
+            for (int64_t f0 = 0; f0 < n; f0 += chunk) {
+                const int64_t cnt = std::min(chunk, n - f0);
+                cudaEvent_t e;
+                PDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                evs.push_back(e);
+                PDB_CUDA(cudaMemcpyAsync(dF.p + f0 * fb, frames + f0 * fb, cnt * fb,
+                                         cudaMemcpyHostToDevice, cs));
+                PDB_CUDA(cudaEventRecord(e, cs));
+                PDB_CUDA(cudaStreamWaitEvent(s, e, 0));
+                launch_featurize_tiles(dF.p + f0 * fb, cnt, H, W, th, tw, bins, mode,
+                                       dX.p + f0 * tpf * D, s);
+            }
+        } catch (...) {
+            for (auto e : evs) cudaEventDestroy(e);
+            cudaStreamDestroy(cs);
+            throw;
+        }
+        for (auto e : evs) cudaEventDestroy(e);
+        cudaStreamDestroy(cs);
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        o.flags |= PDB_JOIN_SELF;
+        o.stream = s;
+        pdb_dev_pairs dp{};
+        try {
+            run_sim_join_dev(dX.p, nt, dX.p, nt, D, tau, o, &dp, nullptr);
+            if (features)
+                PDB_CUDA(cudaMemcpyAsync(features, dX.p, static_cast<size_t>(nt) * D * sizeof(float),
+                                         cudaMemcpyDeviceToHost, s));
+            pairs_to_host(dp, out, s);
+        } catch (...) {
+            pdb_dev_pairs_free(&dp);
+            throw;
+        }
+        pdb_dev_pairs_free(&dp);
+    });
+}
+
+PDB_API void* pdb_host_alloc(int64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, static_cast<size_t>(std::max<int64_t>(bytes, 1)), cudaHostAllocDefault) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+PDB_API void pdb_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}

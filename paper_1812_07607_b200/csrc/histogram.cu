@@ -1,0 +1,358 @@
+// histogram.cu -- K1: fused generate(tiles) -> color_histogram over uint8
+// frames, plus the float-patch apply_transformer path.
+//
+// Reference semantics (proj/):
+//   tile grid, emission order      src/etl.cpp:264-298
+//   uint8 -> float crop            src/core.cpp:88-93   (fused away: the
+//                                  float value of a byte is exact)
+//   binning + normalisation        src/etl.cpp:336-348
+// For a byte v and B < 65793, the reference's float expression
+// (uint32)(v * B / 256.0f) is exactly (v*B) >> 8: v*B < 2^24 is an exact
+// float, /256 is exact and the cast truncates.  Counts are integers; the
+// reference accumulates them with `+= 1.0f`, which is exact below 2^24 and
+// sticks at 2^24 above it, so count -> min(count, 2^24) reproduces it.  The
+// normalisation is one IEEE round-to-nearest float division by
+// (float)(h*w), done with __fdiv_rn (the library is built without
+// fast-math).
+//
+// B200 mapping: one warp per tile, 4 tiles per 128-thread CTA.  Frames are
+// read with 16-byte non-allocating loads, three per lane per task so each
+// lane owns 16 whole RGB pixels (48 B); a 60x80 tile row is 5 such tasks.
+// Counts live in shared memory as lane-private columns cnt[bin][lane]
+// (bank = lane, so updates never conflict and need no atomics) and are
+// reduced with one REDUX per bin at the end of the tile.  Bin counts too
+// large for lane-private columns use per-warp shared-memory atomics.
+
+#include "pdb_internal.cuh"
+
+namespace pdb {
+
+namespace {
+
+constexpr int kWarpsPerCta = 4;
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Reference float binning for arbitrary float values / large B.
+__device__ __forceinline__ uint32_t bin_float(float v, uint32_t B) {
+    float t = __fdiv_rn(__fmul_rn(v, __uint2float_rn(B)), 256.0f);
+    uint32_t b = __float2uint_rz(t);  // NaN / negative -> 0, saturates high
+    return b >= B ? B - 1 : b;
+}
+
+__device__ __forceinline__ float normalise(uint32_t cnt, float npix) {
+    float c = cnt >= (1u << 24) ? 16777216.0f : __uint2float_rn(cnt);
+    return __fdiv_rn(c, npix);
+}
+
+__device__ __forceinline__ uint32_t byte_at(const uint32_t (&w)[12], int k) {
+    return (w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+}
+
+// ---------------------------------------------------------------------------
+// Lane-private counter kernel: D = number of bins <= NB <= 64.
+// BT > 0 fixes B at compile time (B=4 -> shifts), BT == 0 reads it at run time.
+template <int NB, bool JOINT, int BT, bool VEC>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_hist_tiles_lane(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, int W, int th,
+                  int tw, int ntx, int tiles_per_frame, int B_rt, int D, float npix,
+                  float* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tile = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+    if (tile >= n_tiles) return;  // warp-uniform; the CTA never synchronises
+    const uint32_t B = BT > 0 ? static_cast<uint32_t>(BT) : static_cast<uint32_t>(B_rt);
+    uint32_t* cnt = smem + warp * NB * 32 + lane;
+
+#pragma unroll
+    for (int b = 0; b < NB; b++) cnt[b * 32] = 0;
+
+    const int64_t f = tile / tiles_per_frame;
+    const int t = static_cast<int>(tile - f * tiles_per_frame);
+    const int ty = t / ntx, tx = t - (t / ntx) * ntx;
+    const uint8_t* base =
+        frames + (static_cast<size_t>(f) * H * W + static_cast<size_t>(ty) * th * W +
+                  static_cast<size_t>(tx) * tw) * 3;
+
+    auto count_pixel = [&](uint32_t r, uint32_t g, uint32_t b) {
+        const uint32_t br = (r * B) >> 8, bg = (g * B) >> 8, bb = (b * B) >> 8;
+        if (JOINT) {
+            cnt[((br * B + bg) * B + bb) * 32] += 1;
+        } else {
+            cnt[br * 32] += 1;
+            cnt[(B + bg) * 32] += 1;
+            cnt[(2 * B + bb) * 32] += 1;
+        }
+    };
+
+    if (VEC) {
+        // 16-pixel tasks: rows of the tile split in tw/16 segments of 48 B.
+        const int segs = tw >> 4;
+        const int ntask = th * segs;
+        for (int task = lane; task < ntask; task += 32) {
+            const int r = task / segs, s = task - r * segs;
+            const uint8_t* p = base + (static_cast<size_t>(r) * W + s * 16) * 3;
+            const uint4 a = ldg_stream(p), b = ldg_stream(p + 16), c = ldg_stream(p + 32);
+            const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int px = 0; px < 16; px++)
+                count_pixel(byte_at(w, 3 * px), byte_at(w, 3 * px + 1), byte_at(w, 3 * px + 2));
+        }
+    } else {
+        const int npx = th * tw;
+        for (int i = lane; i < npx; i += 32) {
+            const int r = i / tw, x = i - r * tw;
+            const uint8_t* p = base + (static_cast<size_t>(r) * W + x) * 3;
+            count_pixel(p[0], p[1], p[2]);
+        }
+    }
+    __syncwarp();
+
+    // One REDUX per bin; lane (b % 32) keeps bin b, then coalesced stores.
+    uint32_t mine[(NB + 31) / 32];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        if (b < D) {
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt[b * 32]);
+            if ((b & 31) == lane) mine[b >> 5] = tot;
+        }
+    }
+    float* o = out + tile * D;
+#pragma unroll
+    for (int j = 0; j < (NB + 31) / 32; j++) {
+        const int b = j * 32 + lane;
+        if (b < D) o[b] = normalise(mine[j], npix);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp shared-memory atomic counters for larger bin counts.
+// JOINT: B^3 <= 4096 bins.  Per-channel: raw byte-value counts [3][256],
+// mapped to bins at the end (bin(v) is monotone in v), which handles any B.
+template <bool JOINT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_hist_tiles_atomic(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, int W, int th,
+                    int tw, int ntx, int tiles_per_frame, int B_rt, int64_t D, int slots,
+                    float npix, float* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tile = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+    if (tile >= n_tiles) return;
+    const uint32_t B = static_cast<uint32_t>(B_rt);
+    uint32_t* cnt = smem + static_cast<size_t>(warp) * slots;
+    for (int k = lane; k < slots; k += 32) cnt[k] = 0;
+    __syncwarp();
+
+    const int64_t f = tile / tiles_per_frame;
+    const int t = static_cast<int>(tile - f * tiles_per_frame);
+    const int ty = t / ntx, tx = t - (t / ntx) * ntx;
+    const uint8_t* base =
+        frames + (static_cast<size_t>(f) * H * W + static_cast<size_t>(ty) * th * W +
+                  static_cast<size_t>(tx) * tw) * 3;
+    const int npx = th * tw;
+    for (int i = lane; i < npx; i += 32) {
+        const int r = i / tw, x = i - r * tw;
+        const uint8_t* p = base + (static_cast<size_t>(r) * W + x) * 3;
+        const uint32_t cr = p[0], cg = p[1], cb = p[2];
+        if (JOINT) {
+            const uint32_t idx = (((cr * B) >> 8) * B + ((cg * B) >> 8)) * B + ((cb * B) >> 8);
+            atomicAdd(&cnt[idx], 1u);
+        } else {
+            atomicAdd(&cnt[cr], 1u);
+            atomicAdd(&cnt[256 + cg], 1u);
+            atomicAdd(&cnt[512 + cb], 1u);
+        }
+    }
+    __syncwarp();
+    float* o = out + tile * D;
+    if (JOINT) {
+        for (int k = lane; k < D; k += 32) o[k] = normalise(cnt[k], npix);
+        return;
+    }
+    for (int64_t k = lane; k < D; k += 32) o[k] = 0.0f;
+    __syncwarp();
+    for (int c = 0; c < 3; c++) {
+        const uint32_t* cc = cnt + 256 * c;
+        for (int v = lane; v < 256; v += 32) {
+            const uint32_t bv = bin_float(static_cast<float>(v), B);
+            if (v > 0 && bin_float(static_cast<float>(v - 1), B) == bv) continue;
+            uint32_t sum = 0;
+            for (int u = v; u < 256 && bin_float(static_cast<float>(u), B) == bv; u++) sum += cc[u];
+            o[static_cast<int64_t>(c) * B + bv] = normalise(sum, npix);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// apply_transformer over float pixel patches [n, h, w, 3]: one CTA per
+// patch, shared-memory atomic counters (D <= kF32SmemBins) or global u32
+// counters for very large D.
+constexpr int kF32SmemBins = 12288;
+
+__device__ __forceinline__ uint32_t f32_slot(const float* p, uint32_t B, bool joint, int c) {
+    if (joint)
+        return (bin_float(p[0], B) * B + bin_float(p[1], B)) * B + bin_float(p[2], B);
+    return static_cast<uint32_t>(c) * B + bin_float(p[c], B);
+}
+
+__global__ void __launch_bounds__(256)
+k_hist_f32_smem(const float* __restrict__ px, int64_t n, int64_t npx, int B_rt, int joint,
+                int D, float npix, float* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    const int64_t patch = blockIdx.x;
+    const uint32_t B = static_cast<uint32_t>(B_rt);
+    for (int k = threadIdx.x; k < D; k += blockDim.x) smem[k] = 0;
+    __syncthreads();
+    const float* base = px + patch * npx * 3;
+    for (int64_t i = threadIdx.x; i < npx; i += blockDim.x) {
+        const float* p = base + i * 3;
+        if (joint) {
+            atomicAdd(&smem[f32_slot(p, B, true, 0)], 1u);
+        } else {
+            for (int c = 0; c < 3; c++) atomicAdd(&smem[f32_slot(p, B, false, c)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < D; k += blockDim.x)
+        out[patch * D + k] = normalise(smem[k], npix);
+}
+
+__global__ void k_hist_f32_global(const float* __restrict__ px, int64_t n, int64_t npx,
+                                  int B_rt, int joint, int64_t D, uint32_t* __restrict__ cnt) {
+    const int64_t patch = blockIdx.y;
+    const uint32_t B = static_cast<uint32_t>(B_rt);
+    const float* base = px + patch * npx * 3;
+    uint32_t* cc = cnt + patch * D;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < npx;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float* p = base + i * 3;
+        if (joint) {
+            atomicAdd(&cc[f32_slot(p, B, true, 0)], 1u);
+        } else {
+            for (int c = 0; c < 3; c++) atomicAdd(&cc[f32_slot(p, B, false, c)], 1u);
+        }
+    }
+}
+
+__global__ void k_normalise(const uint32_t* __restrict__ cnt, int64_t total, float npix,
+                            float* __restrict__ out) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[k] = normalise(cnt[k], npix);
+}
+
+template <int NB, bool JOINT, int BT>
+void launch_lane(bool vec, dim3 grid, size_t smem, cudaStream_t s, const uint8_t* frames,
+                 int64_t n_tiles, int H, int W, int th, int tw, int ntx, int tpf, int B, int D,
+                 float npix, float* out) {
+    if (vec) {
+        auto k = k_hist_tiles_lane<NB, JOINT, BT, true>;
+        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k<<<grid, kWarpsPerCta * 32, smem, s>>>(frames, n_tiles, H, W, th, tw, ntx, tpf, B, D,
+                                                npix, out);
+    } else {
+        auto k = k_hist_tiles_lane<NB, JOINT, BT, false>;
+        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k<<<grid, kWarpsPerCta * 32, smem, s>>>(frames, n_tiles, H, W, th, tw, ntx, tpf, B, D,
+                                                npix, out);
+    }
+}
+
+}  // namespace
+
+int hist_dim(int32_t bins, int32_t mode) {
+    if (bins < 2) return -1;
+    if (mode == PDB_HIST_PER_CHANNEL) {
+        if (bins > (INT32_MAX / 3)) return -1;
+        return 3 * bins;
+    }
+    if (mode == PDB_HIST_JOINT) return bins <= 16 ? bins * bins * bins : -1;
+    return -1;
+}
+
+void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H, int32_t W,
+                            int32_t th, int32_t tw, int32_t bins, int32_t mode, float* d_out,
+                            cudaStream_t s) {
+    const int D = hist_dim(bins, mode);
+    const int ntx = W / tw, nty = H / th;
+    const int tpf = ntx * nty;
+    const int64_t n_tiles = n_frames * tpf;
+    if (n_tiles == 0) return;
+    const float npix_h = static_cast<float>(static_cast<uint64_t>(th) * static_cast<uint64_t>(tw));
+    const bool vec = (W % 16 == 0) && (tw % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(d_frames) % 16 == 0);
+    const dim3 grid(static_cast<unsigned>(ceil_div(n_tiles, kWarpsPerCta)));
+    const bool joint = mode == PDB_HIST_JOINT;
+    if (D <= 64) {
+        const size_t smem = static_cast<size_t>(kWarpsPerCta) * 64 * 32 * 4;
+        if (joint && bins == 4)
+            launch_lane<64, true, 4>(vec, grid, smem, s, d_frames, n_tiles, H, W, th, tw, ntx,
+                                     tpf, bins, D, npix_h, d_out);
+        else if (joint)
+            launch_lane<64, true, 0>(vec, grid, smem, s, d_frames, n_tiles, H, W, th, tw, ntx,
+                                     tpf, bins, D, npix_h, d_out);
+        else if (bins == 4)
+            launch_lane<12, false, 4>(vec, grid, static_cast<size_t>(kWarpsPerCta) * 12 * 32 * 4,
+                                      s, d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D,
+                                      npix_h, d_out);
+        else if (bins == 8)
+            launch_lane<24, false, 8>(vec, grid, static_cast<size_t>(kWarpsPerCta) * 24 * 32 * 4,
+                                      s, d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D,
+                                      npix_h, d_out);
+        else
+            launch_lane<64, false, 0>(vec, grid, smem, s, d_frames, n_tiles, H, W, th, tw, ntx,
+                                      tpf, bins, D, npix_h, d_out);
+    } else {
+        const int slots = joint ? D : 768;
+        const size_t smem = static_cast<size_t>(kWarpsPerCta) * slots * 4;
+        if (joint) {
+            PDB_CUDA(cudaFuncSetAttribute(k_hist_tiles_atomic<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            k_hist_tiles_atomic<true><<<grid, kWarpsPerCta * 32, smem, s>>>(
+                d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D, slots, npix_h, d_out);
+        } else {
+            PDB_CUDA(cudaFuncSetAttribute(k_hist_tiles_atomic<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            k_hist_tiles_atomic<false><<<grid, kWarpsPerCta * 32, smem, s>>>(
+                d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D, slots, npix_h, d_out);
+        }
+    }
+    PDB_CUDA(cudaGetLastError());
+}
+
+void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t w, int32_t bins,
+                     int32_t mode, float* d_out, cudaStream_t s) {
+    const int64_t D = hist_dim(bins, mode);
+    const int64_t npx = static_cast<int64_t>(h) * w;
+    if (n == 0) return;
+    const float npix = static_cast<float>(static_cast<uint64_t>(npx));
+    const int joint = mode == PDB_HIST_JOINT;
+    if (D <= kF32SmemBins) {
+        const size_t smem = static_cast<size_t>(D) * 4;
+        PDB_CUDA(cudaFuncSetAttribute(k_hist_f32_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k_hist_f32_smem<<<static_cast<unsigned>(n), 256, smem, s>>>(d_px, n, npx, bins, joint,
+                                                                    static_cast<int>(D), npix,
+                                                                    d_out);
+    } else {
+        DevBuf<uint32_t> cnt(static_cast<size_t>(n * D), s);
+        PDB_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(n * D) * 4, s));
+        dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(npx, 256), 64)),
+               static_cast<unsigned>(n));
+        k_hist_f32_global<<<g, 256, 0, s>>>(d_px, n, npx, bins, joint, D, cnt.p);
+        k_normalise<<<592, 256, 0, s>>>(cnt.p, n * D, npix, d_out);
+    }
+    PDB_CUDA(cudaGetLastError());
+}
+
+}  // namespace pdb

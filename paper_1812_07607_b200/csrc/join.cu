@@ -1,0 +1,782 @@
+// join.cu -- K2 (tensor-core screen) + K3 (exact fp64 re-check and
+// compaction) of the threshold similarity join.
+//
+// Contract (proj/): emit (i, j) iff euclidean(L_i, R_j) <= tau, with
+// euclidean the sequential, unfused fp64 chain of src/index.cpp:69-76 and
+// the inclusive `<=` of src/index.cpp:833 / tests/oracles.hpp:77-85.  The
+// reference reaches that set through a ball tree (src/query.cpp:485-528,
+// src/index.cpp:811-842); here it is reached by a dense screen plus an exact
+// re-check, and the two agree pair for pair.
+//
+// Pipeline per call:
+//   k_col_partial / k_col_final  column mean mu of (a sample of) L
+//   k_prep       x~ = tf32_rna(x - mu) per row (padded to DP columns),
+//                ||x~||^2 (fp64 -> f32), ||x~|| (rounded up), row class
+//   k_tile_stats per 256-row tile of R: max ||y~||, max ||y~||^2;
+//                g_j = ||y~_j||^2 / 2 padded with +inf
+//   k_screen     tcgen05 kind::tf32 GEMM, 128x256 tiles, TMA-staged
+//                128B-swizzled operands, fp32 accumulators double-buffered
+//                in TMEM; epilogue warps test dot - g_j >= h_i(tile) and
+//                append candidate (i, j) with warp-aggregated atomics
+//   k_recheck    exact fp64 euclidean of every candidate on the ORIGINAL
+//                fp32 rows, warp-ballot compaction of the survivors into
+//                (left, right, dist)
+//
+// Why the screen never drops a true pair (the margin band):
+//   x~, y~ are the rounded, centred vectors the MMA sees; centring does not
+//   change distances and |x~ - x| <= U ||x~|| per row with
+//   U = 2^-11 + 2^-20 (fp32 subtraction + round-to-nearest tf32), so
+//   ||x~ - y~|| <= ||x - y|| + U (||x~|| + ||y~||).  The norms are computed
+//   from x~ itself, so S = ||x~||^2 + ||y~||^2 - 2 x~.y~ is a near-exact
+//   squared distance of two perturbed points: tf32 x tf32 products are exact
+//   in fp32 and the accumulation of DP terms errs by at most
+//   DP * 2^-23 * sum|x~_k y~_k| <= DP * 2^-23 (||x~||^2 + ||y~||^2) / 2
+//   (truncating adds), plus the few fp32 epilogue roundings (2^-19 slack).
+//   A true pair (fp64 distance <= tau, so exact distance <= tau (1 + 1e-9))
+//   therefore has
+//     S <= T = (tau' + U (||x~_i|| + max_J ||y~||))^2
+//              + (DP 2^-23 + 2^-19) (||x~_i||^2 + max_J ||y~||^2)
+//   and the epilogue keeps every (i, j) with dot - ||y~_j||^2/2 >=
+//   (||x~_i||^2 - T)/2, rounded conservatively.  Everything kept is then
+//   decided by the exact fp64 chain, so the output is the reference's set.
+//   Rows with non-finite values never match (NaN/inf compare false in the
+//   reference) and are excluded; rows too large for fp32 squares are
+//   zeroed in the screen copy and forced to candidate status.
+
+#include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pdb_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace pdb {
+
+namespace {
+
+constexpr int BM = 128;  // L rows per tile (TMEM lanes)
+constexpr int BN = 256;  // R rows per tile (UMMA N)
+constexpr int BK = 32;   // fp32 per 128-byte swizzle row
+constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
+constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
+constexpr int kThreads = 192;         // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr uint32_t kTmemCols = 512;   // two 256-column fp32 accumulators
+constexpr uint32_t kIdesc = ptx::idesc_tf32(BM, BN);
+
+constexpr float kFlagNonFinite = -1.0f;
+constexpr float kFlagBig = -2.0f;
+constexpr float kBigLimit = 1.152921504606846976e18f;  // 2^60
+
+constexpr double kU = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
+
+struct ScreenParams {
+    int64_t nL, nR;
+    int32_t self_join;
+    int32_t shard_index, shard_count;
+    int32_t ch;         // column tiles per work unit
+    int32_t nt;         // column tiles of R
+    int32_t n_chunks;
+    int64_t n_units;
+    const int64_t* chunk_off;  // [n_chunks + 1]
+    const float* hnL;   // ||x~_i||^2
+    const float* snL;   // ||x~_i|| (rounded up) or a flag
+    const float* gR;    // ||y~_j||^2 / 2, +inf / -inf flags, padded to nt*256
+    const float* tmaxS; // per R tile
+    const float* tmaxN;
+    double tau_p;       // tau (1 + 1e-9)
+    double gam;         // DP 2^-23 + 2^-19
+    int2* cand;
+    unsigned long long cap;
+    unsigned long long* counter;
+    unsigned long long* tiles;
+};
+
+struct Unit {
+    int32_t rb, j0, j1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
+    int lo = 0, hi = p.n_chunks;  // chunk_off[lo] <= u < chunk_off[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(p.chunk_off + mid) <= u) lo = mid;
+        else hi = mid;
+    }
+    const int64_t k = u - __ldg(p.chunk_off + lo);
+    Unit r;
+    r.rb = static_cast<int32_t>(p.shard_index + p.shard_count * k);
+    r.j0 = lo * p.ch;
+    r.j1 = min(r.j0 + p.ch, p.nt);
+    if (p.self_join) r.j0 = max(r.j0, r.rb >> 1);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// K2: the tensor-core screen.  A_RES: the CTA's 128-row block of L stays
+// resident in shared memory for a whole unit (DP <= 128); otherwise A is
+// streamed with B through the stage ring.
+template <int DP, bool A_RES, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         const ScreenParams p) {
+    constexpr int NKB = DP / BK;
+    constexpr int kStageBytes = A_RES ? kBBytes : (kABytes + kBBytes);
+    constexpr int kAResBytes = A_RES ? NKB * kABytes : 0;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = ptx::smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+    uint8_t* smA = smem;                       // resident A (A_RES)
+    uint8_t* smS = smem + kAResBytes;          // stage ring
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smS + STAGES * kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* a_full = bars + 2 * STAGES;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* t_full = a_full + 2;   // [2]
+    uint64_t* t_empty = a_full + 4;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(a_full, 1);
+        ptx::mbar_init(a_empty, 1);
+        for (int a = 0; a < 2; a++) {
+            ptx::mbar_init(&t_full[a], 1);
+            ptx::mbar_init(&t_empty[a], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0, a_phase = 0;
+            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                if (A_RES) {
+                    ptx::mbar_wait(a_empty, a_phase ^ 1);
+                    a_phase ^= 1;
+                    ptx::mbar_arrive_expect_tx(a_full, NKB * kABytes);
+                    for (int kb = 0; kb < NKB; kb++)
+                        ptx::tma_load_2d(smA + kb * kABytes, &tmA, a_full, kb * BK, w.rb * BM);
+                }
+                for (int J = w.j0; J < w.j1; J++) {
+                    for (int kb = 0; kb < NKB; kb++) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smS + stage * kStageBytes;
+                        ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+                        if (!A_RES) {
+                            ptx::tma_load_2d(st, &tmA, &full[stage], kb * BK, w.rb * BM);
+                            st += kABytes;
+                        }
+                        ptx::tma_load_2d(st, &tmB, &full[stage], kb * BK, J * BN);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (one thread) =====================
+        if (lane == 0) {
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0, a_phase = 0;
+            unsigned long long ntiles = 0;
+            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                if (A_RES) {
+                    ptx::mbar_wait(a_full, a_phase);
+                    a_phase ^= 1;
+                    ptx::tc_fence_after();
+                }
+                for (int J = w.j0; J < w.j1; J++) {
+                    ptx::mbar_wait(&t_empty[acc], acc_phase ^ 1);
+                    ptx::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                    for (int kb = 0; kb < NKB; kb++) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::tc_fence_after();
+                        const uint8_t* st = smS + stage * kStageBytes;
+                        const uint32_t a_addr =
+                            ptx::smem_u32(A_RES ? smA + kb * kABytes : st);
+                        const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; kk++)
+                            ptx::mma_tf32(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
+                                          ptx::sdesc_k_sw128(b_addr + kk * 32), kIdesc,
+                                          (kb | kk) != 0);
+                        ptx::mma_commit(&empty[stage]);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                    ptx::mma_commit(&t_full[acc]);
+                    ntiles++;
+                    if (++acc == 2) {
+                        acc = 0;
+                        acc_phase ^= 1;
+                    }
+                }
+                if (A_RES) ptx::mma_commit(a_empty);
+            }
+            atomicAdd(p.tiles, ntiles);
+        }
+    } else {
+        // ===================== epilogue (warps 2-5) =====================
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;
+        const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            const Unit w = decode_unit(p, u);
+            const int64_t i = static_cast<int64_t>(w.rb) * BM + row;
+            const bool row_ok = i < p.nL;
+            const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
+            const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
+            for (int J = w.j0; J < w.j1; J++) {
+                // Per-(row, tile) threshold h_i, conservative in every rounding.
+                float h;
+                if (sn == kFlagNonFinite) {
+                    h = __int_as_float(0x7f800000);  // +inf: never a candidate
+                } else if (sn == kFlagBig) {
+                    h = -__int_as_float(0x7f800000);  // always a candidate
+                } else {
+                    const double r = p.tau_p + kU * (static_cast<double>(sn) + __ldg(p.tmaxS + J)) + 1e-30;
+                    const double T = r * r + p.gam * (static_cast<double>(hn) + __ldg(p.tmaxN + J));
+                    h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
+                }
+                ptx::mbar_wait(&t_full[acc], acc_phase);
+                ptx::tc_fence_after();
+                const int64_t col0 = static_cast<int64_t>(J) * BN;
+                const uint32_t t_acc = tmem_base + t_lane + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; c++) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(t_acc + c * 32, v);
+                    const float4* gp = reinterpret_cast<const float4*>(p.gR + col0 + c * 32);
+                    float g[32];
+#pragma unroll
+                    for (int k4 = 0; k4 < 8; k4++) {
+                        const float4 t = __ldg(gp + k4);
+                        g[4 * k4 + 0] = t.x;
+                        g[4 * k4 + 1] = t.y;
+                        g[4 * k4 + 2] = t.z;
+                        g[4 * k4 + 3] = t.w;
+                    }
+                    ptx::tmem_ld_wait();
+                    float m = -__int_as_float(0x7f800000);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) m = fmaxf(m, __uint_as_float(v[k]) - g[k]);
+                    const bool hit = row_ok && m >= h;
+                    if (__any_sync(0xffffffffu, hit)) {
+                        uint32_t mask = 0;
+                        if (hit) {
+#pragma unroll
+                            for (int k = 0; k < 32; k++) {
+                                const int64_t j = col0 + c * 32 + k;
+                                const bool ok = (__uint_as_float(v[k]) - g[k] >= h) && j < p.nR &&
+                                                (!p.self_join || j > i);
+                                mask |= static_cast<uint32_t>(ok) << k;
+                            }
+                        }
+                        const uint32_t n = __popc(mask);
+                        uint32_t incl = n;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += t;
+                        }
+                        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                        unsigned long long base = 0;
+                        if (lane == 31 && total) base = atomicAdd(p.counter, total);
+                        base = __shfl_sync(0xffffffffu, base, 31);
+                        unsigned long long pos = base + incl - n;
+                        while (mask) {
+                            const int k = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            if (pos < p.cap)
+                                p.cand[pos] = make_int2(static_cast<int>(i),
+                                                        static_cast<int>(col0 + c * 32 + k));
+                            pos++;
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Preparation kernels.
+constexpr int kMeanRows = 16384;
+constexpr int kMeanSplits = 64;
+
+__global__ void k_col_partial(const float* __restrict__ X, int64_t n, int d,
+                              double* __restrict__ part) {
+    const int col = blockIdx.x * 32 + threadIdx.x;
+    const int split = blockIdx.y * blockDim.y + threadIdx.y;  // 0..kMeanSplits-1
+    if (col >= d) return;
+    double s = 0.0;
+    for (int64_t r = split; r < n; r += kMeanSplits) {
+        const float v = X[r * d + col];
+        if (isfinite(v)) s += static_cast<double>(v);
+    }
+    part[static_cast<int64_t>(split) * d + col] = s;
+}
+
+__global__ void k_col_final(const double* __restrict__ part, int64_t n, int d, int DP,
+                            float* __restrict__ mu) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= DP) return;
+    if (col >= d || n == 0) {
+        mu[col] = 0.0f;
+        return;
+    }
+    double s = 0.0;
+    for (int k = 0; k < kMeanSplits; k++) s += part[static_cast<int64_t>(k) * d + col];
+    const float m = static_cast<float>(s / static_cast<double>(n));
+    mu[col] = isfinite(m) ? m : 0.0f;
+}
+
+// One warp per row: centred, tf32-rounded, zero-padded copy + norms + class.
+__global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
+                       const float* __restrict__ mu, float* __restrict__ Xp,
+                       float* __restrict__ hn, float* __restrict__ sn) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float* x = X + row * d;
+    float* xp = Xp + row * DP;
+    double acc = 0.0;
+    bool finite = true, big = false;
+    for (int k = lane; k < DP; k += 32) {
+        float t = 0.0f;
+        if (k < d) {
+            const float a = x[k];
+            if (!isfinite(a)) finite = false;
+            t = ptx::tf32_rna(__fsub_rn(a, mu[k]));
+            if (!(fabsf(t) <= kBigLimit)) big = true;
+        }
+        xp[k] = t;
+        acc += static_cast<double>(t) * static_cast<double>(t);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    finite = __all_sync(0xffffffffu, finite);
+    big = __any_sync(0xffffffffu, big);
+    if (!finite || big) {
+        for (int k = lane; k < DP; k += 32) xp[k] = 0.0f;
+    }
+    if (lane == 0) {
+        if (!finite) {
+            hn[row] = 0.0f;
+            sn[row] = kFlagNonFinite;
+        } else if (big) {
+            hn[row] = 0.0f;
+            sn[row] = kFlagBig;
+        } else {
+            hn[row] = static_cast<float>(acc);
+            sn[row] = __double2float_ru(sqrt(acc));
+        }
+    }
+}
+
+// Per 256-row tile of R: max norms over regular rows, and g_j = ||y~||^2/2
+// with +inf for non-finite rows and padding, -inf for forced rows.
+__global__ void k_tile_stats(const float* __restrict__ hn, const float* __restrict__ sn,
+                             int64_t n, float* __restrict__ g, float* __restrict__ tmaxS,
+                             float* __restrict__ tmaxN) {
+    const int J = blockIdx.x;
+    const int64_t j = static_cast<int64_t>(J) * BN + threadIdx.x;  // blockDim.x == BN
+    float s = 0.0f, nn = 0.0f, gv = __int_as_float(0x7f800000);
+    if (j < n) {
+        const float f = sn[j];
+        if (f == kFlagBig) {
+            gv = -__int_as_float(0x7f800000);
+        } else if (f != kFlagNonFinite) {
+            s = f;
+            nn = hn[j];
+            gv = hn[j] * 0.5f;
+        }
+    }
+    g[j] = gv;
+    __shared__ float rs[BN / 32], rn[BN / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
+        nn = fmaxf(nn, __shfl_xor_sync(0xffffffffu, nn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        rs[threadIdx.x >> 5] = s;
+        rn[threadIdx.x >> 5] = nn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < BN / 32; k++) {
+            s = fmaxf(s, rs[k]);
+            nn = fmaxf(nn, rn[k]);
+        }
+        s = fmaxf(s, rs[0]);
+        nn = fmaxf(nn, rn[0]);
+        tmaxS[J] = s;
+        tmaxN[J] = nn;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: exact re-check.  The fp64 chain is written with explicit _rn
+// intrinsics so it can never be contracted into FMAs: diff = a - b,
+// acc = acc + diff * diff, sequential in k, then sqrt -- src/index.cpp:69-76.
+__device__ __forceinline__ double exact_dist(const float* __restrict__ a,
+                                             const float* __restrict__ b, int d, bool vec4) {
+    double acc = 0.0;
+    if (vec4) {
+        const float4* a4 = reinterpret_cast<const float4*>(a);
+        const float4* b4 = reinterpret_cast<const float4*>(b);
+        for (int k = 0; k < d / 4; k++) {
+            const float4 x = __ldg(a4 + k), y = __ldg(b4 + k);
+            double t;
+            t = __dsub_rn(static_cast<double>(x.x), static_cast<double>(y.x));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(static_cast<double>(x.y), static_cast<double>(y.y));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(static_cast<double>(x.z), static_cast<double>(y.z));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(static_cast<double>(x.w), static_cast<double>(y.w));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+    } else {
+        for (int k = 0; k < d; k++) {
+            const double t = __dsub_rn(static_cast<double>(__ldg(a + k)),
+                                       static_cast<double>(__ldg(b + k)));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+    }
+    return __dsqrt_rn(acc);
+}
+
+__global__ void __launch_bounds__(256)
+k_recheck(const int2* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
+          unsigned long long cap, const float* __restrict__ L, const float* __restrict__ R,
+          int d, double tau, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
+          float* __restrict__ out_d, unsigned long long out_cap,
+          unsigned long long* __restrict__ out_count) {
+    const unsigned long long n = min(*n_cand, cap);
+    const int lane = threadIdx.x & 31;
+    const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                                   (threadIdx.x & ~31u);
+         base < n; base += stride) {
+        const unsigned long long idx = base + lane;
+        bool ok = false;
+        int2 c = make_int2(0, 0);
+        double dist = 0.0;
+        if (idx < n) {
+            c = cand[idx];
+            dist = exact_dist(L + static_cast<int64_t>(c.x) * d, R + static_cast<int64_t>(c.y) * d,
+                              d, vec4);
+            ok = dist <= tau;
+        }
+        const uint32_t ball = __ballot_sync(0xffffffffu, ok);
+        if (!ball) continue;
+        unsigned long long w = 0;
+        if (lane == 0) w = atomicAdd(out_count, static_cast<unsigned long long>(__popc(ball)));
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (ok) {
+            const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
+            if (pos < out_cap) {
+                out_l[pos] = c.x;
+                out_r[pos] = c.y;
+                out_d[pos] = static_cast<float>(dist);
+            }
+        }
+    }
+}
+
+__global__ void k_pack_keys(const int32_t* __restrict__ l, const int32_t* __restrict__ r,
+                            int64_t n, unsigned long long* __restrict__ keys) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        keys[k] = (static_cast<unsigned long long>(static_cast<uint32_t>(l[k])) << 32) |
+                  static_cast<uint32_t>(r[k]);
+}
+
+__global__ void k_unpack_keys(const unsigned long long* __restrict__ keys, int64_t n,
+                              int32_t* __restrict__ l, int32_t* __restrict__ r) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        l[k] = static_cast<int32_t>(keys[k] >> 32);
+        r[k] = static_cast<int32_t>(keys[k] & 0xffffffffu);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side.
+CUtensorMap make_tmap(const DeviceCtx& ctx, const float* base, int64_t rows, int DP,
+                      int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(DP), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(DP) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PDB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+struct Prepped {
+    float* Xp;
+    float* hn;
+    float* sn;
+};
+
+template <int DP, bool A_RES, int STAGES>
+void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
+                   const ScreenParams& p, cudaStream_t s) {
+    constexpr int NKB = DP / BK;
+    constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
+    constexpr size_t smem = 1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256;
+    static_assert(smem <= 232448, "shared memory budget");
+    auto k = k_screen<DP, A_RES, STAGES>;
+    PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
+    k<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(tA, tB, p);
+    PDB_CUDA(cudaGetLastError());
+}
+
+void dispatch_screen(int DP, const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
+                     const ScreenParams& p, cudaStream_t s) {
+    switch (DP) {
+        case 32: launch_screen<32, true, 6>(ctx, tA, tB, p, s); break;
+        case 64: launch_screen<64, true, 5>(ctx, tA, tB, p, s); break;
+        case 96: launch_screen<96, true, 4>(ctx, tA, tB, p, s); break;
+        case 128: launch_screen<128, true, 4>(ctx, tA, tB, p, s); break;
+        case 256: launch_screen<256, false, 4>(ctx, tA, tB, p, s); break;
+        case 512: launch_screen<512, false, 4>(ctx, tA, tB, p, s); break;
+        case 1024: launch_screen<1024, false, 4>(ctx, tA, tB, p, s); break;
+        case 2048: launch_screen<2048, false, 4>(ctx, tA, tB, p, s); break;
+        default: fail(PDB_ERR_CONFIG, "similarity join: unsupported padded dimension");
+    }
+}
+
+// Resident-A variants for d <= 128; beyond that A streams with B and the
+// padded width is the next power of two (zero columns change no dot).
+int padded_dim(int d) {
+    if (d <= 32) return 32;
+    if (d <= 64) return 64;
+    if (d <= 96) return 96;
+    if (d <= 128) return 128;
+    int DP = 256;
+    while (DP < d) DP *= 2;
+    return DP;
+}
+
+}  // namespace
+
+void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR, int32_t d,
+                      double tau, const pdb_join_opts& o, pdb_dev_pairs* out,
+                      pdb_join_stats* stats) {
+    const DeviceCtx& ctx = device_ctx();
+    cudaStream_t s = static_cast<cudaStream_t>(o.stream);
+    const bool self = (o.flags & PDB_JOIN_SELF) != 0;
+    if (self) {
+        d_R = d_L;
+        nR = nL;
+    }
+    const int P = o.shard_count > 1 ? o.shard_count : 1;
+    const int shard = o.shard_count > 1 ? o.shard_index : 0;
+    if (stats) *stats = pdb_join_stats{};
+    out->count = 0;
+    if (nL == 0 || nR == 0) return;
+
+    const int DP = padded_dim(d);
+    if (DP > 2048) fail(PDB_ERR_CONFIG, "similarity join: d > 2048 is not supported by this build");
+
+    // ---- preparation ----------------------------------------------------
+    DevBuf<float> mu(DP, s);
+    {
+        const int64_t nm = std::min<int64_t>(nL, kMeanRows);
+        DevBuf<double> part(static_cast<size_t>(kMeanSplits) * d, s);
+        dim3 blk(32, 8), grd(static_cast<unsigned>(ceil_div(d, 32)), kMeanSplits / 8);
+        k_col_partial<<<grd, blk, 0, s>>>(d_L, nm, d, part.p);
+        k_col_final<<<static_cast<unsigned>(ceil_div(DP, 128)), 128, 0, s>>>(part.p, nm, d, DP, mu.p);
+        PDB_CUDA(cudaGetLastError());
+    }
+    auto prep = [&](const float* X, int64_t n, DevBuf<float>& Xp, DevBuf<float>& hn,
+                    DevBuf<float>& sn) {
+        k_prep<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p,
+                                                                           hn.p, sn.p);
+        PDB_CUDA(cudaGetLastError());
+    };
+    DevBuf<float> XpL(static_cast<size_t>(nL) * DP, s), hnL(nL, s), snL(nL, s);
+    prep(d_L, nL, XpL, hnL, snL);
+    DevBuf<float> XpR_own, hnR_own, snR_own;
+    const float *XpR = XpL.p, *hnR = hnL.p, *snR = snL.p;
+    if (!self) {
+        XpR_own.reset(static_cast<size_t>(nR) * DP, s);
+        hnR_own.reset(nR, s);
+        snR_own.reset(nR, s);
+        prep(d_R, nR, XpR_own, hnR_own, snR_own);
+        XpR = XpR_own.p;
+        hnR = hnR_own.p;
+        snR = snR_own.p;
+    }
+    const int nt = static_cast<int>(ceil_div(nR, BN));
+    DevBuf<float> gR(static_cast<size_t>(nt) * BN, s), tmaxS(nt, s), tmaxN(nt, s);
+    k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR.p, tmaxS.p, tmaxN.p);
+    PDB_CUDA(cudaGetLastError());
+
+    // ---- work units: (column chunk c, row block rb), chunk-major ----------
+    const int64_t n_rb = ceil_div(nL, BM);
+    double total_tiles = 0;
+    for (int64_t rb = shard; rb < n_rb; rb += P)
+        total_tiles += self ? static_cast<double>(nt - (rb >> 1)) : static_cast<double>(nt);
+    int ch = static_cast<int>(std::clamp<double>(total_tiles / (8.0 * ctx.sm_count), 1.0, 64.0));
+    const int n_chunks = static_cast<int>(ceil_div(nt, ch));
+    std::vector<int64_t> off(static_cast<size_t>(n_chunks) + 1, 0);
+    for (int c = 0; c < n_chunks; c++) {
+        int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
+        if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * ch);
+        const int64_t cnt = lim > shard ? ceil_div(lim - shard, P) : 0;
+        off[c + 1] = off[c] + cnt;
+    }
+    const int64_t n_units = off[n_chunks];
+    DevBuf<int64_t> d_off(off.size(), s);
+    PDB_CUDA(cudaMemcpyAsync(d_off.p, off.data(), off.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+
+    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM);
+    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN);
+
+    DevBuf<unsigned long long> counters(4, s);  // [cand, tiles, pairs, spare]
+    unsigned long long cap = static_cast<unsigned long long>(
+        std::max<int64_t>(1 << 20, 4 * (nL + nR)));
+    ScreenParams p{};
+    p.nL = nL;
+    p.nR = nR;
+    p.self_join = self;
+    p.shard_index = shard;
+    p.shard_count = P;
+    p.ch = ch;
+    p.nt = nt;
+    p.n_chunks = n_chunks;
+    p.n_units = n_units;
+    p.chunk_off = d_off.p;
+    p.hnL = hnL.p;
+    p.snL = snL.p;
+    p.gR = gR.p;
+    p.tmaxS = tmaxS.p;
+    p.tmaxN = tmaxN.p;
+    p.tau_p = tau * (1.0 + 1e-9);
+    p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
+
+    unsigned long long h_cnt[4] = {0, 0, 0, 0};
+    DevBuf<int2> cand;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        cand.reset(cap, s);
+        p.cand = cand.p;
+        p.cap = cap;
+        p.counter = counters.p;
+        p.tiles = counters.p + 1;
+        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
+        if (n_units > 0) dispatch_screen(DP, ctx, tA, tB, p, s);
+        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+        if (h_cnt[0] <= cap) break;
+        cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
+    }
+    const unsigned long long n_cand = h_cnt[0];
+
+    // ---- exact re-check + compaction ----------------------------------------
+    if (static_cast<unsigned long long>(out->capacity) < n_cand || !out->left) {
+        if (out->left) pdb_dev_pairs_free(out);
+        const int64_t c = static_cast<int64_t>(std::max<unsigned long long>(n_cand, 1));
+        out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
+        out->capacity = c;
+    }
+    unsigned long long n_pairs = 0;
+    if (n_cand > 0) {
+        const int grid = static_cast<int>(std::min<unsigned long long>(
+            ceil_div(static_cast<int64_t>(n_cand), 256), static_cast<unsigned long long>(ctx.sm_count) * 8));
+        k_recheck<<<grid, 256, 0, s>>>(cand.p, counters.p, cap, d_L, d_R, d, tau, out->left,
+                                       out->right, out->dist,
+                                       static_cast<unsigned long long>(out->capacity),
+                                       counters.p + 2);
+        PDB_CUDA(cudaGetLastError());
+        PDB_CUDA(cudaMemcpyAsync(&n_pairs, counters.p + 2, sizeof(n_pairs),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    }
+    out->count = static_cast<int64_t>(n_pairs);
+
+    if ((o.flags & PDB_JOIN_SORTED) && n_pairs > 1) {
+        const int64_t n = static_cast<int64_t>(n_pairs);
+        DevBuf<unsigned long long> k_in(n, s), k_out(n, s);
+        DevBuf<float> v_out(n, s);
+        k_pack_keys<<<592, 256, 0, s>>>(out->left, out->right, n, k_in.p);
+        size_t tmp_bytes = 0;
+        PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in.p, k_out.p, out->dist,
+                                                 v_out.p, n, 0, 64, s));
+        DevBuf<uint8_t> tmp(tmp_bytes, s);
+        PDB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k_in.p, k_out.p, out->dist,
+                                                 v_out.p, n, 0, 64, s));
+        k_unpack_keys<<<592, 256, 0, s>>>(k_out.p, n, out->left, out->right);
+        PDB_CUDA(cudaMemcpyAsync(out->dist, v_out.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        PDB_CUDA(cudaGetLastError());
+    }
+    if (stats) {
+        stats->candidates = static_cast<int64_t>(n_cand);
+        stats->pairs = static_cast<int64_t>(n_pairs);
+        stats->tiles = static_cast<int64_t>(h_cnt[1]);
+        stats->candidate_capacity = static_cast<int64_t>(cap);
+    }
+}
+
+}  // namespace pdb

@@ -1,0 +1,91 @@
+// pdb_internal.cuh -- shared plumbing of libpdb_cuda.so: status/error
+// propagation, the per-device context, and small launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "pdb_cuda.h"
+
+#define PDB_HIDDEN __attribute__((visibility("hidden")))
+
+namespace pdb {
+
+// Thread-local error state behind pdb_last_error().
+PDB_HIDDEN void set_error(const std::string& msg);
+PDB_HIDDEN void clear_error();
+
+// A failure carried from deep inside a launcher to the C-ABI boundary,
+// which converts it into a status code (nothing throws across extern "C").
+struct Failure {
+    int status;
+    std::string msg;
+};
+
+[[noreturn]] PDB_HIDDEN void fail(int status, const std::string& msg);
+PDB_HIDDEN void check_cuda(cudaError_t e, const char* what);
+
+#define PDB_CUDA(call) ::pdb::check_cuda((call), #call)
+
+struct DeviceCtx {
+    int device = -1;
+    int sm_count = 0;
+    int cc_major = 0, cc_minor = 0;
+    size_t smem_optin = 0;
+    void* encode_tiled = nullptr;  // cuTensorMapEncodeTiled from the driver
+};
+
+// Context of the calling thread's current device; fails with
+// PDB_ERR_NO_DEVICE when there is no sm_100 GPU (there is no CPU path).
+PDB_HIDDEN const DeviceCtx& device_ctx();
+
+// Stream-ordered scratch allocation from the device's default memory pool
+// (release threshold raised once, so repeated calls reuse memory).
+PDB_HIDDEN void* dev_alloc(size_t bytes, cudaStream_t s);
+PDB_HIDDEN void dev_free(void* p, cudaStream_t s);
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t n, cudaStream_t st) : s(st) {
+        if (n) p = static_cast<T*>(dev_alloc(n * sizeof(T), st));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) dev_free(p, s);
+        p = nullptr;
+    }
+    void reset(size_t n, cudaStream_t st) {
+        reset();
+        s = st;
+        if (n) p = static_cast<T*>(dev_alloc(n * sizeof(T), st));
+    }
+    T* release() {
+        T* q = p;
+        p = nullptr;
+        return q;
+    }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- K1 launchers (histogram.cu) -----------------------------------------
+PDB_HIDDEN int hist_dim(int32_t bins, int32_t mode);
+PDB_HIDDEN void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H,
+                                       int32_t W, int32_t th, int32_t tw, int32_t bins,
+                                       int32_t mode, float* d_out, cudaStream_t s);
+PDB_HIDDEN void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t w,
+                                int32_t bins, int32_t mode, float* d_out, cudaStream_t s);
+
+// ---- K2/K3 (join.cu) -------------------------------------------------------
+PDB_HIDDEN void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
+                                 int32_t d, double tau, const pdb_join_opts& o,
+                                 pdb_dev_pairs* out, pdb_join_stats* stats);
+
+}  // namespace pdb

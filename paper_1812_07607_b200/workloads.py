@@ -1,0 +1,105 @@
+"""Seeded synthetic workloads for BASELINE.json's configs (libpdb_gen.so).
+
+The paper's datasets are not available; like the
+reference's own bench harness every workload is a seeded
+synthetic stand-in with the configured shapes and value distributions.
+Seeds: config 1 uses 0 (as BASELINE.json states); configs 2-5 are unseeded
+there and use 2, 3, 4, 5.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi as capi
+
+
+def _threads() -> int:
+    return max(1, min(os.cpu_count() or 1, 64))
+
+
+def clusters(n: int, d: int, centres: int, sigma: float, l1_normalise: bool, seed: int,
+             row_seed: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+    x = out if out is not None else np.empty((n, d), dtype=np.float32)
+    rs = seed if row_seed is None else row_seed
+    rc = capi.gen().pdb_gen_clusters(capi.ptr(x), n, d, centres, sigma, int(l1_normalise), seed,
+                                     rs, _threads())
+    assert rc == 0
+    return x
+
+
+def uniform(n: int, d: int, seed: int) -> np.ndarray:
+    x = np.empty((n, d), dtype=np.float32)
+    capi.gen().pdb_gen_uniform(capi.ptr(x), n, d, seed, _threads())
+    return x
+
+
+def plant(L: np.ndarray, R: np.ndarray, frac: float, sigma: float, seed: int):
+    """Config 3 planting; returns (left_idx, right_idx) of the planted pairs."""
+    cap = int(L.shape[0] * frac * 2 + 1024)
+    pl = np.empty(cap, dtype=np.int32)
+    pr = np.empty(cap, dtype=np.int32)
+    n = capi.gen().pdb_gen_plant(capi.ptr(L), L.shape[0], capi.ptr(R), R.shape[0], L.shape[1],
+                                 frac, sigma, seed, capi.ptr(pl), capi.ptr(pr), cap)
+    assert n <= cap
+    return pl[:n].copy(), pr[:n].copy()
+
+
+def simplex(n: int, d: int, centres: int, clustered: float, sigma: float, seed: int) -> np.ndarray:
+    x = np.empty((n, d), dtype=np.float32)
+    capi.gen().pdb_gen_simplex(capi.ptr(x), n, d, centres, clustered, sigma, seed, _threads())
+    return x
+
+
+def frames(F: int, H: int = 480, W: int = 640, *, block: int = 40, noise: int = 8,
+           copy_noise: int = 4, period: int = 20, seed: int = 2, out=None):
+    """Config 2 frames [F, H, W, 3] uint8 and the source frame of each
+    near-copy (-1 for originals).  ``out`` may be any writable uint8 buffer
+    (e.g. pinned host memory) of F*H*W*3 bytes exposing a numpy array."""
+    x = out if out is not None else np.empty((F, H, W, 3), dtype=np.uint8)
+    src = np.empty(F, dtype=np.int64)
+    rc = capi.gen().pdb_gen_frames(capi.ptr(x), F, H, W, block, noise, copy_noise, period, seed,
+                                   capi.ptr(src), _threads())
+    assert rc == 0
+    return x, src
+
+
+@dataclass(frozen=True)
+class JoinConfig:
+    name: str
+    n: int
+    d: int
+    tau: float
+    self_join: bool
+
+
+CONFIG1 = JoinConfig("config1_selfjoin_20k_d64", 20_000, 64, 0.05, True)
+CONFIG3 = JoinConfig("config3_cross_1M_d128", 1_048_576, 128, 0.02, False)
+CONFIG5 = JoinConfig("config5_selfjoin_4M_d64", 4_194_304, 64, 0.01, True)
+
+
+def config1(n: int = 20_000, seed: int = 0) -> np.ndarray:
+    """200 Gaussian clusters (centres U[0,1]^64, sigma 0.02), L1-normalised."""
+    return clusters(n, 64, 200, 0.02, True, seed)
+
+
+def config3(n: int = 1_048_576, seed: int = 3, centres: int = 10_000):
+    """L, R: 10,000-cluster mixture (sigma 0.01, unit cube), d=128, with 0.5%
+    of L rows planted as R rows + 1e-3 N(0,1)."""
+    R = clusters(n, 128, centres, 0.01, False, seed, row_seed=seed * 1000 + 1)
+    L = clusters(n, 128, centres, 0.01, False, seed, row_seed=seed * 1000 + 2)
+    pl, pr = plant(L, R, 0.005, 1e-3, seed)
+    return L, R, pl, pr
+
+
+def config5(n: int = 4_194_304, seed: int = 5) -> np.ndarray:
+    """64-d simplex points: 20% in 50 clusters of sigma 1e-3, 80% Dirichlet(1)."""
+    return simplex(n, 64, 50, 0.2, 1e-3, seed)
+
+
+CONFIG2 = dict(frames=1000, H=480, W=640, tile_h=60, tile_w=80, bins=4, mode="joint",
+               tau=0.05, seed=2)

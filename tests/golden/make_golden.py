@@ -1,0 +1,131 @@
+"""Mints tests/golden/*.npz from the REFERENCE ITSELF (oracle/_ref/libpdb_ref.so,
+the unmodified proj/ sources compiled by oracle/Makefile).
+
+Run here (where /root/reference exists):  python tests/golden/make_golden.py
+The fixtures pin both the C restatement (tests/test_oracle.py, CPU) and the
+CUDA path (tests/test_*_gpu.py) to the reference's own outputs.  Inputs are
+stored alongside outputs, so nothing needs the reference at test time.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle  # noqa: E402
+from paper_1812_07607_b200 import workloads  # noqa: E402
+
+
+def textured_frame(w, h, f):
+    """tests/oracles.hpp:168-177 pixel formula."""
+    y, x, c = np.meshgrid(np.arange(h), np.arange(w), np.arange(3), indexing="ij")
+    return ((x * 7 + y * 13 + c * 29 + f * 31) & 0xFF).astype(np.uint8)
+
+
+def solid_frame(w, h, rgb):
+    a = np.empty((h, w, 3), np.uint8)
+    a[...] = np.array(rgb, np.uint8)
+    return a
+
+
+def hist_fixtures():
+    out = {}
+    # test_etl.cpp:226-256 textured 16x12 whole-frame patch, B=8
+    fr = textured_frame(16, 12, 0)[None]
+    out["textured_b8"] = (fr, 12, 16, 8)
+    # test_etl.cpp: solid (255,0,129), B=8 -> bins 7 / 0 / 4
+    out["solid_b8"] = (solid_frame(8, 8, (255, 0, 129))[None], 8, 8, 8)
+    # SPEC.md:372 all-128 patch, B=8 -> 1.0 at 4, 12, 20
+    out["gray128_b8"] = (solid_frame(8, 8, (128, 128, 128))[None], 8, 8, 8)
+    # test_etl.cpp:278-300 tiles 8x6 over 4 textured 16x12 frames, B=4
+    out["tiles_textured_b4"] = (np.stack([textured_frame(16, 12, f) for f in range(4)]), 6, 8, 4)
+    # partial edges dropped (test_etl.cpp:91-115): 14x8 frame, tiles 4x3
+    out["tiles_partial_b4"] = (textured_frame(14, 8, 0)[None], 3, 4, 4)
+    rng = np.random.default_rng(1234)
+    frames = rng.integers(0, 256, size=(3, 48, 64, 3), dtype=np.uint8)
+    for b in (2, 3, 4, 5, 8, 16, 21, 64, 300):
+        out[f"random_b{b}"] = (frames, 12, 16, b)
+    # config-2 shaped frames at full resolution (2 frames) with the 60x80 grid
+    cf, _ = workloads.frames(2, 480, 640, seed=2)
+    out["config2_b4"] = (cf, 60, 80, 4)
+    out["config2_b8"] = (cf, 60, 80, 8)
+    res = {}
+    for name, (fr, th, tw, b) in out.items():
+        if name.startswith("config2"):
+            # regenerated at test time by workloads.frames(2, seed=2); pin the bytes
+            res[f"{name}__sha256"] = np.frombuffer(hashlib.sha256(fr.tobytes()).digest(), np.uint8)
+        else:
+            res[f"{name}__frames"] = fr
+        res[f"{name}__params"] = np.array([th, tw, b], np.int32)
+        res[f"{name}__want"] = oracle.ref_featurize_tiles(fr, th, tw, b)
+    # float-patch apply_transformer with values >= 256 (clamped to the top bin)
+    px = rng.integers(0, 300, size=(5, 7, 9, 3)).astype(np.float32)
+    res["f32_clamp_b8__px"] = px
+    res["f32_clamp_b8__want"] = oracle.ref_color_histogram(px, 8)
+    np.savez_compressed(os.path.join(HERE, "hist_golden.npz"), **res)
+    print("hist fixtures:", len(out) + 1)
+
+
+def join_case(res, name, L, R, tau, sides=(0, 1, 2), store_inputs=True):
+    if store_inputs:
+        res[f"{name}__L"] = L
+        res[f"{name}__R"] = R
+    else:
+        h = hashlib.sha256(L.tobytes() + R.tobytes()).digest()
+        res[f"{name}__sha256"] = np.frombuffer(h, np.uint8)
+    res[f"{name}__tau"] = np.array([tau])
+    for side in sides:
+        li, ri, probes = oracle.ref_sim_join(L, R, tau, side)
+        res[f"{name}__side{side}_left"] = li
+        res[f"{name}__side{side}_right"] = ri
+        res[f"{name}__side{side}_probes"] = np.array([probes], np.int64)
+    li = res[f"{name}__side{sides[0]}_left"]
+    ri = res[f"{name}__side{sides[0]}_right"]
+    res[f"{name}__dist"] = np.array(
+        [oracle.ref_euclidean(L[a], R[b]) for a, b in zip(li, ri)], np.float64)
+
+
+def join_fixtures():
+    res = {}
+    rng = np.random.default_rng(77)
+    # test_query.cpp:268-300 shape: 60 x 40, d=6, U[0,1), tau=0.45
+    join_case(res, "random_d6", rng.random((60, 6), dtype=np.float32),
+              rng.random((40, 6), dtype=np.float32), 0.45)
+    # acceptance.cpp:140-198 shape (scaled): clustered 24-d, sigma 0.005, tau 0.1
+    allp = workloads.clusters(1200, 24, 60, 0.005, False, 4242)
+    join_case(res, "clustered_d24", allp[:600].copy(), allp[600:].copy(), 0.1, sides=(0,),
+              store_inputs=False)
+    # config-1 shaped self-join (3,000 rows), reference semantics: ordered
+    # pairs incl. (i,i) and both orientations
+    x = workloads.config1(3000, seed=0)
+    join_case(res, "config1_3k", x, x, 0.05, sides=(2,), store_inputs=False)
+    # uniform 128-d (config-3 dimensionality), sparse matches
+    u = workloads.uniform(700, 128, 9)
+    join_case(res, "uniform_d128", u, u[::-1].copy(), 1.5, sides=(0,), store_inputs=False)
+    # exact-radius boundary: test_index.cpp:330-342 and test_query.cpp:128-151
+    pts = np.array([[1, 1]] * 5 + [[2, 1]], np.float32)
+    join_case(res, "radius_exact", pts, np.array([[1, 1]], np.float32), 1.0)
+    join_case(res, "radius_below", pts, np.array([[1, 1]], np.float32), 0.999)
+    tri_a = np.array([[0, 0]], np.float32)
+    tri_b = np.array([[3, 4]], np.float32)
+    join_case(res, "triangle_5", tri_a, tri_b, 5.0)
+    join_case(res, "triangle_499", tri_a, tri_b, 4.99)
+    # error behaviour: tau < 0 -> ConfigError(1); mixed dims cannot be
+    # expressed as arrays, DimensionMismatch is checked in the object API.
+    rc = oracle.ref_sim_join(tri_a, tri_b, -0.5, 0)
+    res["error_tau_negative"] = np.array([rc])
+    np.savez_compressed(os.path.join(HERE, "join_golden.npz"), **res)
+    print("join fixtures written")
+
+
+if __name__ == "__main__":
+    assert oracle.ref() is not None, "build oracle/_ref first: make -C oracle ref"
+    hist_fixtures()
+    join_fixtures()
