@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path on BASELINE.json's configs[1] workload (config 2):
+
+    1000 synthetic 480x640 uint8 frames -> 8x8 grid of 60x80 tiles (64,000)
+    -> 4x4x4 joint colour histograms (64-d fp32, K1)
+    -> L2 self-join, eps = 0.05, all (i<j, dist) pairs (K2 screen + K3 re-check)
+
+One step = one pass of that pipeline over the 1000 frames.  ``value`` is
+frames/s with the frames already resident in HBM (device-timed with CUDA
+events, L2 flushed between steps); ``e2e`` is the same metric through the
+public C-ABI call pdb_featurize_join with pinned host frames in and host
+pairs out, copies inside the timed region.  The join alone is reported in
+Gpairs/s (N(N-1)/2 candidate pairs per step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU: each rank featurizes its
+frame shard, the 64,000 features are all-gathered over NCCL (16 MB), and
+each rank joins the 128-row blocks b = rank (mod N) of the features against
+all of them (strong scaling: the 1000-frame workload is fixed).
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref, the unmodified proj/ sources) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(frames=1000, H=480, W=640, tile_h=60, tile_w=80, bins=4, mode="joint", tau=0.05,
+           seed=2)
+METRIC = "similarity-join Gpairs/s + featurization frames/s, 1/2/4/8 B200 vs host-CPU ref"
+WORKLOAD = "config2_featurize_join: 1000x480x640 u8 frames -> 64000 tiles 60x80 -> joint 4x4x4 hist (64-d) -> L2 self-join eps=0.05"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    tf32 = None
+    try:
+        tf32 = json.load(open(os.path.join(ROOT, "profiles", "peaks_tf32.json")))
+    except Exception:
+        pass
+    return p, tf32
+
+
+class ClockSampler:
+    """Polls SM clock and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": int(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own implementation on the host cores.
+
+def reference_sample(feats: np.ndarray, frames_sample: np.ndarray, threads: int,
+                     probe_rows: int):
+    """Times oracle/_ref (the reference compiled from its sources):
+    featurization of `frames_sample` through transform(generate(tiles),
+    color_histogram{B=4}) -- the reference's per-channel operator; it has no
+    joint mode, whose binning cost is the same -- and its sim_join probe
+    (ball tree over all 64,000 features, balltree_within per probe row) on
+    `probe_rows` rows.  Returns extrapolated seconds for the full step."""
+    from oracle import oracle
+    if oracle.ref() is None:
+        raise RuntimeError("oracle/_ref/libpdb_ref.so missing")
+    t0 = time.perf_counter()
+    oracle.ref_featurize_tiles(frames_sample, CFG["tile_h"], CFG["tile_w"], CFG["bins"],
+                               threads=threads)
+    t_feat = (time.perf_counter() - t0) * CFG["frames"] / frames_sample.shape[0]
+    n = feats.shape[0]
+    rows = min(probe_rows, n)
+    # spread the probe sample evenly over the relation (the self-join's work
+    # per probe row does not depend on its position for the ball tree)
+    stride = max(1, n // rows)
+    sub = np.ascontiguousarray(feats[::stride][:rows])
+    m, t_build, t_probe = _probe(sub, feats, threads)
+    t_join = t_build + t_probe * n / rows
+    return t_feat, t_join, {"frames": int(frames_sample.shape[0]), "probe_rows": rows,
+                            "build_s": t_build, "probe_s": t_probe, "matches_in_sample": m}
+
+
+def _probe(sub, feats, threads):
+    from oracle import oracle
+    import ctypes as C
+    R = np.ascontiguousarray(feats, dtype=np.float32)
+    L = np.ascontiguousarray(sub, dtype=np.float32)
+    b, p = C.c_double(), C.c_double()
+    m = oracle.ref().ref_join_probe_timed(L.ctypes.data, L.shape[0], R.ctypes.data, R.shape[0],
+                                          R.shape[1], CFG["tau"], 0, 0, L.shape[0], threads,
+                                          C.byref(b), C.byref(p))
+    return int(m), b.value, p.value
+
+
+def run_reference(args, rank, world):
+    from paper_1812_07607_b200 import workloads
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    frames, _ = workloads.frames(CFG["frames"], CFG["H"], CFG["W"], seed=CFG["seed"])
+    # the features the reference joins are the K1 output definition; compute
+    # them with the restatement's bit-identical CPU code (no GPU in this arm)
+    from oracle import oracle
+    feats = oracle.featurize_tiles(frames, CFG["tile_h"], CFG["tile_w"], CFG["bins"], 1)
+    fs = frames[:max(threads * 2, 16)]
+    probe_rows = _env_int("PDB_REF_PROBE_ROWS", 1024)
+    times = []
+    info = None
+    for k in range(args.warmup + args.steps):
+        t_feat, t_join, info = reference_sample(feats, fs, threads, probe_rows)
+        if k >= args.warmup:
+            times.append(t_feat + t_join)
+    step_s = statistics.mean(times)
+    value = CFG["frames"] / step_s
+    n = feats.shape[0]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8/f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "frames": CFG["frames"], "tiles": n, "d": 64,
+                   "tau": CFG["tau"]},
+        "join_gpairs_per_s": n * (n - 1) / 2 / (
+            info["build_s"] + info["probe_s"] * n / info["probe_rows"]) / 1e9,
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
+                         "sample": f"per step: reference transform(generate(tiles),color_histogram) on "
+                                   f"{info['frames']} frames + build_balltree(64000) and "
+                                   f"balltree_within for {info['probe_rows']} probe rows, "
+                                   f"extrapolated to 1000 frames / 64000 probes"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# Our arm.
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_07607_b200 import _capi as capi
+    from paper_1812_07607_b200 import patchdb, workloads
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = capi.lib()
+    F, H, W, th, tw, B = (CFG[k] for k in ("frames", "H", "W", "tile_h", "tile_w", "bins"))
+    tau = CFG["tau"]
+    mode = capi.PDB_HIST_JOINT
+    D = B ** 3
+    tpf = (H // th) * (W // tw)
+    f0, f1 = F * rank // world, F * (rank + 1) // world
+    nf = f1 - f0
+    n_tiles = F * tpf
+
+    # pinned host frames of this rank's shard (the e2e input) + a device copy
+    hbuf = lib.pdb_host_alloc(nf * H * W * 3)
+    assert hbuf, "pinned allocation failed"
+    host = np.ctypeslib.as_array(C.cast(hbuf, C.POINTER(C.c_uint8)), shape=(nf, H, W, 3))
+    workloads.frames(nf, H, W, seed=CFG["seed"], first=f0, out=host)
+    d_frames = torch.from_numpy(host).to(dev)
+    feats = torch.empty((n_tiles, D), dtype=torch.float32, device=dev)
+    my_feats = feats[f0 * tpf:f1 * tpf] if world == 1 else torch.empty((nf * tpf, D),
+                                                                        dtype=torch.float32,
+                                                                        device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    sptr = C.c_void_p(stream.cuda_stream)
+    pairs = patchdb.DevicePairs()
+    opts = capi.JoinOpts()
+    opts.flags = capi.PDB_JOIN_SELF
+    opts.shard_index, opts.shard_count = rank, world
+    opts.stream = sptr
+
+    def featurize():
+        rc = lib.pdb_featurize_tiles_dev(d_frames.data_ptr(), nf, H, W, th, tw, B, mode,
+                                         my_feats.data_ptr(), sptr)
+        assert rc == 0, capi.last_error()
+
+    def gather():
+        if world > 1:
+            dist.all_gather_into_tensor(feats, my_feats)
+
+    def join():
+        rc = lib.pdb_sim_join_dev(feats.data_ptr(), n_tiles, feats.data_ptr(), n_tiles, D, tau,
+                                  C.byref(opts), C.byref(pairs._p), C.byref(pairs.stats))
+        assert rc == 0, capi.last_error()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    rec = {"step": [], "feat": [], "gather": [], "join": [], "screen": [], "recheck": [],
+           "prep": []}
+    launches = 0
+
+    def step(timed: bool):
+        nonlocal launches
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        featurize()
+        ev[1].record(stream)
+        gather()
+        ev[2].record(stream)
+        join()
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        if timed:
+            rec["step"].append(ev[0].elapsed_time(ev[3]))
+            rec["feat"].append(ev[0].elapsed_time(ev[1]))
+            rec["gather"].append(ev[1].elapsed_time(ev[2]))
+            rec["join"].append(ev[2].elapsed_time(ev[3]))
+            st = pairs.stats
+            rec["screen"].append(st.screen_ms)
+            rec["recheck"].append(st.recheck_ms)
+            rec["prep"].append(st.prep_ms)
+            launches += 1 + st.launches
+
+    for _ in range(args.warmup):
+        step(False)
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        for _ in range(args.steps):
+            step(True)
+
+    def maxred(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_step = maxred(statistics.mean(rec["step"]))
+    ms_feat = maxred(statistics.mean(rec["feat"]))
+    ms_join = maxred(statistics.mean(rec["join"]))
+    ms_screen = maxred(statistics.mean(rec["screen"]))
+    ms_recheck = maxred(statistics.mean(rec["recheck"]))
+    n_pairs_local = pairs.count
+    tot = torch.tensor([n_pairs_local, pairs.stats.candidates], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    n_pairs, n_cand = int(tot[0]), int(tot[1])
+
+    # ---- e2e: host pinned frames -> public API -> host pairs -----------------
+    e2e_times = []
+    h2d = nf * H * W * 3
+    d2h = 0
+    for k in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world == 1:
+            o = capi.JoinOpts()
+            pr = capi.Pairs()
+            rc = lib.pdb_featurize_join(hbuf, nf, H, W, th, tw, B, mode, tau, C.byref(o), None,
+                                        C.byref(pr))
+            assert rc == 0, capi.last_error()
+            npairs = pr.count
+            lib.pdb_pairs_free(C.byref(pr))
+        else:
+            d_frames.copy_(torch.from_numpy(host), non_blocking=True)
+            featurize()
+            gather()
+            join()
+            l_, r_, d_ = pairs.to_torch(dev, copy=False)
+            hl = torch.empty(l_.shape, dtype=torch.int32, pin_memory=True)
+            hr = torch.empty(r_.shape, dtype=torch.int32, pin_memory=True)
+            hd = torch.empty(d_.shape, dtype=torch.float32, pin_memory=True)
+            hl.copy_(l_)
+            hr.copy_(r_)
+            hd.copy_(d_)
+            torch.cuda.synchronize()
+            npairs = pairs.count
+        t1 = time.perf_counter()
+        d2h = npairs * 12
+        if k >= args.warmup:
+            e2e_times.append(t1 - t0)
+    e2e_s = maxred(statistics.mean(e2e_times))
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle
+            threads = os.cpu_count() or 1
+            fh = feats.cpu().numpy()
+            t_feat, t_join, info = reference_sample(fh, host[:max(2 * threads, 16)], threads,
+                                                    _env_int("PDB_REF_PROBE_ROWS", 1024))
+            v = F / (t_feat + t_join)
+            cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
+                   "sample": f"reference (oracle/_ref) featurization of {info['frames']} frames "
+                             f"(per-channel B=4 operator) + build_balltree(64000) and "
+                             f"balltree_within on {info['probe_rows']} probe rows, "
+                             f"{threads} threads, extrapolated to the full step",
+                   "featurize_s_per_1000_frames": t_feat, "join_s": t_join}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        mp, tf32 = peaks()
+        pairs_cand = n_tiles * (n_tiles - 1) / 2
+        hbm = mp.get("hbm_gbs", 6650.0)
+        feat_bytes = F * (H * W * 3 + tpf * D * 4) / world
+        feat_gbs = feat_bytes / (ms_feat * 1e-3) / 1e9
+        flops = pairs_cand * 2 * D / world
+        screen_tflops = flops / (ms_screen * 1e-3) / 1e12
+        if tf32 and tf32.get("tf32_tflops"):
+            tpeak, tsrc = tf32["tf32_tflops"], "profiles/peaks_tf32.json (cuBLAS TF32, measured)"
+        else:
+            tpeak, tsrc = mp.get("bf16_tflops", 1590.0) / 2, "MEASURED_PEAKS bf16/2"
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        except Exception:
+            pass
+        rl_screen = {"kernel": "k_screen (K2, tcgen05 kind::tf32)", "bound": "tensor",
+                     "achieved": screen_tflops, "peak": tpeak, "unit": "TFLOP/s",
+                     "frac": screen_tflops / tpeak, "peak_source": tsrc,
+                     "frac_of_bf16_peak": screen_tflops / mp.get("bf16_tflops", 1590.0),
+                     "algorithmic": f"{pairs_cand:.4g} candidate pairs x 2*{D} flop",
+                     "ms": ms_screen,
+                     "traffic": (traffic or {}).get("k_screen")}
+        rl_feat = {"kernel": "k_hist_tiles_lane (K1)", "bound": "hbm", "achieved": feat_gbs,
+                   "peak": hbm, "unit": "GB/s", "frac": feat_gbs / hbm,
+                   "algorithmic": "937,984 B/frame (921,600 read + 64 x 64 x 4 written)",
+                   "ms": ms_feat, "traffic": (traffic or {}).get("k_hist_tiles_lane")}
+        dominant = rl_screen if ms_screen >= ms_feat else rl_feat
+        line = {
+            "metric": METRIC, "value": F / (ms_step * 1e-3), "unit": "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8 hist / tf32 screen / f64 exact", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "frames": F, "tiles": n_tiles, "d": D, "tau": tau,
+                       "candidate_pairs": pairs_cand, "l2": "flushed (256 MB write) before each step",
+                       "parallelism": f"frames sharded x{world}, features all-gathered, join row-blocks cyclic x{world}"},
+            "join_gpairs_per_s": pairs_cand / (ms_join * 1e-3) / 1e9,
+            "featurize_frames_per_s": F / (ms_feat * 1e-3),
+            "phase_ms": {"featurize": ms_feat, "gather": maxred(statistics.mean(rec["gather"])),
+                         "join": ms_join, "join_prep": maxred(statistics.mean(rec["prep"])),
+                         "join_screen": ms_screen, "join_recheck": ms_recheck},
+            "pairs": n_pairs, "candidates": n_cand,
+            "roofline": dominant, "roofline_all": [rl_feat, rl_screen],
+            "cpu_baseline": cpu,
+            "e2e": {"value": F / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                    "api": "pdb_featurize_join (pinned host frames -> host pairs)" if world == 1
+                           else "featurize_tiles_dev + all_gather + pdb_sim_join_dev + D2H"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line))
+    pairs.free()
+    lib.pdb_host_free(hbuf)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

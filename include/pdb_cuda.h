@@ -140,12 +140,19 @@ typedef struct pdb_pairs {
     float* dist;
 } pdb_pairs;
 
-/* Per-call counters (optional out-parameter of the _dev variant). */
+/* Per-call counters and device timings (optional out-parameter of the _dev
+ * variant).  The *_ms fields are CUDA-event times on the call's stream. */
 typedef struct pdb_join_stats {
     int64_t candidates;      /* pairs passing the tensor-core screen */
     int64_t pairs;           /* pairs passing the exact fp64 re-check */
     int64_t tiles;           /* 128x256 screen tiles executed */
     int64_t candidate_capacity;
+    int32_t launches;        /* kernels this call launched */
+    int32_t screen_passes;   /* 1, or 2 after a candidate-buffer overflow */
+    float prep_ms;           /* centring, tf32 copies, norms, tile stats */
+    float screen_ms;         /* K2, the tcgen05 screen */
+    float recheck_ms;        /* K3, exact re-check + compaction */
+    float sort_ms;           /* optional canonical ordering */
 } pdb_join_stats;
 
 /* Host pointers: L [nL, d] and R [nR, d] fp32 row-major. */

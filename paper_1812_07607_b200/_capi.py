@@ -62,7 +62,9 @@ class DevPairs(C.Structure):
 
 class JoinStats(C.Structure):
     _fields_ = [("candidates", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64),
-                ("candidate_capacity", C.c_int64)]
+                ("candidate_capacity", C.c_int64), ("launches", C.c_int32),
+                ("screen_passes", C.c_int32), ("prep_ms", C.c_float), ("screen_ms", C.c_float),
+                ("recheck_ms", C.c_float), ("sort_ms", C.c_float)]
 
 
 _lib: Optional[C.CDLL] = None
@@ -119,7 +121,7 @@ def gen() -> C.CDLL:
         G.pdb_gen_plant.restype = i64
         G.pdb_gen_simplex.argtypes = [vp, i64, i32, i32, f64, f64, u64, i32]
         G.pdb_gen_uniform.argtypes = [vp, i64, i32, u64, i32]
-        G.pdb_gen_frames.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, u64, vp, i32]
+        G.pdb_gen_frames.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, i32, u64, vp, i32]
         _gen = G
     return _gen
 

@@ -187,45 +187,56 @@ GEN_API int pdb_gen_uniform(float* out, int64_t n, int32_t d, uint64_t seed,
     return 0;
 }
 
-// Config 2 frames [F,H,W,3] uint8.  Background: piecewise-constant colour
-// blocks of block x block pixels, one uniform RGB colour per block per
-// frame.  Noise: per pixel and channel, uniform integer in [-noise, noise],
-// clamped to [0,255].  Every frame f with f % period == period-1 is a
-// near-copy: it reuses the block colours of an earlier frame
-// src = f - 1 - (mix % min(f, 10)) and is re-noised with `copy_noise`
-// (period 20 -> exactly 5% of frames).  src_of[f] receives the source frame
-// index (or -1) when non-null.
-GEN_API int pdb_gen_frames(uint8_t* out, int64_t F, int32_t H, int32_t W, int32_t block,
-                           int32_t noise, int32_t copy_noise, int32_t period, uint64_t seed,
-                           int64_t* src_of, int32_t threads) {
-    if (F < 0 || H < 1 || W < 1 || block < 1 || period < 1) return 1;
-    std::vector<int64_t> src(static_cast<size_t>(F), -1);
-    for (int64_t f = 1; f < F; f++) {
-        if (f % period != period - 1) continue;
+// Config 2 frames [count,H,W,3] uint8: frames f0 .. f0+count-1 of the
+// video (any range can be generated independently, so ranks generate only
+// their own shard).  Background: piecewise-constant colour blocks of
+// block x block pixels, one uniform RGB colour per block per frame.  Noise:
+// per pixel and channel, uniform integer in [-noise, noise], clamped to
+// [0,255].  Every frame f with f % period == period-1 is a near-copy: it
+// reuses the block colours of an earlier original frame
+// (f - 1 - (mix % min(f, 10)), followed back to an original) and is
+// re-noised with `copy_noise` (period 20 -> exactly 5% of frames).
+// src_of[k] receives the source frame of frame f0+k (or -1) when non-null.
+namespace {
+int64_t frame_source(int64_t f, int32_t period, uint64_t seed) {
+    while (f >= 1 && f % period == period - 1) {
         uint64_t m = mix_seed(mix_seed(seed, kSaltCopy), static_cast<uint64_t>(f));
         int64_t span = std::min<int64_t>(f, 10);
-        int64_t s = f - 1 - static_cast<int64_t>(m % static_cast<uint64_t>(span));
-        while (src[s] >= 0) s = src[s];  // copy of a copy -> the original
-        src[f] = s;
+        f = f - 1 - static_cast<int64_t>(m % static_cast<uint64_t>(span));
+    }
+    return f;
+}
+}  // namespace
+
+GEN_API int pdb_gen_frames(uint8_t* out, int64_t f0, int64_t count, int32_t H, int32_t W,
+                           int32_t block, int32_t noise, int32_t copy_noise, int32_t period,
+                           uint64_t seed, int64_t* src_of, int32_t threads) {
+    if (f0 < 0 || count < 0 || H < 1 || W < 1 || block < 1 || period < 1) return 1;
+    std::vector<int64_t> src(static_cast<size_t>(count), -1);
+    for (int64_t k = 0; k < count; k++) {
+        const int64_t f = f0 + k;
+        const int64_t s = frame_source(f, period, seed);
+        if (s != f) src[k] = s;
     }
     if (src_of) std::memcpy(src_of, src.data(), src.size() * sizeof(int64_t));
     const int32_t bx = (W + block - 1) / block, by = (H + block - 1) / block;
-    parallel_for(F, default_threads(threads), [&](int64_t a, int64_t b) {
+    parallel_for(count, default_threads(threads), [&](int64_t a, int64_t b) {
         std::vector<uint8_t> col(static_cast<size_t>(bx) * by * 3);
-        for (int64_t f = a; f < b; f++) {
-            int64_t cf = src[f] >= 0 ? src[f] : f;
-            for (int64_t k = 0; k < static_cast<int64_t>(bx) * by; k++) {
+        for (int64_t k = a; k < b; k++) {
+            const int64_t f = f0 + k;
+            const int64_t cf = src[k] >= 0 ? src[k] : f;
+            for (int64_t q = 0; q < static_cast<int64_t>(bx) * by; q++) {
                 Rng g(mix_seed(mix_seed(mix_seed(seed, kSaltBlock), static_cast<uint64_t>(cf)),
-                               static_cast<uint64_t>(k)));
+                               static_cast<uint64_t>(q)));
                 uint64_t v = g.next();
-                col[k * 3 + 0] = static_cast<uint8_t>(v);
-                col[k * 3 + 1] = static_cast<uint8_t>(v >> 8);
-                col[k * 3 + 2] = static_cast<uint8_t>(v >> 16);
+                col[q * 3 + 0] = static_cast<uint8_t>(v);
+                col[q * 3 + 1] = static_cast<uint8_t>(v >> 8);
+                col[q * 3 + 2] = static_cast<uint8_t>(v >> 16);
             }
-            const int32_t amp = src[f] >= 0 ? copy_noise : noise;
+            const int32_t amp = src[k] >= 0 ? copy_noise : noise;
             const uint64_t span = static_cast<uint64_t>(2 * amp + 1);
             uint64_t fseed = mix_seed(mix_seed(seed, kSaltNoise), static_cast<uint64_t>(f));
-            uint8_t* fr = out + f * static_cast<int64_t>(H) * W * 3;
+            uint8_t* fr = out + k * static_cast<int64_t>(H) * W * 3;
             for (int32_t y = 0; y < H; y++) {
                 Rng g(mix_seed(fseed, static_cast<uint64_t>(y)));
                 const uint8_t* crow = col.data() + static_cast<size_t>(y / block) * bx * 3;

@@ -615,6 +615,31 @@ int padded_dim(int d) {
     return DP;
 }
 
+// Optional CUDA-event timing of the phases of one call.
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[6] = {};
+    PhaseTimer(bool enable, cudaStream_t st) : on(enable), s(st) {
+        if (!on) return;
+        for (auto& e : ev) PDB_CUDA(cudaEventCreate(&e));
+    }
+    ~PhaseTimer() {
+        if (!on) return;
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    void mark(int k) {
+        if (on) PDB_CUDA(cudaEventRecord(ev[k], s));
+    }
+    float ms(int a, int b) {
+        if (!on) return 0.0f;
+        float t = 0.0f;
+        PDB_CUDA(cudaEventSynchronize(ev[b]));
+        PDB_CUDA(cudaEventElapsedTime(&t, ev[a], ev[b]));
+        return t;
+    }
+};
+
 }  // namespace
 
 void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR, int32_t d,
@@ -632,6 +657,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     if (stats) *stats = pdb_join_stats{};
     out->count = 0;
     if (nL == 0 || nR == 0) return;
+    PhaseTimer tm(stats != nullptr, s);
+    int launches = 0;
+    tm.mark(0);
 
     const int DP = padded_dim(d);
     if (DP > 2048) fail(PDB_ERR_CONFIG, "similarity join: d > 2048 is not supported by this build");
@@ -645,12 +673,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         k_col_partial<<<grd, blk, 0, s>>>(d_L, nm, d, part.p);
         k_col_final<<<static_cast<unsigned>(ceil_div(DP, 128)), 128, 0, s>>>(part.p, nm, d, DP, mu.p);
         PDB_CUDA(cudaGetLastError());
+        launches += 2;
     }
     auto prep = [&](const float* X, int64_t n, DevBuf<float>& Xp, DevBuf<float>& hn,
                     DevBuf<float>& sn) {
         k_prep<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p,
                                                                            hn.p, sn.p);
         PDB_CUDA(cudaGetLastError());
+        launches++;
     };
     DevBuf<float> XpL(static_cast<size_t>(nL) * DP, s), hnL(nL, s), snL(nL, s);
     prep(d_L, nL, XpL, hnL, snL);
@@ -669,6 +699,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     DevBuf<float> gR(static_cast<size_t>(nt) * BN, s), tmaxS(nt, s), tmaxN(nt, s);
     k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR.p, tmaxS.p, tmaxN.p);
     PDB_CUDA(cudaGetLastError());
+    launches++;
 
     // ---- work units: (column chunk c, row block rb), chunk-major ----------
     const int64_t n_rb = ceil_div(nL, BM);
@@ -716,6 +747,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
 
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
     DevBuf<int2> cand;
+    int passes = 0;
+    tm.mark(1);
     for (int attempt = 0; attempt < 2; attempt++) {
         cand.reset(cap, s);
         p.cand = cand.p;
@@ -723,7 +756,12 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         p.counter = counters.p;
         p.tiles = counters.p + 1;
         PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
-        if (n_units > 0) dispatch_screen(DP, ctx, tA, tB, p, s);
+        if (n_units > 0) {
+            dispatch_screen(DP, ctx, tA, tB, p, s);
+            launches++;
+        }
+        tm.mark(2);
+        passes++;
         PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 2 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
@@ -731,6 +769,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
     }
     const unsigned long long n_cand = h_cnt[0];
+    tm.mark(5);  // recheck phase starts after the count read-back
 
     // ---- exact re-check + compaction ----------------------------------------
     if (static_cast<unsigned long long>(out->capacity) < n_cand || !out->left) {
@@ -750,11 +789,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                        static_cast<unsigned long long>(out->capacity),
                                        counters.p + 2);
         PDB_CUDA(cudaGetLastError());
+        launches++;
+        tm.mark(3);
         PDB_CUDA(cudaMemcpyAsync(&n_pairs, counters.p + 2, sizeof(n_pairs),
                                  cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
     }
     out->count = static_cast<int64_t>(n_pairs);
+    if (n_cand == 0) tm.mark(3);
 
     if ((o.flags & PDB_JOIN_SORTED) && n_pairs > 1) {
         const int64_t n = static_cast<int64_t>(n_pairs);
@@ -770,12 +812,20 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         k_unpack_keys<<<592, 256, 0, s>>>(k_out.p, n, out->left, out->right);
         PDB_CUDA(cudaMemcpyAsync(out->dist, v_out.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
         PDB_CUDA(cudaGetLastError());
+        launches += 4;  // pack, 2 cub passes (upper bound), unpack
     }
+    tm.mark(4);
     if (stats) {
         stats->candidates = static_cast<int64_t>(n_cand);
         stats->pairs = static_cast<int64_t>(n_pairs);
         stats->tiles = static_cast<int64_t>(h_cnt[1]);
         stats->candidate_capacity = static_cast<int64_t>(cap);
+        stats->launches = launches;
+        stats->screen_passes = passes;
+        stats->prep_ms = tm.ms(0, 1);
+        stats->screen_ms = tm.ms(1, 2);
+        stats->recheck_ms = tm.ms(5, 3);
+        stats->sort_ms = tm.ms(3, 4);
     }
 }
 

@@ -56,14 +56,14 @@ def simplex(n: int, d: int, centres: int, clustered: float, sigma: float, seed: 
 
 
 def frames(F: int, H: int = 480, W: int = 640, *, block: int = 40, noise: int = 8,
-           copy_noise: int = 4, period: int = 20, seed: int = 2, out=None):
-    """Config 2 frames [F, H, W, 3] uint8 and the source frame of each
-    near-copy (-1 for originals).  ``out`` may be any writable uint8 buffer
-    (e.g. pinned host memory) of F*H*W*3 bytes exposing a numpy array."""
+           copy_noise: int = 4, period: int = 20, seed: int = 2, first: int = 0, out=None):
+    """Config 2 frames first .. first+F-1 as [F, H, W, 3] uint8, and the
+    source frame of each near-copy (-1 for originals).  ``out`` may be any
+    writable [F, H, W, 3] uint8 numpy view (e.g. of pinned host memory)."""
     x = out if out is not None else np.empty((F, H, W, 3), dtype=np.uint8)
     src = np.empty(F, dtype=np.int64)
-    rc = capi.gen().pdb_gen_frames(capi.ptr(x), F, H, W, block, noise, copy_noise, period, seed,
-                                   capi.ptr(src), _threads())
+    rc = capi.gen().pdb_gen_frames(capi.ptr(x), first, F, H, W, block, noise, copy_noise, period,
+                                   seed, capi.ptr(src), _threads())
     assert rc == 0
     return x, src
 
