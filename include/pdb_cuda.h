@@ -118,9 +118,11 @@ int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, in
  *                    emission order when the build side is R (probe order,
  *                    ascending build id).  Without it the order is
  *                    unspecified.
- * Sharding (multi-GPU, one process per GPU): with shard_count > 1 this call
- * only scans the 128-row blocks b of L with b % shard_count == shard_index
- * (indices stay global), so the shards partition the pair set. */
+ * Sharding (multi-GPU, one process per GPU): with shard_count = P > 1 this
+ * call only scans the 128-row blocks of L assigned to shard_index: block
+ * b = k*P + (k even ? shard_index : P-1-shard_index), k = 0, 1, ...
+ * (boustrophedon rounds; indices stay global), so the shards partition the
+ * pair set and share the triangular self-join work evenly. */
 #define PDB_JOIN_SELF 1u
 #define PDB_JOIN_SORTED 2u
 

@@ -23,6 +23,8 @@
 // reduced with one REDUX per bin at the end of the tile.  Bin counts too
 // large for lane-private columns use per-warp shared-memory atomics.
 
+#include <cstdlib>
+
 #include "pdb_internal.cuh"
 
 namespace pdb {
@@ -128,6 +130,124 @@ k_hist_tiles_lane(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
     for (int j = 0; j < (NB + 31) / 32; j++) {
         const int b = j * 32 + lane;
         if (b < D) o[b] = normalise(mine[j], npix);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Joint histogram with B = 2^LB (LB = 1, 2 -> 8 or 64 bins): the config-2
+// hot kernel, one warp per tile.
+//
+// Loads: a tile row is rc = 3*tw/16 16-byte chunks; a batch of RB =
+// floor(96/rc) rows (6 for 80-px tiles) is fetched with three coalesced
+// 16-byte loads per lane (consecutive lanes -> consecutive chunks, so each
+// load instruction reads whole 240-byte row segments), staged in a 1.4 KB
+// per-warp shared buffer, and re-read as one 48-byte group (16 whole RGB
+// pixels) per lane.  The next batch's loads are issued before the current
+// batch is binned.  (Measured on B200: letting each lane load its own 48 B
+// straight from global capped the kernel at ~2 TB/s even with no counting.)
+// Binning is SIMD-within-a-register: four pixels (three words) are
+// quantised with one shift+mask per word, regrouped with byte permutes and
+// combined into four packed joint indices with two multiply-adds.
+// Counts are 16-bit halves of lane-private shared words cnt[bin/2][lane]
+// (bank = lane: conflict-free), bumped with a plain read-modify-write (B200
+// shared atomics measured ~4x slower here; match.any aggregation slower
+// still).  Requires ceil(th*tw/16 / 32)*16 < 65536 pixels per lane.
+template <int LB>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 12)
+k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, int W, int th,
+                  int tw, int ntx, int tiles_per_frame, float npix, float* __restrict__ out) {
+    constexpr int NB = 1 << (3 * LB);
+    constexpr int NW = NB / 2;                       // counter words per lane
+    constexpr int kStageBytes = 96 * 16;             // 32 lanes x 3 chunks
+    constexpr uint32_t kMask = ((1u << LB) - 1u) * 0x01010101u;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tile = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+    if (tile >= n_tiles) return;
+    uint32_t* cnt = smem + warp * (NW * 32 + kStageBytes / 4) + lane;
+    uint8_t* stage = reinterpret_cast<uint8_t*>(smem + warp * (NW * 32 + kStageBytes / 4) + NW * 32);
+#pragma unroll
+    for (int b = 0; b < NW; b++) cnt[b * 32] = 0;
+
+    const int64_t f = tile / tiles_per_frame;
+    const int t = static_cast<int>(tile - f * tiles_per_frame);
+    const int ty = t / ntx, tx = t - (t / ntx) * ntx;
+    const uint8_t* base =
+        frames + (static_cast<size_t>(f) * H * W + static_cast<size_t>(ty) * th * W +
+                  static_cast<size_t>(tx) * tw) * 3;
+    const uint32_t row_bytes = static_cast<uint32_t>(W) * 3;
+    const int segs = tw >> 4;          // 48-byte groups per tile row
+    const int rc = 3 * segs;           // 16-byte chunks per tile row
+    const int RB = 96 / rc;            // rows per batch
+    const int nb = (th + RB - 1) / RB;
+    // this lane's three chunks of a batch: chunk c = 32*j + lane
+    uint32_t goff[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        const int c = 32 * j + lane;
+        goff[j] = static_cast<uint32_t>(c / rc) * row_bytes + static_cast<uint32_t>(c % rc) * 16u;
+    }
+    auto load = [&](int bt, uint4 (&v)[3]) {
+        const int nrows = min(RB, th - bt * RB);
+        const uint8_t* p = base + static_cast<size_t>(bt) * RB * row_bytes;
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            if (32 * j + lane < nrows * rc) v[j] = ldg_stream(p + goff[j]);
+    };
+    uint4 cur[3];
+    load(0, cur);
+    for (int bt = 0; bt < nb; bt++) {
+        const int ngroups = min(RB, th - bt * RB) * segs;
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            reinterpret_cast<uint4*>(stage)[32 * j + lane] = cur[j];
+        __syncwarp();
+        uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a;
+        if (lane < ngroups) {
+            const uint4* g = reinterpret_cast<const uint4*>(stage + lane * 48);
+            a = g[0];
+            b = g[1];
+            c = g[2];
+        }
+        __syncwarp();
+        if (bt + 1 < nb) load(bt + 1, cur);
+        if (lane < ngroups) {
+            const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+                // q0 = [r0 g0 b0 r1], q1 = [g1 b1 r2 g2], q2 = [b2 r3 g3 b3] (byte 0 first)
+                const uint32_t q0 = (w[3 * g] >> (8 - LB)) & kMask;
+                const uint32_t q1 = (w[3 * g + 1] >> (8 - LB)) & kMask;
+                const uint32_t q2 = (w[3 * g + 2] >> (8 - LB)) & kMask;
+                const uint32_t R = __byte_perm(__byte_perm(q0, q1, 0x0630), q2, 0x5210);
+                const uint32_t G = __byte_perm(__byte_perm(q0, q1, 0x0741), q2, 0x6210);
+                const uint32_t Bv = __byte_perm(__byte_perm(q0, q1, 0x0052), q2, 0x7410);
+                const uint32_t idx4 = R * (1u << (2 * LB)) + G * (1u << LB) + Bv;  // no carries
+                const uint32_t word4 = (idx4 >> 1) & 0x7F7F7F7Fu;  // bin / 2
+                const uint32_t sh4 = (idx4 & 0x01010101u) << 4;    // 0 or 16
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t wd = (word4 >> (8 * k)) & 0xFFu;
+                    cnt[wd * 32] += 1u << ((sh4 >> (8 * k)) & 0xFFu);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    uint32_t mine[(NB + 31) / 32];
+#pragma unroll
+    for (int wd = 0; wd < NW; wd++) {
+        const uint32_t v = cnt[wd * 32];
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, v >> 16);
+        if (((2 * wd) & 31) == lane) mine[(2 * wd) >> 5] = lo;
+        if (((2 * wd + 1) & 31) == lane) mine[(2 * wd + 1) >> 5] = hi;
+    }
+    float* o = out + tile * NB;
+#pragma unroll
+    for (int j = 0; j < (NB + 31) / 32; j++) {
+        const int bb = j * 32 + lane;
+        if (bb < NB) o[bb] = normalise(mine[j], npix);
     }
 }
 
@@ -291,7 +411,17 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
                      (reinterpret_cast<uintptr_t>(d_frames) % 16 == 0);
     const dim3 grid(static_cast<unsigned>(ceil_div(n_tiles, kWarpsPerCta)));
     const bool joint = mode == PDB_HIST_JOINT;
-    if (D <= 64) {
+    const int64_t lane_px = ceil_div(static_cast<int64_t>(th) * (tw / 16), 32) * 16;
+    if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {
+        const int lb = bins == 4 ? 2 : 1;
+        const size_t smem =
+            static_cast<size_t>(kWarpsPerCta) * ((1 << (3 * lb)) / 2 * 32 * 4 + 96 * 16);
+        auto k = lb == 2 ? k_hist_joint_pow2<2> : k_hist_joint_pow2<1>;
+        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k<<<grid, kWarpsPerCta * 32, smem, s>>>(d_frames, n_tiles, H, W, th, tw, ntx, tpf, npix_h,
+                                                d_out);
+    } else if (D <= 64) {
         const size_t smem = static_cast<size_t>(kWarpsPerCta) * 64 * 32 * 4;
         if (joint && bins == 4)
             launch_lane<64, true, 4>(vec, grid, smem, s, d_frames, n_tiles, H, W, th, tw, ntx,

@@ -9,7 +9,7 @@
 // re-check, and the two agree pair for pair.
 //
 // Pipeline per call:
-//   k_col_partial / k_col_final  column mean mu of (a sample of) L
+//   k_col_mean   centre mu: column mean of the first 256 rows of L
 //   k_prep       x~ = tf32_rna(x - mu) per row (padded to DP columns),
 //                ||x~||^2 (fp64 -> f32), ||x~|| (rounded up), row class
 //   k_tile_stats per 256-row tile of R: max ||y~||, max ||y~||^2;
@@ -63,7 +63,7 @@ constexpr int BN = 256;  // R rows per tile (UMMA N)
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
-constexpr int kThreads = 192;         // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kThreads = 320;         // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr uint32_t kTmemCols = 512;   // two 256-column fp32 accumulators
 constexpr uint32_t kIdesc = ptx::idesc_tf32(BM, BN);
 
@@ -108,7 +108,11 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
     }
     const int64_t k = u - __ldg(p.chunk_off + lo);
     Unit r;
-    r.rb = static_cast<int32_t>(p.shard_index + p.shard_count * k);
+    // k-th row block of this shard: boustrophedon over rounds of
+    // shard_count blocks, which balances triangular and skewed work.
+    const int P = p.shard_count;
+    const int pos = (k & 1) ? P - 1 - p.shard_index : p.shard_index;
+    r.rb = static_cast<int32_t>(k * P + pos);
     r.j0 = lo * p.ch;
     r.j1 = min(r.j0 + p.ch, p.nt);
     if (p.self_join) r.j0 = max(r.j0, r.rb >> 1);
@@ -140,6 +144,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     uint64_t* t_full = a_full + 2;   // [2]
     uint64_t* t_empty = a_full + 4;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+    float* g_smem = reinterpret_cast<float*>(a_full + 8);  // [8 warps][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -152,7 +157,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         ptx::mbar_init(a_empty, 1);
         for (int a = 0; a < 2; a++) {
             ptx::mbar_init(&t_full[a], 1);
-            ptx::mbar_init(&t_empty[a], 4);
+            ptx::mbar_init(&t_empty[a], 8);
         }
         ptx::fence_mbar_init();
     }
@@ -245,10 +250,18 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             atomicAdd(p.tiles, ntiles);
         }
     } else {
-        // ===================== epilogue (warps 2-5) =====================
+        // ===================== epilogue (warps 2-9) =====================
+        // Two warps per TMEM lane quarter, each owning 128 of the 256
+        // accumulator columns.  Per tile a warp stages its 128 g_j values in
+        // shared memory (prefetched from global one tile ahead) and streams
+        // the accumulator out of TMEM 32 columns at a time, double-buffered
+        // so the next tcgen05.ld overlaps the current chunk's arithmetic.
+        const int ew = warp - 2;
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int half = ew >> 2;
         const int row = q * 32 + lane;
         const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
+        float* gs = g_smem + ew * (BN / 2);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -257,6 +270,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             const bool row_ok = i < p.nL;
             const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
             const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
+            float4 gnext = __ldg(reinterpret_cast<const float4*>(
+                p.gR + static_cast<int64_t>(w.j0) * BN + half * (BN / 2)) + lane);
             for (int J = w.j0; J < w.j1; J++) {
                 // Per-(row, tile) threshold h_i, conservative in every rounding.
                 float h;
@@ -269,35 +284,40 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     const double T = r * r + p.gam * (static_cast<double>(hn) + __ldg(p.tmaxN + J));
                     h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
                 }
+                __syncwarp();
+                reinterpret_cast<float4*>(gs)[lane] = gnext;
+                if (J + 1 < w.j1)
+                    gnext = __ldg(reinterpret_cast<const float4*>(
+                        p.gR + static_cast<int64_t>(J + 1) * BN + half * (BN / 2)) + lane);
+                __syncwarp();
                 ptx::mbar_wait(&t_full[acc], acc_phase);
                 ptx::tc_fence_after();
-                const int64_t col0 = static_cast<int64_t>(J) * BN;
-                const uint32_t t_acc = tmem_base + t_lane + static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-                for (int c = 0; c < BN / 32; c++) {
-                    uint32_t v[32];
-                    ptx::tmem_ld32(t_acc + c * 32, v);
-                    const float4* gp = reinterpret_cast<const float4*>(p.gR + col0 + c * 32);
+                const int64_t colw = static_cast<int64_t>(J) * BN + half * (BN / 2);
+                const uint32_t t_acc =
+                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * (BN / 2));
+
+                auto process = [&](const uint32_t(&v)[32], int c) {
                     float g[32];
+                    const float4* g4 = reinterpret_cast<const float4*>(gs + c * 32);
 #pragma unroll
                     for (int k4 = 0; k4 < 8; k4++) {
-                        const float4 t = __ldg(gp + k4);
+                        const float4 t = g4[k4];
                         g[4 * k4 + 0] = t.x;
                         g[4 * k4 + 1] = t.y;
                         g[4 * k4 + 2] = t.z;
                         g[4 * k4 + 3] = t.w;
                     }
-                    ptx::tmem_ld_wait();
                     float m = -__int_as_float(0x7f800000);
 #pragma unroll
                     for (int k = 0; k < 32; k++) m = fmaxf(m, __uint_as_float(v[k]) - g[k]);
                     const bool hit = row_ok && m >= h;
                     if (__any_sync(0xffffffffu, hit)) {
+                        const int64_t col0 = colw + c * 32;
                         uint32_t mask = 0;
                         if (hit) {
 #pragma unroll
                             for (int k = 0; k < 32; k++) {
-                                const int64_t j = col0 + c * 32 + k;
+                                const int64_t j = col0 + k;
                                 const bool ok = (__uint_as_float(v[k]) - g[k] >= h) && j < p.nR &&
                                                 (!p.self_join || j > i);
                                 mask |= static_cast<uint32_t>(ok) << k;
@@ -319,15 +339,33 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                             const int k = __ffs(mask) - 1;
                             mask &= mask - 1;
                             if (pos < p.cap)
-                                p.cand[pos] = make_int2(static_cast<int>(i),
-                                                        static_cast<int>(col0 + c * 32 + k));
+                                p.cand[pos] =
+                                    make_int2(static_cast<int>(i), static_cast<int>(col0 + k));
                             pos++;
                         }
                     }
-                }
+                };
+
+                uint32_t va[32], vb[32];
+                ptx::tmem_ld32(t_acc, va);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence(va);
+                ptx::tmem_ld32(t_acc + 32, vb);
+                process(va, 0);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence(vb);
+                ptx::tmem_ld32(t_acc + 64, va);
+                process(vb, 1);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence(va);
+                ptx::tmem_ld32(t_acc + 96, vb);
+                process(va, 2);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence(vb);
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);
+                if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);  // TMEM reads done
+                process(vb, 3);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -346,34 +384,38 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
 
 // ---------------------------------------------------------------------------
 // Preparation kernels.
-constexpr int kMeanRows = 16384;
-constexpr int kMeanSplits = 64;
+// The centre mu only has to be a fixed vector (distances are translation
+// invariant and the margin is computed from the centred copies), so the mean
+// of the first kMeanRows rows is plenty; finite values only.
+constexpr int kMeanRows = 256;
 
-__global__ void k_col_partial(const float* __restrict__ X, int64_t n, int d,
-                              double* __restrict__ part) {
+// grid = ceil(DP/32) blocks of 32x32 threads: thread (x, y) sums rows
+// y, y+32, ... of column 32*blockIdx.x + x; the 32 partial sums are then
+// added in a fixed order, so mu is deterministic.
+__global__ void __launch_bounds__(1024)
+k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restrict__ mu) {
+    __shared__ double part[32][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
-    const int split = blockIdx.y * blockDim.y + threadIdx.y;  // 0..kMeanSplits-1
-    if (col >= d) return;
     double s = 0.0;
-    for (int64_t r = split; r < n; r += kMeanSplits) {
-        const float v = X[r * d + col];
-        if (isfinite(v)) s += static_cast<double>(v);
+    if (col < d) {
+#pragma unroll
+        for (int k = 0; k < kMeanRows / 32; k++) {
+            const int64_t r = threadIdx.y + 32 * k;
+            if (r < n) {
+                const float v = X[r * d + col];
+                if (isfinite(v)) s += static_cast<double>(v);
+            }
+        }
     }
-    part[static_cast<int64_t>(split) * d + col] = s;
-}
-
-__global__ void k_col_final(const double* __restrict__ part, int64_t n, int d, int DP,
-                            float* __restrict__ mu) {
-    const int col = blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= DP) return;
-    if (col >= d || n == 0) {
-        mu[col] = 0.0f;
-        return;
+    part[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < DP) {
+        double t = 0.0;
+        for (int k = 0; k < 32; k++) t += part[k][threadIdx.x];
+        const int64_t m = n < kMeanRows ? n : kMeanRows;
+        const float v = (col < d && m > 0) ? static_cast<float>(t / static_cast<double>(m)) : 0.0f;
+        mu[col] = isfinite(v) ? v : 0.0f;
     }
-    double s = 0.0;
-    for (int k = 0; k < kMeanSplits; k++) s += part[static_cast<int64_t>(k) * d + col];
-    const float m = static_cast<float>(s / static_cast<double>(n));
-    mu[col] = isfinite(m) ? m : 0.0f;
 }
 
 // One warp per row: centred, tf32-rounded, zero-padded copy + norms + class.
@@ -578,7 +620,7 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
                    const ScreenParams& p, cudaStream_t s) {
     constexpr int NKB = DP / BK;
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
-    constexpr size_t smem = 1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256;
+    constexpr size_t smem = 1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + 4096;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES>;
     PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -666,15 +708,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
 
     // ---- preparation ----------------------------------------------------
     DevBuf<float> mu(DP, s);
-    {
-        const int64_t nm = std::min<int64_t>(nL, kMeanRows);
-        DevBuf<double> part(static_cast<size_t>(kMeanSplits) * d, s);
-        dim3 blk(32, 8), grd(static_cast<unsigned>(ceil_div(d, 32)), kMeanSplits / 8);
-        k_col_partial<<<grd, blk, 0, s>>>(d_L, nm, d, part.p);
-        k_col_final<<<static_cast<unsigned>(ceil_div(DP, 128)), 128, 0, s>>>(part.p, nm, d, DP, mu.p);
-        PDB_CUDA(cudaGetLastError());
-        launches += 2;
-    }
+    k_col_mean<<<static_cast<unsigned>(ceil_div(DP, 32)), dim3(32, 32), 0, s>>>(d_L, nL, d, DP,
+                                                                              mu.p);
+    PDB_CUDA(cudaGetLastError());
+    launches++;
     auto prep = [&](const float* X, int64_t n, DevBuf<float>& Xp, DevBuf<float>& hn,
                     DevBuf<float>& sn) {
         k_prep<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p,
@@ -704,15 +741,19 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     // ---- work units: (column chunk c, row block rb), chunk-major ----------
     const int64_t n_rb = ceil_div(nL, BM);
     double total_tiles = 0;
-    for (int64_t rb = shard; rb < n_rb; rb += P)
+    for (int64_t rb = 0; rb < n_rb; rb++)
         total_tiles += self ? static_cast<double>(nt - (rb >> 1)) : static_cast<double>(nt);
+    total_tiles /= P;
     int ch = static_cast<int>(std::clamp<double>(total_tiles / (8.0 * ctx.sm_count), 1.0, 64.0));
     const int n_chunks = static_cast<int>(ceil_div(nt, ch));
     std::vector<int64_t> off(static_cast<size_t>(n_chunks) + 1, 0);
     for (int c = 0; c < n_chunks; c++) {
         int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
         if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * ch);
-        const int64_t cnt = lim > shard ? ceil_div(lim - shard, P) : 0;
+        // blocks k*P + pos(k) < lim, pos(k) = shard (k even) / P-1-shard (k odd)
+        const int64_t full = lim / P, rem = lim % P;
+        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
+        const int64_t cnt = full + (pos_last < rem ? 1 : 0);
         off[c + 1] = off[c] + cnt;
     }
     const int64_t n_units = off[n_chunks];

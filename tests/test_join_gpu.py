@@ -174,8 +174,9 @@ def test_shards_partition_the_pair_set():
     r = np.concatenate([p.right for p in parts])
     assert len(l) == len(full)
     assert _same_set(l, r, full.left, full.right)
+    from paper_1812_07607_b200 import shard
     for k, p in enumerate(parts):
-        assert np.all((p.left // 128) % 3 == k)
+        assert np.isin(p.left, shard.shard_rows(k, 3, x.shape[0])).all()
 
 
 def test_device_entry_and_reuse():
