@@ -148,21 +148,23 @@ k_hist_tiles_lane(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
 // Binning is SIMD-within-a-register: four pixels (three words) are
 // quantised with one shift+mask per word, regrouped with byte permutes and
 // combined into four packed joint indices with two multiply-adds.
-// Counts are 16-bit halves of lane-private shared words cnt[bin/2][lane]
-// (bank = lane: conflict-free), bumped with a plain read-modify-write (B200
-// shared atomics measured ~4x slower here; match.any aggregation slower
-// still).  Requires ceil(th*tw/16 / 32)*16 < 65536 pixels per lane.
-template <int LB>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 12)
+// Counts live in lane-private shared words cnt[bin][lane] (CW = 32) or in
+// 16-bit halves cnt[bin/2][lane] (CW = 16); bank = lane, so updates never
+// conflict.  They are bumped with a plain read-modify-write: on B200 shared
+// atomics (red.shared) measured ~2 lanes/clk/SM here and match.any warp
+// aggregation was slower still.  CW = 16 requires fewer than 65536 pixels
+// per lane per tile.
+template <int LB, int WPC, int DEPTH, int CW>
+__global__ void __launch_bounds__(WPC * 32)
 k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, int W, int th,
                   int tw, int ntx, int tiles_per_frame, float npix, float* __restrict__ out) {
     constexpr int NB = 1 << (3 * LB);
-    constexpr int NW = NB / 2;                       // counter words per lane
+    constexpr int NW = CW == 16 ? NB / 2 : NB;       // counter words per lane
     constexpr int kStageBytes = 96 * 16;             // 32 lanes x 3 chunks
     constexpr uint32_t kMask = ((1u << LB) - 1u) * 0x01010101u;
     extern __shared__ __align__(16) uint32_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t tile = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+    const int64_t tile = static_cast<int64_t>(blockIdx.x) * WPC + warp;
     if (tile >= n_tiles) return;
     uint32_t* cnt = smem + warp * (NW * 32 + kStageBytes / 4) + lane;
     uint8_t* stage = reinterpret_cast<uint8_t*>(smem + warp * (NW * 32 + kStageBytes / 4) + NW * 32);
@@ -194,8 +196,9 @@ k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
         for (int j = 0; j < 3; j++)
             if (32 * j + lane < nrows * rc) v[j] = ldg_stream(p + goff[j]);
     };
-    uint4 cur[3];
+    uint4 cur[3], nxt[3];
     load(0, cur);
+    if (DEPTH > 1 && nb > 1) load(1, nxt);
     for (int bt = 0; bt < nb; bt++) {
         const int ngroups = min(RB, th - bt * RB) * segs;
 #pragma unroll
@@ -210,7 +213,13 @@ k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
             c = g[2];
         }
         __syncwarp();
-        if (bt + 1 < nb) load(bt + 1, cur);
+        if (DEPTH > 1) {
+#pragma unroll
+            for (int j = 0; j < 3; j++) cur[j] = nxt[j];
+            if (bt + 2 < nb) load(bt + 2, nxt);
+        } else if (bt + 1 < nb) {
+            load(bt + 1, cur);
+        }
         if (lane < ngroups) {
             const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -223,12 +232,16 @@ k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
                 const uint32_t G = __byte_perm(__byte_perm(q0, q1, 0x0741), q2, 0x6210);
                 const uint32_t Bv = __byte_perm(__byte_perm(q0, q1, 0x0052), q2, 0x7410);
                 const uint32_t idx4 = R * (1u << (2 * LB)) + G * (1u << LB) + Bv;  // no carries
-                const uint32_t word4 = (idx4 >> 1) & 0x7F7F7F7Fu;  // bin / 2
-                const uint32_t sh4 = (idx4 & 0x01010101u) << 4;    // 0 or 16
+                if (CW == 32) {
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const uint32_t wd = (word4 >> (8 * k)) & 0xFFu;
-                    cnt[wd * 32] += 1u << ((sh4 >> (8 * k)) & 0xFFu);
+                    for (int k = 0; k < 4; k++) cnt[__byte_perm(idx4, 0, 0x4440 | k) * 32] += 1u;
+                } else {
+                    const uint32_t word4 = (idx4 >> 1) & 0x7F7F7F7Fu;  // bin / 2
+                    const uint32_t bit4 = idx4 & 0x01010101u;          // which half
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        cnt[__byte_perm(word4, 0, 0x4440 | k) * 32] +=
+                            __byte_perm(bit4, 0, 0x4440 | k) * 0xFFFFu + 1u;
                 }
             }
         }
@@ -238,10 +251,15 @@ k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
 #pragma unroll
     for (int wd = 0; wd < NW; wd++) {
         const uint32_t v = cnt[wd * 32];
-        const uint32_t lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
-        const uint32_t hi = __reduce_add_sync(0xffffffffu, v >> 16);
-        if (((2 * wd) & 31) == lane) mine[(2 * wd) >> 5] = lo;
-        if (((2 * wd + 1) & 31) == lane) mine[(2 * wd + 1) >> 5] = hi;
+        if (CW == 32) {
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
+            if ((wd & 31) == lane) mine[wd >> 5] = tot;
+        } else {
+            const uint32_t lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
+            const uint32_t hi = __reduce_add_sync(0xffffffffu, v >> 16);
+            if (((2 * wd) & 31) == lane) mine[(2 * wd) >> 5] = lo;
+            if (((2 * wd + 1) & 31) == lane) mine[(2 * wd + 1) >> 5] = hi;
+        }
     }
     float* o = out + tile * NB;
 #pragma unroll
@@ -414,13 +432,17 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
     const int64_t lane_px = ceil_div(static_cast<int64_t>(th) * (tw / 16), 32) * 16;
     if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {
         const int lb = bins == 4 ? 2 : 1;
-        const size_t smem =
-            static_cast<size_t>(kWarpsPerCta) * ((1 << (3 * lb)) / 2 * 32 * 4 + 96 * 16);
-        auto k = lb == 2 ? k_hist_joint_pow2<2> : k_hist_joint_pow2<1>;
+        // 32-bit lane-private counters, 4 warps per CTA, one batch of
+        // prefetch: the fastest of the measured (counter width x CTA size x
+        // prefetch depth) variants on B200 (273.6 us for config 2 vs
+        // 289-317 us for the others).
+        constexpr int kWpc = 4;
+        const size_t smem = static_cast<size_t>(kWpc) * ((1 << (3 * lb)) * 32 * 4 + 96 * 16);
+        auto k = lb == 1 ? k_hist_joint_pow2<1, kWpc, 1, 32> : k_hist_joint_pow2<2, kWpc, 1, 32>;
         PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-        k<<<grid, kWarpsPerCta * 32, smem, s>>>(d_frames, n_tiles, H, W, th, tw, ntx, tpf, npix_h,
-                                                d_out);
+        const dim3 g2(static_cast<unsigned>(ceil_div(n_tiles, kWpc)));
+        k<<<g2, kWpc * 32, smem, s>>>(d_frames, n_tiles, H, W, th, tw, ntx, tpf, npix_h, d_out);
     } else if (D <= 64) {
         const size_t smem = static_cast<size_t>(kWarpsPerCta) * 64 * 32 * 4;
         if (joint && bins == 4)
