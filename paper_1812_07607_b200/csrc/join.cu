@@ -272,23 +272,30 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
             float4 gnext = __ldg(reinterpret_cast<const float4*>(
                 p.gR + static_cast<int64_t>(w.j0) * BN + half * (BN / 2)) + lane);
-            for (int J = w.j0; J < w.j1; J++) {
-                // Per-(row, tile) threshold h_i, conservative in every rounding.
-                float h;
-                if (sn == kFlagNonFinite) {
-                    h = __int_as_float(0x7f800000);  // +inf: never a candidate
-                } else if (sn == kFlagBig) {
-                    h = -__int_as_float(0x7f800000);  // always a candidate
-                } else {
-                    const double r = p.tau_p + kU * (static_cast<double>(sn) + __ldg(p.tmaxS + J)) + 1e-30;
-                    const double T = r * r + p.gam * (static_cast<double>(hn) + __ldg(p.tmaxN + J));
-                    h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
+            // Threshold h_i for the whole unit, from the largest R norms over
+            // its tiles (conservative; fp64 once per unit, not per tile).
+            float h;
+            if (sn == kFlagNonFinite) {
+                h = __int_as_float(0x7f800000);  // +inf: never a candidate
+            } else if (sn == kFlagBig) {
+                h = -__int_as_float(0x7f800000);  // always a candidate
+            } else {
+                float ms = 0.0f, mn = 0.0f;
+                for (int J = w.j0; J < w.j1; J++) {
+                    ms = fmaxf(ms, __ldg(p.tmaxS + J));
+                    mn = fmaxf(mn, __ldg(p.tmaxN + J));
                 }
+                const double r = p.tau_p + kU * (static_cast<double>(sn) + ms) + 1e-30;
+                const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
+                h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
+            }
+            for (int J = w.j0; J < w.j1; J++) {
                 __syncwarp();
                 reinterpret_cast<float4*>(gs)[lane] = gnext;
-                if (J + 1 < w.j1)
-                    gnext = __ldg(reinterpret_cast<const float4*>(
-                        p.gR + static_cast<int64_t>(J + 1) * BN + half * (BN / 2)) + lane);
+                // unconditional (clamped) prefetch: a predicated load would
+                // force a wait at the register move
+                gnext = __ldg(reinterpret_cast<const float4*>(
+                    p.gR + static_cast<int64_t>(min(J + 1, w.j1 - 1)) * BN + half * (BN / 2)) + lane);
                 __syncwarp();
                 ptx::mbar_wait(&t_full[acc], acc_phase);
                 ptx::tc_fence_after();
