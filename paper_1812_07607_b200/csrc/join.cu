@@ -81,6 +81,7 @@ struct ScreenParams {
     int32_t nt;         // column tiles of R
     int32_t n_chunks;
     int64_t n_units;
+    int64_t unit_step;  // 1, or S > 1 to screen only every S-th unit (output-size estimate)
     const int64_t* chunk_off;  // [n_chunks + 1]
     const float* hnL;   // ||x~_i||^2
     const float* snL;   // ||x~_i|| (rounded up) or a flag
@@ -89,9 +90,10 @@ struct ScreenParams {
     const float* tmaxN;
     double tau_p;       // tau (1 + 1e-9)
     double gam;         // DP 2^-23 + 2^-19
-    int2* cand;
-    unsigned long long cap;
-    unsigned long long* counter;
+    int4* rec;                  // (row i, first column j0, hit mask, 0)
+    unsigned long long cap;     // record capacity
+    unsigned long long* counter;  // records written
+    unsigned long long* ncand;    // candidate pairs (popc of the masks)
     unsigned long long* tiles;
 };
 
@@ -145,6 +147,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     uint64_t* t_empty = a_full + 4;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
     float* g_smem = reinterpret_cast<float*>(a_full + 8);  // [8 warps][128]
+    int4* r_smem = reinterpret_cast<int4*>(g_smem + 8 * (BN / 2));  // [8 warps][32] record staging
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -176,7 +179,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
+                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
                 const Unit w = decode_unit(p, u);
                 if (A_RES) {
                     ptx::mbar_wait(a_empty, a_phase ^ 1);
@@ -209,7 +213,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0, a_phase = 0;
             unsigned long long ntiles = 0;
-            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
+                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
                 const Unit w = decode_unit(p, u);
                 if (A_RES) {
                     ptx::mbar_wait(a_full, a_phase);
@@ -262,9 +267,23 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         const int row = q * 32 + lane;
         const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
         float* gs = g_smem + ew * (BN / 2);
+        int4* rbuf = r_smem + ew * 32;
+        uint32_t nbuf = 0;                 // staged records (warp-uniform)
+        unsigned long long ncand = 0;      // this lane's candidate pairs
+        // write the staged records out: one atomic per flush, coalesced 16 B stores
+        auto flush = [&]() {
+            __syncwarp();
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(nbuf));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (lane < static_cast<int>(nbuf) && base + lane < p.cap) p.rec[base + lane] = rbuf[lane];
+            __syncwarp();
+            nbuf = 0;
+        };
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
+                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
             const Unit w = decode_unit(p, u);
             const int64_t i = static_cast<int64_t>(w.rb) * BM + row;
             const bool row_ok = i < p.nL;
@@ -330,25 +349,18 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                                 mask |= static_cast<uint32_t>(ok) << k;
                             }
                         }
-                        const uint32_t n = __popc(mask);
-                        uint32_t incl = n;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += t;
-                        }
-                        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                        unsigned long long base = 0;
-                        if (lane == 31 && total) base = atomicAdd(p.counter, total);
-                        base = __shfl_sync(0xffffffffu, base, 31);
-                        unsigned long long pos = base + incl - n;
-                        while (mask) {
-                            const int k = __ffs(mask) - 1;
-                            mask &= mask - 1;
-                            if (pos < p.cap)
-                                p.cand[pos] =
-                                    make_int2(static_cast<int>(i), static_cast<int>(col0 + k));
-                            pos++;
+                        // one record (row, first column, 32-bit hit mask) per lane with
+                        // hits, staged in shared memory and flushed 32 at a time
+                        const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
+                        if (bal) {
+                            const uint32_t nr = __popc(bal);
+                            if (nbuf + nr > 32) flush();
+                            ncand += __popc(mask);
+                            if (mask)
+                                rbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] =
+                                    make_int4(static_cast<int>(i), static_cast<int>(col0),
+                                              static_cast<int>(mask), 0);
+                            nbuf += nr;
                         }
                     }
                 };
@@ -379,6 +391,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 }
             }
         }
+        if (nbuf) flush();
+        unsigned long long nc = ncand;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
+        if (lane == 0 && nc) atomicAdd(p.ncand, nc);
     }
 
     ptx::tc_fence_before();
@@ -542,40 +559,51 @@ __device__ __forceinline__ double exact_dist(const float* __restrict__ a,
     return __dsqrt_rn(acc);
 }
 
+// One thread per candidate record: each lane walks the set bits of its
+// record's mask (warp-uniform loop, so every iteration compacts survivors
+// with a ballot and one atomic per warp).
 __global__ void __launch_bounds__(256)
-k_recheck(const int2* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
+k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n_rec,
           unsigned long long cap, const float* __restrict__ L, const float* __restrict__ R,
           int d, double tau, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
           float* __restrict__ out_d, unsigned long long out_cap,
           unsigned long long* __restrict__ out_count) {
-    const unsigned long long n = min(*n_cand, cap);
+    const unsigned long long n = min(*n_rec, cap);
     const int lane = threadIdx.x & 31;
-    const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
+    const bool vec4 =
+        (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
                                    (threadIdx.x & ~31u);
          base < n; base += stride) {
         const unsigned long long idx = base + lane;
-        bool ok = false;
-        int2 c = make_int2(0, 0);
-        double dist = 0.0;
-        if (idx < n) {
-            c = cand[idx];
-            dist = exact_dist(L + static_cast<int64_t>(c.x) * d, R + static_cast<int64_t>(c.y) * d,
-                              d, vec4);
-            ok = dist <= tau;
-        }
-        const uint32_t ball = __ballot_sync(0xffffffffu, ok);
-        if (!ball) continue;
-        unsigned long long w = 0;
-        if (lane == 0) w = atomicAdd(out_count, static_cast<unsigned long long>(__popc(ball)));
-        w = __shfl_sync(0xffffffffu, w, 0);
-        if (ok) {
-            const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
-            if (pos < out_cap) {
-                out_l[pos] = c.x;
-                out_r[pos] = c.y;
-                out_d[pos] = static_cast<float>(dist);
+        int4 rc = make_int4(0, 0, 0, 0);
+        if (idx < n) rc = rec[idx];
+        uint32_t mask = static_cast<uint32_t>(rc.z);
+        while (__any_sync(0xffffffffu, mask != 0)) {
+            bool ok = false;
+            double dist = 0.0;
+            int j = 0;
+            if (mask) {
+                const int k = __ffs(mask) - 1;
+                mask &= mask - 1;
+                j = rc.y + k;
+                dist = exact_dist(L + static_cast<int64_t>(rc.x) * d,
+                                  R + static_cast<int64_t>(j) * d, d, vec4);
+                ok = dist <= tau;
+            }
+            const uint32_t ball = __ballot_sync(0xffffffffu, ok);
+            if (!ball) continue;
+            unsigned long long w = 0;
+            if (lane == 0) w = atomicAdd(out_count, static_cast<unsigned long long>(__popc(ball)));
+            w = __shfl_sync(0xffffffffu, w, 0);
+            if (ok) {
+                const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
+                if (pos < out_cap) {
+                    out_l[pos] = rc.x;
+                    out_r[pos] = j;
+                    out_d[pos] = static_cast<float>(dist);
+                }
             }
         }
     }
@@ -627,7 +655,8 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
                    const ScreenParams& p, cudaStream_t s) {
     constexpr int NKB = DP / BK;
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
-    constexpr size_t smem = 1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + 4096;
+    constexpr size_t smem =
+        1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + 4096 + 8 * 32 * 16;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES>;
     PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -771,9 +800,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN);
 
-    DevBuf<unsigned long long> counters(4, s);  // [cand, tiles, pairs, spare]
+    DevBuf<unsigned long long> counters(4, s);  // [records, tiles, pairs, candidates]
     unsigned long long cap = static_cast<unsigned long long>(
-        std::max<int64_t>(1 << 20, 4 * (nL + nR)));
+        std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;
@@ -793,48 +822,91 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tau_p = tau * (1.0 + 1e-9);
     p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
 
-    // Screen and re-check run back to back; the host reads the three
-    // counters (candidates, tiles, pairs) once.  Output arrays are sized to
-    // the candidate capacity (pairs <= candidates), so only a candidate
-    // overflow -- detected from the count -- costs a second pass.
+    // Screen and re-check run back to back and the host reads the counters
+    // (records, tiles, pairs, candidates) once.  A record overflow re-runs
+    // the screen with the exact record count; an output overflow re-runs
+    // only the re-check into a larger buffer.
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
-    DevBuf<int2> cand;
+    DevBuf<int4> recs;
     int passes = 0;
+    unsigned long long out_need = static_cast<unsigned long long>(
+        std::max<int64_t>(1 << 20, 4 * (nL + nR)));
+    auto ensure_out = [&](unsigned long long need) {
+        if (static_cast<unsigned long long>(out->capacity) >= need && out->left) return;
+        if (out->left) pdb_dev_pairs_free(out);
+        const int64_t c = static_cast<int64_t>(need);
+        out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
+        out->capacity = c;
+    };
+    auto recheck = [&] {
+        k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
+            recs.p, counters.p, cap, d_L, d_R, d, tau, out->left, out->right, out->dist,
+            static_cast<unsigned long long>(out->capacity), counters.p + 2);
+        PDB_CUDA(cudaGetLastError());
+        launches++;
+    };
+    auto read_counters = [&] {
+        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    };
+    p.unit_step = 1;
     tm.mark(1);
-    for (int attempt = 0; attempt < 2; attempt++) {
-        cand.reset(cap, s);
-        if (static_cast<unsigned long long>(out->capacity) < cap || !out->left) {
-            if (out->left) pdb_dev_pairs_free(out);
-            const int64_t c = static_cast<int64_t>(cap);
-            out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
-            out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
-            out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
-            out->capacity = c;
-        }
-        p.cand = cand.p;
+    // Large problems: screen every 64th work unit first and size the record
+    // and output buffers from that sample, so a heavy output (config 5:
+    // ~1.4e9 candidates) does not cost a second full screen pass.
+    constexpr int64_t kSampleStep = 64;
+    if (n_units >= kSampleStep * ctx.sm_count) {
+        recs.reset(cap, s);
+        p.rec = recs.p;
         p.cap = cap;
         p.counter = counters.p;
         p.tiles = counters.p + 1;
+        p.ncand = counters.p + 3;
+        p.unit_step = kSampleStep;
+        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
+        dispatch_screen(DP, ctx, tA, tB, p, s);
+        launches++;
+        read_counters();
+        p.unit_step = 1;
+        const double scale = static_cast<double>(kSampleStep) * 1.3;
+        const unsigned long long est_rec = static_cast<unsigned long long>(h_cnt[0] * scale) + (1 << 20);
+        const unsigned long long est_cand = static_cast<unsigned long long>(h_cnt[3] * scale) + (1 << 20);
+        cap = std::max(cap, est_rec);
+        out_need = std::max(out_need, est_cand);
+    }
+    for (int attempt = 0; attempt < 2; attempt++) {
+        recs.reset(cap, s);
+        ensure_out(out_need);
+        p.rec = recs.p;
+        p.cap = cap;
+        p.counter = counters.p;
+        p.tiles = counters.p + 1;
+        p.ncand = counters.p + 3;
         PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
         if (n_units > 0) {
             dispatch_screen(DP, ctx, tA, tB, p, s);
             launches++;
         }
         tm.mark(2);
-        k_recheck<<<ctx.sm_count * 8, 256, 0, s>>>(
-            cand.p, counters.p, cap, d_L, d_R, d, tau, out->left, out->right, out->dist,
-            static_cast<unsigned long long>(out->capacity), counters.p + 2);
-        PDB_CUDA(cudaGetLastError());
-        launches++;
+        recheck();
         tm.mark(3);
         passes++;
-        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 3 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-        PDB_CUDA(cudaStreamSynchronize(s));
+        read_counters();
         if (h_cnt[0] <= cap) break;
         cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
+        out_need = std::max(out_need, h_cnt[3]);
     }
-    const unsigned long long n_cand = h_cnt[0];
+    if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
+        ensure_out(h_cnt[2]);
+        PDB_CUDA(cudaMemsetAsync(counters.p + 2, 0, sizeof(unsigned long long), s));
+        recheck();
+        tm.mark(3);
+        read_counters();
+    }
+    const unsigned long long n_cand = h_cnt[3];
     const unsigned long long n_pairs = h_cnt[2];
     out->count = static_cast<int64_t>(n_pairs);
 
@@ -859,7 +931,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         stats->candidates = static_cast<int64_t>(n_cand);
         stats->pairs = static_cast<int64_t>(n_pairs);
         stats->tiles = static_cast<int64_t>(h_cnt[1]);
-        stats->candidate_capacity = static_cast<int64_t>(cap);
+        stats->candidate_capacity = static_cast<int64_t>(cap) * 32;
         stats->launches = launches;
         stats->screen_passes = passes;
         stats->prep_ms = tm.ms(0, 1);

