@@ -178,6 +178,20 @@ int pdb_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
                      pdb_join_stats* stats);
 void pdb_dev_pairs_free(pdb_dev_pairs* p);
 
+/* Cosine threshold join over bf16-stored rows (BASELINE config 4; restated --
+ * the reference has no cosine predicate and stores fp32).
+ * Emits every (i, j) with cos(L_i, R_j) >= min_cos, where
+ *   cos = dot / (sqrt(na) * sqrt(nb)),  dot/na/nb accumulated sequentially in
+ * fp64 over k = 0..d-1 from the exact bf16 values (the oracle's
+ * orc_cosine_join_bf16); `dist` receives fp32(cos).  Zero or non-finite
+ * rows never match.  L, R: [n, d] bf16 bit patterns (uint16). Same flags,
+ * sharding and ownership rules as pdb_sim_join. */
+int pdb_cosine_join_bf16(const uint16_t* L, int64_t nL, const uint16_t* R, int64_t nR, int32_t d,
+                         double min_cos, const pdb_join_opts* opts, pdb_pairs* out);
+int pdb_cosine_join_bf16_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int64_t nR,
+                             int32_t d, double min_cos, const pdb_join_opts* opts,
+                             pdb_dev_pairs* out, pdb_join_stats* stats);
+
 /* The q1 pipeline in one call (src/bench.cpp:695-730 shape: featurize
  * tiles, then self-join the features): host frames in, host pairs out
  * (PDB_JOIN_SELF semantics).  `features` (host, [tiles, D]) is optional. */

@@ -48,6 +48,10 @@ def port():
         L.orc_sim_join_count.argtypes = [vp, i64, vp, i64, i64, f64, i32, i64, i64]
         L.orc_sim_join_count.restype = i64
         L.orc_hist_dim.argtypes = [C.c_int, C.c_int]
+        L.orc_cosine_join_bf16.argtypes = [vp, i64, vp, i64, i64, f64, i32, i64, i64, i32,
+                                           C.POINTER(OrcPairs)]
+        L.orc_cosine_bf16.argtypes = [vp, vp, i64]
+        L.orc_cosine_bf16.restype = f64
         _port = L
     return _port
 
@@ -118,6 +122,32 @@ def sim_join(L: np.ndarray, R, tau: float, self_join: bool = False, rows=(0, -1)
                              int(self_join), rows[0], rows[1], th, C.byref(out))
     if rc:
         raise RuntimeError(f"oracle join failed: {rc}")
+    n = out.count
+    try:
+        if n:
+            res = (np.ctypeslib.as_array(out.left, (n,)).copy(),
+                   np.ctypeslib.as_array(out.right, (n,)).copy(),
+                   np.ctypeslib.as_array(out.dist, (n,)).copy())
+        else:
+            res = (np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0, np.float64))
+    finally:
+        port().orc_pairs_free(C.byref(out))
+    return res
+
+
+def cosine_join_bf16(L: np.ndarray, R, min_cos: float, self_join: bool = False, rows=(0, -1),
+                     threads: int | None = None):
+    """RESTATED cosine join over bf16 bit patterns (uint16 [n, d]): pairs
+    sorted by (i, j) with cos >= min_cos: (left, right, cos f64)."""
+    L = np.ascontiguousarray(L, dtype=np.uint16)
+    R = L if self_join else np.ascontiguousarray(R, dtype=np.uint16)
+    out = OrcPairs()
+    th = threads or max(1, os.cpu_count() or 1)
+    rc = port().orc_cosine_join_bf16(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1],
+                                     float(min_cos), int(self_join), rows[0], rows[1], th,
+                                     C.byref(out))
+    if rc:
+        raise RuntimeError(f"oracle cosine join failed: {rc}")
     n = out.count
     try:
         if n:

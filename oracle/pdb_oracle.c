@@ -144,8 +144,10 @@ double orc_euclidean(const float* a, const float* b, int64_t d) {
  * independent of the thread count. */
 typedef struct {
     const float *L, *R;
+    const uint16_t *Lb, *Rb; /* cosine mode: bf16 bit patterns */
+    int cosine;
     int64_t nR, d;
-    double tau;
+    double tau;              /* L2: max distance; cosine: min cosine */
     int self_join;
     int64_t rb, re;
     int32_t* li;
@@ -177,11 +179,43 @@ static int orc_push(orc_join_task* t, int64_t i, int64_t j, double dd) {
     return 0;
 }
 
+/* RESTATED cosine over bf16 rows (BASELINE config 4; the reference has no
+ * cosine predicate and stores fp32 data): dot, na, nb
+ * accumulated sequentially in fp64 over k = 0..d-1 from the exact bf16
+ * values, cos = dot / (sqrt(na) * sqrt(nb)).  Zero / non-finite rows give
+ * NaN, which never compares >= min_cos. */
+static inline double orc_bf16(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+double orc_cosine_bf16(const uint16_t* a, const uint16_t* b, int64_t d) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int64_t k = 0; k < d; k++) {
+        double x = orc_bf16(a[k]), y = orc_bf16(b[k]);
+        dot += x * y;
+        na += x * x;
+        nb += y * y;
+    }
+    return dot / (sqrt(na) * sqrt(nb));
+}
+
 static void* orc_join_worker(void* arg) {
     orc_join_task* t = (orc_join_task*)arg;
     for (int64_t i = t->rb; i < t->re; i++) {
-        const float* a = t->L + (size_t)i * t->d;
         int64_t j0 = t->self_join ? i + 1 : 0;
+        if (t->cosine) {
+            const uint16_t* a = t->Lb + (size_t)i * t->d;
+            for (int64_t j = j0; j < t->nR; j++) {
+                double c = orc_cosine_bf16(a, t->Rb + (size_t)j * t->d, t->d);
+                if (c >= t->tau)
+                    if (orc_push(t, i, j, c)) return NULL;
+            }
+            continue;
+        }
+        const float* a = t->L + (size_t)i * t->d;
         for (int64_t j = j0; j < t->nR; j++) {
             double dd = orc_euclidean(a, t->R + (size_t)j * t->d, t->d);
             if (dd <= t->tau)
@@ -208,11 +242,12 @@ void orc_pairs_free(orc_pairs* p) {
     p->count = 0;
 }
 
-int orc_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int64_t d,
-                 double tau, int32_t self_join, int64_t row_begin, int64_t row_end,
-                 int32_t threads, orc_pairs* out) {
+static int orc_join_core(const float* L, const uint16_t* Lb, int64_t nL, const float* R,
+                         const uint16_t* Rb, int64_t nR, int64_t d, double tau, int cosine,
+                         int32_t self_join, int64_t row_begin, int64_t row_end, int32_t threads,
+                         orc_pairs* out) {
     memset(out, 0, sizeof(*out));
-    if (tau < 0.0) return ORC_ERR_CONFIG;
+    if (!cosine && tau < 0.0) return ORC_ERR_CONFIG;
     if (d < 1) return ORC_ERR_SHAPE;
     if (row_begin < 0) row_begin = 0;
     if (row_end < 0 || row_end > nL) row_end = nL;
@@ -246,6 +281,9 @@ int orc_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int64_t
         orc_join_task* t = &tasks[k];
         t->L = L;
         t->R = R;
+        t->Lb = Lb;
+        t->Rb = Rb;
+        t->cosine = cosine;
         t->nR = nR;
         t->d = d;
         t->tau = tau;
@@ -293,6 +331,20 @@ int orc_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int64_t
     free(tasks);
     free(th);
     return rc;
+}
+
+int orc_sim_join(const float* L, int64_t nL, const float* R, int64_t nR, int64_t d,
+                 double tau, int32_t self_join, int64_t row_begin, int64_t row_end,
+                 int32_t threads, orc_pairs* out) {
+    return orc_join_core(L, NULL, nL, R, NULL, nR, d, tau, 0, self_join, row_begin, row_end,
+                         threads, out);
+}
+
+int orc_cosine_join_bf16(const uint16_t* L, int64_t nL, const uint16_t* R, int64_t nR,
+                         int64_t d, double min_cos, int32_t self_join, int64_t row_begin,
+                         int64_t row_end, int32_t threads, orc_pairs* out) {
+    return orc_join_core(NULL, L, nL, NULL, R, nR, d, min_cos, 1, self_join, row_begin, row_end,
+                         threads, out);
 }
 
 /* Count-only variant (no buffers) for timing large samples. */

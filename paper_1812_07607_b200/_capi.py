@@ -41,6 +41,7 @@ EXPORTS = (
     "pdb_color_histogram_f32", "pdb_color_histogram_f32_dev",
     "pdb_sim_join", "pdb_pairs_free", "pdb_sim_join_dev", "pdb_dev_pairs_free",
     "pdb_featurize_join", "pdb_host_alloc", "pdb_host_free",
+    "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev",
 )
 
 
@@ -103,6 +104,10 @@ def lib() -> C.CDLL:
         L.pdb_dev_pairs_free.restype = None
         L.pdb_featurize_join.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, f64,
                                          C.POINTER(JoinOpts), vp, C.POINTER(Pairs)]
+        L.pdb_cosine_join_bf16.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(JoinOpts),
+                                           C.POINTER(Pairs)]
+        L.pdb_cosine_join_bf16_dev.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(JoinOpts),
+                                               C.POINTER(DevPairs), C.POINTER(JoinStats)]
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

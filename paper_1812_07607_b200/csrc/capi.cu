@@ -337,6 +337,61 @@ PDB_API int pdb_sim_join(const float* L, int64_t nL, const float* R, int64_t nR,
     });
 }
 
+static void check_cos_args(const void* L, int64_t nL, const void* R, int64_t nR, int32_t d,
+                           double min_cos, const pdb_join_opts* o) {
+    if (!(min_cos >= -1.0 && min_cos <= 1.0))
+        fail(PDB_ERR_CONFIG, "cosine join needs -1 <= min_cos <= 1");
+    check_join_args(L, nL, R, nR, d, 0.0, o);
+}
+
+PDB_API int pdb_cosine_join_bf16_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R,
+                                     int64_t nR, int32_t d, double min_cos,
+                                     const pdb_join_opts* opts, pdb_dev_pairs* out,
+                                     pdb_join_stats* stats) {
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_cos_args(d_L, nL, d_R, nR, d, min_cos, opts);
+        device_ctx();
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        o.stream = stream_of(o.stream);
+        run_cos_join_dev(d_L, nL, d_R, nR, d, min_cos, o, out, stats);
+    });
+}
+
+PDB_API int pdb_cosine_join_bf16(const uint16_t* L, int64_t nL, const uint16_t* R, int64_t nR,
+                                 int32_t d, double min_cos, const pdb_join_opts* opts,
+                                 pdb_pairs* out) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_cos_args(L, nL, R, nR, d, min_cos, opts);
+        device_ctx();
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        cudaStream_t s = cudaStreamPerThread;
+        o.stream = s;
+        const bool self = (o.flags & PDB_JOIN_SELF) != 0;
+        DevBuf<uint16_t> dL(static_cast<size_t>(nL) * std::max(d, 1), s), dR;
+        if (nL > 0)
+            PDB_CUDA(cudaMemcpyAsync(dL.p, L, static_cast<size_t>(nL) * d * 2,
+                                     cudaMemcpyHostToDevice, s));
+        if (!self && nR > 0) {
+            dR.reset(static_cast<size_t>(nR) * d, s);
+            PDB_CUDA(cudaMemcpyAsync(dR.p, R, static_cast<size_t>(nR) * d * 2,
+                                     cudaMemcpyHostToDevice, s));
+        }
+        pdb_dev_pairs dp{};
+        try {
+            run_cos_join_dev(dL.p, nL, self ? dL.p : dR.p, self ? nL : nR, d, min_cos, o, &dp,
+                             nullptr);
+            pairs_to_host(dp, out, s);
+        } catch (...) {
+            pdb_dev_pairs_free(&dp);
+            throw;
+        }
+        pdb_dev_pairs_free(&dp);
+    });
+}
+
 PDB_API void pdb_pairs_free(pdb_pairs* p) {
     if (!p) return;
     std::free(p->left);

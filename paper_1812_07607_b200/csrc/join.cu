@@ -60,12 +60,13 @@ namespace {
 
 constexpr int BM = 128;  // L rows per tile (TMEM lanes)
 constexpr int BN = 256;  // R rows per tile (UMMA N)
-constexpr int BK = 32;   // fp32 per 128-byte swizzle row
+constexpr int BK = 32;   // fp32 per 128-byte swizzle row (64 for bf16)
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
 constexpr int kThreads = 320;         // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr uint32_t kTmemCols = 512;   // two 256-column fp32 accumulators
-constexpr uint32_t kIdesc = ptx::idesc_tf32(BM, BN);
+constexpr uint32_t kIdescTf32 = ptx::idesc_tf32(BM, BN);
+constexpr uint32_t kIdescBf16 = ptx::idesc_bf16(BM, BN);
 
 constexpr float kFlagNonFinite = -1.0f;
 constexpr float kFlagBig = -2.0f;
@@ -83,9 +84,10 @@ struct ScreenParams {
     int64_t n_units;
     int64_t unit_step;  // 1, or S > 1 to screen only every S-th unit (output-size estimate)
     const int64_t* chunk_off;  // [n_chunks + 1]
-    const float* hnL;   // ||x~_i||^2
-    const float* snL;   // ||x~_i|| (rounded up) or a flag
-    const float* gR;    // ||y~_j||^2 / 2, +inf / -inf flags, padded to nt*256
+    const float* hnL;   // L2: ||x~_i||^2;  COS: the row threshold h_i itself
+    const float* snL;   // L2: ||x~_i|| (rounded up) or a flag;  COS: unused
+    const float* gR;    // L2: ||y~_j||^2 / 2 (+inf / -inf flags);  COS: 1/||y_j|| rounded up
+                        // (0 for zero / non-finite rows); padded to nt*256
     const float* tmaxS; // per R tile
     const float* tmaxN;
     double tau_p;       // tau (1 + 1e-9)
@@ -124,12 +126,16 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
 // ---------------------------------------------------------------------------
 // K2: the tensor-core screen.  A_RES: the CTA's 128-row block of L stays
 // resident in shared memory for a whole unit (DP <= 128); otherwise A is
-// streamed with B through the stage ring.
-template <int DP, bool A_RES, int STAGES>
+// streamed with B through the stage ring.  COS: bf16 operands
+// (kind::f16) and the cosine test dot * (1/||y_j||) >= h_i; otherwise tf32
+// operands (kind::tf32) and the L2 test dot - ||y_j||^2/2 >= h_i.  DP is in
+// elements; every K-block is 128 bytes of each row either way.
+template <int DP, bool A_RES, int STAGES, bool COS>
 __global__ void __launch_bounds__(kThreads, 1)
 k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const ScreenParams p) {
-    constexpr int NKB = DP / BK;
+    constexpr int KE = COS ? 64 : 32;  // elements per 128-byte K-block
+    constexpr int NKB = DP / KE;
     constexpr int kStageBytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr int kAResBytes = A_RES ? NKB * kABytes : 0;
 
@@ -187,7 +193,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     a_phase ^= 1;
                     ptx::mbar_arrive_expect_tx(a_full, NKB * kABytes);
                     for (int kb = 0; kb < NKB; kb++)
-                        ptx::tma_load_2d(smA + kb * kABytes, &tmA, a_full, kb * BK, w.rb * BM);
+                        ptx::tma_load_2d(smA + kb * kABytes, &tmA, a_full, kb * KE, w.rb * BM);
                 }
                 for (int J = w.j0; J < w.j1; J++) {
                     for (int kb = 0; kb < NKB; kb++) {
@@ -195,10 +201,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         uint8_t* st = smS + stage * kStageBytes;
                         ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
                         if (!A_RES) {
-                            ptx::tma_load_2d(st, &tmA, &full[stage], kb * BK, w.rb * BM);
+                            ptx::tma_load_2d(st, &tmA, &full[stage], kb * KE, w.rb * BM);
                             st += kABytes;
                         }
-                        ptx::tma_load_2d(st, &tmB, &full[stage], kb * BK, J * BN);
+                        ptx::tma_load_2d(st, &tmB, &full[stage], kb * KE, J * BN);
                         if (++stage == STAGES) {
                             stage = 0;
                             phase ^= 1;
@@ -233,10 +239,16 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                             ptx::smem_u32(A_RES ? smA + kb * kABytes : st);
                         const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
 #pragma unroll
-                        for (int kk = 0; kk < BK / 8; kk++)
-                            ptx::mma_tf32(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
-                                          ptx::sdesc_k_sw128(b_addr + kk * 32), kIdesc,
-                                          (kb | kk) != 0);
+                        for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
+                            if (COS)
+                                ptx::mma_f16(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
+                                             ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescBf16,
+                                             (kb | kk) != 0);
+                            else
+                                ptx::mma_tf32(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
+                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescTf32,
+                                              (kb | kk) != 0);
+                        }
                         ptx::mma_commit(&empty[stage]);
                         if (++stage == STAGES) {
                             stage = 0;
@@ -294,7 +306,9 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
-            if (sn == kFlagNonFinite) {
+            if (COS) {
+                h = row_ok ? hn : __int_as_float(0x7f800000);  // prep stored h_i itself
+            } else if (sn == kFlagNonFinite) {
                 h = __int_as_float(0x7f800000);  // +inf: never a candidate
             } else if (sn == kFlagBig) {
                 h = -__int_as_float(0x7f800000);  // always a candidate
@@ -335,7 +349,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     }
                     float m = -__int_as_float(0x7f800000);
 #pragma unroll
-                    for (int k = 0; k < 32; k++) m = fmaxf(m, __uint_as_float(v[k]) - g[k]);
+                    for (int k = 0; k < 32; k++)
+                        m = fmaxf(m, COS ? __uint_as_float(v[k]) * g[k] : __uint_as_float(v[k]) - g[k]);
                     const bool hit = row_ok && m >= h;
                     if (__any_sync(0xffffffffu, hit)) {
                         const int64_t col0 = colw + c * 32;
@@ -344,8 +359,9 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
 #pragma unroll
                             for (int k = 0; k < 32; k++) {
                                 const int64_t j = col0 + k;
-                                const bool ok = (__uint_as_float(v[k]) - g[k] >= h) && j < p.nR &&
-                                                (!p.self_join || j > i);
+                                const float vk = COS ? __uint_as_float(v[k]) * g[k]
+                                                     : __uint_as_float(v[k]) - g[k];
+                                const bool ok = (vk >= h) && j < p.nR && (!p.self_join || j > i);
                                 mask |= static_cast<uint32_t>(ok) << k;
                             }
                         }
@@ -627,38 +643,141 @@ __global__ void k_unpack_keys(const unsigned long long* __restrict__ keys, int64
 }
 
 // ---------------------------------------------------------------------------
+// Cosine join over bf16 rows (BASELINE config 4; restated, not in the
+// reference).  Contract: cos = dot / (sqrt(na) * sqrt(nb)) >= min_cos with
+// dot, na, nb accumulated sequentially in fp64 over k = 0..d-1 from the
+// exact bf16 values (oracle/pdb_oracle.c orc_cosine_join_bf16).
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+__global__ void k_pad_bf16(const uint16_t* __restrict__ X, int64_t n, int d, int DP,
+                           uint16_t* __restrict__ Xp) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    for (int k = lane; k < DP; k += 32) Xp[row * DP + k] = k < d ? X[row * d + k] : 0;
+}
+
+// One warp per row.  L mode (h != null): h_i = rd(cmarg * ||x_i||), +inf
+// for zero / non-finite rows, -inf when cmarg <= 0.  R mode (g != null,
+// rows up to npad): g_j = ru(1 / ||y_j||), 0 for zero / non-finite rows and
+// padding.
+__global__ void k_prep_cos(const uint16_t* __restrict__ X, int64_t n, int d, double cmarg,
+                           float* __restrict__ h, float* __restrict__ g, int64_t npad) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = h ? n : npad;
+    if (row >= rows) return;
+    double acc = 0.0;
+    bool finite = true;
+    if (row < n) {
+        for (int k = lane; k < d; k += 32) {
+            const float v = bf16_to_f32(X[row * d + k]);
+            if (!isfinite(v)) finite = false;
+            acc += static_cast<double>(v) * static_cast<double>(v);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    finite = __all_sync(0xffffffffu, finite);
+    if (lane) return;
+    const bool valid = row < n && finite && acc > 0.0 && isfinite(acc);
+    const float inf = __int_as_float(0x7f800000);
+    if (h) {
+        if (!valid) h[row] = inf;
+        else if (cmarg <= 0.0) h[row] = -inf;
+        else h[row] = __double2float_rd(cmarg * sqrt(acc));
+    } else {
+        g[row] = valid ? __double2float_ru(1.0 / sqrt(acc)) : 0.0f;
+    }
+}
+
+__device__ __forceinline__ double exact_cos(const uint16_t* __restrict__ a,
+                                            const uint16_t* __restrict__ b, int d) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int k = 0; k < d; k++) {
+        const double x = bf16_to_f32(__ldg(a + k)), y = bf16_to_f32(__ldg(b + k));
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+    }
+    return __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
+}
+
+__global__ void __launch_bounds__(256)
+k_recheck_cos(const int4* __restrict__ rec, const unsigned long long* __restrict__ n_rec,
+              unsigned long long cap, const uint16_t* __restrict__ L,
+              const uint16_t* __restrict__ R, int d, double min_cos, int32_t* __restrict__ out_l,
+              int32_t* __restrict__ out_r, float* __restrict__ out_d, unsigned long long out_cap,
+              unsigned long long* __restrict__ out_count) {
+    const unsigned long long n = min(*n_rec, cap);
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                                   (threadIdx.x & ~31u);
+         base < n; base += stride) {
+        const unsigned long long idx = base + lane;
+        int4 rc = make_int4(0, 0, 0, 0);
+        if (idx < n) rc = rec[idx];
+        uint32_t mask = static_cast<uint32_t>(rc.z);
+        while (__any_sync(0xffffffffu, mask != 0)) {
+            bool ok = false;
+            double cs = 0.0;
+            int j = 0;
+            if (mask) {
+                const int k = __ffs(mask) - 1;
+                mask &= mask - 1;
+                j = rc.y + k;
+                cs = exact_cos(L + static_cast<int64_t>(rc.x) * d, R + static_cast<int64_t>(j) * d, d);
+                ok = cs >= min_cos;
+            }
+            const uint32_t ball = __ballot_sync(0xffffffffu, ok);
+            if (!ball) continue;
+            unsigned long long w = 0;
+            if (lane == 0) w = atomicAdd(out_count, static_cast<unsigned long long>(__popc(ball)));
+            w = __shfl_sync(0xffffffffu, w, 0);
+            if (ok) {
+                const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
+                if (pos < out_cap) {
+                    out_l[pos] = rc.x;
+                    out_r[pos] = j;
+                    out_d[pos] = static_cast<float>(cs);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Host side.
-CUtensorMap make_tmap(const DeviceCtx& ctx, const float* base, int64_t rows, int DP,
-                      int box_rows) {
+CUtensorMap make_tmap(const DeviceCtx& ctx, const void* base, int64_t rows, int DP, int box_rows,
+                      bool bf16) {
     CUtensorMap m;
+    const int es = bf16 ? 2 : 4;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(DP), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(DP) * 4};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(DP) * es};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
-    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = enc(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(PDB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     return m;
 }
 
-struct Prepped {
-    float* Xp;
-    float* hn;
-    float* sn;
-};
-
-template <int DP, bool A_RES, int STAGES>
+template <int DP, bool A_RES, int STAGES, bool COS>
 void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
                    const ScreenParams& p, cudaStream_t s) {
-    constexpr int NKB = DP / BK;
+    constexpr int NKB = DP / (COS ? 64 : 32);
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr size_t smem =
         1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + 4096 + 8 * 32 * 16;
     static_assert(smem <= 232448, "shared memory budget");
-    auto k = k_screen<DP, A_RES, STAGES>;
+    auto k = k_screen<DP, A_RES, STAGES, COS>;
     PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
@@ -666,19 +785,31 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     PDB_CUDA(cudaGetLastError());
 }
 
-void dispatch_screen(int DP, const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
-                     const ScreenParams& p, cudaStream_t s) {
-    switch (DP) {
-        case 32: launch_screen<32, true, 6>(ctx, tA, tB, p, s); break;
-        case 64: launch_screen<64, true, 5>(ctx, tA, tB, p, s); break;
-        case 96: launch_screen<96, true, 4>(ctx, tA, tB, p, s); break;
-        case 128: launch_screen<128, true, 4>(ctx, tA, tB, p, s); break;
-        case 256: launch_screen<256, false, 4>(ctx, tA, tB, p, s); break;
-        case 512: launch_screen<512, false, 4>(ctx, tA, tB, p, s); break;
-        case 1024: launch_screen<1024, false, 4>(ctx, tA, tB, p, s); break;
-        case 2048: launch_screen<2048, false, 4>(ctx, tA, tB, p, s); break;
-        default: fail(PDB_ERR_CONFIG, "similarity join: unsupported padded dimension");
+void dispatch_screen(int DP, bool cos, const DeviceCtx& ctx, const CUtensorMap& tA,
+                     const CUtensorMap& tB, const ScreenParams& p, cudaStream_t s) {
+    if (cos) {
+        switch (DP) {
+            case 64: launch_screen<64, true, 4, true>(ctx, tA, tB, p, s); return;
+            case 128: launch_screen<128, true, 4, true>(ctx, tA, tB, p, s); return;
+            case 256: launch_screen<256, false, 4, true>(ctx, tA, tB, p, s); return;
+            case 512: launch_screen<512, false, 4, true>(ctx, tA, tB, p, s); return;
+            case 1024: launch_screen<1024, false, 4, true>(ctx, tA, tB, p, s); return;
+            case 2048: launch_screen<2048, false, 4, true>(ctx, tA, tB, p, s); return;
+            case 4096: launch_screen<4096, false, 4, true>(ctx, tA, tB, p, s); return;
+        }
+        fail(PDB_ERR_CONFIG, "cosine join: unsupported padded dimension");
     }
+    switch (DP) {
+        case 32: launch_screen<32, true, 6, false>(ctx, tA, tB, p, s); return;
+        case 64: launch_screen<64, true, 5, false>(ctx, tA, tB, p, s); return;
+        case 96: launch_screen<96, true, 4, false>(ctx, tA, tB, p, s); return;
+        case 128: launch_screen<128, true, 4, false>(ctx, tA, tB, p, s); return;
+        case 256: launch_screen<256, false, 4, false>(ctx, tA, tB, p, s); return;
+        case 512: launch_screen<512, false, 4, false>(ctx, tA, tB, p, s); return;
+        case 1024: launch_screen<1024, false, 4, false>(ctx, tA, tB, p, s); return;
+        case 2048: launch_screen<2048, false, 4, false>(ctx, tA, tB, p, s); return;
+    }
+    fail(PDB_ERR_CONFIG, "similarity join: unsupported padded dimension");
 }
 
 // Resident-A variants for d <= 128; beyond that A streams with B and the
@@ -687,6 +818,15 @@ int padded_dim(int d) {
     if (d <= 32) return 32;
     if (d <= 64) return 64;
     if (d <= 96) return 96;
+    if (d <= 128) return 128;
+    int DP = 256;
+    while (DP < d) DP *= 2;
+    return DP;
+}
+
+// bf16: K-blocks of 64 elements; resident A up to 128, then powers of two.
+int padded_dim_bf16(int d) {
+    if (d <= 64) return 64;
     if (d <= 128) return 128;
     int DP = 256;
     while (DP < d) DP *= 2;
@@ -717,6 +857,159 @@ struct PhaseTimer {
         return t;
     }
 };
+
+// Work units (column chunk c, row block rb), chunk-major, for this shard.
+struct UnitPlan {
+    DevBuf<int64_t> off;
+    int ch = 1, nt = 0, n_chunks = 0;
+    int64_t n_units = 0;
+};
+
+void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, int shard,
+                cudaStream_t s, UnitPlan& u) {
+    u.nt = static_cast<int>(ceil_div(nR, BN));
+    const int64_t n_rb = ceil_div(nL, BM);
+    double total_tiles = 0;
+    for (int64_t rb = 0; rb < n_rb; rb++)
+        total_tiles += self ? static_cast<double>(u.nt - (rb >> 1)) : static_cast<double>(u.nt);
+    total_tiles /= P;
+    u.ch = static_cast<int>(std::clamp<double>(total_tiles / (8.0 * ctx.sm_count), 1.0, 64.0));
+    u.n_chunks = static_cast<int>(ceil_div(u.nt, u.ch));
+    std::vector<int64_t> off(static_cast<size_t>(u.n_chunks) + 1, 0);
+    for (int c = 0; c < u.n_chunks; c++) {
+        int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
+        if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * u.ch);
+        // blocks k*P + pos(k) < lim, pos(k) = shard (k even) / P-1-shard (k odd)
+        const int64_t full = lim / P, rem = lim % P;
+        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
+        off[c + 1] = off[c] + full + (pos_last < rem ? 1 : 0);
+    }
+    u.n_units = off[u.n_chunks];
+    u.off.reset(off.size(), s);
+    PDB_CUDA(cudaMemcpyAsync(u.off.p, off.data(), off.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+}
+
+// The shared back half of both joins: screen (with a sampled output-size
+// estimate for large problems), exact re-check, one counter read-back,
+// overflow handling, optional sort, stats.  `recheck(recs, cap, out)`
+// enqueues the mode's re-check kernel.
+template <class Recheck>
+void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
+                        const CUtensorMap& tA, const CUtensorMap& tB, ScreenParams p,
+                        int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
+                        pdb_join_stats* stats, PhaseTimer& tm, int launches, Recheck&& recheck) {
+    DevBuf<unsigned long long> counters(4, s);  // [records, tiles, pairs, candidates]
+    unsigned long long cap = static_cast<unsigned long long>(
+        std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
+    unsigned long long out_need = static_cast<unsigned long long>(
+        std::max<int64_t>(1 << 20, 4 * (nL + nR)));
+    unsigned long long h_cnt[4] = {0, 0, 0, 0};
+    DevBuf<int4> recs;
+    int passes = 0;
+    auto ensure_out = [&](unsigned long long need) {
+        if (static_cast<unsigned long long>(out->capacity) >= need && out->left) return;
+        if (out->left) pdb_dev_pairs_free(out);
+        const int64_t c = static_cast<int64_t>(need);
+        out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
+        out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
+        out->capacity = c;
+    };
+    auto read_counters = [&] {
+        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    };
+    auto arm = [&] {
+        p.rec = recs.p;
+        p.cap = cap;
+        p.counter = counters.p;
+        p.tiles = counters.p + 1;
+        p.ncand = counters.p + 3;
+        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
+    };
+    p.unit_step = 1;
+    tm.mark(1);
+    // Large problems: screen every 64th work unit first and size the record
+    // and output buffers from that sample, so a heavy output (config 5:
+    // ~1.4e9 candidates) does not cost a second full screen pass.
+    constexpr int64_t kSampleStep = 64;
+    if (p.n_units >= kSampleStep * ctx.sm_count) {
+        recs.reset(cap, s);
+        arm();
+        p.unit_step = kSampleStep;
+        dispatch_screen(DP, cos, ctx, tA, tB, p, s);
+        launches++;
+        read_counters();
+        p.unit_step = 1;
+        const double scale = static_cast<double>(kSampleStep) * 1.3;
+        cap = std::max(cap, static_cast<unsigned long long>(h_cnt[0] * scale) + (1 << 20));
+        out_need = std::max(out_need, static_cast<unsigned long long>(h_cnt[3] * scale) + (1 << 20));
+    }
+    // Screen and re-check run back to back and the host reads the counters
+    // once.  A record overflow re-runs the screen with the exact record
+    // count; an output overflow re-runs only the re-check.
+    for (int attempt = 0; attempt < 2; attempt++) {
+        recs.reset(cap, s);
+        ensure_out(out_need);
+        arm();
+        if (p.n_units > 0) {
+            dispatch_screen(DP, cos, ctx, tA, tB, p, s);
+            launches++;
+        }
+        tm.mark(2);
+        recheck(recs.p, counters.p, cap, out);
+        launches++;
+        tm.mark(3);
+        passes++;
+        read_counters();
+        if (h_cnt[0] <= cap) break;
+        cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
+        out_need = std::max(out_need, h_cnt[3]);
+    }
+    if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
+        ensure_out(h_cnt[2]);
+        PDB_CUDA(cudaMemsetAsync(counters.p + 2, 0, sizeof(unsigned long long), s));
+        recheck(recs.p, counters.p, cap, out);
+        launches++;
+        tm.mark(3);
+        read_counters();
+    }
+    const unsigned long long n_cand = h_cnt[3];
+    const unsigned long long n_pairs = h_cnt[2];
+    out->count = static_cast<int64_t>(n_pairs);
+
+    if ((o.flags & PDB_JOIN_SORTED) && n_pairs > 1) {
+        const int64_t n = static_cast<int64_t>(n_pairs);
+        DevBuf<unsigned long long> k_in(n, s), k_out(n, s);
+        DevBuf<float> v_out(n, s);
+        k_pack_keys<<<592, 256, 0, s>>>(out->left, out->right, n, k_in.p);
+        size_t tmp_bytes = 0;
+        PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in.p, k_out.p, out->dist,
+                                                 v_out.p, n, 0, 64, s));
+        DevBuf<uint8_t> tmp(tmp_bytes, s);
+        PDB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k_in.p, k_out.p, out->dist,
+                                                 v_out.p, n, 0, 64, s));
+        k_unpack_keys<<<592, 256, 0, s>>>(k_out.p, n, out->left, out->right);
+        PDB_CUDA(cudaMemcpyAsync(out->dist, v_out.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        PDB_CUDA(cudaGetLastError());
+        launches += 4;  // pack, 2 cub passes (upper bound), unpack
+    }
+    tm.mark(4);
+    if (stats) {
+        stats->candidates = static_cast<int64_t>(n_cand);
+        stats->pairs = static_cast<int64_t>(n_pairs);
+        stats->tiles = static_cast<int64_t>(h_cnt[1]);
+        stats->candidate_capacity = static_cast<int64_t>(cap) * 32;
+        stats->launches = launches;
+        stats->screen_passes = passes;
+        stats->prep_ms = tm.ms(0, 1);
+        stats->screen_ms = tm.ms(1, 2);
+        stats->recheck_ms = tm.ms(2, 3);
+        stats->sort_ms = tm.ms(3, 4);
+    }
+}
 
 }  // namespace
 
@@ -768,52 +1061,27 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         hnR = hnR_own.p;
         snR = snR_own.p;
     }
-    const int nt = static_cast<int>(ceil_div(nR, BN));
+    UnitPlan plan;
+    plan_units(ctx, nL, nR, self, P, shard, s, plan);
+    const int nt = plan.nt;
     DevBuf<float> gR(static_cast<size_t>(nt) * BN, s), tmaxS(nt, s), tmaxN(nt, s);
     k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR.p, tmaxS.p, tmaxN.p);
     PDB_CUDA(cudaGetLastError());
     launches++;
 
-    // ---- work units: (column chunk c, row block rb), chunk-major ----------
-    const int64_t n_rb = ceil_div(nL, BM);
-    double total_tiles = 0;
-    for (int64_t rb = 0; rb < n_rb; rb++)
-        total_tiles += self ? static_cast<double>(nt - (rb >> 1)) : static_cast<double>(nt);
-    total_tiles /= P;
-    int ch = static_cast<int>(std::clamp<double>(total_tiles / (8.0 * ctx.sm_count), 1.0, 64.0));
-    const int n_chunks = static_cast<int>(ceil_div(nt, ch));
-    std::vector<int64_t> off(static_cast<size_t>(n_chunks) + 1, 0);
-    for (int c = 0; c < n_chunks; c++) {
-        int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
-        if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * ch);
-        // blocks k*P + pos(k) < lim, pos(k) = shard (k even) / P-1-shard (k odd)
-        const int64_t full = lim / P, rem = lim % P;
-        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
-        const int64_t cnt = full + (pos_last < rem ? 1 : 0);
-        off[c + 1] = off[c] + cnt;
-    }
-    const int64_t n_units = off[n_chunks];
-    DevBuf<int64_t> d_off(off.size(), s);
-    PDB_CUDA(cudaMemcpyAsync(d_off.p, off.data(), off.size() * sizeof(int64_t),
-                             cudaMemcpyHostToDevice, s));
-
-    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM);
-    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN);
-
-    DevBuf<unsigned long long> counters(4, s);  // [records, tiles, pairs, candidates]
-    unsigned long long cap = static_cast<unsigned long long>(
-        std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
+    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM, false);
+    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, false);
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;
     p.self_join = self;
     p.shard_index = shard;
     p.shard_count = P;
-    p.ch = ch;
+    p.ch = plan.ch;
     p.nt = nt;
-    p.n_chunks = n_chunks;
-    p.n_units = n_units;
-    p.chunk_off = d_off.p;
+    p.n_chunks = plan.n_chunks;
+    p.n_units = plan.n_units;
+    p.chunk_off = plan.off.p;
     p.hnL = hnL.p;
     p.snL = snL.p;
     p.gR = gR.p;
@@ -821,124 +1089,97 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tmaxN = tmaxN.p;
     p.tau_p = tau * (1.0 + 1e-9);
     p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
+    screen_and_recheck(ctx, s, DP, false, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+                       [&](const int4* recs, unsigned long long* counters,
+                           unsigned long long cap, pdb_dev_pairs* o2) {
+                           k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
+                               recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
+                               o2->dist, static_cast<unsigned long long>(o2->capacity),
+                               counters + 2);
+                           PDB_CUDA(cudaGetLastError());
+                       });
+}
 
-    // Screen and re-check run back to back and the host reads the counters
-    // (records, tiles, pairs, candidates) once.  A record overflow re-runs
-    // the screen with the exact record count; an output overflow re-runs
-    // only the re-check into a larger buffer.
-    unsigned long long h_cnt[4] = {0, 0, 0, 0};
-    DevBuf<int4> recs;
-    int passes = 0;
-    unsigned long long out_need = static_cast<unsigned long long>(
-        std::max<int64_t>(1 << 20, 4 * (nL + nR)));
-    auto ensure_out = [&](unsigned long long need) {
-        if (static_cast<unsigned long long>(out->capacity) >= need && out->left) return;
-        if (out->left) pdb_dev_pairs_free(out);
-        const int64_t c = static_cast<int64_t>(need);
-        out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
-        out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
-        out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
-        out->capacity = c;
-    };
-    auto recheck = [&] {
-        k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
-            recs.p, counters.p, cap, d_L, d_R, d, tau, out->left, out->right, out->dist,
-            static_cast<unsigned long long>(out->capacity), counters.p + 2);
-        PDB_CUDA(cudaGetLastError());
-        launches++;
-    };
-    auto read_counters = [&] {
-        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-        PDB_CUDA(cudaStreamSynchronize(s));
-    };
-    p.unit_step = 1;
-    tm.mark(1);
-    // Large problems: screen every 64th work unit first and size the record
-    // and output buffers from that sample, so a heavy output (config 5:
-    // ~1.4e9 candidates) does not cost a second full screen pass.
-    constexpr int64_t kSampleStep = 64;
-    if (n_units >= kSampleStep * ctx.sm_count) {
-        recs.reset(cap, s);
-        p.rec = recs.p;
-        p.cap = cap;
-        p.counter = counters.p;
-        p.tiles = counters.p + 1;
-        p.ncand = counters.p + 3;
-        p.unit_step = kSampleStep;
-        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
-        dispatch_screen(DP, ctx, tA, tB, p, s);
-        launches++;
-        read_counters();
-        p.unit_step = 1;
-        const double scale = static_cast<double>(kSampleStep) * 1.3;
-        const unsigned long long est_rec = static_cast<unsigned long long>(h_cnt[0] * scale) + (1 << 20);
-        const unsigned long long est_cand = static_cast<unsigned long long>(h_cnt[3] * scale) + (1 << 20);
-        cap = std::max(cap, est_rec);
-        out_need = std::max(out_need, est_cand);
+void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int64_t nR,
+                      int32_t d, double min_cos, const pdb_join_opts& o, pdb_dev_pairs* out,
+                      pdb_join_stats* stats) {
+    const DeviceCtx& ctx = device_ctx();
+    cudaStream_t s = static_cast<cudaStream_t>(o.stream);
+    const bool self = (o.flags & PDB_JOIN_SELF) != 0;
+    if (self) {
+        d_R = d_L;
+        nR = nL;
     }
-    for (int attempt = 0; attempt < 2; attempt++) {
-        recs.reset(cap, s);
-        ensure_out(out_need);
-        p.rec = recs.p;
-        p.cap = cap;
-        p.counter = counters.p;
-        p.tiles = counters.p + 1;
-        p.ncand = counters.p + 3;
-        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
-        if (n_units > 0) {
-            dispatch_screen(DP, ctx, tA, tB, p, s);
+    const int P = o.shard_count > 1 ? o.shard_count : 1;
+    const int shard = o.shard_count > 1 ? o.shard_index : 0;
+    if (stats) *stats = pdb_join_stats{};
+    out->count = 0;
+    if (nL == 0 || nR == 0) return;
+    PhaseTimer tm(stats != nullptr, s);
+    int launches = 0;
+    tm.mark(0);
+    const int DP = padded_dim_bf16(d);
+    if (DP > 4096) fail(PDB_ERR_CONFIG, "cosine join: d > 4096 is not supported by this build");
+    // Screen threshold on the cosine: c' - margin with c' = c - 1e-9 (the
+    // fp64 reference's rounding) and margin = DP 2^-23 (fp32 accumulation of
+    // exact bf16 products, relative to ||x|| ||y||) + 2^-20 (epilogue
+    // roundings).  A threshold at or below 0 makes every pair a candidate.
+    const double cmarg = min_cos - 1e-9 - (DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -20));
+    // The MMA reads the original rows when they already are a whole number
+    // of 64-element K-blocks; otherwise through a zero-padded copy.
+    const bool direct = d == DP && reinterpret_cast<uintptr_t>(d_L) % 16 == 0 &&
+                        reinterpret_cast<uintptr_t>(d_R) % 16 == 0;
+    DevBuf<uint16_t> padL, padR;
+    const uint16_t *XL = d_L, *XR = d_R;
+    if (!direct) {
+        padL.reset(static_cast<size_t>(nL) * DP, s);
+        k_pad_bf16<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, DP, padL.p);
+        launches++;
+        XL = padL.p;
+        if (!self) {
+            padR.reset(static_cast<size_t>(nR) * DP, s);
+            k_pad_bf16<<<static_cast<unsigned>(ceil_div(nR * 32, 256)), 256, 0, s>>>(d_R, nR, d, DP, padR.p);
             launches++;
+            XR = padR.p;
+        } else {
+            XR = XL;
         }
-        tm.mark(2);
-        recheck();
-        tm.mark(3);
-        passes++;
-        read_counters();
-        if (h_cnt[0] <= cap) break;
-        cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
-        out_need = std::max(out_need, h_cnt[3]);
-    }
-    if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
-        ensure_out(h_cnt[2]);
-        PDB_CUDA(cudaMemsetAsync(counters.p + 2, 0, sizeof(unsigned long long), s));
-        recheck();
-        tm.mark(3);
-        read_counters();
-    }
-    const unsigned long long n_cand = h_cnt[3];
-    const unsigned long long n_pairs = h_cnt[2];
-    out->count = static_cast<int64_t>(n_pairs);
-
-    if ((o.flags & PDB_JOIN_SORTED) && n_pairs > 1) {
-        const int64_t n = static_cast<int64_t>(n_pairs);
-        DevBuf<unsigned long long> k_in(n, s), k_out(n, s);
-        DevBuf<float> v_out(n, s);
-        k_pack_keys<<<592, 256, 0, s>>>(out->left, out->right, n, k_in.p);
-        size_t tmp_bytes = 0;
-        PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in.p, k_out.p, out->dist,
-                                                 v_out.p, n, 0, 64, s));
-        DevBuf<uint8_t> tmp(tmp_bytes, s);
-        PDB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k_in.p, k_out.p, out->dist,
-                                                 v_out.p, n, 0, 64, s));
-        k_unpack_keys<<<592, 256, 0, s>>>(k_out.p, n, out->left, out->right);
-        PDB_CUDA(cudaMemcpyAsync(out->dist, v_out.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
         PDB_CUDA(cudaGetLastError());
-        launches += 4;  // pack, 2 cub passes (upper bound), unpack
     }
-    tm.mark(4);
-    if (stats) {
-        stats->candidates = static_cast<int64_t>(n_cand);
-        stats->pairs = static_cast<int64_t>(n_pairs);
-        stats->tiles = static_cast<int64_t>(h_cnt[1]);
-        stats->candidate_capacity = static_cast<int64_t>(cap) * 32;
-        stats->launches = launches;
-        stats->screen_passes = passes;
-        stats->prep_ms = tm.ms(0, 1);
-        stats->screen_ms = tm.ms(1, 2);
-        stats->recheck_ms = tm.ms(2, 3);
-        stats->sort_ms = tm.ms(3, 4);
-    }
+    UnitPlan plan;
+    plan_units(ctx, nL, nR, self, P, shard, s, plan);
+    const int nt = plan.nt;
+    DevBuf<float> hL(nL, s), gR(static_cast<size_t>(nt) * BN, s);
+    k_prep_cos<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, cmarg, hL.p,
+                                                                            nullptr, 0);
+    k_prep_cos<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(nt) * BN * 32, 256)), 256, 0, s>>>(
+        d_R, nR, d, cmarg, nullptr, gR.p, static_cast<int64_t>(nt) * BN);
+    PDB_CUDA(cudaGetLastError());
+    launches += 2;
+    const CUtensorMap tA = make_tmap(ctx, XL, nL, DP, BM, true);
+    const CUtensorMap tB = make_tmap(ctx, XR, nR, DP, BN, true);
+    ScreenParams p{};
+    p.nL = nL;
+    p.nR = nR;
+    p.self_join = self;
+    p.shard_index = shard;
+    p.shard_count = P;
+    p.ch = plan.ch;
+    p.nt = nt;
+    p.n_chunks = plan.n_chunks;
+    p.n_units = plan.n_units;
+    p.chunk_off = plan.off.p;
+    p.hnL = hL.p;
+    p.gR = gR.p;
+    screen_and_recheck(ctx, s, DP, true, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+                       [&](const int4* recs, unsigned long long* counters,
+                           unsigned long long cap, pdb_dev_pairs* o2) {
+                           k_recheck_cos<<<ctx.sm_count * 16, 256, 0, s>>>(
+                               recs, counters, cap, d_L, d_R, d, min_cos, o2->left, o2->right,
+                               o2->dist, static_cast<unsigned long long>(o2->capacity),
+                               counters + 2);
+                           PDB_CUDA(cudaGetLastError());
+                       });
 }
 
 }  // namespace pdb

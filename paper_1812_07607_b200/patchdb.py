@@ -204,6 +204,37 @@ def sim_join(L: np.ndarray, R: Optional[np.ndarray], tau: float, *, self_join: b
     return JoinResult(left, right, dist)
 
 
+def _pairs_to_result(pr) -> JoinResult:
+    try:
+        n = int(pr.count)
+        if n:
+            return JoinResult(np.ctypeslib.as_array(pr.left, shape=(n,)).copy(),
+                              np.ctypeslib.as_array(pr.right, shape=(n,)).copy(),
+                              np.ctypeslib.as_array(pr.dist, shape=(n,)).copy())
+        return JoinResult(np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0, np.float32))
+    finally:
+        capi.lib().pdb_pairs_free(C.byref(pr))
+
+
+def cosine_join_bf16(L: np.ndarray, R: Optional[np.ndarray], min_cos: float, *,
+                     self_join: bool = False, sort: bool = True,
+                     shard: Tuple[int, int] = (0, 1)) -> JoinResult:
+    """Cosine threshold join over bf16 rows given as uint16 bit patterns
+    [n, d] (BASELINE config 4, restated).  ``dist`` = fp32(cos)."""
+    L = np.ascontiguousarray(L, dtype=np.uint16)
+    R_ = L if self_join else np.ascontiguousarray(R, dtype=np.uint16)
+    if L.ndim != 2 or R_.ndim != 2:
+        raise ShapeError("L and R must be [n, d] uint16 (bf16 bits)")
+    if not self_join and L.shape[0] and R_.shape[0] and L.shape[1] != R_.shape[1]:
+        raise DimensionMismatchError(
+            f"cosine join over {L.shape[1]} and {R_.shape[1]} dimensional sides")
+    o = _opts(self_join, sort, shard)
+    pr = capi.Pairs()
+    _check(capi.lib().pdb_cosine_join_bf16(capi.ptr(L), L.shape[0], capi.ptr(R_), R_.shape[0],
+                                           L.shape[1], float(min_cos), C.byref(o), C.byref(pr)))
+    return _pairs_to_result(pr)
+
+
 class DevicePairs:
     """Device-resident join output, reusable across calls (pdb_dev_pairs)."""
 
@@ -247,6 +278,26 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
                                          "data": (int(ptr_), False), "version": 3,
                                          "strides": None}
+
+
+def cosine_join_bf16_device(L, R, min_cos: float, *, self_join: bool = False, sort: bool = False,
+                            shard: Tuple[int, int] = (0, 1), out: Optional["DevicePairs"] = None,
+                            stream=None) -> "DevicePairs":
+    """Device cosine join on CUDA bf16 torch tensors; the result stays in HBM."""
+    import torch
+    assert L.is_cuda and L.dtype == torch.bfloat16 and L.is_contiguous()
+    nL, d = int(L.shape[0]), int(L.shape[1])
+    if self_join or R is None:
+        Rp, nR = L.data_ptr(), nL
+    else:
+        assert R.is_cuda and R.dtype == torch.bfloat16 and R.is_contiguous()
+        Rp, nR = R.data_ptr(), int(R.shape[0])
+    s = stream if stream is not None else torch.cuda.current_stream(L.device)
+    o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream))
+    res = out if out is not None else DevicePairs()
+    _check(capi.lib().pdb_cosine_join_bf16_dev(L.data_ptr(), nL, Rp, nR, d, float(min_cos),
+                                               C.byref(o), C.byref(res._p), C.byref(res.stats)))
+    return res
 
 
 def sim_join_device(L, R, tau: float, *, self_join: bool = False, sort: bool = False,

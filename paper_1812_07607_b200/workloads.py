@@ -103,3 +103,38 @@ def config5(n: int = 4_194_304, seed: int = 5) -> np.ndarray:
 
 CONFIG2 = dict(frames=1000, H=480, W=640, tile_h=60, tile_w=80, bins=4, mode="joint",
                tau=0.05, seed=2)
+
+
+def config4(n: int = 200_000, d: int = 2048, seed: int = 4, plant_frac: float = 0.005,
+            plant_sigma: float = 0.2, device: str = "cpu"):
+    """Config 4: e = normalize(ReLU(P z)) stored as bf16, z ~ N(0,1)^d, P a
+    fixed seeded d x d N(0,1)/sqrt(d) projection (torch's seeded CPU
+    generator).  Independent ReLU'd projections sit near cosine ~0.3, so as
+    stated the join would be empty; a fraction `plant_frac` of rows are
+    therefore near-duplicates (z_i = z_src + plant_sigma * N(0,1)) to make
+    the cos >= 0.95 parity check non-vacuous.  Returns a [n, d] torch bf16
+    tensor on `device` (the product reads it; the oracle reads its uint16
+    bits via .view(torch.int16))."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    P = torch.randn(d, d, generator=g) / d ** 0.5
+    Z = torch.randn(n, d, generator=g)
+    k = int(n * plant_frac)
+    if k:
+        dst = torch.randperm(n, generator=g)[:k]
+        src = torch.randint(0, n, (k,), generator=g)
+        Z[dst] = Z[src] + plant_sigma * torch.randn(k, d, generator=g)
+    P, Z = P.to(device), Z.to(device)
+    out = torch.empty((n, d), dtype=torch.bfloat16, device=device)
+    step = 16384
+    for a in range(0, n, step):
+        e = torch.relu(Z[a:a + step] @ P.T)
+        e = e / e.norm(dim=1, keepdim=True).clamp_min(1e-30)
+        out[a:a + step] = e.to(torch.bfloat16)
+    return out
+
+
+def bf16_bits(t) -> np.ndarray:
+    """uint16 bit patterns of a bf16 torch tensor (host numpy)."""
+    import torch
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)

@@ -23,6 +23,9 @@ elif which.startswith("c5"):   # config 5 (optionally scaled: c5:<n>)
     n5 = int(which.split(":")[1]) if ":" in which else 4_194_304
     X = torch.from_numpy(workloads.config5(n5)).cuda()
     R, tau, self_join = None, 0.01, True
+elif which == "c4":
+    X = workloads.config4(device="cuda")
+    R, tau, self_join = None, 0.95, True
 out = patchdb.DevicePairs()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 n = X.shape[0]
@@ -30,7 +33,10 @@ pairs = n * (n - 1) / 2 if self_join else n * R.shape[0]
 for k in range(6):
     flush.zero_()
     torch.cuda.synchronize()
-    patchdb.sim_join_device(X, R, tau, self_join=self_join, out=out)
+    if which == "c4":
+        patchdb.cosine_join_bf16_device(X, R, tau, self_join=self_join, out=out)
+    else:
+        patchdb.sim_join_device(X, R, tau, self_join=self_join, out=out)
     st = out.stats
     if k >= 2:
         print(f"{which}: pairs={st.pairs} cand={st.candidates} tiles={st.tiles} prep={st.prep_ms:.3f} "
