@@ -215,8 +215,9 @@ def run_ours(args, rank, world, local_rank):
     from paper_1812_07607_b200 import _capi as capi
     from paper_1812_07607_b200 import patchdb, workloads
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     lib = capi.lib()
     F, H, W, th, tw, B = (CFG[k] for k in ("frames", "H", "W", "tile_h", "tile_w", "bins"))
     tau = CFG["tau"]
@@ -253,7 +254,13 @@ def run_ours(args, rank, world, local_rank):
 
     def gather():
         if world > 1:
-            dist.all_gather_into_tensor(feats, my_feats)
+            if dist.get_backend() == "nccl":
+                dist.all_gather_into_tensor(feats, my_feats)
+            else:  # gloo (multi-rank smoke on one GPU): list all-gather
+                parts = list(feats.split(my_feats.shape[0]))
+                dist.all_gather(parts, my_feats)
+                for k, part in enumerate(parts):
+                    feats[k * my_feats.shape[0]:(k + 1) * my_feats.shape[0]].copy_(part)
 
     def join():
         rc = lib.pdb_sim_join_dev(feats.data_ptr(), n_tiles, feats.data_ptr(), n_tiles, D, tau,
@@ -293,7 +300,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step(False)
     # clocks are sampled across both timed regions (device steps and e2e)
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     sampler.__enter__()
     for _ in range(args.steps):
         step(True)
@@ -309,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
     ms_join = maxred(statistics.mean(rec["join"]))
     ms_screen = maxred(statistics.mean(rec["screen"]))
     ms_recheck = maxred(statistics.mean(rec["recheck"]))
+    ms_gather = maxred(statistics.mean(rec["gather"]))
+    ms_prep = maxred(statistics.mean(rec["prep"]))
     n_pairs_local = pairs.count
     tot = torch.tensor([n_pairs_local, pairs.stats.candidates], dtype=torch.int64, device=dev)
     if world > 1:
@@ -412,8 +421,8 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"frames sharded x{world}, features all-gathered, join row-blocks cyclic x{world}"},
             "join_gpairs_per_s": pairs_cand / (ms_join * 1e-3) / 1e9,
             "featurize_frames_per_s": F / (ms_feat * 1e-3),
-            "phase_ms": {"featurize": ms_feat, "gather": maxred(statistics.mean(rec["gather"])),
-                         "join": ms_join, "join_prep": maxred(statistics.mean(rec["prep"])),
+            "phase_ms": {"featurize": ms_feat, "gather": ms_gather,
+                         "join": ms_join, "join_prep": ms_prep,
                          "join_screen": ms_screen, "join_recheck": ms_recheck},
             "pairs": n_pairs, "candidates": n_cand,
             "roofline": dominant, "roofline_all": [rl_feat, rl_screen],
@@ -448,8 +457,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_index = local_rank % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev_index)
+        # PDB_DIST_BACKEND=gloo runs the multi-rank code path on fewer GPUs
+        # than ranks (host collectives; kernels of different ranks never wait
+        # on one another).  Real runs use NCCL, one process per GPU.
+        backend = os.environ.get("PDB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     try:
         return run_ours(args, rank, world, local_rank)
     finally:

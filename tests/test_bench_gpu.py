@@ -1,0 +1,46 @@
+"""bench.py contract on the B200: one JSON line with the driver's keys, and
+the multi-rank path (torchrun, 2 ranks; gloo so both ranks may share the one
+GPU of this box) finds the same pairs as one rank."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+        "gpu_launches", "clocks"}
+
+
+def _run(cmd, env=None):
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, **(env or {})})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_json_contract_one_gpu():
+    d = _run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    assert KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["bound"] in ("hbm", "tensor") and 0 < d["roofline"]["frac"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 1000 * 480 * 640 * 3
+    assert d["pairs"] > 0
+    _run.one = d
+
+
+def test_bench_two_ranks_same_pairs():
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+              "--steps", "2", "--warmup", "3"], env={"PDB_DIST_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2
+    one = getattr(_run, "one", None) or _run([sys.executable, "bench.py", "--steps", "3",
+                                              "--warmup", "3", "--no-cpu-baseline"])
+    assert d["pairs"] == one["pairs"]
