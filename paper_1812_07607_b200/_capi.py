@@ -14,7 +14,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdb_cuda.so")
+# PDB_CUDA_LIB points at an alternative build (kernel-variant experiments).
+LIB_PATH = os.environ.get("PDB_CUDA_LIB") or os.path.join(_HERE, "libpdb_cuda.so")
 GEN_PATH = os.path.join(_HERE, "libpdb_gen.so")
 
 PDB_OK = 0

@@ -48,7 +48,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "pdb_internal.cuh"
@@ -63,7 +65,13 @@ constexpr int BN = 256;  // R rows per tile (UMMA N)
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row (64 for bf16)
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
-constexpr int kThreads = 320;         // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+#ifndef PDB_EPI_WARPS
+#define PDB_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = PDB_EPI_WARPS;             // epilogue warps (multiple of 4)
+constexpr int kColsPerWarp = BN / (kEpiWarps / 4);   // accumulator columns per epilogue warp
+constexpr int kChunks = kColsPerWarp / 32;           // 32-column TMEM loads per warp per tile
+constexpr int kThreads = 64 + 32 * kEpiWarps;        // warp 0 TMA, warp 1 MMA, then epilogue
 constexpr uint32_t kTmemCols = 512;   // two 256-column fp32 accumulators
 constexpr uint32_t kIdescTf32 = ptx::idesc_tf32(BM, BN);
 constexpr uint32_t kIdescBf16 = ptx::idesc_bf16(BM, BN);
@@ -97,6 +105,7 @@ struct ScreenParams {
     unsigned long long* counter;  // records written
     unsigned long long* ncand;    // candidate pairs (popc of the masks)
     unsigned long long* tiles;
+    unsigned long long* next_unit;  // dynamic work-unit counter (zeroed per launch)
 };
 
 struct Unit {
@@ -152,8 +161,13 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     uint64_t* t_full = a_full + 2;   // [2]
     uint64_t* t_empty = a_full + 4;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
-    float* g_smem = reinterpret_cast<float*>(a_full + 8);  // [8 warps][128]
-    int4* r_smem = reinterpret_cast<int4*>(g_smem + 8 * (BN / 2));  // [8 warps][32] record staging
+    float* g_smem = reinterpret_cast<float*>(a_full + 8);  // [epilogue warps][kColsPerWarp]
+    int4* r_smem = reinterpret_cast<int4*>(g_smem + kEpiWarps * kColsPerWarp);  // [warps][32] records
+    // dynamic scheduler: the producer claims work units with one global
+    // atomic and hands them to the MMA and epilogue warps through a 4-slot ring
+    uint64_t* u_full = reinterpret_cast<uint64_t*>(r_smem + kEpiWarps * 32);
+    uint64_t* u_empty = u_full + 4;
+    volatile int64_t* u_val = reinterpret_cast<volatile int64_t*>(u_full + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -166,7 +180,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         ptx::mbar_init(a_empty, 1);
         for (int a = 0; a < 2; a++) {
             ptx::mbar_init(&t_full[a], 1);
-            ptx::mbar_init(&t_empty[a], 8);
+            ptx::mbar_init(&t_empty[a], kEpiWarps);
+        }
+        for (int k = 0; k < 4; k++) {
+            ptx::mbar_init(&u_full[k], 1);
+            ptx::mbar_init(&u_empty[k], 1 + kEpiWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -179,14 +197,39 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // consumer side of the unit ring (MMA warp: lane 0 only; epilogue: whole warp)
+    int u_slot = 0;
+    uint32_t u_phase = 0;
+    auto take_unit = [&](bool whole_warp) -> int64_t {
+        ptx::mbar_wait(&u_full[u_slot], u_phase);
+        const int64_t u = u_val[u_slot];
+        if (whole_warp) __syncwarp();
+        if (!whole_warp || lane == 0) ptx::mbar_arrive(&u_empty[u_slot]);
+        if (++u_slot == 4) {
+            u_slot = 0;
+            u_phase ^= 1;
+        }
+        return u;
+    };
 
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
-            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
-                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
+            int ps = 0;
+            uint32_t pph = 0;
+            for (;;) {
+                int64_t u = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
+                if (u >= p.n_units) u = -1;
+                ptx::mbar_wait(&u_empty[ps], pph ^ 1);
+                u_val[ps] = u;
+                ptx::mbar_arrive(&u_full[ps]);
+                if (++ps == 4) {
+                    ps = 0;
+                    pph ^= 1;
+                }
+                if (u < 0) break;
                 const Unit w = decode_unit(p, u);
                 if (A_RES) {
                     ptx::mbar_wait(a_empty, a_phase ^ 1);
@@ -219,8 +262,9 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0, a_phase = 0;
             unsigned long long ntiles = 0;
-            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
-                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
+            for (;;) {
+                const int64_t u = take_unit(false);
+                if (u < 0) break;
                 const Unit w = decode_unit(p, u);
                 if (A_RES) {
                     ptx::mbar_wait(a_full, a_phase);
@@ -275,10 +319,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         // so the next tcgen05.ld overlaps the current chunk's arithmetic.
         const int ew = warp - 2;
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int half = ew >> 2;
+        const int half = ew >> 2;  // which kColsPerWarp-wide column slice
         const int row = q * 32 + lane;
         const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
-        float* gs = g_smem + ew * (BN / 2);
+        float* gs = g_smem + ew * kColsPerWarp;
         int4* rbuf = r_smem + ew * 32;
         uint32_t nbuf = 0;                 // staged records (warp-uniform)
         unsigned long long ncand = 0;      // this lane's candidate pairs
@@ -294,15 +338,17 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         };
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.unit_step; u < p.n_units;
-                 u += static_cast<int64_t>(gridDim.x) * p.unit_step) {
+        for (;;) {
+            const int64_t u = take_unit(true);
+            if (u < 0) break;
             const Unit w = decode_unit(p, u);
             const int64_t i = static_cast<int64_t>(w.rb) * BM + row;
             const bool row_ok = i < p.nL;
             const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
             const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
-            float4 gnext = __ldg(reinterpret_cast<const float4*>(
-                p.gR + static_cast<int64_t>(w.j0) * BN + half * (BN / 2)) + lane);
+            using GV = typename std::conditional<kColsPerWarp == 128, float4, float2>::type;
+            GV gnext = __ldg(reinterpret_cast<const GV*>(
+                p.gR + static_cast<int64_t>(w.j0) * BN + half * kColsPerWarp) + lane);
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
@@ -324,17 +370,17 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             }
             for (int J = w.j0; J < w.j1; J++) {
                 __syncwarp();
-                reinterpret_cast<float4*>(gs)[lane] = gnext;
+                reinterpret_cast<GV*>(gs)[lane] = gnext;
                 // unconditional (clamped) prefetch: a predicated load would
                 // force a wait at the register move
-                gnext = __ldg(reinterpret_cast<const float4*>(
-                    p.gR + static_cast<int64_t>(min(J + 1, w.j1 - 1)) * BN + half * (BN / 2)) + lane);
+                gnext = __ldg(reinterpret_cast<const GV*>(
+                    p.gR + static_cast<int64_t>(min(J + 1, w.j1 - 1)) * BN + half * kColsPerWarp) + lane);
                 __syncwarp();
                 ptx::mbar_wait(&t_full[acc], acc_phase);
                 ptx::tc_fence_after();
-                const int64_t colw = static_cast<int64_t>(J) * BN + half * (BN / 2);
+                const int64_t colw = static_cast<int64_t>(J) * BN + half * kColsPerWarp;
                 const uint32_t t_acc =
-                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * (BN / 2));
+                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * kColsPerWarp);
 
                 auto process = [&](const uint32_t(&v)[32], int c) {
                     float g[32];
@@ -381,26 +427,26 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     }
                 };
 
-                uint32_t va[32], vb[32];
-                ptx::tmem_ld32(t_acc, va);
+                // double-buffered TMEM reads: chunk c+1 is in flight while c is tested
+                uint32_t vbuf[2][32];
+                ptx::tmem_ld32(t_acc, vbuf[0]);
                 ptx::tmem_ld_wait();
-                ptx::reg_fence(va);
-                ptx::tmem_ld32(t_acc + 32, vb);
-                process(va, 0);
-                ptx::tmem_ld_wait();
-                ptx::reg_fence(vb);
-                ptx::tmem_ld32(t_acc + 64, va);
-                process(vb, 1);
-                ptx::tmem_ld_wait();
-                ptx::reg_fence(va);
-                ptx::tmem_ld32(t_acc + 96, vb);
-                process(va, 2);
-                ptx::tmem_ld_wait();
-                ptx::reg_fence(vb);
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);  // TMEM reads done
-                process(vb, 3);
+                ptx::reg_fence(vbuf[0]);
+#pragma unroll
+                for (int c = 0; c < kChunks; c++) {
+                    if (c + 1 < kChunks) {
+                        ptx::tmem_ld32(t_acc + (c + 1) * 32, vbuf[(c + 1) & 1]);
+                    } else {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);  // TMEM reads done
+                    }
+                    process(vbuf[c & 1], c);
+                    if (c + 1 < kChunks) {
+                        ptx::tmem_ld_wait();
+                        ptx::reg_fence(vbuf[(c + 1) & 1]);
+                    }
+                }
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -775,7 +821,8 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     constexpr int NKB = DP / (COS ? 64 : 32);
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr size_t smem =
-        1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + 4096 + 8 * 32 * 16;
+        1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + kEpiWarps * kColsPerWarp * 4 +
+        kEpiWarps * 32 * 16 + 128;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES, COS>;
     PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -873,7 +920,11 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
     for (int64_t rb = 0; rb < n_rb; rb++)
         total_tiles += self ? static_cast<double>(u.nt - (rb >> 1)) : static_cast<double>(u.nt);
     total_tiles /= P;
-    u.ch = static_cast<int>(std::clamp<double>(total_tiles / (8.0 * ctx.sm_count), 1.0, 64.0));
+    static const double div = [] {
+        const char* e = getenv("PDB_UNIT_DIV");
+        return e ? atof(e) : 16.0;
+    }();
+    u.ch = static_cast<int>(std::clamp<double>(total_tiles / (div * ctx.sm_count), 1.0, 64.0));
     u.n_chunks = static_cast<int>(ceil_div(u.nt, u.ch));
     std::vector<int64_t> off(static_cast<size_t>(u.n_chunks) + 1, 0);
     for (int c = 0; c < u.n_chunks; c++) {
@@ -899,7 +950,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
                         const CUtensorMap& tA, const CUtensorMap& tB, ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
                         pdb_join_stats* stats, PhaseTimer& tm, int launches, Recheck&& recheck) {
-    DevBuf<unsigned long long> counters(4, s);  // [records, tiles, pairs, candidates]
+    DevBuf<unsigned long long> counters(5, s);  // [records, tiles, pairs, candidates, next unit]
     unsigned long long cap = static_cast<unsigned long long>(
         std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
     unsigned long long out_need = static_cast<unsigned long long>(
@@ -927,7 +978,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
         p.counter = counters.p;
         p.tiles = counters.p + 1;
         p.ncand = counters.p + 3;
-        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), s));
+        p.next_unit = counters.p + 4;
+        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 5 * sizeof(unsigned long long), s));
     };
     p.unit_step = 1;
     tm.mark(1);
