@@ -66,7 +66,7 @@ constexpr int BK = 32;   // fp32 per 128-byte swizzle row (64 for bf16)
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
 #ifndef PDB_EPI_WARPS
-#define PDB_EPI_WARPS 8
+#define PDB_EPI_WARPS 16
 #endif
 constexpr int kEpiWarps = PDB_EPI_WARPS;             // epilogue warps (multiple of 4)
 constexpr int kColsPerWarp = BN / (kEpiWarps / 4);   // accumulator columns per epilogue warp
