@@ -118,6 +118,10 @@ int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, in
  *                    emission order when the build side is R (probe order,
  *                    ascending build id).  Without it the order is
  *                    unspecified.
+ *   PDB_JOIN_TF32    screen on tf32 instead of bf16 copies.  The screen only
+ *                    selects candidates (with a margin covering its rounding);
+ *                    every emitted pair is decided by the exact fp64 re-check,
+ *                    so the output does not depend on this flag.
  * Sharding (multi-GPU, one process per GPU): with shard_count = P > 1 this
  * call only scans the 128-row blocks of L assigned to shard_index: block
  * b = k*P + (k even ? shard_index : P-1-shard_index), k = 0, 1, ...
@@ -125,6 +129,8 @@ int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, in
  * pair set and share the triangular self-join work evenly. */
 #define PDB_JOIN_SELF 1u
 #define PDB_JOIN_SORTED 2u
+#define PDB_JOIN_TF32 4u   /* screen on tf32 copies (tighter candidate band) instead of bf16;
+                              the result is identical either way */
 
 typedef struct pdb_join_opts {
     uint32_t flags;

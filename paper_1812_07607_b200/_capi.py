@@ -34,6 +34,7 @@ PDB_HIST_PER_CHANNEL = 0
 PDB_HIST_JOINT = 1
 PDB_JOIN_SELF = 1
 PDB_JOIN_SORTED = 2
+PDB_JOIN_TF32 = 4
 
 # Every symbol include/pdb_cuda.h declares (checked by tests/test_capi.py).
 EXPORTS = (

@@ -45,6 +45,7 @@
 
 #include <cub/cub.cuh>
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -80,7 +81,14 @@ constexpr float kFlagNonFinite = -1.0f;
 constexpr float kFlagBig = -2.0f;
 constexpr float kBigLimit = 1.152921504606846976e18f;  // 2^60
 
-constexpr double kU = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
+// Screen modes: L2 distance on tf32 or bf16 copies, or cosine on bf16 rows.
+constexpr int kModeL2Tf32 = 0;
+constexpr int kModeL2Bf16 = 1;
+constexpr int kModeCosBf16 = 2;
+// Per-element perturbation bound U of the screen copies (round-to-nearest
+// to the MMA input type after an fp32 subtraction).
+constexpr double kU_tf32 = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
+constexpr double kU_bf16 = 1.953125e-3 + 9.5367431640625e-7;   // 2^-9 + 2^-20
 
 struct ScreenParams {
     int64_t nL, nR;
@@ -99,6 +107,7 @@ struct ScreenParams {
     const float* tmaxS; // per R tile
     const float* tmaxN;
     double tau_p;       // tau (1 + 1e-9)
+    double u;           // perturbation bound U of the screen copies (L2 modes)
     double gam;         // DP 2^-23 + 2^-19
     int4* rec;                  // (row i, first column j0, hit mask, 0)
     unsigned long long cap;     // record capacity
@@ -135,15 +144,21 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
 // ---------------------------------------------------------------------------
 // K2: the tensor-core screen.  A_RES: the CTA's 128-row block of L stays
 // resident in shared memory for a whole unit (DP <= 128); otherwise A is
-// streamed with B through the stage ring.  COS: bf16 operands
-// (kind::f16) and the cosine test dot * (1/||y_j||) >= h_i; otherwise tf32
-// operands (kind::tf32) and the L2 test dot - ||y_j||^2/2 >= h_i.  DP is in
-// elements; every K-block is 128 bytes of each row either way.
-template <int DP, bool A_RES, int STAGES, bool COS>
+// streamed with B through the stage ring.  MODE: kModeL2Bf16 / kModeL2Tf32
+// screen the L2 test dot - ||y_j||^2/2 >= h_i on bf16 (kind::f16) or tf32
+// (kind::tf32) copies; kModeCosBf16 the cosine test dot * (1/||y_j||) >= h_i
+// on bf16 rows.  DP is in elements; every K-block is 128 bytes of each row.
+// (On B200 the single-CTA SS MMA is bound by shared-memory operand reads,
+// ~12 KB per 128x256x(32 B of K) step, so bf16 operands -- twice the K per
+// byte -- run the same screen about twice as fast as tf32; the wider margin
+// band costs only candidates, which the exact re-check discards.)
+template <int DP, bool A_RES, int STAGES, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const ScreenParams p) {
-    constexpr int KE = COS ? 64 : 32;  // elements per 128-byte K-block
+    constexpr bool COS = MODE == kModeCosBf16;
+    constexpr bool BF16 = MODE != kModeL2Tf32;
+    constexpr int KE = BF16 ? 64 : 32;  // elements per 128-byte K-block
     constexpr int NKB = DP / KE;
     constexpr int kStageBytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr int kAResBytes = A_RES ? NKB * kABytes : 0;
@@ -284,7 +299,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
 #pragma unroll
                         for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
-                            if (COS)
+                            if (BF16)
                                 ptx::mma_f16(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescBf16,
                                              (kb | kk) != 0);
@@ -364,7 +379,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     ms = fmaxf(ms, __ldg(p.tmaxS + J));
                     mn = fmaxf(mn, __ldg(p.tmaxN + J));
                 }
-                const double r = p.tau_p + kU * (static_cast<double>(sn) + ms) + 1e-30;
+                const double r = p.tau_p + p.u * (static_cast<double>(sn) + ms) + 1e-30;
                 const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
                 h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
             }
@@ -383,32 +398,41 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * kColsPerWarp);
 
                 auto process = [&](const uint32_t(&v)[32], int c) {
-                    float g[32];
-                    const float4* g4 = reinterpret_cast<const float4*>(gs + c * 32);
+                    // e_k = dot_k - g_k (L2) or dot_k * g_k (cosine), two
+                    // columns per packed f32x2 instruction (IEEE RN per lane)
+                    float e[32];
+                    const uint2* g2 = reinterpret_cast<const uint2*>(gs + c * 32);
 #pragma unroll
-                    for (int k4 = 0; k4 < 8; k4++) {
-                        const float4 t = g4[k4];
-                        g[4 * k4 + 0] = t.x;
-                        g[4 * k4 + 1] = t.y;
-                        g[4 * k4 + 2] = t.z;
-                        g[4 * k4 + 3] = t.w;
+                    for (int k2 = 0; k2 < 16; k2++) {
+                        const uint2 gg = g2[k2];
+                        const unsigned long long a =
+                            (static_cast<unsigned long long>(v[2 * k2 + 1]) << 32) | v[2 * k2];
+                        const unsigned long long b =
+                            (static_cast<unsigned long long>(gg.y) << 32) | gg.x;
+                        unsigned long long r;
+                        if (COS)
+                            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+                        else
+                            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+                        e[2 * k2] = __uint_as_float(static_cast<uint32_t>(r));
+                        e[2 * k2 + 1] = __uint_as_float(static_cast<uint32_t>(r >> 32));
                     }
                     float m = -__int_as_float(0x7f800000);
 #pragma unroll
-                    for (int k = 0; k < 32; k++)
-                        m = fmaxf(m, COS ? __uint_as_float(v[k]) * g[k] : __uint_as_float(v[k]) - g[k]);
+                    for (int k = 0; k < 32; k++) m = fmaxf(m, e[k]);
                     const bool hit = row_ok && m >= h;
                     if (__any_sync(0xffffffffu, hit)) {
                         const int64_t col0 = colw + c * 32;
                         uint32_t mask = 0;
                         if (hit) {
 #pragma unroll
-                            for (int k = 0; k < 32; k++) {
-                                const int64_t j = col0 + k;
-                                const float vk = COS ? __uint_as_float(v[k]) * g[k]
-                                                     : __uint_as_float(v[k]) - g[k];
-                                const bool ok = (vk >= h) && j < p.nR && (!p.self_join || j > i);
-                                mask |= static_cast<uint32_t>(ok) << k;
+                            for (int k = 0; k < 32; k++) mask |= static_cast<uint32_t>(e[k] >= h) << k;
+                            // columns past R's end, and j <= i in a self-join
+                            if (col0 + 32 > p.nR)
+                                mask &= p.nR > col0 ? (0xffffffffu >> (32 - (p.nR - col0))) : 0u;
+                            if (p.self_join) {
+                                const int64_t lo = i + 1 - col0;  // first allowed k
+                                mask &= lo <= 0 ? 0xffffffffu : (lo >= 32 ? 0u : (0xffffffffu << lo));
                             }
                         }
                         // one record (row, first column, 32-bit hit mask) per lane with
@@ -504,15 +528,24 @@ k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restr
     }
 }
 
-// One warp per row: centred, tf32-rounded, zero-padded copy + norms + class.
+// One warp per row: centred copy rounded to the MMA input type (tf32 via
+// cvt.rna, or bf16 round-to-nearest), zero-padded to DP columns, with the
+// norms of that rounded copy and the row class.
+__device__ __forceinline__ float round_tf32(float x) { return ptx::tf32_rna(x); }
+__device__ __forceinline__ uint16_t to_bf16_bits(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+template <bool BF16>
 __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
-                       const float* __restrict__ mu, float* __restrict__ Xp,
+                       const float* __restrict__ mu, void* __restrict__ Xp_,
                        float* __restrict__ hn, float* __restrict__ sn) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const float* x = X + row * d;
-    float* xp = Xp + row * DP;
+    float* xpf = static_cast<float*>(Xp_) + row * DP;
+    uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
     double acc = 0.0;
     bool finite = true, big = false;
     for (int k = lane; k < DP; k += 32) {
@@ -520,10 +553,17 @@ __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
         if (k < d) {
             const float a = x[k];
             if (!isfinite(a)) finite = false;
-            t = ptx::tf32_rna(__fsub_rn(a, mu[k]));
+            const float c = __fsub_rn(a, mu[k]);
+            if (BF16) {
+                const uint16_t b = to_bf16_bits(c);
+                t = __uint_as_float(static_cast<uint32_t>(b) << 16);
+            } else {
+                t = round_tf32(c);
+            }
             if (!(fabsf(t) <= kBigLimit)) big = true;
         }
-        xp[k] = t;
+        if (BF16) xpb[k] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
+        else xpf[k] = t;
         acc += static_cast<double>(t) * static_cast<double>(t);
     }
 #pragma unroll
@@ -531,7 +571,10 @@ __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
     finite = __all_sync(0xffffffffu, finite);
     big = __any_sync(0xffffffffu, big);
     if (!finite || big) {
-        for (int k = lane; k < DP; k += 32) xp[k] = 0.0f;
+        for (int k = lane; k < DP; k += 32) {
+            if (BF16) xpb[k] = 0;
+            else xpf[k] = 0.0f;
+        }
     }
     if (lane == 0) {
         if (!finite) {
@@ -815,16 +858,16 @@ CUtensorMap make_tmap(const DeviceCtx& ctx, const void* base, int64_t rows, int 
     return m;
 }
 
-template <int DP, bool A_RES, int STAGES, bool COS>
+template <int DP, bool A_RES, int STAGES, int MODE>
 void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
                    const ScreenParams& p, cudaStream_t s) {
-    constexpr int NKB = DP / (COS ? 64 : 32);
+    constexpr int NKB = DP / (MODE == kModeL2Tf32 ? 32 : 64);
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr size_t smem =
         1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + kEpiWarps * kColsPerWarp * 4 +
         kEpiWarps * 32 * 16 + 128;
     static_assert(smem <= 232448, "shared memory budget");
-    auto k = k_screen<DP, A_RES, STAGES, COS>;
+    auto k = k_screen<DP, A_RES, STAGES, MODE>;
     PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
@@ -832,29 +875,36 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     PDB_CUDA(cudaGetLastError());
 }
 
-void dispatch_screen(int DP, bool cos, const DeviceCtx& ctx, const CUtensorMap& tA,
+void dispatch_screen(int DP, int mode, const DeviceCtx& ctx, const CUtensorMap& tA,
                      const CUtensorMap& tB, const ScreenParams& p, cudaStream_t s) {
-    if (cos) {
-        switch (DP) {
-            case 64: launch_screen<64, true, 4, true>(ctx, tA, tB, p, s); return;
-            case 128: launch_screen<128, true, 4, true>(ctx, tA, tB, p, s); return;
-            case 256: launch_screen<256, false, 4, true>(ctx, tA, tB, p, s); return;
-            case 512: launch_screen<512, false, 4, true>(ctx, tA, tB, p, s); return;
-            case 1024: launch_screen<1024, false, 4, true>(ctx, tA, tB, p, s); return;
-            case 2048: launch_screen<2048, false, 4, true>(ctx, tA, tB, p, s); return;
-            case 4096: launch_screen<4096, false, 4, true>(ctx, tA, tB, p, s); return;
+    if (mode == kModeL2Bf16 || mode == kModeCosBf16) {
+#define PDB_BF16_CASES(M)                                                          \
+        switch (DP) {                                                              \
+            case 64: launch_screen<64, true, 5, M>(ctx, tA, tB, p, s); return;     \
+            case 128: launch_screen<128, true, 4, M>(ctx, tA, tB, p, s); return;   \
+            case 256: launch_screen<256, false, 4, M>(ctx, tA, tB, p, s); return;  \
+            case 512: launch_screen<512, false, 4, M>(ctx, tA, tB, p, s); return;  \
+            case 1024: launch_screen<1024, false, 4, M>(ctx, tA, tB, p, s); return; \
+            case 2048: launch_screen<2048, false, 4, M>(ctx, tA, tB, p, s); return; \
+            case 4096: launch_screen<4096, false, 4, M>(ctx, tA, tB, p, s); return; \
         }
-        fail(PDB_ERR_CONFIG, "cosine join: unsupported padded dimension");
+        if (mode == kModeL2Bf16) {
+            PDB_BF16_CASES(kModeL2Bf16)
+        } else {
+            PDB_BF16_CASES(kModeCosBf16)
+        }
+#undef PDB_BF16_CASES
+        fail(PDB_ERR_CONFIG, "join: unsupported padded dimension");
     }
     switch (DP) {
-        case 32: launch_screen<32, true, 6, false>(ctx, tA, tB, p, s); return;
-        case 64: launch_screen<64, true, 5, false>(ctx, tA, tB, p, s); return;
-        case 96: launch_screen<96, true, 4, false>(ctx, tA, tB, p, s); return;
-        case 128: launch_screen<128, true, 4, false>(ctx, tA, tB, p, s); return;
-        case 256: launch_screen<256, false, 4, false>(ctx, tA, tB, p, s); return;
-        case 512: launch_screen<512, false, 4, false>(ctx, tA, tB, p, s); return;
-        case 1024: launch_screen<1024, false, 4, false>(ctx, tA, tB, p, s); return;
-        case 2048: launch_screen<2048, false, 4, false>(ctx, tA, tB, p, s); return;
+        case 32: launch_screen<32, true, 6, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 64: launch_screen<64, true, 5, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 96: launch_screen<96, true, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 128: launch_screen<128, true, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 256: launch_screen<256, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 512: launch_screen<512, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 1024: launch_screen<1024, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 2048: launch_screen<2048, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
     }
     fail(PDB_ERR_CONFIG, "similarity join: unsupported padded dimension");
 }
@@ -946,7 +996,7 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
 // overflow handling, optional sort, stats.  `recheck(recs, cap, out)`
 // enqueues the mode's re-check kernel.
 template <class Recheck>
-void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
+void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
                         const CUtensorMap& tA, const CUtensorMap& tB, ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
                         pdb_join_stats* stats, PhaseTimer& tm, int launches, Recheck&& recheck) {
@@ -991,7 +1041,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
         recs.reset(cap, s);
         arm();
         p.unit_step = kSampleStep;
-        dispatch_screen(DP, cos, ctx, tA, tB, p, s);
+        dispatch_screen(DP, mode, ctx, tA, tB, p, s);
         launches++;
         read_counters();
         p.unit_step = 1;
@@ -1007,7 +1057,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, bool cos,
         ensure_out(out_need);
         arm();
         if (p.n_units > 0) {
-            dispatch_screen(DP, cos, ctx, tA, tB, p, s);
+            dispatch_screen(DP, mode, ctx, tA, tB, p, s);
             launches++;
         }
         tm.mark(2);
@@ -1084,8 +1134,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     int launches = 0;
     tm.mark(0);
 
-    const int DP = padded_dim(d);
-    if (DP > 2048) fail(PDB_ERR_CONFIG, "similarity join: d > 2048 is not supported by this build");
+    // bf16 screen copies by default (twice the MMA rate of tf32 on this
+    // SMEM-operand-bound screen); PDB_JOIN_TF32 asks for the tighter tf32 band.
+    const bool tf32 = (o.flags & PDB_JOIN_TF32) != 0;
+    const int mode = tf32 ? kModeL2Tf32 : kModeL2Bf16;
+    const int DP = tf32 ? padded_dim(d) : padded_dim_bf16(d);
+    if (DP > (tf32 ? 2048 : 4096))
+        fail(PDB_ERR_CONFIG, "similarity join: d is larger than this build supports");
+    const size_t es = tf32 ? 4 : 2;
 
     // ---- preparation ----------------------------------------------------
     DevBuf<float> mu(DP, s);
@@ -1093,19 +1149,23 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                                                               mu.p);
     PDB_CUDA(cudaGetLastError());
     launches++;
-    auto prep = [&](const float* X, int64_t n, DevBuf<float>& Xp, DevBuf<float>& hn,
+    auto prep = [&](const float* X, int64_t n, DevBuf<uint8_t>& Xp, DevBuf<float>& hn,
                     DevBuf<float>& sn) {
-        k_prep<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p,
-                                                                           hn.p, sn.p);
+        const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
+        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p, hn.p, sn.p);
+        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p, hn.p, sn.p);
         PDB_CUDA(cudaGetLastError());
         launches++;
     };
-    DevBuf<float> XpL(static_cast<size_t>(nL) * DP, s), hnL(nL, s), snL(nL, s);
+    DevBuf<uint8_t> XpL(static_cast<size_t>(nL) * DP * es, s);
+    DevBuf<float> hnL(nL, s), snL(nL, s);
     prep(d_L, nL, XpL, hnL, snL);
-    DevBuf<float> XpR_own, hnR_own, snR_own;
-    const float *XpR = XpL.p, *hnR = hnL.p, *snR = snL.p;
+    DevBuf<uint8_t> XpR_own;
+    DevBuf<float> hnR_own, snR_own;
+    const uint8_t* XpR = XpL.p;
+    const float *hnR = hnL.p, *snR = snL.p;
     if (!self) {
-        XpR_own.reset(static_cast<size_t>(nR) * DP, s);
+        XpR_own.reset(static_cast<size_t>(nR) * DP * es, s);
         hnR_own.reset(nR, s);
         snR_own.reset(nR, s);
         prep(d_R, nR, XpR_own, hnR_own, snR_own);
@@ -1121,8 +1181,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     PDB_CUDA(cudaGetLastError());
     launches++;
 
-    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM, false);
-    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, false);
+    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM, !tf32);
+    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;
@@ -1140,8 +1200,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tmaxS = tmaxS.p;
     p.tmaxN = tmaxN.p;
     p.tau_p = tau * (1.0 + 1e-9);
+    p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
-    screen_and_recheck(ctx, s, DP, false, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+    screen_and_recheck(ctx, s, DP, mode, tA, tB, p, nL, nR, o, out, stats, tm, launches,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
@@ -1223,7 +1284,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     p.chunk_off = plan.off.p;
     p.hnL = hL.p;
     p.gR = gR.p;
-    screen_and_recheck(ctx, s, DP, true, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+    screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, p, nL, nR, o, out, stats, tm, launches,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            k_recheck_cos<<<ctx.sm_count * 16, 256, 0, s>>>(

@@ -28,10 +28,11 @@ def _check(res, ol, orr, od):
     assert np.array_equal(res.dist[order], od.astype(np.float32))
 
 
-def test_golden_cases_cross_join():
+@pytest.mark.parametrize("tf32", [False, True])
+def test_golden_cases_cross_join(tf32):
     for name, L, R, tau, sides, dist in golden_io.join_cases():
         li, ri, _ = next(iter(sides.values()))
-        res = patchdb.sim_join(L, R, tau)
+        res = patchdb.sim_join(L, R, tau, tf32=tf32)
         assert _same_set(res.left, res.right, li, ri), name
         # sorted flag -> ascending (left, right); distances = fp32(euclidean)
         order = np.lexsort((ri, li))
@@ -74,9 +75,10 @@ def test_config1_full_selfjoin_vs_oracle():
     _check(res, ol, orr, od)
 
 
+@pytest.mark.parametrize("tf32", [False, True])
 @pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 24, 31, 32, 33, 63, 64, 65, 96, 100, 128, 129,
-                               200, 256, 300, 512])
-def test_dims_cross_join(d):
+                               200, 256, 300, 512, 1000, 2048])
+def test_dims_cross_join(d, tf32):
     rng = np.random.default_rng(d)
     L = rng.random((700, d), dtype=np.float32)
     R = np.concatenate([L[rng.integers(0, 700, 300)] +
@@ -84,25 +86,27 @@ def test_dims_cross_join(d):
                         rng.random((500, d), dtype=np.float32)]).astype(np.float32)
     dd = np.sqrt(((L[:, None, :].astype(np.float64) - R[None]) ** 2).sum(-1))
     tau = float(np.quantile(dd, 0.01))
-    res = patchdb.sim_join(L, R, tau)
+    res = patchdb.sim_join(L, R, tau, tf32=tf32)
     ol, orr, od = oracle.sim_join(L, R, tau, threads=8)
     assert len(ol) > 0
     _check(res, ol, orr, od)
 
 
+@pytest.mark.parametrize("tf32", [False, True])
 @pytest.mark.parametrize("scale", [1e-6, 1e-2, 1.0, 1e3, 1e8])
-def test_value_scales_and_offsets(scale):
+def test_value_scales_and_offsets(scale, tf32):
     rng = np.random.default_rng(int(scale * 7) % 1000)
     off = rng.normal(0, 50 * scale, (1, 48)).astype(np.float32)
     L = (rng.random((900, 48)) * scale + off).astype(np.float32)
     R = (L[::3] + rng.normal(0, 0.02 * scale, (300, 48))).astype(np.float32)
     tau = 0.2 * scale * np.sqrt(48) * 0.05
-    res = patchdb.sim_join(L, R, tau)
+    res = patchdb.sim_join(L, R, tau, tf32=tf32)
     ol, orr, od = oracle.sim_join(L, R, tau, threads=8)
     _check(res, ol, orr, od)
 
 
-def test_boundary_pairs_exactly_at_tau():
+@pytest.mark.parametrize("tf32", [False, True])
+def test_boundary_pairs_exactly_at_tau(tf32):
     # Pairs whose fp64 distance is EXACTLY tau must be kept (inclusive <=),
     # and tau one ulp below must drop them.
     rng = np.random.default_rng(4)
@@ -111,18 +115,19 @@ def test_boundary_pairs_exactly_at_tau():
     R[:, 0] += np.float32(0.25)          # exact shift: distance exactly 0.25 when representable
     d = np.array([oracle.euclidean(L[i], R[i]) for i in range(len(L))])
     tau = float(np.median(d))
-    res = patchdb.sim_join(L, R, tau)
+    res = patchdb.sim_join(L, R, tau, tf32=tf32)
     ol, orr, od = oracle.sim_join(L, R, tau, threads=8)
     _check(res, ol, orr, od)
     assert (od == tau).sum() > 0
     below = np.nextafter(tau, 0)
-    res2 = patchdb.sim_join(L, R, below)
+    res2 = patchdb.sim_join(L, R, below, tf32=tf32)
     ol2, orr2, od2 = oracle.sim_join(L, R, below, threads=8)
     _check(res2, ol2, orr2, od2)
     assert len(ol2) < len(ol)
 
 
-def test_nonfinite_and_huge_rows():
+@pytest.mark.parametrize("tf32", [False, True])
+def test_nonfinite_and_huge_rows(tf32):
     rng = np.random.default_rng(8)
     L = rng.random((300, 16), dtype=np.float32)
     R = L[::-1].copy()
@@ -133,7 +138,7 @@ def test_nonfinite_and_huge_rows():
     R[20] = 3e30
     L[11] = 1e19
     R[21] = 1e19
-    res = patchdb.sim_join(L, R, 0.3)
+    res = patchdb.sim_join(L, R, 0.3, tf32=tf32)
     ol, orr, od = oracle.sim_join(L, R, 0.3, threads=4)
     _check(res, ol, orr, od)
     assert (5 not in res.left) and (6 not in res.left)

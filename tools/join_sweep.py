@@ -36,7 +36,8 @@ for k in range(6):
     if which == "c4":
         patchdb.cosine_join_bf16_device(X, R, tau, self_join=self_join, out=out)
     else:
-        patchdb.sim_join_device(X, R, tau, self_join=self_join, out=out)
+        patchdb.sim_join_device(X, R, tau, self_join=self_join, out=out,
+                                tf32=os.environ.get("PDB_TF32") == "1")
     st = out.stats
     if k >= 2:
         print(f"{which}: pairs={st.pairs} cand={st.candidates} tiles={st.tiles} prep={st.prep_ms:.3f} "
