@@ -89,6 +89,18 @@ void dev_free(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+void set_max_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> done;  // ((func, dev), bytes)
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : done)
+        if (e.first.first == func && e.first.second == dev && e.second >= bytes) return;
+    PDB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.push_back({{func, dev}, bytes});
+}
+
 }  // namespace pdb
 
 using namespace pdb;

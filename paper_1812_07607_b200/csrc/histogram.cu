@@ -391,14 +391,12 @@ void launch_lane(bool vec, dim3 grid, size_t smem, cudaStream_t s, const uint8_t
                  float npix, float* out) {
     if (vec) {
         auto k = k_hist_tiles_lane<NB, JOINT, BT, true>;
-        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+        set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
         k<<<grid, kWarpsPerCta * 32, smem, s>>>(frames, n_tiles, H, W, th, tw, ntx, tpf, B, D,
                                                 npix, out);
     } else {
         auto k = k_hist_tiles_lane<NB, JOINT, BT, false>;
-        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+        set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
         k<<<grid, kWarpsPerCta * 32, smem, s>>>(frames, n_tiles, H, W, th, tw, ntx, tpf, B, D,
                                                 npix, out);
     }
@@ -439,8 +437,7 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
         constexpr int kWpc = 4;
         const size_t smem = static_cast<size_t>(kWpc) * ((1 << (3 * lb)) * 32 * 4 + 96 * 16);
         auto k = lb == 1 ? k_hist_joint_pow2<1, kWpc, 1, 32> : k_hist_joint_pow2<2, kWpc, 1, 32>;
-        PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+        set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
         const dim3 g2(static_cast<unsigned>(ceil_div(n_tiles, kWpc)));
         k<<<g2, kWpc * 32, smem, s>>>(d_frames, n_tiles, H, W, th, tw, ntx, tpf, npix_h, d_out);
     } else if (D <= 64) {
@@ -466,15 +463,11 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
         const int slots = joint ? D : 768;
         const size_t smem = static_cast<size_t>(kWarpsPerCta) * slots * 4;
         if (joint) {
-            PDB_CUDA(cudaFuncSetAttribute(k_hist_tiles_atomic<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
+            set_max_smem(reinterpret_cast<const void*>(k_hist_tiles_atomic<true>), static_cast<int>(smem));
             k_hist_tiles_atomic<true><<<grid, kWarpsPerCta * 32, smem, s>>>(
                 d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D, slots, npix_h, d_out);
         } else {
-            PDB_CUDA(cudaFuncSetAttribute(k_hist_tiles_atomic<false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
+            set_max_smem(reinterpret_cast<const void*>(k_hist_tiles_atomic<false>), static_cast<int>(smem));
             k_hist_tiles_atomic<false><<<grid, kWarpsPerCta * 32, smem, s>>>(
                 d_frames, n_tiles, H, W, th, tw, ntx, tpf, bins, D, slots, npix_h, d_out);
         }
@@ -491,8 +484,7 @@ void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t w, int32_t
     const int joint = mode == PDB_HIST_JOINT;
     if (D <= kF32SmemBins) {
         const size_t smem = static_cast<size_t>(D) * 4;
-        PDB_CUDA(cudaFuncSetAttribute(k_hist_f32_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+        set_max_smem(reinterpret_cast<const void*>(k_hist_f32_smem), static_cast<int>(smem));
         k_hist_f32_smem<<<static_cast<unsigned>(n), 256, smem, s>>>(d_px, n, npx, bins, joint,
                                                                     static_cast<int>(D), npix,
                                                                     d_out);

@@ -868,8 +868,7 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
         kEpiWarps * 32 * 16 + 128;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES, MODE>;
-    PDB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
     k<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(tA, tB, p);
     PDB_CUDA(cudaGetLastError());
@@ -934,14 +933,19 @@ int padded_dim_bf16(int d) {
 struct PhaseTimer {
     bool on = false;
     cudaStream_t s = nullptr;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t* ev = nullptr;
     PhaseTimer(bool enable, cudaStream_t st) : on(enable), s(st) {
         if (!on) return;
-        for (auto& e : ev) PDB_CUDA(cudaEventCreate(&e));
-    }
-    ~PhaseTimer() {
-        if (!on) return;
-        for (auto& e : ev) cudaEventDestroy(e);
+        // events are created once per host thread and device, then reused
+        thread_local cudaEvent_t cache[64][6];
+        thread_local bool made[64] = {};
+        int dev = 0;
+        PDB_CUDA(cudaGetDevice(&dev));
+        if (!made[dev]) {
+            for (auto& e : cache[dev]) PDB_CUDA(cudaEventCreate(&e));
+            made[dev] = true;
+        }
+        ev = cache[dev];
     }
     void mark(int k) {
         if (on) PDB_CUDA(cudaEventRecord(ev[k], s));
@@ -957,7 +961,7 @@ struct PhaseTimer {
 
 // Work units (column chunk c, row block rb), chunk-major, for this shard.
 struct UnitPlan {
-    DevBuf<int64_t> off;
+    int64_t* off = nullptr;  // device [n_chunks + 1], caller-provided (<= nt + 1 entries)
     int ch = 1, nt = 0, n_chunks = 0;
     int64_t n_units = 0;
 };
@@ -986,8 +990,8 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
         off[c + 1] = off[c] + full + (pos_last < rem ? 1 : 0);
     }
     u.n_units = off[u.n_chunks];
-    u.off.reset(off.size(), s);
-    PDB_CUDA(cudaMemcpyAsync(u.off.p, off.data(), off.size() * sizeof(int64_t),
+    // pageable source: the copy is staged synchronously, so `off` may die
+    PDB_CUDA(cudaMemcpyAsync(u.off, off.data(), off.size() * sizeof(int64_t),
                              cudaMemcpyHostToDevice, s));
 }
 
@@ -999,8 +1003,11 @@ template <class Recheck>
 void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
                         const CUtensorMap& tA, const CUtensorMap& tB, ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
-                        pdb_join_stats* stats, PhaseTimer& tm, int launches, Recheck&& recheck) {
-    DevBuf<unsigned long long> counters(5, s);  // [records, tiles, pairs, candidates, next unit]
+                        pdb_join_stats* stats, PhaseTimer& tm, int launches,
+                        unsigned long long* counters_p, Recheck&& recheck) {
+    struct {
+        unsigned long long* p;
+    } counters{counters_p};  // [records, tiles, pairs, candidates, next unit]
     unsigned long long cap = static_cast<unsigned long long>(
         std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
     unsigned long long out_need = static_cast<unsigned long long>(
@@ -1143,45 +1150,57 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         fail(PDB_ERR_CONFIG, "similarity join: d is larger than this build supports");
     const size_t es = tf32 ? 4 : 2;
 
+    // ---- scratch: one pool allocation for every small buffer ---------------
+    const int64_t nt_ = ceil_div(nR, BN);
+    Arena ar;
+    ar.reserve(Arena::need(DP, 4) + Arena::need(static_cast<size_t>(nL) * DP, es) +
+                   2 * Arena::need(nL, 4) +
+                   (self ? 0 : Arena::need(static_cast<size_t>(nR) * DP, es) + 2 * Arena::need(nR, 4)) +
+                   Arena::need(static_cast<size_t>(nt_) * BN, 4) + 2 * Arena::need(nt_, 4) +
+                   Arena::need(nt_ + 2, 8) + Arena::need(5, 8),
+               s);
+    float* mu = ar.take<float>(DP);
+
     // ---- preparation ----------------------------------------------------
-    DevBuf<float> mu(DP, s);
     k_col_mean<<<static_cast<unsigned>(ceil_div(DP, 32)), dim3(32, 32), 0, s>>>(d_L, nL, d, DP,
-                                                                              mu.p);
+                                                                              mu);
     PDB_CUDA(cudaGetLastError());
     launches++;
-    auto prep = [&](const float* X, int64_t n, DevBuf<uint8_t>& Xp, DevBuf<float>& hn,
-                    DevBuf<float>& sn) {
+    auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn) {
         const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
-        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p, hn.p, sn.p);
-        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu.p, Xp.p, hn.p, sn.p);
+        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn);
+        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn);
         PDB_CUDA(cudaGetLastError());
         launches++;
     };
-    DevBuf<uint8_t> XpL(static_cast<size_t>(nL) * DP * es, s);
-    DevBuf<float> hnL(nL, s), snL(nL, s);
+    uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
+    float* hnL = ar.take<float>(nL);
+    float* snL = ar.take<float>(nL);
     prep(d_L, nL, XpL, hnL, snL);
-    DevBuf<uint8_t> XpR_own;
-    DevBuf<float> hnR_own, snR_own;
-    const uint8_t* XpR = XpL.p;
-    const float *hnR = hnL.p, *snR = snL.p;
+    const uint8_t* XpR = XpL;
+    const float *hnR = hnL, *snR = snL;
     if (!self) {
-        XpR_own.reset(static_cast<size_t>(nR) * DP * es, s);
-        hnR_own.reset(nR, s);
-        snR_own.reset(nR, s);
-        prep(d_R, nR, XpR_own, hnR_own, snR_own);
-        XpR = XpR_own.p;
-        hnR = hnR_own.p;
-        snR = snR_own.p;
+        uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
+        float* hr = ar.take<float>(nR);
+        float* sr = ar.take<float>(nR);
+        prep(d_R, nR, xr, hr, sr);
+        XpR = xr;
+        hnR = hr;
+        snR = sr;
     }
     UnitPlan plan;
+    plan.off = ar.take<int64_t>(nt_ + 2);
     plan_units(ctx, nL, nR, self, P, shard, s, plan);
     const int nt = plan.nt;
-    DevBuf<float> gR(static_cast<size_t>(nt) * BN, s), tmaxS(nt, s), tmaxN(nt, s);
-    k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR.p, tmaxS.p, tmaxN.p);
+    float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
+    float* tmaxS = ar.take<float>(nt);
+    float* tmaxN = ar.take<float>(nt);
+    unsigned long long* counters = ar.take<unsigned long long>(5);
+    k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR, tmaxS, tmaxN);
     PDB_CUDA(cudaGetLastError());
     launches++;
 
-    const CUtensorMap tA = make_tmap(ctx, XpL.p, nL, DP, BM, !tf32);
+    const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
     ScreenParams p{};
     p.nL = nL;
@@ -1193,16 +1212,16 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.nt = nt;
     p.n_chunks = plan.n_chunks;
     p.n_units = plan.n_units;
-    p.chunk_off = plan.off.p;
-    p.hnL = hnL.p;
-    p.snL = snL.p;
-    p.gR = gR.p;
-    p.tmaxS = tmaxS.p;
-    p.tmaxN = tmaxN.p;
+    p.chunk_off = plan.off;
+    p.hnL = hnL;
+    p.snL = snL;
+    p.gR = gR;
+    p.tmaxS = tmaxS;
+    p.tmaxN = tmaxN;
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
-    screen_and_recheck(ctx, s, DP, mode, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+    screen_and_recheck(ctx, s, DP, mode, tA, tB, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
@@ -1259,14 +1278,22 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
         }
         PDB_CUDA(cudaGetLastError());
     }
+    const int64_t nt_ = ceil_div(nR, BN);
+    Arena ar;
+    ar.reserve(Arena::need(nL, 4) + Arena::need(static_cast<size_t>(nt_) * BN, 4) +
+                   Arena::need(nt_ + 2, 8) + Arena::need(5, 8),
+               s);
     UnitPlan plan;
+    plan.off = ar.take<int64_t>(nt_ + 2);
     plan_units(ctx, nL, nR, self, P, shard, s, plan);
     const int nt = plan.nt;
-    DevBuf<float> hL(nL, s), gR(static_cast<size_t>(nt) * BN, s);
-    k_prep_cos<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, cmarg, hL.p,
+    float* hL = ar.take<float>(nL);
+    float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
+    unsigned long long* counters = ar.take<unsigned long long>(5);
+    k_prep_cos<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, cmarg, hL,
                                                                             nullptr, 0);
     k_prep_cos<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(nt) * BN * 32, 256)), 256, 0, s>>>(
-        d_R, nR, d, cmarg, nullptr, gR.p, static_cast<int64_t>(nt) * BN);
+        d_R, nR, d, cmarg, nullptr, gR, static_cast<int64_t>(nt) * BN);
     PDB_CUDA(cudaGetLastError());
     launches += 2;
     const CUtensorMap tA = make_tmap(ctx, XL, nL, DP, BM, true);
@@ -1281,10 +1308,11 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     p.nt = nt;
     p.n_chunks = plan.n_chunks;
     p.n_units = plan.n_units;
-    p.chunk_off = plan.off.p;
-    p.hnL = hL.p;
-    p.gR = gR.p;
+    p.chunk_off = plan.off;
+    p.hnL = hL;
+    p.gR = gR;
     screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+                       counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            k_recheck_cos<<<ctx.sm_count * 16, 256, 0, s>>>(

@@ -75,6 +75,29 @@ struct DevBuf {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// One stream-ordered allocation carved into 256-byte aligned pieces: a join
+// call takes its dozen small scratch buffers from one pool allocation.
+struct Arena {
+    DevBuf<uint8_t> buf;
+    size_t used = 0, cap = 0;
+    void reserve(size_t bytes, cudaStream_t s) {
+        buf.reset(bytes, s);
+        cap = bytes;
+        used = 0;
+    }
+    template <class T>
+    T* take(size_t n) {
+        const size_t off = (used + 255) & ~size_t(255);
+        used = off + n * sizeof(T);
+        if (used > cap) fail(PDB_ERR_OUT_OF_MEMORY, "internal arena overflow");
+        return reinterpret_cast<T*>(buf.p + off);
+    }
+    static size_t need(size_t n, size_t elem) { return ((n * elem + 255) & ~size_t(255)) + 256; }
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel.
+PDB_HIDDEN void set_max_smem(const void* func, int bytes);
+
 // ---- K1 launchers (histogram.cu) -----------------------------------------
 PDB_HIDDEN int hist_dim(int32_t bins, int32_t mode);
 PDB_HIDDEN void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H,
