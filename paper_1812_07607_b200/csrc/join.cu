@@ -85,6 +85,10 @@ constexpr float kBigLimit = 1.152921504606846976e18f;  // 2^60
 constexpr int kModeL2Tf32 = 0;
 constexpr int kModeL2Bf16 = 1;
 constexpr int kModeCosBf16 = 2;
+// L2 on bf16 copies with -||y_j||^2/2 folded into the accumulator by one
+// extra K=16 MMA per tile (A: constant [1,1,1,0..] rows, B: the three bf16
+// parts of -g_j), so the epilogue tests raw accumulators (DP <= 128 only).
+constexpr int kModeL2Bf16Aug = 3;
 // Per-element perturbation bound U of the screen copies (round-to-nearest
 // to the MMA input type after an fp32 subtraction).
 constexpr double kU_tf32 = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
@@ -155,13 +159,16 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
 template <int DP, bool A_RES, int STAGES, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-         const ScreenParams p) {
+         const __grid_constant__ CUtensorMap tmG, const ScreenParams p) {
     constexpr bool COS = MODE == kModeCosBf16;
+    constexpr bool AUG = MODE == kModeL2Bf16Aug;
     constexpr bool BF16 = MODE != kModeL2Tf32;
+    static_assert(!AUG || A_RES, "the folded-g mode keeps A resident");
     constexpr int KE = BF16 ? 64 : 32;  // elements per 128-byte K-block
     constexpr int NKB = DP / KE;
+    constexpr int NKL = NKB + (AUG ? 1 : 0);  // K-blocks streamed per tile (+ the g block)
     constexpr int kStageBytes = A_RES ? kBBytes : (kABytes + kBBytes);
-    constexpr int kAResBytes = A_RES ? NKB * kABytes : 0;
+    constexpr int kAResBytes = A_RES ? NKL * kABytes : 0;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = ptx::smem_u32(smem_raw);
@@ -206,6 +213,19 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
+        if (AUG) ptx::tma_prefetch_desc(&tmG);
+    }
+    if (AUG) {
+        // constant A block for the folded g: every row is [1, 1, 1, 0, ...]
+        // (bf16), written in the 128B-swizzled K-major layout TMA would use:
+        // logical 16-byte chunk c of row r sits at chunk c ^ (r & 7).
+        uint4* xa = reinterpret_cast<uint4*>(smA + NKB * kABytes);
+        for (int q = threadIdx.x; q < BM * 8; q += blockDim.x) {
+            const int r = q >> 3, c = q & 7;
+            xa[q] = c == (r & 7) ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) ptx::tmem_alloc(tmem_slot, kTmemCols);
     ptx::tc_fence_before();
@@ -254,7 +274,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         ptx::tma_load_2d(smA + kb * kABytes, &tmA, a_full, kb * KE, w.rb * BM);
                 }
                 for (int J = w.j0; J < w.j1; J++) {
-                    for (int kb = 0; kb < NKB; kb++) {
+                    for (int kb = 0; kb < NKL; kb++) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* st = smS + stage * kStageBytes;
                         ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
@@ -262,7 +282,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                             ptx::tma_load_2d(st, &tmA, &full[stage], kb * KE, w.rb * BM);
                             st += kABytes;
                         }
-                        ptx::tma_load_2d(st, &tmB, &full[stage], kb * KE, J * BN);
+                        if (AUG && kb == NKB)
+                            ptx::tma_load_2d(st, &tmG, &full[stage], 0, J * BN);
+                        else
+                            ptx::tma_load_2d(st, &tmB, &full[stage], kb * KE, J * BN);
                         if (++stage == STAGES) {
                             stage = 0;
                             phase ^= 1;
@@ -290,15 +313,18 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     ptx::mbar_wait(&t_empty[acc], acc_phase ^ 1);
                     ptx::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                    for (int kb = 0; kb < NKB; kb++) {
+                    for (int kb = 0; kb < NKL; kb++) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::tc_fence_after();
                         const uint8_t* st = smS + stage * kStageBytes;
                         const uint32_t a_addr =
                             ptx::smem_u32(A_RES ? smA + kb * kABytes : st);
                         const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
+                        // the folded-g block only has data in its first K=16 slice
+                        const int nkk = (AUG && kb == NKB) ? 1 : 4;
 #pragma unroll
                         for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
+                            if (kk >= nkk) break;
                             if (BF16)
                                 ptx::mma_f16(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescBf16,
@@ -362,8 +388,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
             const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
             using GV = typename std::conditional<kColsPerWarp == 128, float4, float2>::type;
-            GV gnext = __ldg(reinterpret_cast<const GV*>(
-                p.gR + static_cast<int64_t>(w.j0) * BN + half * kColsPerWarp) + lane);
+            GV gnext{};
+            if (!AUG)
+                gnext = __ldg(reinterpret_cast<const GV*>(
+                    p.gR + static_cast<int64_t>(w.j0) * BN + half * kColsPerWarp) + lane);
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
@@ -385,9 +413,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             }
             for (int J = w.j0; J < w.j1; J++) {
                 __syncwarp();
-                reinterpret_cast<GV*>(gs)[lane] = gnext;
+                if (!AUG) reinterpret_cast<GV*>(gs)[lane] = gnext;
                 // unconditional (clamped) prefetch: a predicated load would
-                // force a wait at the register move
+                // force a wait at the register move (none needed when g is folded)
+                if (!AUG)
                 gnext = __ldg(reinterpret_cast<const GV*>(
                     p.gR + static_cast<int64_t>(min(J + 1, w.j1 - 1)) * BN + half * kColsPerWarp) + lane);
                 __syncwarp();
@@ -402,6 +431,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     // columns per packed f32x2 instruction (IEEE RN per lane)
                     float e[32];
                     const uint2* g2 = reinterpret_cast<const uint2*>(gs + c * 32);
+                    if (AUG) {
+#pragma unroll
+                        for (int k = 0; k < 32; k++) e[k] = __uint_as_float(v[k]);
+                    } else
 #pragma unroll
                     for (int k2 = 0; k2 < 16; k2++) {
                         const uint2 gg = g2[k2];
@@ -539,7 +572,8 @@ __device__ __forceinline__ uint16_t to_bf16_bits(float x) {
 template <bool BF16>
 __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
                        const float* __restrict__ mu, void* __restrict__ Xp_,
-                       float* __restrict__ hn, float* __restrict__ sn) {
+                       float* __restrict__ hn, float* __restrict__ sn,
+                       uint16_t* __restrict__ gx) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -587,6 +621,28 @@ __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
             hn[row] = static_cast<float>(acc);
             sn[row] = __double2float_ru(sqrt(acc));
         }
+    }
+    if (gx) {
+        // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
+        // parts (24 significant bits), zeros elsewhere; -inf never matches,
+        // +inf is always a candidate (rows too large for the screen)
+        uint16_t part[3] = {0, 0, 0};
+        if (!finite) {
+            part[0] = 0xFF80u;
+        } else if (big) {
+            part[0] = 0x7F80u;
+        } else {
+            double r = -0.5 * acc;
+            for (int q = 0; q < 3; q++) {
+                const uint16_t b = to_bf16_bits(static_cast<float>(r));
+                part[q] = b;
+                r -= static_cast<double>(__uint_as_float(static_cast<uint32_t>(b) << 16));
+            }
+        }
+        uint32_t* gw = reinterpret_cast<uint32_t*>(gx + row * 64);
+        const uint32_t w = lane == 0 ? (static_cast<uint32_t>(part[1]) << 16) | part[0]
+                         : lane == 1 ? part[2] : 0u;
+        gw[lane] = w;
     }
 }
 
@@ -860,32 +916,40 @@ CUtensorMap make_tmap(const DeviceCtx& ctx, const void* base, int64_t rows, int 
 
 template <int DP, bool A_RES, int STAGES, int MODE>
 void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
-                   const ScreenParams& p, cudaStream_t s) {
-    constexpr int NKB = DP / (MODE == kModeL2Tf32 ? 32 : 64);
+                   const CUtensorMap& tG, const ScreenParams& p, cudaStream_t s) {
+    constexpr int NKL = DP / (MODE == kModeL2Tf32 ? 32 : 64) + (MODE == kModeL2Bf16Aug ? 1 : 0);
     constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
     constexpr size_t smem =
-        1024 + (A_RES ? NKB * kABytes : 0) + STAGES * stage_bytes + 256 + kEpiWarps * kColsPerWarp * 4 +
+        1024 + (A_RES ? NKL * kABytes : 0) + STAGES * stage_bytes + 256 + kEpiWarps * kColsPerWarp * 4 +
         kEpiWarps * 32 * 16 + 128;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES, MODE>;
     set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
-    k<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(tA, tB, p);
+    k<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(tA, tB, tG, p);
     PDB_CUDA(cudaGetLastError());
 }
 
 void dispatch_screen(int DP, int mode, const DeviceCtx& ctx, const CUtensorMap& tA,
-                     const CUtensorMap& tB, const ScreenParams& p, cudaStream_t s) {
+                     const CUtensorMap& tB, const CUtensorMap& tG, const ScreenParams& p,
+                     cudaStream_t s) {
+    if (mode == kModeL2Bf16Aug) {
+        switch (DP) {
+            case 64: launch_screen<64, true, 5, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
+            case 128: launch_screen<128, true, 4, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
+        }
+        fail(PDB_ERR_CONFIG, "join: unsupported padded dimension for the folded-g screen");
+    }
     if (mode == kModeL2Bf16 || mode == kModeCosBf16) {
-#define PDB_BF16_CASES(M)                                                          \
-        switch (DP) {                                                              \
-            case 64: launch_screen<64, true, 5, M>(ctx, tA, tB, p, s); return;     \
-            case 128: launch_screen<128, true, 4, M>(ctx, tA, tB, p, s); return;   \
-            case 256: launch_screen<256, false, 4, M>(ctx, tA, tB, p, s); return;  \
-            case 512: launch_screen<512, false, 4, M>(ctx, tA, tB, p, s); return;  \
-            case 1024: launch_screen<1024, false, 4, M>(ctx, tA, tB, p, s); return; \
-            case 2048: launch_screen<2048, false, 4, M>(ctx, tA, tB, p, s); return; \
-            case 4096: launch_screen<4096, false, 4, M>(ctx, tA, tB, p, s); return; \
+#define PDB_BF16_CASES(M)                                                                 \
+        switch (DP) {                                                                     \
+            case 64: launch_screen<64, true, 5, M>(ctx, tA, tB, tG, p, s); return;        \
+            case 128: launch_screen<128, true, 4, M>(ctx, tA, tB, tG, p, s); return;      \
+            case 256: launch_screen<256, false, 4, M>(ctx, tA, tB, tG, p, s); return;     \
+            case 512: launch_screen<512, false, 4, M>(ctx, tA, tB, tG, p, s); return;     \
+            case 1024: launch_screen<1024, false, 4, M>(ctx, tA, tB, tG, p, s); return;   \
+            case 2048: launch_screen<2048, false, 4, M>(ctx, tA, tB, tG, p, s); return;   \
+            case 4096: launch_screen<4096, false, 4, M>(ctx, tA, tB, tG, p, s); return;   \
         }
         if (mode == kModeL2Bf16) {
             PDB_BF16_CASES(kModeL2Bf16)
@@ -896,14 +960,14 @@ void dispatch_screen(int DP, int mode, const DeviceCtx& ctx, const CUtensorMap& 
         fail(PDB_ERR_CONFIG, "join: unsupported padded dimension");
     }
     switch (DP) {
-        case 32: launch_screen<32, true, 6, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 64: launch_screen<64, true, 5, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 96: launch_screen<96, true, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 128: launch_screen<128, true, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 256: launch_screen<256, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 512: launch_screen<512, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 1024: launch_screen<1024, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
-        case 2048: launch_screen<2048, false, 4, kModeL2Tf32>(ctx, tA, tB, p, s); return;
+        case 32: launch_screen<32, true, 6, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 64: launch_screen<64, true, 5, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 96: launch_screen<96, true, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 128: launch_screen<128, true, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 256: launch_screen<256, false, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 512: launch_screen<512, false, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 1024: launch_screen<1024, false, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
+        case 2048: launch_screen<2048, false, 4, kModeL2Tf32>(ctx, tA, tB, tG, p, s); return;
     }
     fail(PDB_ERR_CONFIG, "similarity join: unsupported padded dimension");
 }
@@ -1001,7 +1065,8 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
 // enqueues the mode's re-check kernel.
 template <class Recheck>
 void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
-                        const CUtensorMap& tA, const CUtensorMap& tB, ScreenParams p,
+                        const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tG,
+                        ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
                         pdb_join_stats* stats, PhaseTimer& tm, int launches,
                         unsigned long long* counters_p, Recheck&& recheck) {
@@ -1048,7 +1113,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         recs.reset(cap, s);
         arm();
         p.unit_step = kSampleStep;
-        dispatch_screen(DP, mode, ctx, tA, tB, p, s);
+        dispatch_screen(DP, mode, ctx, tA, tB, tG, p, s);
         launches++;
         read_counters();
         p.unit_step = 1;
@@ -1064,7 +1129,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         ensure_out(out_need);
         arm();
         if (p.n_units > 0) {
-            dispatch_screen(DP, mode, ctx, tA, tB, p, s);
+            dispatch_screen(DP, mode, ctx, tA, tB, tG, p, s);
             launches++;
         }
         tm.mark(2);
@@ -1143,9 +1208,16 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
 
     // bf16 screen copies by default (twice the MMA rate of tf32 on this
     // SMEM-operand-bound screen); PDB_JOIN_TF32 asks for the tighter tf32 band.
+    // For DP <= 128 the -||y||^2/2 term is folded into the accumulator by one
+    // extra MMA (the screen is epilogue-bound there); PDB_NO_FOLD=1 disables.
     const bool tf32 = (o.flags & PDB_JOIN_TF32) != 0;
-    const int mode = tf32 ? kModeL2Tf32 : kModeL2Bf16;
     const int DP = tf32 ? padded_dim(d) : padded_dim_bf16(d);
+    static const bool no_fold = [] {
+        const char* e = getenv("PDB_NO_FOLD");
+        return e && e[0] == '1';
+    }();
+    const bool fold = !tf32 && DP <= 128 && !no_fold;
+    const int mode = tf32 ? kModeL2Tf32 : (fold ? kModeL2Bf16Aug : kModeL2Bf16);
     if (DP > (tf32 ? 2048 : 4096))
         fail(PDB_ERR_CONFIG, "similarity join: d is larger than this build supports");
     const size_t es = tf32 ? 4 : 2;
@@ -1157,33 +1229,35 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                    2 * Arena::need(nL, 4) +
                    (self ? 0 : Arena::need(static_cast<size_t>(nR) * DP, es) + 2 * Arena::need(nR, 4)) +
                    Arena::need(static_cast<size_t>(nt_) * BN, 4) + 2 * Arena::need(nt_, 4) +
-                   Arena::need(nt_ + 2, 8) + Arena::need(5, 8),
+                   Arena::need(nt_ + 2, 8) + Arena::need(5, 8) +
+                   (fold ? Arena::need(static_cast<size_t>(nR) * 64, 2) : 0),
                s);
     float* mu = ar.take<float>(DP);
+    uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * 64) : nullptr;
 
     // ---- preparation ----------------------------------------------------
     k_col_mean<<<static_cast<unsigned>(ceil_div(DP, 32)), dim3(32, 32), 0, s>>>(d_L, nL, d, DP,
                                                                               mu);
     PDB_CUDA(cudaGetLastError());
     launches++;
-    auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn) {
+    auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out) {
         const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
-        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn);
-        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn);
+        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn, nullptr);
+        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn, g_out);
         PDB_CUDA(cudaGetLastError());
         launches++;
     };
     uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
     float* hnL = ar.take<float>(nL);
     float* snL = ar.take<float>(nL);
-    prep(d_L, nL, XpL, hnL, snL);
+    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr);
     const uint8_t* XpR = XpL;
     const float *hnR = hnL, *snR = snL;
     if (!self) {
         uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
         float* hr = ar.take<float>(nR);
         float* sr = ar.take<float>(nR);
-        prep(d_R, nR, xr, hr, sr);
+        prep(d_R, nR, xr, hr, sr, gx);
         XpR = xr;
         hnR = hr;
         snR = sr;
@@ -1202,6 +1276,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
+    const CUtensorMap tG = fold ? make_tmap(ctx, gx, nR, 64, BN, true) : tB;
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;
@@ -1220,8 +1295,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tmaxN = tmaxN;
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = tf32 ? kU_tf32 : kU_bf16;
-    p.gam = DP * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
-    screen_and_recheck(ctx, s, DP, mode, tA, tB, p, nL, nR, o, out, stats, tm, launches, counters,
+    p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
+    screen_and_recheck(ctx, s, DP, mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
@@ -1311,7 +1386,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     p.chunk_off = plan.off;
     p.hnL = hL;
     p.gR = gR;
-    screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, p, nL, nR, o, out, stats, tm, launches,
+    screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, tB, p, nL, nR, o, out, stats, tm, launches,
                        counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
