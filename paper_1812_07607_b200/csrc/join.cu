@@ -67,7 +67,7 @@ constexpr int BK = 32;   // fp32 per 128-byte swizzle row (64 for bf16)
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
 #ifndef PDB_EPI_WARPS
-#define PDB_EPI_WARPS 16
+#define PDB_EPI_WARPS 8
 #endif
 constexpr int kEpiWarps = PDB_EPI_WARPS;             // epilogue warps (multiple of 4)
 constexpr int kColsPerWarp = BN / (kEpiWarps / 4);   // accumulator columns per epilogue warp
@@ -110,6 +110,8 @@ struct ScreenParams {
                         // (0 for zero / non-finite rows); padded to nt*256
     const float* tmaxS; // per R tile
     const float* tmaxN;
+    const float* cmaxS; // per column chunk (max over its tiles)
+    const float* cmaxN;
     double tau_p;       // tau (1 + 1e-9)
     double u;           // perturbation bound U of the screen copies (L2 modes)
     double gam;         // DP 2^-23 + 2^-19
@@ -122,7 +124,7 @@ struct ScreenParams {
 };
 
 struct Unit {
-    int32_t rb, j0, j1;
+    int32_t rb, j0, j1, chunk;
 };
 
 __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
@@ -139,6 +141,7 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
     const int P = p.shard_count;
     const int pos = (k & 1) ? P - 1 - p.shard_index : p.shard_index;
     r.rb = static_cast<int32_t>(k * P + pos);
+    r.chunk = lo;
     r.j0 = lo * p.ch;
     r.j1 = min(r.j0 + p.ch, p.nt);
     if (p.self_join) r.j0 = max(r.j0, r.rb >> 1);
@@ -402,11 +405,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             } else if (sn == kFlagBig) {
                 h = -__int_as_float(0x7f800000);  // always a candidate
             } else {
-                float ms = 0.0f, mn = 0.0f;
-                for (int J = w.j0; J < w.j1; J++) {
-                    ms = fmaxf(ms, __ldg(p.tmaxS + J));
-                    mn = fmaxf(mn, __ldg(p.tmaxN + J));
-                }
+                // per-chunk maxima (a superset of the unit's tiles), one load each
+                const float ms = __ldg(p.cmaxS + w.chunk), mn = __ldg(p.cmaxN + w.chunk);
                 const double r = p.tau_p + p.u * (static_cast<double>(sn) + ms) + 1e-30;
                 const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
                 h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
@@ -686,6 +686,21 @@ __global__ void k_tile_stats(const float* __restrict__ hn, const float* __restri
         tmaxS[J] = s;
         tmaxN[J] = nn;
     }
+}
+
+// Per column chunk (ch consecutive 256-row tiles): max of the tile maxima.
+__global__ void k_chunk_stats(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN,
+                              int nt, int ch, int n_chunks, float* __restrict__ cmaxS,
+                              float* __restrict__ cmaxN) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_chunks) return;
+    float a = 0.0f, b = 0.0f;
+    for (int J = c * ch; J < min((c + 1) * ch, nt); J++) {
+        a = fmaxf(a, tmaxS[J]);
+        b = fmaxf(b, tmaxN[J]);
+    }
+    cmaxS[c] = a;
+    cmaxN[c] = b;
 }
 
 // ---------------------------------------------------------------------------
@@ -1228,7 +1243,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     ar.reserve(Arena::need(DP, 4) + Arena::need(static_cast<size_t>(nL) * DP, es) +
                    2 * Arena::need(nL, 4) +
                    (self ? 0 : Arena::need(static_cast<size_t>(nR) * DP, es) + 2 * Arena::need(nR, 4)) +
-                   Arena::need(static_cast<size_t>(nt_) * BN, 4) + 2 * Arena::need(nt_, 4) +
+                   Arena::need(static_cast<size_t>(nt_) * BN, 4) + 4 * Arena::need(nt_ + 1, 4) +
                    Arena::need(nt_ + 2, 8) + Arena::need(5, 8) +
                    (fold ? Arena::need(static_cast<size_t>(nR) * 64, 2) : 0),
                s);
@@ -1271,8 +1286,12 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     float* tmaxN = ar.take<float>(nt);
     unsigned long long* counters = ar.take<unsigned long long>(5);
     k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR, tmaxS, tmaxN);
+    float* cmaxS = ar.take<float>(nt + 1);
+    float* cmaxN = ar.take<float>(nt + 1);
+    k_chunk_stats<<<static_cast<unsigned>(ceil_div(plan.n_chunks, 128)), 128, 0, s>>>(
+        tmaxS, tmaxN, nt, plan.ch, plan.n_chunks, cmaxS, cmaxN);
     PDB_CUDA(cudaGetLastError());
-    launches++;
+    launches += 2;
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
@@ -1293,6 +1312,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.gR = gR;
     p.tmaxS = tmaxS;
     p.tmaxN = tmaxN;
+    p.cmaxS = cmaxS;
+    p.cmaxN = cmaxN;
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
