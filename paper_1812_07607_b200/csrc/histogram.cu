@@ -23,9 +23,13 @@
 // reduced with one REDUX per bin at the end of the tile.  Bin counts too
 // large for lane-private columns use per-warp shared-memory atomics.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "pdb_internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace pdb {
 
@@ -270,6 +274,169 @@ k_hist_joint_pow2(const uint8_t* __restrict__ frames, int64_t n_tiles, int H, in
 }
 
 // ---------------------------------------------------------------------------
+// Same TMA ring as k_hist_joint_rows, with 8-bit lane-private counters so
+// that 3-5 CTAs (24-40 counting warps) fit per SM and the load -> add ->
+// store chains of the counting warps hide each other's shared-memory
+// latency (the 32-bit version measured 27 % warp occupancy, latency-bound),
+// and with the per-pixel arithmetic cut to two instructions (the 32-bit
+// version was bound by the integer ALU pipe: ~126 ALU ops per 16 pixels).
+//
+// Pixel -> counter address: mask every byte to its top LB bits (the
+// reference bin of byte v is v >> (8-LB), src/etl.cpp:343-344), so a word
+// holding a pixel's R, G, B in bytes 0-2 is r<<(8-LB) | g<<(16-LB) |
+// b<<(24-LB) | junk<<(32-LB).  One multiply-high by a 3-term constant
+// gathers r, g, b into an 11-bit offset (an exhaustive search over all
+// (r, g, b, junk) picked the constant; tests re-check the map is a
+// bijection onto distinct counters), whose bits 2-6 are zero so the lane
+// (bits 2-6) is OR-ed in: offset = (umulhi(p, M) & Q) | 4*lane | warp base.
+// A counter is the byte at `offset`: bank = lane, so updates never
+// conflict, and a warp needs 2 KB (B = 4).  Pixels 1-3 of each 12-byte
+// group are aligned into a word with funnel shifts.
+//
+// A lane counts at most nb*16 <= 255 pixels per tile (checked by the
+// launcher), so bytes never overflow; they are zeroed per tile and summed
+// over lanes two bytes at a time in 16-bit halves with REDUX.
+template <int LB>
+struct PixMap;
+template <>
+struct PixMap<2> {  // 64 bins, offsets <= 1923
+    static constexpr uint32_t kM = (1u << 16) | (1u << 20) | (1u << 26);
+    static constexpr uint32_t kQ = 0x783u;
+    static constexpr int kWords = 16;
+};
+template <>
+struct PixMap<1> {  // 8 bins, offsets <= 259
+    static constexpr uint32_t kM = (1u << 10) | (1u << 11) | (1u << 25);
+    static constexpr uint32_t kQ = 0x183u;
+    static constexpr int kWords = 3;
+};
+
+template <int LB>
+__device__ __forceinline__ uint32_t pix_offset(uint32_t p) {
+    return __umulhi(p, PixMap<LB>::kM) & PixMap<LB>::kQ;
+}
+
+template <int LB, int S>
+__global__ void __launch_bounds__(17 * 32, 1)
+k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty, int H, int th,
+                   int tw, int ntx, uint32_t stage_bytes, float npix, float* __restrict__ out) {
+    constexpr int NB = 1 << (3 * LB);
+    constexpr int B = 1 << LB;
+    constexpr int NWD = PixMap<LB>::kWords;        // counter words per lane
+    constexpr uint32_t kTop = (((1u << LB) - 1u) << (8 - LB)) * 0x01010101u;
+    extern __shared__ __align__(1024) uint8_t smem_r8[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // counter blocks: 2 KB-aligned shared-window address per warp
+    const uint32_t s0 = ptx::smem_u32(smem_r8);
+    const uint32_t cpad = (2048u - (s0 & 2047u)) & 2047u;
+    uint8_t* stages = smem_r8 + cpad + ntx * 2048;  // 128-B aligned TMA destinations
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + S * stage_bytes);
+    uint64_t* empty = full + S;
+    const int segs = tw >> 4;
+    const int RB = 96 / (3 * segs);
+    const int nb = (th + RB - 1) / RB;
+    const int tile_bytes = RB * 3 * tw;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], ntx);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == ntx) {  // producer
+        if (lane == 0) {
+            ptx::tma_prefetch_desc(&tmap);
+            uint32_t it = 0;
+            for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
+                const int f = tr / nty, ty = tr - f * nty;
+                const int row0 = f * H + ty * th;
+                for (int bt = 0; bt < nb; bt++, it++) {
+                    const uint32_t s = it % S;
+                    if (it >= S) ptx::mbar_wait_sleep(&empty[s], ((it / S) - 1) & 1);
+                    ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    ptx::tma_load_3d(stages + s * stage_bytes, &tmap, &full[s], 0, row0 + bt * RB, 0);
+                }
+            }
+        }
+        return;
+    }
+
+    uint8_t* wcnt = smem_r8 + cpad + warp * 2048;
+    uint32_t* wcnt32 = reinterpret_cast<uint32_t*>(wcnt);
+    const uint32_t lbase = s0 + cpad + warp * 2048 + lane * 4;  // bits 0-1, 7-10 clear
+    // where the counters of this lane's output bins (lane, lane + 32) live
+    auto bin_word = [&](int bin) {
+        const uint32_t r = bin / (B * B), g = (bin / B) % B, b = bin % B;
+        return pix_offset<LB>((r << (8 - LB)) | (g << (16 - LB)) | (b << (24 - LB)));
+    };
+    const uint32_t o0 = bin_word(lane & (NB - 1)), o1 = bin_word((lane + 32) & (NB - 1));
+    uint32_t it = 0;
+    for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
+#pragma unroll
+        for (int wd = 0; wd < NWD; wd++) wcnt32[wd * 32 + lane] = 0;
+        __syncwarp();
+        for (int bt = 0; bt < nb; bt++, it++) {
+            const uint32_t s = it % S;
+            ptx::mbar_wait_sleep(&full[s], (it / S) & 1);
+            const int ngroups = min(RB, th - bt * RB) * segs;
+            uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a;
+            if (lane < ngroups) {
+                const uint4* g = reinterpret_cast<const uint4*>(stages + s * stage_bytes +
+                                                                warp * tile_bytes + lane * 48);
+                a = g[0];
+                b = g[1];
+                c = g[2];
+            }
+            const uint32_t w[12] = {a.x & kTop, a.y & kTop, a.z & kTop, a.w & kTop,
+                                    b.x & kTop, b.y & kTop, b.z & kTop, b.w & kTop,
+                                    c.x & kTop, c.y & kTop, c.z & kTop, c.w & kTop};
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            if (lane < ngroups) {
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    // pixels 4g..4g+3: [r0 g0 b0 r1][g1 b1 r2 g2][b2 r3 g3 b3]
+                    const uint32_t w0 = w[3 * g], w1 = w[3 * g + 1], w2 = w[3 * g + 2];
+                    const uint32_t px[4] = {w0, __funnelshift_r(w0, w1, 24),
+                                            __funnelshift_r(w1, w2, 16), w2 >> 8};
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t ad = pix_offset<LB>(px[k]) | lbase;
+                        uint32_t v;
+                        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(ad) : "memory");
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad), "r"(v + 1u) : "memory");
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // sum bytes 0,2 and 1,3 of every counter word over lanes in 16-bit
+        // halves; lane l keeps the totals of bins l and l+32.
+        uint32_t mine0 = 0, mine1 = 0;
+#pragma unroll
+        for (int wd = 0; wd < NWD; wd++) {
+            const uint32_t v = wcnt32[wd * 32 + lane];
+            const uint32_t s02 = __reduce_add_sync(0xffffffffu, v & 0x00FF00FFu);
+            const uint32_t s13 = __reduce_add_sync(0xffffffffu, (v >> 8) & 0x00FF00FFu);
+            auto pick = [&](uint32_t o) {
+                const uint32_t v2 = (o & 1) ? s13 : s02;
+                return (o & 2) ? v2 >> 16 : v2 & 0xFFFFu;
+            };
+            if ((o0 >> 7) == static_cast<uint32_t>(wd)) mine0 = pick(o0);
+            if ((o1 >> 7) == static_cast<uint32_t>(wd)) mine1 = pick(o1);
+        }
+        __syncwarp();
+        const int f = tr / nty, ty = tr - f * nty;
+        float* o = out + ((static_cast<int64_t>(f) * nty + ty) * ntx + warp) * NB;
+        if (lane < NB) o[lane] = normalise(mine0, npix);
+        if (NB > 32) o[lane + 32] = normalise(mine1, npix);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Per-warp shared-memory atomic counters for larger bin counts.
 // JOINT: B^3 <= 4096 bins.  Per-channel: raw byte-value counts [3][256],
 // mapped to bins at the end (bin(v) is monotone in v), which handles any B.
@@ -428,7 +595,55 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
     const dim3 grid(static_cast<unsigned>(ceil_div(n_tiles, kWarpsPerCta)));
     const bool joint = mode == PDB_HIST_JOINT;
     const int64_t lane_px = ceil_div(static_cast<int64_t>(th) * (tw / 16), 32) * 16;
-    if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {
+    // PDB_K1_LEGACY=1 forces the LDG-staged kernel (A/B measurements only).
+    static const bool k1_legacy = [] {
+        const char* e = getenv("PDB_K1_LEGACY");
+        return e && atoi(e) != 0;
+    }();
+    const int64_t n_rows = n_frames * nty;  // tile rows (frame, ty)
+    const int rows_rb = (vec && tw >= 16) ? 96 / (3 * (tw / 16)) : 0;
+    const int64_t row_smem = rows_rb > 0 ? static_cast<int64_t>(ntx) * rows_rb * 3 * tw : 0;
+    const int nb_rows = rows_rb > 0 ? (th + rows_rb - 1) / rows_rb : 0;
+    if (joint && (bins == 4 || bins == 2) && vec && 3 * tw <= 256 && ntx <= 16 &&
+        nb_rows * 16 <= 255 && n_frames * H < (int64_t{1} << 31) && row_smem % 128 == 0 &&
+        !k1_legacy) {
+        const int lb = bins == 4 ? 2 : 1;
+        const DeviceCtx& ctx = device_ctx();
+        // 3-D view of the frames: {byte within a tile row, frame row, tile
+        // column}, strides {W*3, 3*tw}; the box {3*tw, RB, ntx} lands a
+        // stage tile-major.
+        CUtensorMap m;
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(3 * tw),
+                                    static_cast<cuuint64_t>(n_frames) * H,
+                                    static_cast<cuuint64_t>(ntx)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(W) * 3,
+                                       static_cast<cuuint64_t>(3 * tw)};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(3 * tw),
+                                   static_cast<cuuint32_t>(rows_rb), static_cast<cuuint32_t>(ntx)};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
+        const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(d_frames),
+                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            fail(PDB_ERR_CUDA, "cuTensorMapEncodeTiled (frames) failed (" + std::to_string(r) + ")");
+        // 3 stages: with 2 KB of counters per warp this fits 4 CTAs (32
+        // counting warps) per SM; measured 212 us on config 2 vs 218-248 us
+        // for 4-6 stages.
+        constexpr int kStages = 3;
+        auto kern = lb == 1 ? k_hist_joint_rows8<1, kStages> : k_hist_joint_rows8<2, kStages>;
+        const size_t smem = 2048 + static_cast<size_t>(ntx) * 2048 +
+                            static_cast<size_t>(kStages) * row_smem + kStages * 16;
+        set_max_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
+        const int threads = (ntx + 1) * 32;
+        int per_sm = 0;
+        PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * ctx.sm_count;
+        const dim3 g(static_cast<unsigned>(std::min(n_rows, cap)));
+        kern<<<g, threads, smem, s>>>(m, static_cast<int>(n_rows), nty, H, th, tw, ntx,
+                                      static_cast<uint32_t>(row_smem), npix_h, d_out);
+    } else if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {
         const int lb = bins == 4 ? 2 : 1;
         // 32-bit lane-private counters, 4 warps per CTA, one batch of
         // prefetch: the fastest of the measured (counter width x CTA size x

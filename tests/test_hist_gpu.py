@@ -101,3 +101,43 @@ def test_empty_and_degenerate():
     assert patchdb.featurize_tiles(fr, 4, 4, 4).shape[0] == 0
     fr = np.zeros((2, 8, 8, 3), np.uint8)
     assert patchdb.featurize_tiles(fr, 9, 4, 4).shape[0] == 0   # tile taller than the frame
+
+
+@pytest.mark.parametrize("H,W,th,tw", [
+    (90, 640, 90, 80),     # 15 batches of 6 rows: 240 pixels per lane (8-bit counter limit)
+    (91, 640, 91, 80),     # 16 batches -> over the 8-bit limit, LDG-staged fallback
+    (120, 256, 60, 16),    # 16 tile columns, 48-byte tile rows
+    (120, 272, 60, 16),    # 17 tile columns -> fallback
+    (70, 160, 35, 80),     # partial last batch (35 = 5*6 + 5)
+    (96, 192, 32, 64),     # 192-byte tile rows
+    (64, 96, 64, 32),
+])
+@pytest.mark.parametrize("bins", [2, 4])
+@pytest.mark.parametrize("content", ["uniform", "solid", "blocks"])
+def test_joint_tma_kernel_edges(H, W, th, tw, bins, content):
+    """The TMA-fed 8-bit-counter kernel (and its fallbacks) at its shape
+    limits; solid frames put every pixel of a lane in one counter."""
+    rng = np.random.default_rng(H + W + th + tw + bins)
+    if content == "uniform":
+        fr = rng.integers(0, 256, (5, H, W, 3), dtype=np.uint8)
+    elif content == "solid":
+        fr = np.empty((5, H, W, 3), np.uint8)
+        fr[:] = rng.integers(0, 256, (5, 1, 1, 3), dtype=np.uint8)
+    else:
+        fr, _ = workloads.frames(5, H, W, seed=H + W)
+    dev = torch.from_numpy(fr).cuda()
+    got = patchdb.featurize_tiles(dev, th, tw, bins, "joint").cpu().numpy()
+    want = oracle.featurize_tiles(fr, th, tw, bins, 1)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_joint_tma_kernel_offset_frames():
+    """Frames starting at a 16-byte but not 128-byte aligned device address,
+    and a frame count that leaves CTAs with unequal tile-row counts."""
+    fr, _ = workloads.frames(37, 480, 640, seed=5)
+    big = torch.empty(fr.nbytes + 64, dtype=torch.uint8, device="cuda")
+    view = big[16:16 + fr.nbytes].view(37, 480, 640, 3)
+    view.copy_(torch.from_numpy(fr))
+    got = patchdb.featurize_tiles(view, 60, 80, 4, "joint").cpu().numpy()
+    want = oracle.featurize_tiles(fr, 60, 80, 4, 1)
+    assert np.array_equal(_bits(got), _bits(want))
