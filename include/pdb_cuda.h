@@ -131,6 +131,10 @@ int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, in
 #define PDB_JOIN_SORTED 2u
 #define PDB_JOIN_TF32 4u   /* screen on tf32 copies (tighter candidate band) instead of bf16;
                               the result is identical either way */
+#define PDB_JOIN_PHASE_TIMES 8u  /* fill pdb_join_stats' *_ms with CUDA events between the
+                                    phases.  The events serialise the phase boundaries (the
+                                    kernels are otherwise chained with programmatic dependent
+                                    launch), so leave it unset for throughput runs. */
 
 typedef struct pdb_join_opts {
     uint32_t flags;
@@ -149,7 +153,8 @@ typedef struct pdb_pairs {
 } pdb_pairs;
 
 /* Per-call counters and device timings (optional out-parameter of the _dev
- * variant).  The *_ms fields are CUDA-event times on the call's stream. */
+ * variant).  The *_ms fields are CUDA-event times on the call's stream,
+ * recorded only with PDB_JOIN_PHASE_TIMES (0 otherwise). */
 typedef struct pdb_join_stats {
     int64_t candidates;      /* pairs passing the tensor-core screen */
     int64_t pairs;           /* pairs passing the exact fp64 re-check */

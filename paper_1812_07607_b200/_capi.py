@@ -35,6 +35,7 @@ PDB_HIST_JOINT = 1
 PDB_JOIN_SELF = 1
 PDB_JOIN_SORTED = 2
 PDB_JOIN_TF32 = 4
+PDB_JOIN_PHASE_TIMES = 8
 
 # Every symbol include/pdb_cuda.h declares (checked by tests/test_capi.py).
 EXPORTS = (

@@ -235,6 +235,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();  // the prep kernels' outputs (copies, norms, unit plan)
     // consumer side of the unit ring (MMA warp: lane 0 only; epilogue: whole warp)
     int u_slot = 0;
     uint32_t u_phase = 0;
@@ -537,6 +539,8 @@ constexpr int kMeanRows = 256;
 // added in a fixed order, so mu is deterministic.
 __global__ void __launch_bounds__(1024)
 k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restrict__ mu) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     __shared__ double part[32][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
     double s = 0.0;
@@ -569,46 +573,41 @@ __device__ __forceinline__ uint16_t to_bf16_bits(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
-template <bool BF16>
-__global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
-                       const float* __restrict__ mu, void* __restrict__ Xp_,
-                       float* __restrict__ hn, float* __restrict__ sn,
-                       uint16_t* __restrict__ gx) {
-    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= n) return;
-    const float* x = X + row * d;
+// Row epilogue shared by both prep kernels: lane holds the raw values x[k]
+// of columns k = lane + 32*i (i < NV, NV*32 == DP), writes the centred,
+// rounded copy, the norms / row class and the folded-g block.
+template <bool BF16, int NV>
+__device__ __forceinline__ void prep_row(int64_t row, int lane, int d, int DP,
+                                         const float (&x)[NV], const float (&m)[NV],
+                                         void* __restrict__ Xp_, float* __restrict__ hn,
+                                         float* __restrict__ sn, uint16_t* __restrict__ gx) {
     float* xpf = static_cast<float*>(Xp_) + row * DP;
     uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
     double acc = 0.0;
     bool finite = true, big = false;
-    for (int k = lane; k < DP; k += 32) {
-        float t = 0.0f;
+    float t[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        const int k = lane + 32 * i;
+        t[i] = 0.0f;
         if (k < d) {
-            const float a = x[k];
-            if (!isfinite(a)) finite = false;
-            const float c = __fsub_rn(a, mu[k]);
-            if (BF16) {
-                const uint16_t b = to_bf16_bits(c);
-                t = __uint_as_float(static_cast<uint32_t>(b) << 16);
-            } else {
-                t = round_tf32(c);
-            }
-            if (!(fabsf(t) <= kBigLimit)) big = true;
+            if (!isfinite(x[i])) finite = false;
+            const float c = __fsub_rn(x[i], m[i]);
+            t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
+                        : round_tf32(c);
+            if (!(fabsf(t[i]) <= kBigLimit)) big = true;
         }
-        if (BF16) xpb[k] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
-        else xpf[k] = t;
-        acc += static_cast<double>(t) * static_cast<double>(t);
+        acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     finite = __all_sync(0xffffffffu, finite);
     big = __any_sync(0xffffffffu, big);
-    if (!finite || big) {
-        for (int k = lane; k < DP; k += 32) {
-            if (BF16) xpb[k] = 0;
-            else xpf[k] = 0.0f;
-        }
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        const float v = (!finite || big) ? 0.0f : t[i];
+        if (BF16) xpb[lane + 32 * i] = static_cast<uint16_t>(__float_as_uint(v) >> 16);
+        else xpf[lane + 32 * i] = v;
     }
     if (lane == 0) {
         if (!finite) {
@@ -646,11 +645,95 @@ __global__ void k_prep(const float* __restrict__ X, int64_t n, int d, int DP,
     }
 }
 
+// DP <= 128: each warp loads kRowsPerWarp rows up front (all loads in
+// flight together), then finishes them one by one.
+constexpr int kRowsPerWarp = 4;
+template <bool BF16, int NV>
+__global__ void __launch_bounds__(256)
+k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
+       void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn,
+       uint16_t* __restrict__ gx) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = w * kRowsPerWarp;
+    if (r0 >= n) return;
+    float m[NV], x[kRowsPerWarp][NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) m[i] = lane + 32 * i < d ? mu[lane + 32 * i] : 0.0f;
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; r++)
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            const int k = lane + 32 * i;
+            x[r][i] = (r0 + r < n && k < d) ? __ldg(X + (r0 + r) * d + k) : 0.0f;
+        }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; r++)
+        if (r0 + r < n) prep_row<BF16, NV>(r0 + r, lane, d, DP, x[r], m, Xp_, hn, sn, gx);
+}
+
+// Any DP: one warp per row, 32 columns at a time.
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
+            void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float* x = X + row * d;
+    float* xpf = static_cast<float*>(Xp_) + row * DP;
+    uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
+    double acc = 0.0;
+    bool finite = true, big = false;
+    for (int k = lane; k < DP; k += 32) {
+        float t = 0.0f;
+        if (k < d) {
+            const float a = x[k];
+            if (!isfinite(a)) finite = false;
+            const float c = __fsub_rn(a, mu[k]);
+            t = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
+                     : round_tf32(c);
+            if (!(fabsf(t) <= kBigLimit)) big = true;
+        }
+        if (BF16) xpb[k] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
+        else xpf[k] = t;
+        acc += static_cast<double>(t) * static_cast<double>(t);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    finite = __all_sync(0xffffffffu, finite);
+    big = __any_sync(0xffffffffu, big);
+    if (!finite || big) {
+        for (int k = lane; k < DP; k += 32) {
+            if (BF16) xpb[k] = 0;
+            else xpf[k] = 0.0f;
+        }
+    }
+    if (lane == 0) {
+        if (!finite) {
+            hn[row] = 0.0f;
+            sn[row] = kFlagNonFinite;
+        } else if (big) {
+            hn[row] = 0.0f;
+            sn[row] = kFlagBig;
+        } else {
+            hn[row] = static_cast<float>(acc);
+            sn[row] = __double2float_ru(sqrt(acc));
+        }
+    }
+}
+
 // Per 256-row tile of R: max norms over regular rows, and g_j = ||y~||^2/2
 // with +inf for non-finite rows and padding, -inf for forced rows.
 __global__ void k_tile_stats(const float* __restrict__ hn, const float* __restrict__ sn,
                              int64_t n, float* __restrict__ g, float* __restrict__ tmaxS,
                              float* __restrict__ tmaxN) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int J = blockIdx.x;
     const int64_t j = static_cast<int64_t>(J) * BN + threadIdx.x;  // blockDim.x == BN
     float s = 0.0f, nn = 0.0f, gv = __int_as_float(0x7f800000);
@@ -689,18 +772,65 @@ __global__ void k_tile_stats(const float* __restrict__ hn, const float* __restri
 }
 
 // Per column chunk (ch consecutive 256-row tiles): max of the tile maxima.
-__global__ void k_chunk_stats(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN,
-                              int nt, int ch, int n_chunks, float* __restrict__ cmaxS,
-                              float* __restrict__ cmaxN) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_chunks) return;
-    float a = 0.0f, b = 0.0f;
-    for (int J = c * ch; J < min((c + 1) * ch, nt); J++) {
-        a = fmaxf(a, tmaxS[J]);
-        b = fmaxf(b, tmaxN[J]);
+// One block: per column chunk, the max row norms over its R tiles and the
+// number of this shard's work units (row blocks rb < lim(c), rb = k*P +
+// pos(k), pos(k) = shard for even k and P-1-shard for odd k -- the
+// boustrophedon shard order), exclusive-scanned into chunk_off; also zeroes
+// the screen / re-check counters (this is the first kernel they follow).
+__global__ void __launch_bounds__(1024)
+k_chunk_plan(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN, int nt, int ch,
+             int n_chunks, int64_t n_rb, int self, int P, int shard, float* __restrict__ cmaxS,
+             float* __restrict__ cmaxN, int64_t* __restrict__ chunk_off,
+             unsigned long long* __restrict__ counters) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int64_t part[1024];
+    const int t = threadIdx.x;
+    if (t < 5) counters[t] = 0;
+    const int per = (n_chunks + 1023) / 1024;  // chunks per thread, contiguous
+    int64_t local = 0;
+    for (int c = t * per; c < min((t + 1) * per, n_chunks); c++) {
+        if (tmaxS) {
+            float a = 0.0f, b = 0.0f;
+            for (int J = c * ch; J < min((c + 1) * ch, nt); J++) {
+                a = fmaxf(a, tmaxS[J]);
+                b = fmaxf(b, tmaxN[J]);
+            }
+            cmaxS[c] = a;
+            cmaxN[c] = b;
+        }
+        int64_t lim = n_rb;
+        if (self) lim = min(n_rb, static_cast<int64_t>(2) * (c + 1) * ch);
+        const int64_t full = lim / P, rem = lim % P;
+        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
+        local += full + (pos_last < rem ? 1 : 0);
     }
-    cmaxS[c] = a;
-    cmaxN[c] = b;
+    part[t] = local;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan
+        const int64_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int64_t run = part[t] - local;  // exclusive prefix of this thread's chunks
+    if (t == 0) chunk_off[0] = 0;
+    for (int c = t * per; c < min((t + 1) * per, n_chunks); c++) {
+        int64_t lim = n_rb;
+        if (self) lim = min(n_rb, static_cast<int64_t>(2) * (c + 1) * ch);
+        const int64_t full = lim / P, rem = lim % P;
+        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
+        run += full + (pos_last < rem ? 1 : 0);
+        chunk_off[c + 1] = run;
+    }
+}
+
+// The counters -> mapped pinned host memory (read after one stream sync).
+__global__ void k_export_counters(const unsigned long long* __restrict__ c,
+                                  volatile unsigned long long* h) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (threadIdx.x < 4) h[threadIdx.x] = c[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -744,6 +874,8 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
           int d, double tau, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
           float* __restrict__ out_d, unsigned long long out_cap,
           unsigned long long* __restrict__ out_count) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const unsigned long long n = min(*n_rec, cap);
     const int lane = threadIdx.x & 31;
     const bool vec4 =
@@ -814,6 +946,8 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
 
 __global__ void k_pad_bf16(const uint16_t* __restrict__ X, int64_t n, int d, int DP,
                            uint16_t* __restrict__ Xp) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -826,6 +960,8 @@ __global__ void k_pad_bf16(const uint16_t* __restrict__ X, int64_t n, int d, int
 // padding.
 __global__ void k_prep_cos(const uint16_t* __restrict__ X, int64_t n, int d, double cmarg,
                            float* __restrict__ h, float* __restrict__ g, int64_t npad) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t rows = h ? n : npad;
@@ -872,6 +1008,8 @@ k_recheck_cos(const int4* __restrict__ rec, const unsigned long long* __restrict
               const uint16_t* __restrict__ R, int d, double min_cos, int32_t* __restrict__ out_l,
               int32_t* __restrict__ out_r, float* __restrict__ out_d, unsigned long long out_cap,
               unsigned long long* __restrict__ out_count) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const unsigned long long n = min(*n_rec, cap);
     const int lane = threadIdx.x & 31;
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
@@ -941,7 +1079,7 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     auto k = k_screen<DP, A_RES, STAGES, MODE>;
     set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
-    k<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(tA, tB, tG, p);
+    launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tA, tB, tG, p);
     PDB_CUDA(cudaGetLastError());
 }
 
@@ -1031,8 +1169,9 @@ struct PhaseTimer {
     }
     float ms(int a, int b) {
         if (!on) return 0.0f;
+        // only read after the call's stream synchronisation: both events
+        // have completed
         float t = 0.0f;
-        PDB_CUDA(cudaEventSynchronize(ev[b]));
         PDB_CUDA(cudaEventElapsedTime(&t, ev[a], ev[b]));
         return t;
     }
@@ -1042,13 +1181,15 @@ struct PhaseTimer {
 struct UnitPlan {
     int64_t* off = nullptr;  // device [n_chunks + 1], caller-provided (<= nt + 1 entries)
     int ch = 1, nt = 0, n_chunks = 0;
+    int64_t n_rb = 0;
     int64_t n_units = 0;
 };
 
 void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, int shard,
-                cudaStream_t s, UnitPlan& u) {
+                UnitPlan& u) {
     u.nt = static_cast<int>(ceil_div(nR, BN));
-    const int64_t n_rb = ceil_div(nL, BM);
+    u.n_rb = ceil_div(nL, BM);
+    const int64_t n_rb = u.n_rb;
     double total_tiles = 0;
     for (int64_t rb = 0; rb < n_rb; rb++)
         total_tiles += self ? static_cast<double>(u.nt - (rb >> 1)) : static_cast<double>(u.nt);
@@ -1059,19 +1200,16 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
     }();
     u.ch = static_cast<int>(std::clamp<double>(total_tiles / (div * ctx.sm_count), 1.0, 64.0));
     u.n_chunks = static_cast<int>(ceil_div(u.nt, u.ch));
-    std::vector<int64_t> off(static_cast<size_t>(u.n_chunks) + 1, 0);
+    // the same unit count k_chunk_plan scans on the device
+    int64_t n_units = 0;
     for (int c = 0; c < u.n_chunks; c++) {
         int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
         if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * u.ch);
-        // blocks k*P + pos(k) < lim, pos(k) = shard (k even) / P-1-shard (k odd)
         const int64_t full = lim / P, rem = lim % P;
         const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
-        off[c + 1] = off[c] + full + (pos_last < rem ? 1 : 0);
+        n_units += full + (pos_last < rem ? 1 : 0);
     }
-    u.n_units = off[u.n_chunks];
-    // pageable source: the copy is staged synchronously, so `off` may die
-    PDB_CUDA(cudaMemcpyAsync(u.off, off.data(), off.size() * sizeof(int64_t),
-                             cudaMemcpyHostToDevice, s));
+    u.n_units = n_units;
 }
 
 // The shared back half of both joins: screen (with a sampled output-size
@@ -1092,6 +1230,23 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         std::max<int64_t>(1 << 21, 4 * (nL + nR)));  // candidate records
     unsigned long long out_need = static_cast<unsigned long long>(
         std::max<int64_t>(1 << 20, 4 * (nL + nR)));
+    // pinned per-thread read-back slot (a pageable destination would add a
+    // staging copy to the one synchronisation of the call)
+    // (mapped: a one-warp kernel stores the counters straight into it, no
+    // copy-engine round trip)
+    thread_local unsigned long long* h_pin = [] {
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, 64, cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            q = nullptr;
+        }
+        return static_cast<unsigned long long*>(q);
+    }();
+    unsigned long long* d_pin = nullptr;
+    if (h_pin && cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pin), h_pin, 0) != cudaSuccess) {
+        cudaGetLastError();
+        d_pin = nullptr;
+    }
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
     DevBuf<int4> recs;
     int passes = 0;
@@ -1105,10 +1260,19 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         out->capacity = c;
     };
     auto read_counters = [&] {
-        PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-        PDB_CUDA(cudaStreamSynchronize(s));
+        if (d_pin) {
+            launch_pdl(k_export_counters, dim3(1), dim3(32), 0, s,
+                       static_cast<const unsigned long long*>(counters.p), d_pin);
+            PDB_CUDA(cudaGetLastError());
+            PDB_CUDA(cudaStreamSynchronize(s));
+            std::copy(h_pin, h_pin + 4, h_cnt);
+        } else {
+            PDB_CUDA(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, s));
+            PDB_CUDA(cudaStreamSynchronize(s));
+        }
     };
+    bool zeroed = true;  // k_chunk_plan zeroed the counters
     auto arm = [&] {
         p.rec = recs.p;
         p.cap = cap;
@@ -1116,7 +1280,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         p.tiles = counters.p + 1;
         p.ncand = counters.p + 3;
         p.next_unit = counters.p + 4;
-        PDB_CUDA(cudaMemsetAsync(counters.p, 0, 5 * sizeof(unsigned long long), s));
+        if (!zeroed) PDB_CUDA(cudaMemsetAsync(counters.p, 0, 5 * sizeof(unsigned long long), s));
+        zeroed = false;
     };
     p.unit_step = 1;
     tm.mark(1);
@@ -1196,7 +1361,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         stats->prep_ms = tm.ms(0, 1);
         stats->screen_ms = tm.ms(1, 2);
         stats->recheck_ms = tm.ms(2, 3);
-        stats->sort_ms = tm.ms(3, 4);
+        if (tm.on && (o.flags & PDB_JOIN_SORTED)) PDB_CUDA(cudaEventSynchronize(tm.ev[4]));
+        stats->sort_ms = (o.flags & PDB_JOIN_SORTED) ? tm.ms(3, 4) : 0.0f;
     }
 }
 
@@ -1217,7 +1383,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     if (stats) *stats = pdb_join_stats{};
     out->count = 0;
     if (nL == 0 || nR == 0) return;
-    PhaseTimer tm(stats != nullptr, s);
+    PhaseTimer tm(stats != nullptr && (o.flags & PDB_JOIN_PHASE_TIMES) != 0, s);
     int launches = 0;
     tm.mark(0);
 
@@ -1251,14 +1417,26 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * 64) : nullptr;
 
     // ---- preparation ----------------------------------------------------
-    k_col_mean<<<static_cast<unsigned>(ceil_div(DP, 32)), dim3(32, 32), 0, s>>>(d_L, nL, d, DP,
-                                                                              mu);
+    launch_pdl(k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
+               nL, d, DP, mu);
     PDB_CUDA(cudaGetLastError());
     launches++;
     auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out) {
-        const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
-        if (tf32) k_prep<false><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn, nullptr);
-        else k_prep<true><<<g, 256, 0, s>>>(X, n, d, DP, mu, Xp, hn, sn, g_out);
+        if (DP <= 128) {  // g_out (the folded block) only exists for DP <= 128
+            const unsigned g = static_cast<unsigned>(ceil_div(ceil_div(n, kRowsPerWarp) * 32, 256));
+            auto pick = [&](auto k32, auto k64, auto k96, auto k128) {
+                const int nv = DP / 32;
+                auto k = nv == 1 ? k32 : nv == 2 ? k64 : nv == 3 ? k96 : k128;
+                launch_pdl(k, dim3(g), dim3(256), 0, s, X, n, d, DP, static_cast<const float*>(mu),
+                           static_cast<void*>(Xp), hn, sn, g_out);
+            };
+            if (tf32) pick(k_prep<false, 1>, k_prep<false, 2>, k_prep<false, 3>, k_prep<false, 4>);
+            else pick(k_prep<true, 1>, k_prep<true, 2>, k_prep<true, 3>, k_prep<true, 4>);
+        } else {
+            const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
+            launch_pdl(tf32 ? k_prep_wide<false> : k_prep_wide<true>, dim3(g), dim3(256), 0, s, X,
+                       n, d, DP, static_cast<const float*>(mu), static_cast<void*>(Xp), hn, sn);
+        }
         PDB_CUDA(cudaGetLastError());
         launches++;
     };
@@ -1279,17 +1457,18 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     UnitPlan plan;
     plan.off = ar.take<int64_t>(nt_ + 2);
-    plan_units(ctx, nL, nR, self, P, shard, s, plan);
+    plan_units(ctx, nL, nR, self, P, shard, plan);
     const int nt = plan.nt;
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     float* tmaxS = ar.take<float>(nt);
     float* tmaxN = ar.take<float>(nt);
     unsigned long long* counters = ar.take<unsigned long long>(5);
-    k_tile_stats<<<nt, BN, 0, s>>>(hnR, snR, nR, gR, tmaxS, tmaxN);
+    launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
     float* cmaxS = ar.take<float>(nt + 1);
     float* cmaxN = ar.take<float>(nt + 1);
-    k_chunk_stats<<<static_cast<unsigned>(ceil_div(plan.n_chunks, 128)), 128, 0, s>>>(
-        tmaxS, tmaxN, nt, plan.ch, plan.n_chunks, cmaxS, cmaxN);
+    launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
+               static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb,
+               static_cast<int>(self), P, shard, cmaxS, cmaxN, plan.off, counters);
     PDB_CUDA(cudaGetLastError());
     launches += 2;
 
@@ -1320,7 +1499,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     screen_and_recheck(ctx, s, DP, mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
-                           k_recheck<<<ctx.sm_count * 16, 256, 0, s>>>(
+                           launch_pdl(k_recheck, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2);
@@ -1343,7 +1522,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     if (stats) *stats = pdb_join_stats{};
     out->count = 0;
     if (nL == 0 || nR == 0) return;
-    PhaseTimer tm(stats != nullptr, s);
+    PhaseTimer tm(stats != nullptr && (o.flags & PDB_JOIN_PHASE_TIMES) != 0, s);
     int launches = 0;
     tm.mark(0);
     const int DP = padded_dim_bf16(d);
@@ -1361,12 +1540,12 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     const uint16_t *XL = d_L, *XR = d_R;
     if (!direct) {
         padL.reset(static_cast<size_t>(nL) * DP, s);
-        k_pad_bf16<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, DP, padL.p);
+        launch_pdl(k_pad_bf16, dim3(static_cast<unsigned>(ceil_div(nL * 32, 256))), dim3(256), 0, s, d_L, nL, d, DP, padL.p);
         launches++;
         XL = padL.p;
         if (!self) {
             padR.reset(static_cast<size_t>(nR) * DP, s);
-            k_pad_bf16<<<static_cast<unsigned>(ceil_div(nR * 32, 256)), 256, 0, s>>>(d_R, nR, d, DP, padR.p);
+            launch_pdl(k_pad_bf16, dim3(static_cast<unsigned>(ceil_div(nR * 32, 256))), dim3(256), 0, s, d_R, nR, d, DP, padR.p);
             launches++;
             XR = padR.p;
         } else {
@@ -1381,14 +1560,19 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
                s);
     UnitPlan plan;
     plan.off = ar.take<int64_t>(nt_ + 2);
-    plan_units(ctx, nL, nR, self, P, shard, s, plan);
+    plan_units(ctx, nL, nR, self, P, shard, plan);
     const int nt = plan.nt;
     float* hL = ar.take<float>(nL);
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     unsigned long long* counters = ar.take<unsigned long long>(5);
-    k_prep_cos<<<static_cast<unsigned>(ceil_div(nL * 32, 256)), 256, 0, s>>>(d_L, nL, d, cmarg, hL,
+    launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(nullptr),
+               static_cast<const float*>(nullptr), nt, plan.ch, plan.n_chunks, plan.n_rb,
+               static_cast<int>(self), P, shard, static_cast<float*>(nullptr),
+               static_cast<float*>(nullptr), plan.off, counters);
+    launches++;
+    launch_pdl(k_prep_cos, dim3(static_cast<unsigned>(ceil_div(nL * 32, 256))), dim3(256), 0, s, d_L, nL, d, cmarg, hL,
                                                                             nullptr, 0);
-    k_prep_cos<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(nt) * BN * 32, 256)), 256, 0, s>>>(
+    launch_pdl(k_prep_cos, dim3(static_cast<unsigned>(ceil_div(static_cast<int64_t>(nt) * BN * 32, 256))), dim3(256), 0, s, 
         d_R, nR, d, cmarg, nullptr, gR, static_cast<int64_t>(nt) * BN);
     PDB_CUDA(cudaGetLastError());
     launches += 2;
@@ -1411,7 +1595,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
                        counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
-                           k_recheck_cos<<<ctx.sm_count * 16, 256, 0, s>>>(
+                           launch_pdl(k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, min_cos, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2);

@@ -98,6 +98,25 @@ struct Arena {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel.
 PDB_HIDDEN void set_max_smem(const void* func, int bytes);
 
+// Launch with programmatic stream serialisation: the kernel may be
+// scheduled while its stream predecessor drains; it must call
+// ptx::pdl_wait() before reading anything the predecessor wrote.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+}
+
 // ---- K1 launchers (histogram.cu) -----------------------------------------
 PDB_HIDDEN int hist_dim(int32_t bins, int32_t mode);
 PDB_HIDDEN void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H,

@@ -51,6 +51,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "memory");
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+// Kernels of the join chain are launched with programmatic stream
+// serialisation (launch_pdl): each lets its dependent grid be scheduled
+// early (launch_dependents) and waits for its predecessor grid to complete
+// and flush (wait) before touching the predecessor's outputs.  Both are
+// no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- TMA ----------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

@@ -158,10 +158,11 @@ class JoinResult:
 
 
 def _opts(self_join: bool, sort: bool, shard: Tuple[int, int], stream=None,
-          tf32: bool = False) -> capi.JoinOpts:
+          tf32: bool = False, phase_times: bool = False) -> capi.JoinOpts:
     o = capi.JoinOpts()
     o.flags = ((capi.PDB_JOIN_SELF if self_join else 0) | (capi.PDB_JOIN_SORTED if sort else 0) |
-               (capi.PDB_JOIN_TF32 if tf32 else 0))
+               (capi.PDB_JOIN_TF32 if tf32 else 0) |
+               (capi.PDB_JOIN_PHASE_TIMES if phase_times else 0))
     o.shard_index, o.shard_count = int(shard[0]), int(shard[1])
     o.stream = stream
     return o
@@ -285,7 +286,7 @@ class _CudaArray:
 
 def cosine_join_bf16_device(L, R, min_cos: float, *, self_join: bool = False, sort: bool = False,
                             shard: Tuple[int, int] = (0, 1), out: Optional["DevicePairs"] = None,
-                            stream=None) -> "DevicePairs":
+                            stream=None, phase_times: bool = False) -> "DevicePairs":
     """Device cosine join on CUDA bf16 torch tensors; the result stays in HBM."""
     import torch
     assert L.is_cuda and L.dtype == torch.bfloat16 and L.is_contiguous()
@@ -296,7 +297,7 @@ def cosine_join_bf16_device(L, R, min_cos: float, *, self_join: bool = False, so
         assert R.is_cuda and R.dtype == torch.bfloat16 and R.is_contiguous()
         Rp, nR = R.data_ptr(), int(R.shape[0])
     s = stream if stream is not None else torch.cuda.current_stream(L.device)
-    o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream))
+    o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream), phase_times=phase_times)
     res = out if out is not None else DevicePairs()
     _check(capi.lib().pdb_cosine_join_bf16_dev(L.data_ptr(), nL, Rp, nR, d, float(min_cos),
                                                C.byref(o), C.byref(res._p), C.byref(res.stats)))
@@ -305,8 +306,9 @@ def cosine_join_bf16_device(L, R, min_cos: float, *, self_join: bool = False, so
 
 def sim_join_device(L, R, tau: float, *, self_join: bool = False, sort: bool = False,
                     shard: Tuple[int, int] = (0, 1), out: Optional[DevicePairs] = None,
-                    stream=None, tf32: bool = False) -> DevicePairs:
-    """Device threshold join on CUDA torch tensors; the result stays in HBM."""
+                    stream=None, tf32: bool = False, phase_times: bool = False) -> DevicePairs:
+    """Device threshold join on CUDA torch tensors; the result stays in HBM.
+    ``phase_times`` fills ``stats.*_ms`` (CUDA events between the phases)."""
     import torch
     assert L.is_cuda and L.dtype == torch.float32 and L.is_contiguous()
     nL, d = int(L.shape[0]), int(L.shape[1])
@@ -316,7 +318,8 @@ def sim_join_device(L, R, tau: float, *, self_join: bool = False, sort: bool = F
         assert R.is_cuda and R.dtype == torch.float32 and R.is_contiguous()
         Rp, nR = R.data_ptr(), int(R.shape[0])
     s = stream if stream is not None else torch.cuda.current_stream(L.device)
-    o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream), tf32=tf32)
+    o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream), tf32=tf32,
+              phase_times=phase_times)
     res = out if out is not None else DevicePairs()
     _check(capi.lib().pdb_sim_join_dev(L.data_ptr(), nL, Rp, nR, d, float(tau), C.byref(o),
                                        C.byref(res._p), C.byref(res.stats)))

@@ -34,10 +34,10 @@ for k in range(6):
     flush.zero_()
     torch.cuda.synchronize()
     if which == "c4":
-        patchdb.cosine_join_bf16_device(X, R, tau, self_join=self_join, out=out)
+        patchdb.cosine_join_bf16_device(X, R, tau, self_join=self_join, out=out, phase_times=True)
     else:
         patchdb.sim_join_device(X, R, tau, self_join=self_join, out=out,
-                                tf32=os.environ.get("PDB_TF32") == "1")
+                                tf32=os.environ.get("PDB_TF32") == "1", phase_times=True)
     st = out.stats
     if k >= 2:
         print(f"{which}: pairs={st.pairs} cand={st.candidates} tiles={st.tiles} prep={st.prep_ms:.3f} "
