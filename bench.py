@@ -13,6 +13,10 @@ pairs out, copies inside the timed region.  The join alone is reported in
 Gpairs/s (N(N-1)/2 candidate pairs per step).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3|c4|c5]
+
+--workload c1/c3/c4/c5 prints the join-only line of that BASELINE config
+instead (bench_join.py); the default line is config 2.
 
 N > 1 runs under torchrun, one process per GPU: each rank featurizes its
 frame shard, the 64,000 features are all-gathered over NCCL (16 MB), and
@@ -479,11 +483,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c2 (default, the headline): featurize -> join pipeline; c1/c3/c4/c5: "
+                         "the join-only configs of BASELINE.json (bench_join.py)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)
+    if args.workload != "c2":
+        import bench_join
+        if args.impl == "reference":
+            return bench_join.run_reference(args, rank, world, args.workload, METRIC)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
@@ -500,6 +511,10 @@ def main():
         else:
             dist.init_process_group(backend)
     try:
+        if args.workload != "c2":
+            import bench_join
+            return bench_join.run_ours(args, rank, world, local_rank, args.workload, METRIC,
+                                       peaks()[0], ClockSampler)
         return run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:

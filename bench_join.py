@@ -1,0 +1,326 @@
+"""Join-only benchmark lines for BASELINE.json's configs 1, 3, 4 and 5
+(``python bench.py --workload c1|c3|c4|c5``; the default bench line is
+config 2, the featurize -> join pipeline).
+
+One step = one full threshold join of the configured relations, device
+resident (``pdb_sim_join_dev`` / ``pdb_cosine_join_bf16_dev``), L2 flushed
+before each step.  ``value`` is candidate pairs per second over the whole
+job (N(N-1)/2 for a self-join, nL*nR for a cross join: the GPU is not
+credited for the lower triangle it skips), in Gpairs/s.  ``e2e`` is the same
+join through the host C-ABI call (pinned host relations in, host pairs out).
+
+Multi-GPU (torchrun, one process per GPU): rank 0 generates the relations
+and broadcasts them once over NCCL (timed separately as ``setup``); every
+rank then scans its boustrophedon share of L's 128-row blocks against all of
+R (``pdb_join_opts.shard_*``), pairs stay on the rank that found them and
+the pair counts are all-reduced.  Strong scaling: the join is fixed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+
+JOINS = {
+    "c1": dict(workload="config1_selfjoin: 20,000 x 64 fp32, 200 Gaussian clusters (sigma 0.02), "
+                        "L1-normalised, seed 0; L2 self-join eps=0.05, (i<j) pairs",
+               kind="l2", self_join=True, tau=0.05),
+    "c3": dict(workload="config3_cross: 1,048,576 x 1,048,576 fp32 d=128, 10,000-cluster mixture "
+                        "(sigma 0.01), 0.5% planted near-duplicates (sigma 1e-3), seed 3; "
+                        "L2 join eps=0.02, L row-sharded",
+               kind="l2", self_join=False, tau=0.02),
+    "c4": dict(workload="config4_cosine: 200,000 x 2048 bf16 normalize(ReLU(P z)), seed 4, "
+                        "0.5% planted near-duplicates; cosine self-join >= 0.95",
+               kind="cos", self_join=True, tau=0.95),
+    "c5": dict(workload="config5_skewed: 4,194,304 x 64 fp32, 20% in 50 simplex clusters "
+                        "(sigma 1e-3), 80% Dirichlet(1), seed 5; L2 self-join eps=0.01",
+               kind="l2", self_join=True, tau=0.01),
+}
+
+
+def _gen(which):
+    from paper_1812_07607_b200 import workloads
+    if which == "c1":
+        return workloads.config1(), None
+    if which == "c3":
+        L, R, _, _ = workloads.config3()
+        return L, R
+    if which == "c4":
+        return workloads.bf16_bits(workloads.config4(device="cuda")), None
+    if which == "c5":
+        return workloads.config5(), None
+    raise ValueError(which)
+
+
+def _cpu_baseline(which, L, R, cfg, threads):
+    """The reference (oracle/_ref, ball tree build + balltree_within probes)
+    for the L2 configs, the C restatement for the restated cosine config, on
+    a bounded random sample of probe rows, extrapolated to the full join."""
+    from oracle import oracle
+    rng = np.random.default_rng(1)
+    n = L.shape[0]
+    cand = n * (n - 1) / 2 if cfg["self_join"] else n * R.shape[0]
+    if cfg["kind"] == "l2":
+        rows = int(os.environ.get("PDB_REF_PROBE_ROWS", {"c1": 2048, "c3": 512, "c5": 512}[which]))
+        idx = np.sort(rng.choice(n, size=min(rows, n), replace=False))
+        sub = np.ascontiguousarray(L[idx])
+        Rf = L if cfg["self_join"] else R
+        _, t_build, t_probe = oracle.ref_join_probe_timed(sub, Rf, cfg["tau"], False, 0,
+                                                          sub.shape[0], threads)
+        t = t_build + t_probe * n / sub.shape[0]
+        kind = "reference"
+        sample = (f"reference build_balltree({Rf.shape[0]}) + balltree_within for {sub.shape[0]} "
+                  f"random probe rows on {threads} threads (build {t_build:.2f} s, probes "
+                  f"{t_probe:.2f} s), extrapolated to {n} probes")
+    else:
+        rows = int(os.environ.get("PDB_REF_PROBE_ROWS", 64))
+        t0 = time.perf_counter()
+        oracle.cosine_join_bf16(L, None, cfg["tau"], self_join=True, rows=(0, rows),
+                                threads=threads)
+        t_s = time.perf_counter() - t0
+        # rows i < rows of the upper triangle: sum_{i<rows} (n-1-i) pairs
+        done = rows * (n - 1) - rows * (rows - 1) / 2
+        t = t_s * cand / done
+        kind = "port"
+        sample = (f"C restatement (oracle/pdb_oracle.c orc_cosine_join_bf16, fp64) on probe rows "
+                  f"0..{rows - 1} ({done:.3g} of {cand:.3g} pairs, {t_s:.2f} s) on {threads} "
+                  f"threads, extrapolated")
+    return {"value": cand / t / 1e9, "unit": "Gpairs/s", "cores": threads, "kind": kind,
+            "sample": sample, "extrapolated_s": t}
+
+
+def run_reference(args, rank, world, which, metric):
+    if rank != 0:
+        return 0
+    cfg = JOINS[which]
+    if which == "c4":  # the generator runs on torch; keep it on the CPU in this arm
+        from paper_1812_07607_b200 import workloads
+        L, R = workloads.bf16_bits(workloads.config4(device="cpu")), None
+    else:
+        L, R = _gen(which)
+    threads = os.cpu_count() or 1
+    vals = []
+    base = None
+    for k in range(args.warmup + args.steps):
+        base = _cpu_baseline(which, L, R, cfg, threads)
+        if k >= args.warmup:
+            vals.append(base["value"])
+    v = statistics.mean(vals)
+    base["value"] = v
+    n = L.shape[0]
+    cand = n * (n - 1) / 2 if cfg["self_join"] else n * R.shape[0]
+    print(json.dumps({
+        "impl": "reference", "metric": metric, "value": v, "unit": "Gpairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cand / (v * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if cfg["kind"] == "l2" else "bf16/f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": n, "candidate_pairs": cand},
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "Gpairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+def run_ours(args, rank, world, local_rank, which, metric, peaks, clock_sampler):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_07607_b200 import _capi as capi
+    from paper_1812_07607_b200 import patchdb
+
+    cfg = JOINS[which]
+    dev_index = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    lib = capi.lib()
+    cos = cfg["kind"] == "cos"
+    dt = torch.int16 if cos else torch.float32
+
+    # ---- data: generated on rank 0, broadcast once over NCCL --------------
+    if rank == 0:
+        Lh, Rh = _gen(which)
+        shape_L = list(Lh.shape)
+        shape_R = list(Rh.shape) if Rh is not None else [0, 0]
+    else:
+        Lh = Rh = None
+        shape_L = shape_R = None
+    if world > 1:
+        box = [shape_L, shape_R]
+        dist.broadcast_object_list(box, src=0)
+        shape_L, shape_R = box
+    Ld = (torch.from_numpy(Lh.view(np.int16) if cos else Lh).to(dev) if rank == 0
+          else torch.empty(shape_L, dtype=dt, device=dev))
+    Rd = None
+    if shape_R[0]:
+        Rd = torch.from_numpy(Rh).to(dev) if rank == 0 else torch.empty(shape_R, dtype=dt,
+                                                                         device=dev)
+    setup_ms = 0.0
+    if world > 1:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dist.broadcast(Ld, src=0)
+        if Rd is not None:
+            dist.broadcast(Rd, src=0)
+        e1.record()
+        torch.cuda.synchronize()
+        setup_ms = e0.elapsed_time(e1)
+    nL, d = shape_L
+    nR = shape_R[0] if Rd is not None else nL
+    cand = nL * (nL - 1) / 2 if cfg["self_join"] else float(nL) * nR
+
+    stream = torch.cuda.current_stream(dev)
+    sptr = C.c_void_p(stream.cuda_stream)
+    pairs = patchdb.DevicePairs()
+
+    def opts(phases):
+        o = capi.JoinOpts()
+        o.flags = ((capi.PDB_JOIN_SELF if cfg["self_join"] else 0) |
+                   (capi.PDB_JOIN_PHASE_TIMES if phases else 0))
+        o.shard_index, o.shard_count = rank, world
+        o.stream = sptr
+        return o
+
+    o_plain, o_ph = opts(False), opts(True)
+    Rp = Rd.data_ptr() if Rd is not None else Ld.data_ptr()
+    fn = lib.pdb_cosine_join_bf16_dev if cos else lib.pdb_sim_join_dev
+
+    def join(phases):
+        rc = fn(Ld.data_ptr(), nL, Rp, nR, d, float(cfg["tau"]),
+                C.byref(o_ph if phases else o_plain), C.byref(pairs._p), C.byref(pairs.stats))
+        assert rc == 0, capi.last_error()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times, screen, recheck, prep, launches = [], [], [], [], 0
+
+    def step(timed, phases=False):
+        nonlocal launches
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        join(phases)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if timed and not phases:
+            times.append(ev0.elapsed_time(ev1))
+            launches += pairs.stats.launches
+        if timed and phases:
+            st = pairs.stats
+            screen.append(st.screen_ms)
+            recheck.append(st.recheck_ms)
+            prep.append(st.prep_ms)
+
+    for _ in range(args.warmup):
+        step(False)
+    sampler = clock_sampler(dev_index)
+    sampler.__enter__()
+    for _ in range(args.steps):
+        step(True)
+    for _ in range(args.steps):
+        step(True, phases=True)
+
+    def maxred(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = maxred(statistics.mean(times))
+    ms_screen = maxred(statistics.mean(screen))
+    ms_recheck = maxred(statistics.mean(recheck))
+    ms_prep = maxred(statistics.mean(prep))
+    tot = torch.tensor([pairs.count, pairs.stats.candidates], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    n_pairs, n_cand = int(tot[0]), int(tot[1])
+    pairs.free()
+
+    # ---- e2e: pinned host relations -> host C-ABI call -> host pairs --------
+    e2e_steps = 1 if which == "c5" else max(1, min(args.steps, 3))
+    Lhost = torch.empty(tuple(shape_L), dtype=dt, pin_memory=True)
+    Lhost.copy_(Ld)
+    Rhost = None
+    if Rd is not None:
+        Rhost = torch.empty(tuple(shape_R), dtype=dt, pin_memory=True)
+        Rhost.copy_(Rd)
+    hfn = lib.pdb_cosine_join_bf16 if cos else lib.pdb_sim_join
+    e2e_t = []
+    d2h = 0
+    for k in range(e2e_steps + 1):
+        if world > 1:
+            dist.barrier()
+        o = opts(False)
+        o.stream = None
+        pr = capi.Pairs()
+        t0 = time.perf_counter()
+        rc = hfn(Lhost.data_ptr(), nL, Rhost.data_ptr() if Rhost is not None else Lhost.data_ptr(),
+                 nR, d, float(cfg["tau"]), C.byref(o), C.byref(pr))
+        t1 = time.perf_counter()
+        assert rc == 0, capi.last_error()
+        d2h = int(pr.count) * 12
+        lib.pdb_pairs_free(C.byref(pr))
+        if k > 0:  # first call warms the pool / host allocator
+            e2e_t.append(t1 - t0)
+    sampler.__exit__()
+    e2e_s = maxred(statistics.mean(e2e_t))
+    h2d = Lhost.numel() * Lhost.element_size() + (Rhost.numel() * Rhost.element_size()
+                                                  if Rhost is not None else 0)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            Lc = Lhost.numpy().view(np.uint16) if cos else Lhost.numpy()
+            Rc = None if Rhost is None else Rhost.numpy()
+            cpu = _cpu_baseline(which, Lc, Rc, cfg, os.cpu_count() or 1)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "Gpairs/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        bpeak = peaks.get("bf16_tflops") or 1590.0
+        flops = cand * 2 * d
+        screen_tf = flops / world / (ms_screen * 1e-3) / 1e12  # one rank's share of the flops
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        out_gbs = n_pairs * 12 / world / (ms_recheck * 1e-3) / 1e9 if ms_recheck > 0 else None
+        line = {
+            "metric": metric, "value": cand / (ms * 1e-3) / 1e9, "unit": "Gpairs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16 screen / f64 exact" if not cos else "bf16 screen / f64 exact (cosine)",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "nL": nL, "nR": nR, "d": d,
+                       "threshold": cfg["tau"], "candidate_pairs": cand,
+                       "l2": "flushed (256 MB write) before each step",
+                       "parallelism": f"L row blocks boustrophedon x{world}, R broadcast once"},
+            "pairs": n_pairs, "candidates": n_cand,
+            "phase_ms": {"prep": ms_prep, "screen": ms_screen, "recheck": ms_recheck},
+            "setup_ms": {"broadcast": setup_ms},
+            "roofline": {"kernel": "k_screen (K2, tcgen05 kind::f16 on bf16 screen copies)",
+                         "bound": "tensor", "achieved": screen_tf, "peak": bpeak,
+                         "unit": "TFLOP/s", "frac": screen_tf / bpeak,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                         "algorithmic": f"{cand:.4g} candidate pairs x 2*{d} flop",
+                         "ms": ms_screen, "traffic": None},
+            "roofline_output": {"kernel": "k_recheck (K3)", "bound": "hbm",
+                                "achieved": out_gbs, "peak": hbm, "unit": "GB/s",
+                                "frac": out_gbs / hbm if out_gbs else None,
+                                "algorithmic": "12 B per emitted pair"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cand / e2e_s / 1e9, "unit": "Gpairs/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3,
+                    "api": ("pdb_cosine_join_bf16" if cos else "pdb_sim_join") +
+                           " (pinned host relations -> host pairs)"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line))
+    return 0

@@ -44,3 +44,18 @@ def test_bench_two_ranks_same_pairs():
     one = getattr(_run, "one", None) or _run([sys.executable, "bench.py", "--steps", "3",
                                               "--warmup", "3", "--no-cpu-baseline"])
     assert d["pairs"] == one["pairs"]
+
+
+def test_bench_join_workload_c1_and_two_ranks():
+    """--workload c1 (join-only line) and its two-rank sharded variant find
+    the same pair count (config 1: 1,001,804 pairs)."""
+    one = _run([sys.executable, "bench.py", "--workload", "c1", "--steps", "3", "--warmup", "3"])
+    assert KEYS <= set(one)
+    assert one["unit"] == "Gpairs/s" and one["pairs"] == 1001804
+    assert one["cpu_baseline"]["kind"] == "reference" and one["cpu_baseline"]["value"] > 0
+    assert 0 < one["roofline"]["frac"] < 1.5
+    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+                "2", "--master-addr", "127.0.0.1", "--master-port", "29534", "bench.py",
+                "--gpus", "2", "--workload", "c1", "--steps", "2", "--warmup", "3"],
+               env={"PDB_DIST_BACKEND": "gloo"})
+    assert two["n_gpus"] == 2 and two["pairs"] == one["pairs"]
