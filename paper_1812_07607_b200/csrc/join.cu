@@ -837,30 +837,34 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 // K3: exact re-check.  The fp64 chain is written with explicit _rn
 // intrinsics so it can never be contracted into FMAs: diff = a - b,
 // acc = acc + diff * diff, sequential in k, then sqrt -- src/index.cpp:69-76.
+// The reference chain, reading each row 32 bytes per load (sm_100's
+// 256-bit LDG): a lane's load touches one 128-byte line, so the L1 data
+// pipe -- which bounds this kernel, the rows of different lanes being
+// unrelated -- spends one wavefront per 32 bytes instead of per 16.
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
 __device__ __forceinline__ double exact_dist(const float* __restrict__ a,
-                                             const float* __restrict__ b, int d, bool vec4) {
+                                             const float* __restrict__ b, int d, bool vec8) {
     double acc = 0.0;
-    if (vec4) {
-        const float4* a4 = reinterpret_cast<const float4*>(a);
-        const float4* b4 = reinterpret_cast<const float4*>(b);
-        for (int k = 0; k < d / 4; k++) {
-            const float4 x = __ldg(a4 + k), y = __ldg(b4 + k);
-            double t;
-            t = __dsub_rn(static_cast<double>(x.x), static_cast<double>(y.x));
-            acc = __dadd_rn(acc, __dmul_rn(t, t));
-            t = __dsub_rn(static_cast<double>(x.y), static_cast<double>(y.y));
-            acc = __dadd_rn(acc, __dmul_rn(t, t));
-            t = __dsub_rn(static_cast<double>(x.z), static_cast<double>(y.z));
-            acc = __dadd_rn(acc, __dmul_rn(t, t));
-            t = __dsub_rn(static_cast<double>(x.w), static_cast<double>(y.w));
-            acc = __dadd_rn(acc, __dmul_rn(t, t));
+    auto step = [&](float x, float y) {
+        const double t = __dsub_rn(static_cast<double>(x), static_cast<double>(y));
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+    };
+    if (vec8) {
+        for (int k = 0; k < d; k += 8) {
+            float x[8], y[8];
+            ldg256(a + k, x);
+            ldg256(b + k, y);
+#pragma unroll
+            for (int q = 0; q < 8; q++) step(x[q], y[q]);
         }
     } else {
-        for (int k = 0; k < d; k++) {
-            const double t = __dsub_rn(static_cast<double>(__ldg(a + k)),
-                                       static_cast<double>(__ldg(b + k)));
-            acc = __dadd_rn(acc, __dmul_rn(t, t));
-        }
+        for (int k = 0; k < d; k++) step(__ldg(a + k), __ldg(b + k));
     }
     return __dsqrt_rn(acc);
 }
@@ -878,8 +882,8 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
     ptx::pdl_trigger();
     const unsigned long long n = min(*n_rec, cap);
     const int lane = threadIdx.x & 31;
-    const bool vec4 =
-        (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 16 == 0);
+    const bool vec8 =
+        (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 32 == 0);
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
                                    (threadIdx.x & ~31u);
@@ -897,7 +901,7 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
                 mask &= mask - 1;
                 j = rc.y + k;
                 dist = exact_dist(L + static_cast<int64_t>(rc.x) * d,
-                                  R + static_cast<int64_t>(j) * d, d, vec4);
+                                  R + static_cast<int64_t>(j) * d, d, vec8);
                 ok = dist <= tau;
             }
             const uint32_t ball = __ballot_sync(0xffffffffu, ok);
@@ -990,10 +994,43 @@ __global__ void k_prep_cos(const uint16_t* __restrict__ X, int64_t n, int d, dou
     }
 }
 
+// Same contract as orc_cosine_join_bf16: dot, |a|^2, |b|^2 accumulated in
+// k order in fp64 from the exact bf16 values; rows are read 8 columns per
+// 16-byte load, 64 columns per batch of loads.
 __device__ __forceinline__ double exact_cos(const uint16_t* __restrict__ a,
                                             const uint16_t* __restrict__ b, int d) {
     double dot = 0.0, na = 0.0, nb = 0.0;
-    for (int k = 0; k < d; k++) {
+    auto step = [&](uint32_t xa, uint32_t yb) {  // two bf16 columns per word
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const double x = __uint_as_float(h ? (xa & 0xFFFF0000u) : (xa << 16));
+            const double y = __uint_as_float(h ? (yb & 0xFFFF0000u) : (yb << 16));
+            dot = __dadd_rn(dot, __dmul_rn(x, y));
+            na = __dadd_rn(na, __dmul_rn(x, x));
+            nb = __dadd_rn(nb, __dmul_rn(y, y));
+        }
+    };
+    int k = 0;
+    if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+        const uint4* a8 = reinterpret_cast<const uint4*>(a);
+        const uint4* b8 = reinterpret_cast<const uint4*>(b);
+        for (; k + 64 <= d; k += 64) {
+            uint4 x[8], y[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                x[q] = __ldg(a8 + k / 8 + q);
+                y[q] = __ldg(b8 + k / 8 + q);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                step(x[q].x, y[q].x);
+                step(x[q].y, y[q].y);
+                step(x[q].z, y[q].z);
+                step(x[q].w, y[q].w);
+            }
+        }
+    }
+    for (; k < d; k++) {
         const double x = bf16_to_f32(__ldg(a + k)), y = bf16_to_f32(__ldg(b + k));
         dot = __dadd_rn(dot, __dmul_rn(x, y));
         na = __dadd_rn(na, __dmul_rn(x, x));
@@ -1499,7 +1536,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     screen_and_recheck(ctx, s, DP, mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
-                           launch_pdl(k_recheck, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
+                           launch_pdl(k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2);
