@@ -66,6 +66,8 @@ constexpr int BN = 256;  // R rows per tile (UMMA N)
 constexpr int BK = 32;   // fp32 per 128-byte swizzle row (64 for bf16)
 constexpr int kABytes = BM * BK * 4;  // 16 KB per K-block of A
 constexpr int kBBytes = BN * BK * 4;  // 32 KB per K-block of B
+constexpr int kGCols = 16;            // folded-g row: 3 bf16 parts + zeros (one K=16 step)
+constexpr int kGBytes = BN * kGCols * 2;  // 8 KB per 256-row g block
 #ifndef PDB_EPI_WARPS
 #define PDB_EPI_WARPS 8
 #endif
@@ -159,6 +161,25 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
 // ~12 KB per 128x256x(32 B of K) step, so bf16 operands -- twice the K per
 // byte -- run the same screen about twice as fast as tf32; the wider margin
 // band costs only candidates, which the exact re-check discards.)
+// Shared-memory plan of k_screen, shared by the kernel and its launcher.
+// Resident A is double-buffered when it fits, so the next work unit's rows
+// load while the current unit's tiles are still multiplying.
+template <int DP, bool A_RES, int STAGES, int MODE>
+struct ScreenSmem {
+    static constexpr bool AUG = MODE == kModeL2Bf16Aug;
+    static constexpr int KE = MODE != kModeL2Tf32 ? 64 : 32;
+    static constexpr int NKB = DP / KE;
+    static constexpr int kStage = A_RES ? kBBytes : (kABytes + kBBytes);
+    // one A slot: NKB 128B-swizzled K-blocks (+ the 32B-swizzled folded-g block)
+    static constexpr int kASlot = A_RES ? (NKB * kABytes + (AUG ? BM * kGCols * 2 : 0) + 1023) / 1024 * 1024 : 0;
+    static constexpr int kTail = 256 + kEpiWarps * kColsPerWarp * 4 + kEpiWarps * 32 * 16 + 128;
+    static constexpr size_t bytes(int slots) {
+        return 1024 + static_cast<size_t>(slots) * kASlot + static_cast<size_t>(STAGES) * kStage + kTail;
+    }
+    static constexpr int kASlots = (A_RES && bytes(2) <= 232448) ? 2 : 1;
+    static constexpr size_t kBytes = bytes(kASlots);
+};
+
 template <int DP, bool A_RES, int STAGES, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -170,8 +191,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     constexpr int KE = BF16 ? 64 : 32;  // elements per 128-byte K-block
     constexpr int NKB = DP / KE;
     constexpr int NKL = NKB + (AUG ? 1 : 0);  // K-blocks streamed per tile (+ the g block)
-    constexpr int kStageBytes = A_RES ? kBBytes : (kABytes + kBBytes);
-    constexpr int kAResBytes = A_RES ? NKL * kABytes : 0;
+    using SM = ScreenSmem<DP, A_RES, STAGES, MODE>;
+    constexpr int kStageBytes = SM::kStage;
+    constexpr int kASlot = SM::kASlot;
+    constexpr int kASlots = SM::kASlots;
+    constexpr int kAResBytes = kASlots * kASlot;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = ptx::smem_u32(smem_raw);
@@ -181,12 +205,12 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     uint64_t* bars = reinterpret_cast<uint64_t*>(smS + STAGES * kStageBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
-    uint64_t* a_full = bars + 2 * STAGES;
-    uint64_t* a_empty = a_full + 1;
-    uint64_t* t_full = a_full + 2;   // [2]
-    uint64_t* t_empty = a_full + 4;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
-    float* g_smem = reinterpret_cast<float*>(a_full + 8);  // [epilogue warps][kColsPerWarp]
+    uint64_t* a_full = bars + 2 * STAGES;   // [2] (one per A slot)
+    uint64_t* a_empty = a_full + 2;         // [2]
+    uint64_t* t_full = a_full + 4;          // [2]
+    uint64_t* t_empty = a_full + 6;         // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
+    float* g_smem = reinterpret_cast<float*>(a_full + 10);  // [epilogue warps][kColsPerWarp]
     int4* r_smem = reinterpret_cast<int4*>(g_smem + kEpiWarps * kColsPerWarp);  // [warps][32] records
     // dynamic scheduler: the producer claims work units with one global
     // atomic and hands them to the MMA and epilogue warps through a 4-slot ring
@@ -201,8 +225,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(a_full, 1);
-        ptx::mbar_init(a_empty, 1);
+        for (int a = 0; a < 2; a++) {
+            ptx::mbar_init(&a_full[a], 1);
+            ptx::mbar_init(&a_empty[a], 1);
+        }
         for (int a = 0; a < 2; a++) {
             ptx::mbar_init(&t_full[a], 1);
             ptx::mbar_init(&t_empty[a], kEpiWarps);
@@ -220,13 +246,14 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     }
     if (AUG) {
         // constant A block for the folded g: every row is [1, 1, 1, 0, ...]
-        // (bf16), written in the 128B-swizzled K-major layout TMA would use:
-        // logical 16-byte chunk c of row r sits at chunk c ^ (r & 7).
-        uint4* xa = reinterpret_cast<uint4*>(smA + NKB * kABytes);
-        for (int q = threadIdx.x; q < BM * 8; q += blockDim.x) {
-            const int r = q >> 3, c = q & 7;
-            xa[q] = c == (r & 7) ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u)
-                                 : make_uint4(0u, 0u, 0u, 0u);
+        // (16 bf16), written in the 32B-swizzled K-major layout: logical
+        // 16-byte chunk c of 32-byte row r sits at chunk c ^ ((r >> 2) & 1).
+        for (int q = threadIdx.x; q < kASlots * BM * 2; q += blockDim.x) {
+            const int slot = q / (BM * 2), qq = q % (BM * 2);
+            const int r = qq >> 1, c = qq & 1;
+            reinterpret_cast<uint4*>(smA + slot * kASlot + NKB * kABytes)[qq] =
+                c == ((r >> 2) & 1) ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u)
+                                    : make_uint4(0u, 0u, 0u, 0u);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -256,12 +283,16 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         // ===================== TMA producer =====================
         if (lane == 0) {
             int stage = 0;
-            uint32_t phase = 0, a_phase = 0;
+            uint32_t phase = 0;
             int ps = 0;
             uint32_t pph = 0;
+            uint32_t na = 0;  // units whose A has been loaded
+            auto claim = [&]() -> int64_t {
+                const int64_t c = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
+                return c < p.n_units ? c : -1;
+            };
+            int64_t u = claim();
             for (;;) {
-                int64_t u = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
-                if (u >= p.n_units) u = -1;
                 ptx::mbar_wait(&u_empty[ps], pph ^ 1);
                 u_val[ps] = u;
                 ptx::mbar_arrive(&u_full[ps]);
@@ -270,19 +301,25 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     pph ^= 1;
                 }
                 if (u < 0) break;
+                // claim the next unit now: the atomic's round trip overlaps
+                // this unit's loads instead of stalling between units
+                const int64_t u_next = claim();
                 const Unit w = decode_unit(p, u);
                 if (A_RES) {
-                    ptx::mbar_wait(a_empty, a_phase ^ 1);
-                    a_phase ^= 1;
-                    ptx::mbar_arrive_expect_tx(a_full, NKB * kABytes);
+                    const uint32_t slot = na % kASlots, use = na / kASlots;
+                    ptx::mbar_wait(&a_empty[slot], (use & 1) ^ 1);
+                    ptx::mbar_arrive_expect_tx(&a_full[slot], NKB * kABytes);
                     for (int kb = 0; kb < NKB; kb++)
-                        ptx::tma_load_2d(smA + kb * kABytes, &tmA, a_full, kb * KE, w.rb * BM);
+                        ptx::tma_load_2d(smA + slot * kASlot + kb * kABytes, &tmA, &a_full[slot],
+                                         kb * KE, w.rb * BM);
+                    na++;
                 }
                 for (int J = w.j0; J < w.j1; J++) {
                     for (int kb = 0; kb < NKL; kb++) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* st = smS + stage * kStageBytes;
-                        ptx::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full[stage],
+                                                   (AUG && kb == NKB) ? kGBytes : kStageBytes);
                         if (!A_RES) {
                             ptx::tma_load_2d(st, &tmA, &full[stage], kb * KE, w.rb * BM);
                             st += kABytes;
@@ -297,21 +334,24 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         }
                     }
                 }
+                u = u_next;
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
             int stage = 0, acc = 0;
-            uint32_t phase = 0, acc_phase = 0, a_phase = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            uint32_t na = 0;  // units consumed
             unsigned long long ntiles = 0;
             for (;;) {
                 const int64_t u = take_unit(false);
                 if (u < 0) break;
                 const Unit w = decode_unit(p, u);
+                const uint32_t slot = na % kASlots;
+                uint8_t* smAu = smA + slot * kASlot;
                 if (A_RES) {
-                    ptx::mbar_wait(a_full, a_phase);
-                    a_phase ^= 1;
+                    ptx::mbar_wait(&a_full[slot], (na / kASlots) & 1);
                     ptx::tc_fence_after();
                 }
                 for (int J = w.j0; J < w.j1; J++) {
@@ -323,13 +363,21 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         ptx::tc_fence_after();
                         const uint8_t* st = smS + stage * kStageBytes;
                         const uint32_t a_addr =
-                            ptx::smem_u32(A_RES ? smA + kb * kABytes : st);
+                            ptx::smem_u32(A_RES ? smAu + kb * kABytes : st);
                         const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
-                        // the folded-g block only has data in its first K=16 slice
-                        const int nkk = (AUG && kb == NKB) ? 1 : 4;
+                        if (AUG && kb == NKB) {
+                            // the folded-g block: one K=16 step on 32-byte rows
+                            ptx::mma_f16(d_tmem, ptx::sdesc_k_sw32(a_addr),
+                                         ptx::sdesc_k_sw32(b_addr), kIdescBf16, 1u);
+                            ptx::mma_commit(&empty[stage]);
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                            continue;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
-                            if (kk >= nkk) break;
                             if (BF16)
                                 ptx::mma_f16(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescBf16,
@@ -352,7 +400,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         acc_phase ^= 1;
                     }
                 }
-                if (A_RES) ptx::mma_commit(a_empty);
+                if (A_RES) ptx::mma_commit(&a_empty[slot]);
+                na++;
             }
             atomicAdd(p.tiles, ntiles);
         }
@@ -638,10 +687,10 @@ __device__ __forceinline__ void prep_row(int64_t row, int lane, int d, int DP,
                 r -= static_cast<double>(__uint_as_float(static_cast<uint32_t>(b) << 16));
             }
         }
-        uint32_t* gw = reinterpret_cast<uint32_t*>(gx + row * 64);
+        uint32_t* gw = reinterpret_cast<uint32_t*>(gx + row * kGCols);
         const uint32_t w = lane == 0 ? (static_cast<uint32_t>(part[1]) << 16) | part[0]
                          : lane == 1 ? part[2] : 0u;
-        gw[lane] = w;
+        if (lane < kGCols / 2) gw[lane] = w;
     }
 }
 
@@ -1104,14 +1153,27 @@ CUtensorMap make_tmap(const DeviceCtx& ctx, const void* base, int64_t rows, int 
     return m;
 }
 
+// The folded-g rows: [n, kGCols] bf16, one 32-byte K=16 slice per row,
+// loaded 256 rows at a time in the 32B-swizzled layout of sdesc_k_sw32.
+CUtensorMap make_tmap_g(const DeviceCtx& ctx, const void* base, int64_t rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kGCols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kGCols) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kGCols), static_cast<cuuint32_t>(BN)};
+    const cuuint32_t estr[2] = {1, 1};
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PDB_ERR_CUDA, "cuTensorMapEncodeTiled (g) failed (" + std::to_string(r) + ")");
+    return m;
+}
+
 template <int DP, bool A_RES, int STAGES, int MODE>
 void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
                    const CUtensorMap& tG, const ScreenParams& p, cudaStream_t s) {
-    constexpr int NKL = DP / (MODE == kModeL2Tf32 ? 32 : 64) + (MODE == kModeL2Bf16Aug ? 1 : 0);
-    constexpr size_t stage_bytes = A_RES ? kBBytes : (kABytes + kBBytes);
-    constexpr size_t smem =
-        1024 + (A_RES ? NKL * kABytes : 0) + STAGES * stage_bytes + 256 + kEpiWarps * kColsPerWarp * 4 +
-        kEpiWarps * 32 * 16 + 128;
+    constexpr size_t smem = ScreenSmem<DP, A_RES, STAGES, MODE>::kBytes;
     static_assert(smem <= 232448, "shared memory budget");
     auto k = k_screen<DP, A_RES, STAGES, MODE>;
     set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
@@ -1448,10 +1510,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                    (self ? 0 : Arena::need(static_cast<size_t>(nR) * DP, es) + 2 * Arena::need(nR, 4)) +
                    Arena::need(static_cast<size_t>(nt_) * BN, 4) + 4 * Arena::need(nt_ + 1, 4) +
                    Arena::need(nt_ + 2, 8) + Arena::need(5, 8) +
-                   (fold ? Arena::need(static_cast<size_t>(nR) * 64, 2) : 0),
+                   (fold ? Arena::need(static_cast<size_t>(nR) * kGCols, 2) : 0),
                s);
     float* mu = ar.take<float>(DP);
-    uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * 64) : nullptr;
+    uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * kGCols) : nullptr;
 
     // ---- preparation ----------------------------------------------------
     launch_pdl(k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
@@ -1511,7 +1573,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
-    const CUtensorMap tG = fold ? make_tmap(ctx, gx, nR, 64, BN, true) : tB;
+    const CUtensorMap tG = fold ? make_tmap_g(ctx, gx, nR) : tB;
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;

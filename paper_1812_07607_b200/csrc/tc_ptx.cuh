@@ -173,6 +173,19 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// K-major, 32-byte swizzle (layout type 6): rows of 32 B (16 bf16 = one
+// K=16 MMA step), 8-row atoms of 256 B (SBO).  Used for the folded-g block,
+// which only has data in its first K=16 slice.
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;             // LBO (16 B) >> 4
+    d |= static_cast<uint64_t>(256 >> 4) << 32;      // SBO
+    d |= static_cast<uint64_t>(1) << 46;             // version
+    d |= static_cast<uint64_t>(6) << 61;             // SWIZZLE_32B
+    return d;
+}
+
 // Instruction descriptor, kind::tf32: D f32 (bits 4-5 = 1), A/B TF32
 // (bits 7-9, 10-12 = 2), both K-major, N >> 3 at bits 17-22, M >> 4 at 24-28.
 constexpr uint32_t idesc_tf32(int M, int N) {
