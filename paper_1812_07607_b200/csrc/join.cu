@@ -169,7 +169,9 @@ struct ScreenSmem {
     static constexpr bool AUG = MODE == kModeL2Bf16Aug;
     static constexpr int KE = MODE != kModeL2Tf32 ? 64 : 32;
     static constexpr int NKB = DP / KE;
-    static constexpr int kStage = A_RES ? kBBytes : (kABytes + kBBytes);
+    // a stage holds one K-block of B (and of A when it streams); with the
+    // folded g, the 8 KB g block rides in the same stage as the last K-block
+    static constexpr int kStage = (A_RES ? kBBytes : (kABytes + kBBytes)) + (AUG ? kGBytes : 0);
     // one A slot: NKB 128B-swizzled K-blocks (+ the 32B-swizzled folded-g block)
     static constexpr int kASlot = A_RES ? (NKB * kABytes + (AUG ? BM * kGCols * 2 : 0) + 1023) / 1024 * 1024 : 0;
     static constexpr int kTail = 256 + kEpiWarps * kColsPerWarp * 4 + kEpiWarps * 32 * 16 + 128;
@@ -190,7 +192,6 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     static_assert(!AUG || A_RES, "the folded-g mode keeps A resident");
     constexpr int KE = BF16 ? 64 : 32;  // elements per 128-byte K-block
     constexpr int NKB = DP / KE;
-    constexpr int NKL = NKB + (AUG ? 1 : 0);  // K-blocks streamed per tile (+ the g block)
     using SM = ScreenSmem<DP, A_RES, STAGES, MODE>;
     constexpr int kStageBytes = SM::kStage;
     constexpr int kASlot = SM::kASlot;
@@ -315,19 +316,18 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     na++;
                 }
                 for (int J = w.j0; J < w.j1; J++) {
-                    for (int kb = 0; kb < NKL; kb++) {
+                    for (int kb = 0; kb < NKB; kb++) {
+                        const bool with_g = AUG && kb == NKB - 1;
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* st = smS + stage * kStageBytes;
-                        ptx::mbar_arrive_expect_tx(&full[stage],
-                                                   (AUG && kb == NKB) ? kGBytes : kStageBytes);
+                        ptx::mbar_arrive_expect_tx(
+                            &full[stage], (A_RES ? kBBytes : kABytes + kBBytes) + (with_g ? kGBytes : 0));
                         if (!A_RES) {
                             ptx::tma_load_2d(st, &tmA, &full[stage], kb * KE, w.rb * BM);
                             st += kABytes;
                         }
-                        if (AUG && kb == NKB)
-                            ptx::tma_load_2d(st, &tmG, &full[stage], 0, J * BN);
-                        else
-                            ptx::tma_load_2d(st, &tmB, &full[stage], kb * KE, J * BN);
+                        ptx::tma_load_2d(st, &tmB, &full[stage], kb * KE, J * BN);
+                        if (with_g) ptx::tma_load_2d(st + kBBytes, &tmG, &full[stage], 0, J * BN);
                         if (++stage == STAGES) {
                             stage = 0;
                             phase ^= 1;
@@ -358,24 +358,13 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                     ptx::mbar_wait(&t_empty[acc], acc_phase ^ 1);
                     ptx::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                    for (int kb = 0; kb < NKL; kb++) {
+                    for (int kb = 0; kb < NKB; kb++) {
                         ptx::mbar_wait(&full[stage], phase);
                         ptx::tc_fence_after();
                         const uint8_t* st = smS + stage * kStageBytes;
                         const uint32_t a_addr =
                             ptx::smem_u32(A_RES ? smAu + kb * kABytes : st);
                         const uint32_t b_addr = ptx::smem_u32(A_RES ? st : st + kABytes);
-                        if (AUG && kb == NKB) {
-                            // the folded-g block: one K=16 step on 32-byte rows
-                            ptx::mma_f16(d_tmem, ptx::sdesc_k_sw32(a_addr),
-                                         ptx::sdesc_k_sw32(b_addr), kIdescBf16, 1u);
-                            ptx::mma_commit(&empty[stage]);
-                            if (++stage == STAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
-                            continue;
-                        }
 #pragma unroll
                         for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
                             if (BF16)
@@ -386,6 +375,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                                 ptx::mma_tf32(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
                                               ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescTf32,
                                               (kb | kk) != 0);
+                        }
+                        if (AUG && kb == NKB - 1) {
+                            // the folded-g block: one K=16 step on 32-byte rows
+                            ptx::mma_f16(d_tmem, ptx::sdesc_k_sw32(ptx::smem_u32(smAu + NKB * kABytes)),
+                                         ptx::sdesc_k_sw32(b_addr + kBBytes), kIdescBf16, 1u);
                         }
                         ptx::mma_commit(&empty[stage]);
                         if (++stage == STAGES) {
@@ -1187,7 +1181,7 @@ void dispatch_screen(int DP, int mode, const DeviceCtx& ctx, const CUtensorMap& 
                      cudaStream_t s) {
     if (mode == kModeL2Bf16Aug) {
         switch (DP) {
-            case 64: launch_screen<64, true, 5, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
+            case 64: launch_screen<64, true, 4, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
             case 128: launch_screen<128, true, 4, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
         }
         fail(PDB_ERR_CONFIG, "join: unsupported padded dimension for the folded-g screen");
