@@ -211,6 +211,23 @@ int pdb_featurize_join(const uint8_t* frames, int64_t n_frames, int32_t height, 
                        double tau, const pdb_join_opts* opts, float* features,
                        pdb_pairs* out);
 
+/* Near-duplicate grouping -- replaces run_dedup (src/query.cpp:535-566),
+ * the grouping of PlanNode::dedup (include/patchdb/query.hpp:142) and the
+ * kept set of dedup_stream (query.hpp:203-204, src/query.cpp:1063-1092).
+ * Items (rows of X [n, d] fp32) are scanned in order; item i is kept as a
+ * representative iff no kept representative lies within tau (the reference
+ * euclidean <= tau); every other item joins the nearest kept
+ * representative, the earliest on ties.  On return rep_of[i] is the index
+ * of item i's representative (i itself for representatives) and *n_reps
+ * their count.  tau < 0 -> PDB_ERR_CONFIG ("dedup needs tau >= 0"); n > 0
+ * with d < 1 -> PDB_ERR_SHAPE.  opts: only `stream` is used (_dev); shards
+ * are not supported (the scan is global).  rep_of: host (pdb_dedup) or
+ * device (pdb_dedup_dev) int64 [n]. */
+int pdb_dedup(const float* X, int64_t n, int32_t d, double tau, const pdb_join_opts* opts,
+              int64_t* rep_of, int64_t* n_reps);
+int pdb_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, const pdb_join_opts* opts,
+                  int64_t* d_rep_of, int64_t* n_reps);
+
 /* Pinned host memory helpers (the e2e path copies from pinned buffers). */
 void* pdb_host_alloc(int64_t bytes);
 void pdb_host_free(void* p);

@@ -52,6 +52,8 @@ def port():
                                            C.POINTER(OrcPairs)]
         L.orc_cosine_bf16.argtypes = [vp, vp, i64]
         L.orc_cosine_bf16.restype = f64
+        L.orc_dedup.argtypes = [vp, i64, i64, f64, vp]
+        L.orc_dedup.restype = i64
         _port = L
     return _port
 
@@ -77,6 +79,9 @@ def ref():
         L.ref_join_probe_timed.argtypes = [vp, i64, vp, i64, i32, f64, i32, i64, i64, i32,
                                            C.POINTER(f64), C.POINTER(f64)]
         L.ref_join_probe_timed.restype = i64
+        L.ref_dedup.argtypes = [vp, i64, i32, f64, vp, C.POINTER(i64)]
+        L.ref_dedup_stream.argtypes = [vp, i64, i32, f64, vp]
+        L.ref_dedup_stream.restype = i64
         _ref = L
     return _ref
 
@@ -161,6 +166,18 @@ def cosine_join_bf16(L: np.ndarray, R, min_cos: float, self_join: bool = False, 
     return res
 
 
+def dedup(X: np.ndarray, tau: float):
+    """Restated run_dedup (src/query.cpp:535-566): (rep_of int64 [n],
+    n_reps); rep_of[i] is the index of item i's representative."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n = X.shape[0]
+    rep_of = np.empty(max(n, 1), dtype=np.int64)
+    nr = port().orc_dedup(_p(X), n, X.shape[1] if X.ndim == 2 else 0, float(tau), _p(rep_of))
+    if nr < 0:
+        raise ValueError("dedup needs tau >= 0")
+    return rep_of[:n], int(nr)
+
+
 # ---- the reference itself ------------------------------------------------------
 
 def ref_featurize_tiles(frames: np.ndarray, th: int, tw: int, bins: int, threads: int = 1):
@@ -219,3 +236,26 @@ def ref_join_probe_timed(L, R, tau, self_join, p0, p1, threads):
     n = ref().ref_join_probe_timed(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
                                    int(self_join), p0, p1, threads, C.byref(b), C.byref(p))
     return n, b.value, p.value
+
+
+def ref_dedup(X, tau):
+    """PlanNode::dedup through execute() on the reference: (rep_of, n_reps),
+    or an int error code."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n = X.shape[0]
+    rep_of = np.empty(max(n, 1), dtype=np.int64)
+    nr = C.c_int64()
+    rc = ref().ref_dedup(_p(X), n, X.shape[1], float(tau), _p(rep_of), C.byref(nr))
+    if rc:
+        return rc
+    return rep_of[:n], nr.value
+
+
+def ref_dedup_stream(X, tau):
+    """dedup_stream on the reference: indices of the kept patches."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    kept = np.empty(max(X.shape[0], 1), dtype=np.int64)
+    m = ref().ref_dedup_stream(_p(X), X.shape[0], X.shape[1], float(tau), _p(kept))
+    if m < 0:
+        return int(-m)
+    return kept[:m]

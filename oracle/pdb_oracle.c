@@ -361,3 +361,38 @@ int64_t orc_sim_join_count(const float* L, int64_t nL, const float* R, int64_t n
     }
     return n;
 }
+
+/* dedup: src/query.cpp:535-566 (run_dedup), the grouping behind
+ * PlanNode::dedup and dedup_stream (src/query.cpp:1063-1092).  Items are
+ * scanned in order; an item is kept as a representative iff no kept
+ * representative lies within tau (euclidean <= tau); otherwise it joins
+ * the nearest kept representative, the earliest one on ties (strict <,
+ * representatives visited in kept order).  rep_of[i] = index of item i's
+ * representative (i for representatives); returns the number of
+ * representatives, or -1 for tau < 0 (the reference's ConfigError). */
+int64_t orc_dedup(const float* X, int64_t n, int64_t d, double tau, int64_t* rep_of) {
+    if (!(tau >= 0.0)) return -1;
+    int64_t* reps = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    if (!reps) return -2;
+    int64_t nr = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const float* x = X + (size_t)i * d;
+        int64_t best = -1;
+        double best_dist = INFINITY;
+        for (int64_t r = 0; r < nr; r++) {
+            double dist = orc_euclidean(x, X + (size_t)reps[r] * d, d);
+            if (dist <= tau && dist < best_dist) {
+                best_dist = dist;
+                best = reps[r];
+            }
+        }
+        if (best < 0) {
+            reps[nr++] = i;
+            rep_of[i] = i;
+        } else {
+            rep_of[i] = best;
+        }
+    }
+    free(reps);
+    return nr;
+}

@@ -253,3 +253,55 @@ REF_API int64_t ref_join_probe_timed(const float* L, int64_t nL, const float* R,
         return -1;
     }
 }
+
+// PlanNode::dedup over memory tuples (src/query.cpp:535-582, executed by
+// compile_dedup): item i carries the unique label "i", so each output
+// group's group_labels lists its members and its lineage parent is the
+// representative.  rep_of[i] = index of item i's representative.
+REF_API int ref_dedup(const float* X, int64_t n, int32_t d, double tau, int64_t* rep_of,
+                      int64_t* n_reps) {
+    try {
+        auto items = make_vecs(X, n, d, 1);
+        std::vector<Tuple> tuples;
+        tuples.reserve(items.size());
+        for (int64_t i = 0; i < n; i++) {
+            Patch& p = items[static_cast<size_t>(i)];
+            p.meta.emplace("label", MetaValue{std::to_string(i)});
+            LineageStep step;
+            step.op_name = "make_patch";
+            step.source = FrameId{"synthetic", 0};
+            p.lineage.push_back(std::move(step));
+            tuples.push_back(Tuple{p});
+        }
+        ExecContext ctx;
+        auto plan = PlanNode::dedup(PlanNode::memory(std::move(tuples)), tau);
+        auto res = execute(*plan, ctx);
+        for (int64_t i = 0; i < n; i++) rep_of[i] = -1;
+        for (const auto& t : res.tuples) {
+            const int64_t rep = static_cast<int64_t>(t[0].lineage[0].parent_id()) - 1;
+            for (const auto& lab : t[0].meta_str_list("group_labels"))
+                rep_of[std::stoll(lab)] = rep;
+        }
+        *n_reps = static_cast<int64_t>(res.tuples.size());
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// dedup_stream (src/query.cpp:1063-1092): indices of the kept patches, in
+// order.  Returns the count; kept must hold n entries.
+REF_API int64_t ref_dedup_stream(const float* X, int64_t n, int32_t d, double tau,
+                                 int64_t* kept) {
+    try {
+        auto items = make_vecs(X, n, d, 1);
+        auto s = dedup_stream(std::make_unique<VectorStream<Patch>>(std::move(items)), tau);
+        int64_t m = 0;
+        while (auto p = s->next()) kept[m++] = static_cast<int64_t>(p->patch_id) - 1;
+        return m;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -code_of(e);
+    }
+}

@@ -44,7 +44,7 @@ EXPORTS = (
     "pdb_color_histogram_f32", "pdb_color_histogram_f32_dev",
     "pdb_sim_join", "pdb_pairs_free", "pdb_sim_join_dev", "pdb_dev_pairs_free",
     "pdb_featurize_join", "pdb_host_alloc", "pdb_host_free",
-    "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev",
+    "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
 )
 
 
@@ -111,6 +111,8 @@ def lib() -> C.CDLL:
                                            C.POINTER(Pairs)]
         L.pdb_cosine_join_bf16_dev.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(JoinOpts),
                                                C.POINTER(DevPairs), C.POINTER(JoinStats)]
+        L.pdb_dedup.argtypes = [vp, i64, i32, f64, C.POINTER(JoinOpts), vp, C.POINTER(i64)]
+        L.pdb_dedup_dev.argtypes = [vp, i64, i32, f64, C.POINTER(JoinOpts), vp, C.POINTER(i64)]
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

@@ -475,6 +475,47 @@ PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int3
     });
 }
 
+static void check_dedup_args(const void* X, int64_t n, int32_t d, double tau,
+                             const pdb_join_opts* o) {
+    // run_dedup order: tau (src/query.cpp:536), then the dimension check
+    if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "dedup needs tau >= 0");
+    if (n < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative row count");
+    if (n > INT32_MAX) fail(PDB_ERR_INVALID_ARGUMENT, "row counts above 2^31-1 are not supported");
+    if (n > 0 && d < 1) fail(PDB_ERR_SHAPE, "dedup needs non-empty patch data");
+    if (n > 0 && !X) fail(PDB_ERR_INVALID_ARGUMENT, "null rows");
+    if (o && o->shard_count > 1) fail(PDB_ERR_INVALID_ARGUMENT, "dedup does not shard");
+}
+
+PDB_API int pdb_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau,
+                          const pdb_join_opts* opts, int64_t* d_rep_of, int64_t* n_reps) {
+    return guarded([&] {
+        if (!n_reps || (n > 0 && !d_rep_of)) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_dedup_args(d_X, n, d, tau, opts);
+        device_ctx();
+        run_dedup_dev(d_X, n, d, tau, stream_of(opts ? opts->stream : nullptr), d_rep_of, n_reps);
+    });
+}
+
+PDB_API int pdb_dedup(const float* X, int64_t n, int32_t d, double tau, const pdb_join_opts* opts,
+                      int64_t* rep_of, int64_t* n_reps) {
+    return guarded([&] {
+        if (!n_reps || (n > 0 && !rep_of)) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_dedup_args(X, n, d, tau, opts);
+        device_ctx();
+        cudaStream_t s = cudaStreamPerThread;
+        DevBuf<float> dX(static_cast<size_t>(n) * std::max(d, 1), s);
+        DevBuf<int64_t> dR(static_cast<size_t>(std::max<int64_t>(n, 1)), s);
+        if (n > 0)
+            PDB_CUDA(cudaMemcpyAsync(dX.p, X, static_cast<size_t>(n) * d * sizeof(float),
+                                     cudaMemcpyHostToDevice, s));
+        run_dedup_dev(dX.p, n, d, tau, s, dR.p, n_reps);
+        if (n > 0)
+            PDB_CUDA(cudaMemcpyAsync(rep_of, dR.p, static_cast<size_t>(n) * sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 PDB_API void* pdb_host_alloc(int64_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, static_cast<size_t>(std::max<int64_t>(bytes, 1)), cudaHostAllocDefault) !=

@@ -1,0 +1,197 @@
+// dedup.cu -- near-duplicate grouping on the tau-graph.
+//
+// Reference semantics: run_dedup (src/query.cpp:535-566) behind
+// PlanNode::dedup, and dedup_stream (src/query.cpp:1063-1092).  Items are
+// scanned in order; item i is kept as a representative iff no kept
+// representative lies within tau (euclidean <= tau, src/index.cpp:69-76);
+// otherwise it joins the nearest kept representative, the earliest on ties.
+//
+// B200 plan:
+//   1. the tau-graph: every pair i < j with euclidean <= tau, from the
+//      similarity self-join (K2 tensor-core screen + K3 exact re-check), so
+//      the graph is exactly the reference's set of "within tau" relations;
+//   2. CSR of each item's lower neighbours: keys (j << 32 | i) radix-sorted;
+//   3. the greedy scan as rounds: an undecided item becomes a non-rep as soon
+//      as one lower neighbour is a rep, and a rep once all lower neighbours
+//      are decided non-reps.  Statuses only move from undecided to final and
+//      each final value is the sequential scan's, so the rounds reproduce it
+//      exactly; a round costs one pass over the undecided items' edges;
+//   4. attach: a non-rep's representative is the rep neighbour with the
+//      smallest distance -- recomputed with the reference's fp64 chain, since
+//      ties between fp32-rounded distances need not be ties in fp64 -- the
+//      lowest index on ties.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "exact.cuh"
+#include "pdb_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace pdb {
+
+namespace {
+
+__global__ void k_graph_keys(const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                             int64_t n, unsigned long long* __restrict__ keys) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        keys[k] = (static_cast<unsigned long long>(static_cast<uint32_t>(right[k])) << 32) |
+                  static_cast<uint32_t>(left[k]);
+}
+
+// off[i] = first key with upper word >= i (keys sorted), i = 0..n.
+__global__ void k_csr_offsets(const unsigned long long* __restrict__ keys, int64_t m, int64_t n,
+                              int64_t* __restrict__ off) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long t = static_cast<unsigned long long>(i) << 32;
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < t) lo = mid + 1;
+            else hi = mid;
+        }
+        off[i] = lo;
+    }
+}
+
+constexpr uint8_t kUndecided = 0, kRep = 1, kMember = 2;
+
+// One round of the greedy scan over the still undecided items.
+__global__ void k_dedup_round(const unsigned long long* __restrict__ keys,
+                              const int64_t* __restrict__ off, int64_t n,
+                              uint8_t* status, unsigned int* undecided) {
+    unsigned int left = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (status[i] != kUndecided) continue;
+        bool any_rep = false, all_done = true;
+        for (int64_t e = off[i]; e < off[i + 1]; e++) {
+            const int64_t j = static_cast<int64_t>(keys[e] & 0xffffffffull);
+            // volatile: statuses decided earlier in this round may be seen
+            const uint8_t sj = *reinterpret_cast<volatile uint8_t*>(status + j);
+            if (sj == kRep) {
+                any_rep = true;
+                break;
+            }
+            if (sj == kUndecided) all_done = false;
+        }
+        if (any_rep) status[i] = kMember;
+        else if (all_done) status[i] = kRep;
+        else left++;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) left += __shfl_xor_sync(0xffffffffu, left, o);
+    if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
+}
+
+// rep_of[i]: i for representatives, else the rep neighbour nearest in the
+// reference's fp64 distance (lowest index on ties; neighbours ascend).
+__global__ void k_dedup_attach(const unsigned long long* __restrict__ keys,
+                               const int64_t* __restrict__ off, int64_t n,
+                               const uint8_t* __restrict__ status, const float* __restrict__ X,
+                               int d, int64_t* __restrict__ rep_of,
+                               unsigned long long* __restrict__ n_reps) {
+    const bool vec8 = (d % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 32 == 0);
+    unsigned int reps = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (status[i] == kRep) {
+            rep_of[i] = i;
+            reps++;
+            continue;
+        }
+        int64_t best = -1;
+        double best_dist = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+        for (int64_t e = off[i]; e < off[i + 1]; e++) {
+            const int64_t j = static_cast<int64_t>(keys[e] & 0xffffffffull);
+            if (status[j] != kRep) continue;
+            // euclidean(items[i], items[rep]) -- the reference's argument order
+            const double dist = exact_dist(X + i * d, X + j * d, d, vec8);
+            if (dist < best_dist) {
+                best_dist = dist;
+                best = j;
+            }
+        }
+        rep_of[i] = best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) reps += __shfl_xor_sync(0xffffffffu, reps, o);
+    if ((threadIdx.x & 31) == 0 && reps) atomicAdd(n_reps, static_cast<unsigned long long>(reps));
+}
+
+}  // namespace
+
+void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStream_t s,
+                   int64_t* d_rep_of, int64_t* n_reps) {
+    *n_reps = 0;
+    if (n == 0) return;
+    const DeviceCtx& ctx = device_ctx();
+    // 1. the tau-graph (i < j, exact euclidean <= tau)
+    pdb_join_opts o{};
+    o.flags = PDB_JOIN_SELF;
+    o.stream = s;
+    pdb_dev_pairs g{};
+    struct PairsGuard {
+        pdb_dev_pairs* p;
+        ~PairsGuard() { pdb_dev_pairs_free(p); }
+    } guard{&g};
+    run_sim_join_dev(d_X, n, d_X, n, d, tau, o, &g, nullptr);
+    const int64_t m = g.count;
+
+    // 2. lower-neighbour CSR: keys (j << 32 | i) sorted ascending
+    DevBuf<unsigned long long> k_in(static_cast<size_t>(std::max<int64_t>(m, 1)), s),
+        keys(static_cast<size_t>(std::max<int64_t>(m, 1)), s);
+    DevBuf<int64_t> off(static_cast<size_t>(n) + 1, s);
+    const unsigned grid = static_cast<unsigned>(ctx.sm_count * 4);
+    if (m > 0) {
+        k_graph_keys<<<grid, 256, 0, s>>>(g.left, g.right, m, k_in.p);
+        int bits = 1;
+        while ((int64_t{1} << bits) < n) bits++;
+        size_t tmp_bytes = 0;
+        PDB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k_in.p, keys.p, m, 0, 32 + bits, s));
+        DevBuf<uint8_t> tmp(tmp_bytes, s);
+        PDB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, k_in.p, keys.p, m, 0, 32 + bits, s));
+    }
+    k_csr_offsets<<<grid, 256, 0, s>>>(keys.p, m, n, off.p);
+    PDB_CUDA(cudaGetLastError());
+
+    // 3. greedy rounds until every item is decided
+    DevBuf<uint8_t> status(static_cast<size_t>(n), s);
+    DevBuf<unsigned long long> cnt(2, s);
+    PDB_CUDA(cudaMemsetAsync(status.p, 0, static_cast<size_t>(n), s));
+    thread_local unsigned long long* h_cnt = [] {
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, 16, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            q = nullptr;
+        }
+        return static_cast<unsigned long long*>(q);
+    }();
+    unsigned long long local[2];
+    unsigned long long* hc = h_cnt ? h_cnt : local;
+    for (int round = 0;; round++) {
+        // a few rounds per host check: most items settle in the first two
+        for (int r = 0; r < 4; r++) {
+            PDB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+            k_dedup_round<<<grid, 256, 0, s>>>(keys.p, off.p, n, status.p,
+                                               reinterpret_cast<unsigned int*>(cnt.p));
+        }
+        PDB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+        if (static_cast<unsigned int>(hc[0]) == 0) break;
+        if (round > n) fail(PDB_ERR_CUDA, "dedup rounds did not converge");  // unreachable
+    }
+
+    // 4. attach members to their nearest representative
+    PDB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, sizeof(unsigned long long), s));
+    k_dedup_attach<<<grid, 256, 0, s>>>(keys.p, off.p, n, status.p, d_X, d, d_rep_of, cnt.p + 1);
+    PDB_CUDA(cudaGetLastError());
+    PDB_CUDA(cudaMemcpyAsync(hc + 1, cnt.p + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PDB_CUDA(cudaStreamSynchronize(s));
+    *n_reps = static_cast<int64_t>(hc[1]);
+}
+
+}  // namespace pdb

@@ -1,0 +1,45 @@
+// exact.cuh -- the reference's distance arithmetic on the device, shared by
+// the join's exact re-check (K3) and the dedup attach step.
+//
+// euclidean(a, b) = sqrt(sum_k ((double)a_k - (double)b_k)^2), accumulated in
+// k order with no contraction (src/index.cpp:69-76): explicit _rn intrinsics
+// keep every operation a separate IEEE round-to-nearest step.
+#pragma once
+
+#include <cstdint>
+
+namespace pdb {
+
+// The reference chain, reading each row 32 bytes per load (sm_100's
+// 256-bit LDG): a lane's load touches one 128-byte line, so the L1 data
+// pipe -- which bounds this kernel, the rows of different lanes being
+// unrelated -- spends one wavefront per 32 bytes instead of per 16.
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
+__device__ __forceinline__ double exact_dist(const float* __restrict__ a,
+                                             const float* __restrict__ b, int d, bool vec8) {
+    double acc = 0.0;
+    auto step = [&](float x, float y) {
+        const double t = __dsub_rn(static_cast<double>(x), static_cast<double>(y));
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+    };
+    if (vec8) {
+        for (int k = 0; k < d; k += 8) {
+            float x[8], y[8];
+            ldg256(a + k, x);
+            ldg256(b + k, y);
+#pragma unroll
+            for (int q = 0; q < 8; q++) step(x[q], y[q]);
+        }
+    } else {
+        for (int k = 0; k < d; k++) step(__ldg(a + k), __ldg(b + k));
+    }
+    return __dsqrt_rn(acc);
+}
+
+}  // namespace pdb

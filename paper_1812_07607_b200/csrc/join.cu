@@ -54,6 +54,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "exact.cuh"
 #include "pdb_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -880,38 +881,6 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 // K3: exact re-check.  The fp64 chain is written with explicit _rn
 // intrinsics so it can never be contracted into FMAs: diff = a - b,
 // acc = acc + diff * diff, sequential in k, then sqrt -- src/index.cpp:69-76.
-// The reference chain, reading each row 32 bytes per load (sm_100's
-// 256-bit LDG): a lane's load touches one 128-byte line, so the L1 data
-// pipe -- which bounds this kernel, the rows of different lanes being
-// unrelated -- spends one wavefront per 32 bytes instead of per 16.
-__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
-    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
-                   "=f"(r[6]), "=f"(r[7])
-                 : "l"(p));
-}
-
-__device__ __forceinline__ double exact_dist(const float* __restrict__ a,
-                                             const float* __restrict__ b, int d, bool vec8) {
-    double acc = 0.0;
-    auto step = [&](float x, float y) {
-        const double t = __dsub_rn(static_cast<double>(x), static_cast<double>(y));
-        acc = __dadd_rn(acc, __dmul_rn(t, t));
-    };
-    if (vec8) {
-        for (int k = 0; k < d; k += 8) {
-            float x[8], y[8];
-            ldg256(a + k, x);
-            ldg256(b + k, y);
-#pragma unroll
-            for (int q = 0; q < 8; q++) step(x[q], y[q]);
-        }
-    } else {
-        for (int k = 0; k < d; k++) step(__ldg(a + k), __ldg(b + k));
-    }
-    return __dsqrt_rn(acc);
-}
-
 // One thread per candidate record: each lane walks the set bits of its
 // record's mask (warp-uniform loop, so every iteration compacts survivors
 // with a ballot and one atomic per warp).

@@ -129,6 +129,8 @@ PDB_HIDDEN void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t
 PDB_HIDDEN void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
                                  int32_t d, double tau, const pdb_join_opts& o,
                                  pdb_dev_pairs* out, pdb_join_stats* stats);
+PDB_HIDDEN void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStream_t s,
+                              int64_t* d_rep_of, int64_t* n_reps);
 PDB_HIDDEN void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int64_t nR,
                                  int32_t d, double min_cos, const pdb_join_opts& o,
                                  pdb_dev_pairs* out, pdb_join_stats* stats);

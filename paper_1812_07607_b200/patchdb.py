@@ -10,6 +10,9 @@ Mirrors (paths relative to the reference's proj/ directory):
                              include/patchdb/etl.hpp:32-74, src/etl.cpp:252-373
 * BuildSide, sim_join_pairs  include/patchdb/query.hpp:84, 206-211,
                              src/query.cpp:467-528, 1094-1104
+* dedup_groups, dedup_stream PlanNode::dedup / dedup_stream,
+                             include/patchdb/query.hpp:142, 203-204,
+                             src/query.cpp:535-582, 1063-1092
 
 Array entry points (featurize_tiles, color_histogram, sim_join,
 sim_join_device, featurize_join) are the C-ABI one level down; the object
@@ -429,16 +432,20 @@ def next_patch_id() -> int:
     return v
 
 
-def _fnv_digest(name: str, items: Sequence[Tuple[str, int]]) -> int:
+def _fnv_digest(name: str, items: Sequence[Tuple[str, object]]) -> int:
     """ParamsDigest (include/patchdb/core.hpp:155-196): FNV-1a-64 over the
-    big-endian byte record str8(op_name) then, per int param, str8(key),
-    tag byte 0, i64."""
+    big-endian byte record str8(op_name) then, per param, str8(key) and
+    either tag 0 + i64 (int) or tag 1 + the f64 bit pattern (float)."""
+    import struct
     buf = bytearray()
     nb = name.encode()
     buf += bytes([len(nb)]) + nb
     for k, v in items:
         kb = k.encode()
-        buf += bytes([len(kb)]) + kb + b"\x00" + int(v & 0xFFFFFFFFFFFFFFFF).to_bytes(8, "big")
+        if isinstance(v, float):
+            buf += bytes([len(kb)]) + kb + b"\x01" + struct.pack(">d", v)
+        else:
+            buf += bytes([len(kb)]) + kb + b"\x00" + int(v & 0xFFFFFFFFFFFFFFFF).to_bytes(8, "big")
     h = 0xCBF29CE484222325
     for x in buf:
         h ^= x
@@ -609,3 +616,101 @@ def sim_join_pairs(left: Sequence[Patch], right: Sequence[Patch], tau: float,
     if probes is not None:
         probes[:] = [len(right) if chosen == BuildSide.left else len(left)]
     return [(left[int(li[k])], right[int(ri[k])]) for k in order]
+
+
+# ---------------------------------------------------------------------------
+# Near-duplicate grouping (run_dedup, src/query.cpp:535-566) on the tau-graph
+# of the B200 join (csrc/dedup.cu).
+
+
+@dataclass
+class DedupGroups:
+    """run_dedup's result: representatives (kept order) and, per
+    representative, its members in arrival order; rep_of[i] is item i's
+    representative."""
+    reps: np.ndarray
+    members: List[np.ndarray]
+    rep_of: np.ndarray
+
+
+def dedup(X: np.ndarray, tau: float) -> DedupGroups:
+    """Host rows [n, d] fp32 -> DedupGroups (the C-ABI's pdb_dedup)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n = X.shape[0]
+    d = X.shape[1] if X.ndim == 2 else 0
+    rep_of = np.empty(max(n, 1), dtype=np.int64)
+    nr = C.c_int64()
+    _check(capi.lib().pdb_dedup(capi.ptr(X), n, d, float(tau), None, capi.ptr(rep_of),
+                                C.byref(nr)))
+    rep_of = rep_of[:n]
+    reps = np.flatnonzero(rep_of == np.arange(n))
+    order = np.argsort(rep_of, kind="stable")      # members keep arrival order
+    bounds = np.searchsorted(rep_of[order], reps)
+    members = np.split(order, bounds[1:]) if n else []
+    return DedupGroups(reps, members, rep_of)
+
+
+def dedup_device(X, tau: float, stream=None):
+    """Device rows (CUDA fp32 tensor [n, d]) -> (rep_of int64 tensor, n_reps)."""
+    import torch
+    assert X.is_cuda and X.dtype == torch.float32 and X.is_contiguous()
+    n, d = int(X.shape[0]), int(X.shape[1])
+    rep_of = torch.empty(max(n, 1), dtype=torch.int64, device=X.device)
+    s = stream if stream is not None else torch.cuda.current_stream(X.device)
+    o = capi.JoinOpts()
+    o.stream = C.c_void_p(s.cuda_stream)
+    nr = C.c_int64()
+    _check(capi.lib().pdb_dedup_dev(X.data_ptr(), n, d, float(tau), C.byref(o),
+                                    rep_of.data_ptr(), C.byref(nr)))
+    return rep_of[:n], int(nr.value)
+
+
+def _dedup_matrix(items: Sequence[Patch], what: str) -> np.ndarray:
+    d = int(np.asarray(items[0].data).size)
+    if d == 0:
+        raise ShapeError(f"{what} needs non-empty patch data")
+    for p in items:
+        if int(np.asarray(p.data).size) != d:
+            raise MixedDimensionError(
+                f"{what} saw {d} and {int(np.asarray(p.data).size)} dimensional patches")
+    return np.stack([np.asarray(p.data, dtype=np.float32).ravel() for p in items])
+
+
+def dedup_groups(items: Sequence[Patch], tau: float) -> List[Patch]:
+    """PlanNode::dedup's output (src/query.cpp:860-880, make_group_patch
+    568-582): one derived patch per representative, in kept order, with
+    metadata group_labels (sorted distinct string labels of the members)
+    and group_size."""
+    if tau < 0.0:
+        raise ConfigError("dedup needs tau >= 0")
+    if not items:
+        return []
+    g = dedup(_dedup_matrix(items, "dedup"), tau)
+    digest = _fnv_digest("dedup_group", [("tau", float(tau))])
+    out = []
+    for r, mem in zip(g.reps, g.members):
+        rep = items[int(r)]
+        labels = sorted({items[int(m)].meta["label"] for m in mem
+                         if isinstance(items[int(m)].meta.get("label"), str)})
+        meta = dict(rep.meta)
+        meta["group_labels"] = labels
+        meta["group_size"] = int(len(mem))
+        step = LineageStep("dedup_group", rep.patch_id, None, digest)
+        out.append(Patch(next_patch_id(), np.asarray(rep.data), tuple(rep.shape), meta,
+                         [step] + list(rep.lineage)))
+    return out
+
+
+def dedup_stream(items: Iterable[Patch], tau: float) -> Iterator[Patch]:
+    """dedup_stream (src/query.cpp:1063-1092): the kept patches, in order.
+    The B200 build drains its input first (the scan is global)."""
+    if tau < 0.0:
+        raise ConfigError("dedup needs tau >= 0")
+    items = list(items)
+    if not items:
+        return iter(())
+    for p in items:
+        if np.asarray(p.data).size == 0:
+            raise ShapeError("dedup needs non-empty patch data")
+    g = dedup(_dedup_matrix(items, "dedup"), tau)
+    return iter([items[int(r)] for r in g.reps])

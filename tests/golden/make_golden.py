@@ -125,7 +125,46 @@ def join_fixtures():
     print("join fixtures written")
 
 
+def dedup_fixtures():
+    """PlanNode::dedup through execute() on the reference (ref_dedup): the
+    full membership (rep_of) and the kept set of dedup_stream."""
+    res = {}
+    cases = {}
+    # test_query.cpp:331-368: three tight clusters well over tau apart
+    cases["test_query_6pts"] = (np.array([[0, 0], [0.01, 0], [1, 1], [0, 0.02], [1.01, 1], [5, 5]],
+                                         np.float32), 0.1)
+    # exact-distance ties: 0.5 is tau from both kept reps 0 and 1 -> earliest
+    cases["tie_1d"] = (np.array([[0.0], [1.0], [0.5], [0.25], [0.75]], np.float32), 0.5)
+    rng = np.random.default_rng(95)
+    # test_query.cpp:370-389 shape: 300 uniform 3-d points, tau 0.3
+    cases["random_300x3"] = (rng.random((300, 3), dtype=np.float32), 0.3)
+    cases["random_2000x8"] = (rng.random((2000, 8), dtype=np.float32), 0.5)
+    # clustered, config-1 shaped (L1-normalised 64-d), tau 0.05
+    cases["config1_4k"] = (workloads.config1(4000, seed=0), 0.05)
+    # config-2 tile histograms of 20 frames (1280 tiles), tau 0.05
+    cf, _ = workloads.frames(20, 480, 640, seed=2)
+    cases["config2_20f"] = (oracle.featurize_tiles(cf, 60, 80, 4, 1), 0.05)
+    generated = {"config1_4k", "config2_20f"}  # regenerated at test time, sha-pinned
+    for name, (X, tau) in cases.items():
+        rep_of, nr = oracle.ref_dedup(X, tau)
+        kept = oracle.ref_dedup_stream(X, tau)
+        if name in generated:
+            res[f"{name}__sha256"] = np.frombuffer(hashlib.sha256(X.tobytes()).digest(), np.uint8)
+        else:
+            res[f"{name}__X"] = X
+        res[f"{name}__tau"] = np.array([tau])
+        res[f"{name}__rep_of"] = rep_of
+        res[f"{name}__kept"] = kept
+        print(name, X.shape, "reps", nr)
+    np.savez_compressed(os.path.join(HERE, "dedup_golden.npz"), **res)
+
+
 if __name__ == "__main__":
     assert oracle.ref() is not None, "build oracle/_ref first: make -C oracle ref"
-    hist_fixtures()
-    join_fixtures()
+    which = sys.argv[1:] or ["hist", "join", "dedup"]
+    if "hist" in which:
+        hist_fixtures()
+    if "join" in which:
+        join_fixtures()
+    if "dedup" in which:
+        dedup_fixtures()

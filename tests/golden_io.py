@@ -78,3 +78,27 @@ def canonical(left, right):
     """Pair set as a sorted structured view for exact comparison."""
     k = (left.astype(np.int64) << 32) | right.astype(np.int64)
     return np.sort(k)
+
+
+def _dedup_input(name):
+    if name == "config1_4k":
+        return workloads.config1(4000, seed=0)
+    if name == "config2_20f":
+        from oracle import oracle
+        cf, _ = workloads.frames(20, 480, 640, seed=2)
+        return oracle.featurize_tiles(cf, 60, 80, 4, 1)
+    raise KeyError(name)
+
+
+def dedup_cases():
+    """(name, X, tau, rep_of, kept) minted from the reference's PlanNode::dedup
+    and dedup_stream (tests/golden/make_golden.py dedup)."""
+    z = np.load(os.path.join(HERE, "dedup_golden.npz"))
+    names = sorted({k.split("__")[0] for k in z.files})
+    for name in names:
+        if f"{name}__X" in z.files:
+            X = z[f"{name}__X"]
+        else:
+            X = _dedup_input(name)
+            assert _sha(X) == z[f"{name}__sha256"].tobytes(), "generator drifted"
+        yield name, X, float(z[f"{name}__tau"][0]), z[f"{name}__rep_of"], z[f"{name}__kept"]

@@ -113,3 +113,30 @@ def test_port_matches_reference_live():
     for b in (2, 7, 13, 255, 256, 1000):
         assert np.array_equal(oracle.featurize_tiles(fr, 10, 8, b, 0).view(np.uint32),
                               oracle.ref_featurize_tiles(fr, 10, 8, b).view(np.uint32)), b
+
+
+def test_dedup_restatement_matches_reference_golden():
+    """orc_dedup (restated run_dedup) vs the reference's PlanNode::dedup
+    membership and dedup_stream kept set, minted from oracle/_ref."""
+    n_cases = 0
+    for name, X, tau, rep_of, kept in golden_io.dedup_cases():
+        got, nr = oracle.dedup(X, tau)
+        assert np.array_equal(got, rep_of), name
+        assert np.array_equal(np.flatnonzero(got == np.arange(X.shape[0])), kept), name
+        assert nr == kept.shape[0]
+        n_cases += 1
+    assert n_cases >= 6
+
+
+def test_dedup_restatement_live_vs_reference():
+    if oracle.ref() is None:
+        pytest.skip("oracle/_ref not built here")
+    rng = np.random.default_rng(7)
+    for n, d, tau in [(500, 2, 0.05), (800, 16, 0.9), (64, 1, 0.0)]:
+        X = rng.random((n, d), dtype=np.float32)
+        if tau == 0.0:
+            X[::3] = X[0]  # exact duplicates at tau = 0
+        got, nr = oracle.dedup(X, tau)
+        want, nw = oracle.ref_dedup(X, tau)
+        assert np.array_equal(got, want) and nr == nw
+    assert oracle.ref_dedup(np.zeros((3, 2), np.float32), -1.0) == 1  # ConfigError
