@@ -483,7 +483,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "dedup"],
                     help="c2 (default, the headline): featurize -> join pipeline; c1/c3/c4/c5: "
                          "the join-only configs of BASELINE.json (bench_join.py)")
     args = ap.parse_args()
@@ -494,6 +494,8 @@ def main():
     if args.workload != "c2":
         import bench_join
         if args.impl == "reference":
+            if args.workload == "dedup":
+                return bench_join.run_dedup_reference(args, rank, world, METRIC)
             return bench_join.run_reference(args, rank, world, args.workload, METRIC)
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -513,6 +515,9 @@ def main():
     try:
         if args.workload != "c2":
             import bench_join
+            if args.workload == "dedup":
+                return bench_join.run_dedup_ours(args, rank, world, local_rank, METRIC,
+                                                 peaks()[0], ClockSampler)
             return bench_join.run_ours(args, rank, world, local_rank, args.workload, METRIC,
                                        peaks()[0], ClockSampler)
         return run_ours(args, rank, world, local_rank)

@@ -40,6 +40,10 @@ JOINS = {
     "c5": dict(workload="config5_skewed: 4,194,304 x 64 fp32, 20% in 50 simplex clusters "
                         "(sigma 1e-3), 80% Dirichlet(1), seed 5; L2 self-join eps=0.01",
                kind="l2", self_join=True, tau=0.01),
+    "dedup": dict(workload="dedup of the config-2 tile histograms: 64,000 x 64 joint 4x4x4 "
+                           "histograms of 1000 synthetic 480x640 frames (seed 2), tau=0.05 "
+                           "(run_dedup / PlanNode::dedup semantics)",
+                  kind="dedup", self_join=True, tau=0.05),
 }
 
 
@@ -54,6 +58,12 @@ def _gen(which):
         return workloads.bf16_bits(workloads.config4(device="cuda")), None
     if which == "c5":
         return workloads.config5(), None
+    if which == "dedup":
+        from paper_1812_07607_b200 import patchdb
+        import torch
+        fr, _ = workloads.frames(1000, 480, 640, seed=2)
+        feats = patchdb.featurize_tiles(torch.from_numpy(fr).cuda(), 60, 80, 4, "joint")
+        return feats.cpu().numpy(), None
     raise ValueError(which)
 
 
@@ -65,6 +75,20 @@ def _cpu_baseline(which, L, R, cfg, threads):
     rng = np.random.default_rng(1)
     n = L.shape[0]
     cand = n * (n - 1) / 2 if cfg["self_join"] else n * R.shape[0]
+    if cfg["kind"] == "dedup":
+        k = int(os.environ.get("PDB_REF_DEDUP_ROWS", 16000))
+        sub = np.ascontiguousarray(L[:k])
+        t0 = time.perf_counter()
+        oracle.ref_dedup(sub, cfg["tau"])
+        t_s = time.perf_counter() - t0
+        # run_dedup's cost grows with n * reps (attach scans every kept rep):
+        # extrapolate quadratically from the prefix sample
+        t = t_s * (n / sub.shape[0]) ** 2
+        return {"value": n / t, "unit": "items/s", "cores": 1, "kind": "reference",
+                "sample": f"reference PlanNode::dedup (oracle/_ref, run_dedup) on the first {k} "
+                          f"items ({t_s:.2f} s, single-threaded as the reference is), "
+                          f"extrapolated quadratically to {n}",
+                "extrapolated_s": t}
     if cfg["kind"] == "l2":
         rows = int(os.environ.get("PDB_REF_PROBE_ROWS", {"c1": 2048, "c3": 512, "c5": 512}[which]))
         idx = np.sort(rng.choice(n, size=min(rows, n), replace=False))
@@ -323,4 +347,111 @@ def run_ours(args, rank, world, local_rank, which, metric, peaks, clock_sampler)
             "clocks": sampler.summary(),
         }
         print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# Dedup line (--workload dedup): the paper's near-duplicate grouping
+# (run_dedup semantics) of the config-2 tile histograms.  One step = one
+# pdb_dedup_dev over the 64,000 device-resident features; value = items/s.
+
+def run_dedup_ours(args, rank, world, local_rank, metric, peaks, clock_sampler):
+    import torch
+
+    from paper_1812_07607_b200 import _capi as capi
+    from paper_1812_07607_b200 import patchdb
+
+    cfg = JOINS["dedup"]
+    if rank != 0:  # a global sequential scan: one GPU runs it ("replicas only")
+        return 0
+    dev = torch.device("cuda", local_rank % max(torch.cuda.device_count(), 1))
+    torch.cuda.set_device(dev)
+    Xh, _ = _gen("dedup")
+    X = torch.from_numpy(Xh).to(dev)
+    n, d = X.shape
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    nr = 0
+    for k in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        rep_of, nr = patchdb.dedup_device(X, cfg["tau"], stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            times.append(ev0.elapsed_time(ev1))
+    sampler = clock_sampler(dev.index)
+    sampler.__enter__()
+    e2e = []
+    for k in range(max(1, min(args.steps, 3)) + 1):
+        t0 = time.perf_counter()
+        g = patchdb.dedup(Xh, cfg["tau"])
+        t1 = time.perf_counter()
+        if k:
+            e2e.append(t1 - t0)
+    sampler.__exit__()
+    ms = statistics.mean(times)
+    e2e_s = statistics.mean(e2e)
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = _cpu_baseline("dedup", Xh, None, cfg, 1)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "items/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    # roofline: the tau-graph's screen dominates -- credit its algorithmic
+    # flops (N(N-1)/2 pairs x 2d) over the whole dedup step (a lower bound)
+    flops = n * (n - 1) / 2 * 2 * d
+    tf = flops / (ms * 1e-3) / 1e12
+    bpeak = peaks.get("bf16_tflops") or 1590.0
+    print(json.dumps({
+        "metric": metric, "value": n / (ms * 1e-3), "unit": "items/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "replicas only", "vs_baseline": None, "dtype": "bf16 screen / f64 exact",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": int(n), "d": int(d), "tau": cfg["tau"],
+                   "l2": "flushed (256 MB write) before each step"},
+        "reps": int(nr), "groups_with_members": int(sum(1 for m in g.members if len(m) > 1)),
+        "roofline": {"kernel": "whole dedup step vs the tau-graph screen's algorithmic flops "
+                               "(k_screen dominates)", "bound": "tensor", "achieved": tf,
+                     "peak": bpeak, "unit": "TFLOP/s", "frac": tf / bpeak,
+                     "algorithmic": f"{n * (n - 1) / 2:.4g} pairs x 2*{d} flop", "ms": ms,
+                     "traffic": None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": n / e2e_s, "unit": "items/s", "h2d_bytes_per_step": int(Xh.nbytes),
+                "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3,
+                "api": "pdb_dedup (host features -> host rep_of)"},
+        "gpu_launches": None,
+        "clocks": sampler.summary(),
+    }))
+    return 0
+
+
+def run_dedup_reference(args, rank, world, metric):
+    if rank != 0:
+        return 0
+    cfg = JOINS["dedup"]
+    from oracle import oracle
+    from paper_1812_07607_b200 import workloads
+    fr, _ = workloads.frames(1000, 480, 640, seed=2)
+    X = oracle.featurize_tiles(fr, 60, 80, 4, 1)
+    vals, base = [], None
+    for k in range(args.warmup + args.steps):
+        base = _cpu_baseline("dedup", X, None, cfg, 1)
+        if k >= args.warmup:
+            vals.append(base["value"])
+    v = statistics.mean(vals)
+    base["value"] = v
+    print(json.dumps({
+        "impl": "reference", "metric": metric, "value": v, "unit": "items/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": X.shape[0] / v * 1e3,
+        "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": int(X.shape[0])},
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
     return 0

@@ -623,14 +623,24 @@ def sim_join_pairs(left: Sequence[Patch], right: Sequence[Patch], tau: float,
 # of the B200 join (csrc/dedup.cu).
 
 
-@dataclass
 class DedupGroups:
     """run_dedup's result: representatives (kept order) and, per
-    representative, its members in arrival order; rep_of[i] is item i's
-    representative."""
-    reps: np.ndarray
-    members: List[np.ndarray]
-    rep_of: np.ndarray
+    representative, its members in arrival order (built on first use);
+    rep_of[i] is item i's representative."""
+
+    def __init__(self, reps: np.ndarray, rep_of: np.ndarray):
+        self.reps = reps
+        self.rep_of = rep_of
+        self._members = None
+
+    @property
+    def members(self) -> List[np.ndarray]:
+        if self._members is None:
+            n = self.rep_of.shape[0]
+            order = np.argsort(self.rep_of, kind="stable")  # members keep arrival order
+            bounds = np.searchsorted(self.rep_of[order], self.reps)
+            self._members = np.split(order, bounds[1:]) if n else []
+        return self._members
 
 
 def dedup(X: np.ndarray, tau: float) -> DedupGroups:
@@ -643,11 +653,7 @@ def dedup(X: np.ndarray, tau: float) -> DedupGroups:
     _check(capi.lib().pdb_dedup(capi.ptr(X), n, d, float(tau), None, capi.ptr(rep_of),
                                 C.byref(nr)))
     rep_of = rep_of[:n]
-    reps = np.flatnonzero(rep_of == np.arange(n))
-    order = np.argsort(rep_of, kind="stable")      # members keep arrival order
-    bounds = np.searchsorted(rep_of[order], reps)
-    members = np.split(order, bounds[1:]) if n else []
-    return DedupGroups(reps, members, rep_of)
+    return DedupGroups(np.flatnonzero(rep_of == np.arange(n)), rep_of)
 
 
 def dedup_device(X, tau: float, stream=None):
