@@ -1,0 +1,11 @@
+# Full round measurement: parity tests, smoke, the default bench line, the
+# join-only / dedup lines, the launch list and full captures of K1 and K2.
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 180 python __graft_entry__.py smoke 2>&1 | tail -1
+timeout 400 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench_rc=$?
+for w in c1 c3 c4 c5 dedup; do
+  timeout 900 python bench.py --workload $w --steps 3 --warmup 3 > gpurun_out/bench_$w.log 2>&1; echo $w rc=$?
+done
+timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.log 2>&1; echo ref_rc=$?
+bash tools/gpu_profile.sh
