@@ -161,6 +161,80 @@ std::vector<std::pair<size_t, size_t>> sim_join_positions(const std::vector<Patc
     return out;
 }
 
+// compile_nl_join with a pure within predicate over single-patch tuples
+// (src/query.cpp:142-151, 705-744): (left index, right index) of every pair
+// with euclidean <= radius, in nested-loop order -- the B200 cross join,
+// sorted.  A dimension mismatch throws as the predicate's first evaluation
+// does; empty sides give nothing.
+template <class PatchT>
+std::vector<std::pair<size_t, size_t>> nl_within_positions(const std::vector<PatchT>& left,
+                                                           const std::vector<PatchT>& right,
+                                                           double radius) {
+    if (left.empty() || right.empty()) return {};
+    const size_t d = left[0].data.size();
+    for (const auto* side : {&left, &right})
+        for (const PatchT& p : *side)
+            if (p.data.size() != d)
+                throw DimensionMismatchError("distance between " + std::to_string(d) + " and " +
+                                             std::to_string(p.data.size()) +
+                                             " dimensional patches");
+    std::vector<std::pair<size_t, size_t>> out;
+    if (!(radius >= 0.0)) return out;
+    if (d == 0) {  // zero-dimensional patches are all at distance 0
+        for (size_t i = 0; i < left.size(); i++)
+            for (size_t j = 0; j < right.size(); j++) out.emplace_back(i, j);
+        return out;
+    }
+    const std::vector<float> L = detail::pack(left, d), R = detail::pack(right, d);
+    pdb_join_opts o{};
+    o.flags = PDB_JOIN_SORTED;
+    pdb_pairs pr{};
+    check(pdb_sim_join(L.data(), static_cast<int64_t>(left.size()), R.data(),
+                       static_cast<int64_t>(right.size()), static_cast<int32_t>(d), radius, &o,
+                       &pr));
+    out.resize(static_cast<size_t>(pr.count));
+    for (int64_t k = 0; k < pr.count; k++)
+        out[static_cast<size_t>(k)] = {static_cast<size_t>(pr.left[k]),
+                                       static_cast<size_t>(pr.right[k])};
+    pdb_pairs_free(&pr);
+    return out;
+}
+
+// run_dedup's grouping (src/query.cpp:535-566) on the B200: representatives
+// in kept order and, per representative, its members in arrival order.
+struct DedupGroups {
+    std::vector<size_t> reps;
+    std::vector<std::vector<size_t>> members;
+};
+
+template <class PatchT>
+DedupGroups dedup_groups(const std::vector<PatchT>& items, double tau) {
+    if (tau < 0.0) throw ConfigError("dedup needs tau >= 0");
+    DedupGroups g;
+    if (items.empty()) return g;
+    const size_t d = items[0].data.size();
+    if (d == 0) throw ShapeError("dedup needs non-empty patch data");
+    for (const PatchT& p : items)
+        if (p.data.size() != d)
+            throw MixedDimensionError("dedup saw " + std::to_string(d) + " and " +
+                                      std::to_string(p.data.size()) + " dimensional patches");
+    const std::vector<float> X = detail::pack(items, d);
+    std::vector<int64_t> rep_of(items.size());
+    int64_t n_reps = 0;
+    check(pdb_dedup(X.data(), static_cast<int64_t>(items.size()), static_cast<int32_t>(d), tau,
+                    nullptr, rep_of.data(), &n_reps));
+    std::vector<size_t> slot(items.size());
+    for (size_t i = 0; i < items.size(); i++) {
+        if (rep_of[i] == static_cast<int64_t>(i)) {
+            slot[i] = g.reps.size();
+            g.reps.push_back(i);
+            g.members.push_back({});
+        }
+        g.members[slot[static_cast<size_t>(rep_of[i])]].push_back(i);
+    }
+    return g;
+}
+
 // patchdb::sim_join_pairs (query.hpp:209-211).
 template <class PatchT>
 std::vector<std::pair<PatchT, PatchT>> sim_join_pairs(const std::vector<PatchT>& left,

@@ -82,6 +82,9 @@ def ref():
         L.ref_dedup.argtypes = [vp, i64, i32, f64, vp, C.POINTER(i64)]
         L.ref_dedup_stream.argtypes = [vp, i64, i32, f64, vp]
         L.ref_dedup_stream.restype = i64
+        pp = C.POINTER(C.POINTER(i32))
+        L.ref_nl_within.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(i64), pp, pp]
+        L.ref_q1.argtypes = [vp, i64, i32, i32, i32, f64, C.POINTER(i64), pp, pp]
         _ref = L
     return _ref
 
@@ -259,3 +262,35 @@ def ref_dedup_stream(X, tau):
     if m < 0:
         return int(-m)
     return kept[:m]
+
+
+def _ref_pairs(fn, *args):
+    n = C.c_int64()
+    a = C.POINTER(C.c_int32)()
+    b = C.POINTER(C.c_int32)()
+    rc = fn(*args, C.byref(n), C.byref(a), C.byref(b))
+    if rc:
+        return rc
+    k = n.value
+    x = np.ctypeslib.as_array(a, (max(k, 1),))[:k].copy()
+    y = np.ctypeslib.as_array(b, (max(k, 1),))[:k].copy()
+    ref().ref_free(C.cast(a, C.c_void_p))
+    ref().ref_free(C.cast(b, C.c_void_p))
+    return x, y
+
+
+def ref_nl_within(L, R, radius):
+    """PlanNode::nl_join(..., within_of(0, 1, radius)) positions in the
+    nested-loop emission order, or an int error code."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = np.ascontiguousarray(R, dtype=np.float32)
+    d = L.shape[1] if L.shape[0] else R.shape[1]
+    return _ref_pairs(ref().ref_nl_within, _p(L), L.shape[0], _p(R), R.shape[0], d, float(radius))
+
+
+def ref_q1(frames, bins, tau):
+    """The reference's q1 plan over whole-frame histograms: (frame a, frame b)
+    per result tuple in emission order."""
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    F, H, W = frames.shape[:3]
+    return _ref_pairs(ref().ref_q1, _p(frames), F, H, W, int(bins), float(tau))

@@ -305,3 +305,84 @@ REF_API int64_t ref_dedup_stream(const float* X, int64_t n, int32_t d, double ta
         return -code_of(e);
     }
 }
+
+namespace {
+std::vector<Tuple> tuples_of(const std::vector<Patch>& ps) {
+    std::vector<Tuple> out;
+    out.reserve(ps.size());
+    for (const auto& p : ps) out.push_back(Tuple{p});
+    return out;
+}
+}  // namespace
+
+// PlanNode::nl_join(memory(L), memory(R), within_of(0, 1, radius))
+// (src/query.cpp:142-151, 705-744): (left index, right index) in the
+// nested-loop emission order.  Caller frees with ref_free.
+REF_API int ref_nl_within(const float* L, int64_t nL, const float* R, int64_t nR, int32_t d,
+                          double radius, int64_t* out_count, int32_t** out_left,
+                          int32_t** out_right) {
+    try {
+        auto left = make_vecs(L, nL, d, 1);
+        auto right = make_vecs(R, nR, d, (1ull << 32) + 1);
+        ExecContext ctx;
+        auto plan = PlanNode::nl_join(PlanNode::memory(tuples_of(left)),
+                                      PlanNode::memory(tuples_of(right)),
+                                      Predicate::within_of(0, 1, radius));
+        auto res = execute(*plan, ctx);
+        int64_t n = static_cast<int64_t>(res.tuples.size());
+        int32_t* a = static_cast<int32_t*>(std::malloc(std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        int32_t* b = static_cast<int32_t*>(std::malloc(std::max<int64_t>(n, 1) * sizeof(int32_t)));
+        for (int64_t k = 0; k < n; k++) {
+            a[k] = static_cast<int32_t>(res.tuples[k][0].patch_id - 1);
+            b[k] = static_cast<int32_t>(res.tuples[k][1].patch_id - ((1ull << 32) + 1));
+        }
+        *out_count = n;
+        *out_left = a;
+        *out_right = b;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// The q1 near-duplicate-frame query (src/bench.cpp:695-730) on in-memory
+// frames: whole-image colour histograms (generate whole_image +
+// color_histogram, B bins), then select(sim_join(h, h, tau), frameno != frameno).
+// Returns (frame a, frame b) per result tuple in emission order; free with ref_free.
+REF_API int ref_q1(const uint8_t* frames, int64_t n, int32_t H, int32_t W, int32_t bins,
+                   double tau, int64_t* out_count, int32_t** out_a, int32_t** out_b) {
+    try {
+        GeneratorSpec g;
+        g.kind = GeneratorKind::whole_image;
+        TransformerSpec t;
+        t.kind = TransformerKind::color_histogram;
+        t.bins = static_cast<uint32_t>(bins);
+        auto stream = transform(
+            generate(std::make_unique<VectorStream<Frame>>(make_frames(frames, n, H, W, 0)), g),
+            t);
+        std::vector<Patch> hist;
+        while (auto p = stream->next()) hist.push_back(std::move(*p));
+        ExecContext ctx;
+        auto plan = PlanNode::select(
+            PlanNode::sim_join(PlanNode::memory(tuples_of(hist)),
+                               PlanNode::memory(tuples_of(hist)), tau),
+            Predicate::cmp_of(CmpOp::ne, Operand::meta(0, "frameno"),
+                              Operand::meta(1, "frameno")));
+        auto res = execute(*plan, ctx);
+        int64_t m = static_cast<int64_t>(res.tuples.size());
+        int32_t* a = static_cast<int32_t*>(std::malloc(std::max<int64_t>(m, 1) * sizeof(int32_t)));
+        int32_t* b = static_cast<int32_t*>(std::malloc(std::max<int64_t>(m, 1) * sizeof(int32_t)));
+        for (int64_t k = 0; k < m; k++) {
+            a[k] = static_cast<int32_t>(res.tuples[k][0].meta_int("frameno"));
+            b[k] = static_cast<int32_t>(res.tuples[k][1].meta_int("frameno"));
+        }
+        *out_count = m;
+        *out_a = a;
+        *out_b = b;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}

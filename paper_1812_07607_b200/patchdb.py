@@ -10,6 +10,9 @@ Mirrors (paths relative to the reference's proj/ directory):
                              include/patchdb/etl.hpp:32-74, src/etl.cpp:252-373
 * BuildSide, sim_join_pairs  include/patchdb/query.hpp:84, 206-211,
                              src/query.cpp:467-528, 1094-1104
+* nl_join_within            PlanNode::nl_join with a within predicate,
+                             include/patchdb/query.hpp:135, src/query.cpp:142-151, 705-744
+* q1_duplicate_frames        the q1 near-duplicate-frame plan, src/bench.cpp:695-730
 * dedup_groups, dedup_stream PlanNode::dedup / dedup_stream,
                              include/patchdb/query.hpp:142, 203-204,
                              src/query.cpp:535-582, 1063-1092
@@ -720,3 +723,52 @@ def dedup_stream(items: Iterable[Patch], tau: float) -> Iterator[Patch]:
             raise ShapeError("dedup needs non-empty patch data")
     g = dedup(_dedup_matrix(items, "dedup"), tau)
     return iter([items[int(r)] for r in g.reps])
+
+
+# ---------------------------------------------------------------------------
+# Plans routed onto the join.
+
+
+def nl_join_within(left: Sequence[Patch], right: Sequence[Patch],
+                   radius: float) -> List[Tuple[Patch, Patch]]:
+    """PlanNode::nl_join(left, right, within_of(0, 1, radius)) over
+    single-patch tuples (src/query.cpp:142-151, 705-744): every (l, r) with
+    euclidean(l, r) <= radius, in nested-loop order (left order, then right
+    order) -- the B200 cross join sorted by (left, right).  A dimension
+    mismatch raises DimensionMismatchError as the predicate's first
+    evaluation would; empty sides give no tuples."""
+    if not left or not right:
+        return []
+    dims = {int(np.asarray(p.data).size) for p in left} | {int(np.asarray(p.data).size)
+                                                            for p in right}
+    if len(dims) != 1:
+        a, b = sorted(dims)[:2]
+        raise DimensionMismatchError(f"distance between {a} and {b} dimensional patches")
+    Lm = np.stack([np.asarray(p.data, dtype=np.float32).ravel() for p in left])
+    Rm = np.stack([np.asarray(p.data, dtype=np.float32).ravel() for p in right])
+    if Lm.shape[1] == 0:
+        # zero-dimensional patches are all at distance 0
+        return [(l, r) for l in left for r in right] if radius >= 0 else []
+    if radius < 0:
+        return []
+    res = sim_join(Lm, Rm, radius, sort=True)
+    return [(left[int(i)], right[int(j)]) for i, j in zip(res.left, res.right)]
+
+
+def q1_duplicate_frames(frames: np.ndarray, bins: int, tau: float):
+    """The q1 near-duplicate-frame query (src/bench.cpp:695-730) on frames
+    numbered 0..F-1: whole-image colour histograms (K1, generate whole_image
+    + color_histogram), then select(sim_join(h, h, tau), frameno != frameno)
+    (K2 + K3).  Returns (frame a, frame b) of every result tuple in the
+    reference's emission order: sim_join's probe order (the right side,
+    build side left on the size tie), then ascending build id."""
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    F, H, W = frames.shape[:3]
+    h = featurize_tiles(frames, H, W, bins, "per_channel")
+    res = sim_join(h, None, tau, self_join=True, sort=False)
+    i = res.left.astype(np.int64)
+    j = res.right.astype(np.int64)
+    a = np.concatenate([i, j])
+    b = np.concatenate([j, i])
+    order = np.lexsort((a, b))
+    return a[order], b[order]

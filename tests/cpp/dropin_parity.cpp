@@ -118,6 +118,45 @@ int main() {
         EXPECT(want.size() == got.size());
         for (size_t k = 0; k < want.size(); k++) EXPECT(want[k].data == got[k]);
     }
+    // nl_join with a pure within predicate (src/query.cpp:142-151, 705-744)
+    for (double r : {0.3, 0.45, 5.0}) {
+        std::vector<Tuple> lt, rt;
+        for (const auto& p : lp) lt.push_back(Tuple{p});
+        for (const auto& p : rp) rt.push_back(Tuple{p});
+        ExecContext ctx;
+        auto res = execute(*PlanNode::nl_join(PlanNode::memory(lt), PlanNode::memory(rt),
+                                              Predicate::within_of(0, 1, r)),
+                           ctx);
+        auto got = pdb::patchdb::nl_within_positions(lp, rp, r);
+        EXPECT(res.tuples.size() == got.size());
+        for (size_t k = 0; k < got.size(); k++) {
+            EXPECT(res.tuples[k][0].patch_id == lp[got[k].first].patch_id);
+            EXPECT(res.tuples[k][1].patch_id == rp[got[k].second].patch_id);
+        }
+    }
+    EXPECT((throws_as<DimensionMismatchError>([&] {
+        pdb::patchdb::nl_within_positions(lp, std::vector<Patch>{oracle::vec_patch(1, {1.0f})}, 1.0);
+    })));
+    // dedup (src/query.cpp:535-582): group sizes and lineage parents of
+    // PlanNode::dedup, kept set of dedup_stream
+    for (double tau : {0.05, 0.2, 0.6}) {
+        auto items = oracle::to_patches(oracle::clustered_points(11, 40, 12, 8, 0.02));
+        std::vector<Tuple> tt;
+        for (const auto& p : items) tt.push_back(Tuple{p});
+        ExecContext ctx;
+        auto res = execute(*PlanNode::dedup(PlanNode::memory(tt), tau), ctx);
+        auto g = pdb::patchdb::dedup_groups(items, tau);
+        EXPECT(res.tuples.size() == g.reps.size());
+        for (size_t r = 0; r < g.reps.size(); r++) {
+            EXPECT(res.tuples[r][0].lineage[0].parent_id() == items[g.reps[r]].patch_id);
+            EXPECT(res.tuples[r][0].meta_int("group_size") ==
+                   static_cast<int64_t>(g.members[r].size()));
+        }
+        auto kept = drain(*dedup_stream(std::make_unique<VectorStream<Patch>>(items), tau));
+        EXPECT(kept.size() == g.reps.size());
+        for (size_t r = 0; r < kept.size(); r++) EXPECT(kept[r].patch_id == items[g.reps[r]].patch_id);
+    }
+    EXPECT((throws_as<ConfigError>([&] { pdb::patchdb::dedup_groups(lp, -0.5); })));
     std::printf("DROPIN OK %d\n", checks);
     return 0;
 }

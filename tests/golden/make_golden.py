@@ -159,12 +159,48 @@ def dedup_fixtures():
     np.savez_compressed(os.path.join(HERE, "dedup_golden.npz"), **res)
 
 
+def nlj_fixtures():
+    """PlanNode::nl_join with a within predicate and the q1 plan, on the
+    reference (ref_nl_within, ref_q1)."""
+    res = {}
+    rng = np.random.default_rng(142)
+    cases = {
+        "random_50x3_r03": (rng.random((50, 3), dtype=np.float32), rng.random((40, 3), dtype=np.float32), 0.3),
+        # test_query.cpp:128-151 shape: 3-4-5 triangle at exactly the radius
+        "triangle_r5": (np.array([[0, 0], [3, 4], [6, 8]], np.float32),
+                        np.array([[0, 0], [3, 4]], np.float32), 5.0),
+        "clustered_d24": (workloads.clusters(300, 24, 20, 0.01, False, 77)[:150].copy(),
+                          workloads.clusters(300, 24, 20, 0.01, False, 77)[150:].copy(), 0.05),
+    }
+    for name, (L, R, r) in cases.items():
+        a, b = oracle.ref_nl_within(L, R, r)
+        res[f"nlj_{name}__L"] = L
+        res[f"nlj_{name}__R"] = R
+        res[f"nlj_{name}__r"] = np.array([r])
+        res[f"nlj_{name}__left"] = a
+        res[f"nlj_{name}__right"] = b
+        print(name, len(a))
+    for name, (F, H, W, bins, tau) in {"q1_60x96x128_b8": (60, 96, 128, 8, 0.2),
+                                       "q1_80x480x640_b4": (80, 480, 640, 4, 0.05)}.items():
+        fr, _ = workloads.frames(F, H, W, seed=2)
+        a, b = oracle.ref_q1(fr, bins, tau)
+        res[f"{name}__params"] = np.array([F, H, W, bins])
+        res[f"{name}__tau"] = np.array([tau])
+        res[f"{name}__sha256"] = np.frombuffer(hashlib.sha256(fr.tobytes()).digest(), np.uint8)
+        res[f"{name}__a"] = a
+        res[f"{name}__b"] = b
+        print(name, len(a))
+    np.savez_compressed(os.path.join(HERE, "nlj_golden.npz"), **res)
+
+
 if __name__ == "__main__":
     assert oracle.ref() is not None, "build oracle/_ref first: make -C oracle ref"
-    which = sys.argv[1:] or ["hist", "join", "dedup"]
+    which = sys.argv[1:] or ["hist", "join", "dedup", "nlj"]
     if "hist" in which:
         hist_fixtures()
     if "join" in which:
         join_fixtures()
     if "dedup" in which:
         dedup_fixtures()
+    if "nlj" in which:
+        nlj_fixtures()

@@ -102,3 +102,21 @@ def dedup_cases():
             X = _dedup_input(name)
             assert _sha(X) == z[f"{name}__sha256"].tobytes(), "generator drifted"
         yield name, X, float(z[f"{name}__tau"][0]), z[f"{name}__rep_of"], z[f"{name}__kept"]
+
+
+def nlj_cases():
+    """(name, L, R, radius, left, right) from PlanNode::nl_join(within)."""
+    z = np.load(os.path.join(HERE, "nlj_golden.npz"))
+    for name in sorted({k.split("__")[0] for k in z.files if k.startswith("nlj_")}):
+        yield (name, z[f"{name}__L"], z[f"{name}__R"], float(z[f"{name}__r"][0]),
+               z[f"{name}__left"], z[f"{name}__right"])
+
+
+def q1_cases():
+    """(name, frames, bins, tau, a, b) from the reference's q1 plan."""
+    z = np.load(os.path.join(HERE, "nlj_golden.npz"))
+    for name in sorted({k.split("__")[0] for k in z.files if k.startswith("q1_")}):
+        F, H, W, bins = (int(v) for v in z[f"{name}__params"])
+        fr, _ = workloads.frames(F, H, W, seed=2)
+        assert _sha(fr) == z[f"{name}__sha256"].tobytes(), "frame generator drifted"
+        yield name, fr, bins, float(z[f"{name}__tau"][0]), z[f"{name}__a"], z[f"{name}__b"]

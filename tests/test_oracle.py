@@ -140,3 +140,21 @@ def test_dedup_restatement_live_vs_reference():
         want, nw = oracle.ref_dedup(X, tau)
         assert np.array_equal(got, want) and nr == nw
     assert oracle.ref_dedup(np.zeros((3, 2), np.float32), -1.0) == 1  # ConfigError
+
+
+def test_nlj_within_and_q1_restatement_match_reference_golden():
+    """The NLJ within contract is the brute-force pair set in (left, right)
+    order; q1 is the self-join over whole-frame histograms in sim_join's
+    emission order (probe = right, then ascending build id) minus same-frame
+    pairs -- both pinned to the reference's own plan outputs."""
+    for name, L, R, r, left, right in golden_io.nlj_cases():
+        ol, orr, _ = oracle.sim_join(L, R, r)
+        assert np.array_equal(ol, left) and np.array_equal(orr, right), name
+    for name, fr, bins, tau, a, b in golden_io.q1_cases():
+        H, W = fr.shape[1:3]
+        h = oracle.featurize_tiles(fr, H, W, bins, 0)
+        i, j, _ = oracle.sim_join(h, None, tau, self_join=True)
+        ai = np.concatenate([i, j]).astype(np.int64)
+        bj = np.concatenate([j, i]).astype(np.int64)
+        order = np.lexsort((ai, bj))          # probe (right) order, then build id
+        assert np.array_equal(ai[order], a) and np.array_equal(bj[order], b), name
