@@ -43,7 +43,8 @@ enum {
     PDB_ERR_INVALID_ARGUMENT = 7, /* null pointer, negative size, bad flags */
     PDB_ERR_CUDA = 10,            /* CUDA runtime / driver failure */
     PDB_ERR_OUT_OF_MEMORY = 11,
-    PDB_ERR_NO_DEVICE = 12        /* no sm_100 device: the product has no CPU path */
+    PDB_ERR_NO_DEVICE = 12,       /* no sm_100 device: the product has no CPU path */
+    PDB_ERR_IO = 13               /* IoError: unreadable / malformed store file */
 };
 
 /* Message of the last failure on this thread ("" if none). */
@@ -227,6 +228,34 @@ int pdb_dedup(const float* X, int64_t n, int32_t d, double tau, const pdb_join_o
               int64_t* rep_of, int64_t* n_reps);
 int pdb_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, const pdb_join_opts* opts,
                   int64_t* d_rep_of, int64_t* n_reps);
+
+/* Frame source -- reads the reference's VideoStore files (record store +
+ * descriptor + frame_file / encoded_file / segmented_file layouts with the
+ * zlib delta clip codec; src/record_store.cpp, src/storage.cpp:170-501).
+ * pdb_store_read replaces VideoStore::open + scan([lo, hi)): frames come out
+ * decoded (lossy stores: the quantised pixels the codec kept), lo >= hi is
+ * PDB_ERR_CONFIG, both ends clamp to the frame count, lo = hi = -1 means
+ * every frame.  Clips decode in parallel on `threads` host threads (zlib).
+ * pdb_store_featurize decodes and runs K1 (pdb_featurize_tiles semantics)
+ * chunk by chunk into device features [frames, tiles, D]. */
+typedef struct pdb_store pdb_store;
+typedef struct pdb_store_info {
+    int64_t frame_count;
+    int32_t width, height;
+    int32_t layout;      /* 0 frame_file, 1 encoded_file, 2 segmented_file */
+    int32_t codec_mode;  /* 0 lossless, 1 lossy */
+    int32_t quant_step;
+    int32_t clip_len;
+    char video_id[256];
+} pdb_store_info;
+int pdb_store_open(const char* path, pdb_store** out);
+void pdb_store_close(pdb_store* s);
+int pdb_store_describe(const pdb_store* s, pdb_store_info* info);
+int pdb_store_read(const pdb_store* s, int64_t lo, int64_t hi, uint8_t* frames,
+                   int64_t* n_frames, int32_t threads);
+int pdb_store_featurize(const pdb_store* s, int64_t lo, int64_t hi, int32_t tile_h,
+                        int32_t tile_w, int32_t bins, int32_t mode, float* d_features,
+                        int64_t* n_frames, int32_t threads, void* stream);
 
 /* Pinned host memory helpers (the e2e path copies from pinned buffers). */
 void* pdb_host_alloc(int64_t bytes);

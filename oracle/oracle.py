@@ -85,6 +85,9 @@ def ref():
         pp = C.POINTER(C.POINTER(i32))
         L.ref_nl_within.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(i64), pp, pp]
         L.ref_q1.argtypes = [vp, i64, i32, i32, i32, f64, C.POINTER(i64), pp, pp]
+        L.ref_store_write.argtypes = [vp, i64, i32, i32, i32, i32, i32, C.c_char_p]
+        L.ref_store_scan.argtypes = [C.c_char_p, i64, i64, vp]
+        L.ref_store_scan.restype = i64
         _ref = L
     return _ref
 
@@ -294,3 +297,22 @@ def ref_q1(frames, bins, tau):
     frames = np.ascontiguousarray(frames, dtype=np.uint8)
     F, H, W = frames.shape[:3]
     return _ref_pairs(ref().ref_q1, _p(frames), F, H, W, int(bins), float(tau))
+
+
+def ref_store_write(frames, path, layout=0, quant_step=0, clip_len=64):
+    """VideoStore::ingest of frames 0..F-1 (layout 0 frame_file, 1
+    encoded_file, 2 segmented_file; quant_step 0 = lossless)."""
+    frames = np.ascontiguousarray(frames, dtype=np.uint8)
+    F, H, W = frames.shape[:3]
+    return ref().ref_store_write(_p(frames), F, H, W, layout, quant_step, clip_len,
+                                 str(path).encode())
+
+
+def ref_store_scan(path, F, H, W, lo=-1, hi=-1):
+    """VideoStore::open(path).scan([lo, hi)) decoded frames."""
+    n = F if lo < 0 else hi - lo
+    out = np.empty((max(n, 1), H, W, 3), np.uint8)
+    k = ref().ref_store_scan(str(path).encode(), lo, hi, _p(out))
+    if k < 0:
+        return int(-k)
+    return out[:k]

@@ -32,6 +32,7 @@
 #include "patchdb/etl.hpp"
 #include "patchdb/index.hpp"
 #include "patchdb/query.hpp"
+#include "patchdb/storage.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -384,5 +385,48 @@ REF_API int ref_q1(const uint8_t* frames, int64_t n, int32_t H, int32_t W, int32
     } catch (const std::exception& e) {
         g_err = e.what();
         return code_of(e);
+    }
+}
+
+// VideoStore::ingest (src/storage.cpp:311-378): writes frames 0..n-1 of
+// video `vid` into a store at `path` (layout 0 frame_file, 1 encoded_file,
+// 2 segmented_file; quant_step 0 = lossless, else lossy with that step).
+REF_API int ref_store_write(const uint8_t* frames, int64_t n, int32_t H, int32_t W, int32_t layout,
+                            int32_t quant_step, int32_t clip_len, const char* path) {
+    try {
+        auto fs = make_frames(frames, n, H, W, 0);
+        StoreDescriptor desc;
+        desc.layout = static_cast<Layout>(layout);
+        desc.codec = quant_step ? CodecConfig::lossy(static_cast<uint8_t>(quant_step))
+                                : CodecConfig::lossless();
+        desc.clip_len = static_cast<uint32_t>(clip_len);
+        desc.path = path;
+        VectorStream<Frame> s(std::move(fs));
+        VideoStore::ingest(s, desc);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+// VideoStore::open + scan([lo, hi)) (src/storage.cpp:380-501): the decoded
+// frames into out [hi-lo, H, W, 3]; returns the frame count (or -code).
+REF_API int64_t ref_store_scan(const char* path, int64_t lo, int64_t hi, uint8_t* out) {
+    try {
+        auto vs = VideoStore::open(path);
+        IoCounters io;
+        std::optional<std::pair<uint64_t, uint64_t>> range;
+        if (lo >= 0) range = std::make_pair(static_cast<uint64_t>(lo), static_cast<uint64_t>(hi));
+        auto s = vs.scan(range, io);
+        int64_t k = 0;
+        while (auto f = s->next()) {
+            std::memcpy(out + k * f->pixels.size(), f->pixels.data(), f->pixels.size());
+            k++;
+        }
+        return k;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -code_of(e);
     }
 }

@@ -29,6 +29,7 @@ PDB_ERR_INVALID_ARGUMENT = 7
 PDB_ERR_CUDA = 10
 PDB_ERR_OUT_OF_MEMORY = 11
 PDB_ERR_NO_DEVICE = 12
+PDB_ERR_IO = 13
 
 PDB_HIST_PER_CHANNEL = 0
 PDB_HIST_JOINT = 1
@@ -45,7 +46,15 @@ EXPORTS = (
     "pdb_sim_join", "pdb_pairs_free", "pdb_sim_join_dev", "pdb_dev_pairs_free",
     "pdb_featurize_join", "pdb_host_alloc", "pdb_host_free",
     "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
+    "pdb_store_open", "pdb_store_close", "pdb_store_describe", "pdb_store_read",
+    "pdb_store_featurize",
 )
+
+
+class StoreInfo(C.Structure):
+    _fields_ = [("frame_count", C.c_int64), ("width", C.c_int32), ("height", C.c_int32),
+                ("layout", C.c_int32), ("codec_mode", C.c_int32), ("quant_step", C.c_int32),
+                ("clip_len", C.c_int32), ("video_id", C.c_char * 256)]
 
 
 class JoinOpts(C.Structure):
@@ -113,6 +122,13 @@ def lib() -> C.CDLL:
                                                C.POINTER(DevPairs), C.POINTER(JoinStats)]
         L.pdb_dedup.argtypes = [vp, i64, i32, f64, C.POINTER(JoinOpts), vp, C.POINTER(i64)]
         L.pdb_dedup_dev.argtypes = [vp, i64, i32, f64, C.POINTER(JoinOpts), vp, C.POINTER(i64)]
+        L.pdb_store_open.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.pdb_store_close.argtypes = [vp]
+        L.pdb_store_close.restype = None
+        L.pdb_store_describe.argtypes = [vp, C.POINTER(StoreInfo)]
+        L.pdb_store_read.argtypes = [vp, i64, i64, vp, C.POINTER(i64), i32]
+        L.pdb_store_featurize.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, C.POINTER(i64),
+                                          i32, vp]
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

@@ -13,6 +13,9 @@ Mirrors (paths relative to the reference's proj/ directory):
 * nl_join_within            PlanNode::nl_join with a within predicate,
                              include/patchdb/query.hpp:135, src/query.cpp:142-151, 705-744
 * q1_duplicate_frames        the q1 near-duplicate-frame plan, src/bench.cpp:695-730
+* VideoStore (open, scan, featurize)  the frame source: the reference's
+                             store files, include/patchdb/storage.hpp:60-89,
+                             src/storage.cpp:170-501, src/record_store.cpp
 * dedup_groups, dedup_stream PlanNode::dedup / dedup_stream,
                              include/patchdb/query.hpp:142, 203-204,
                              src/query.cpp:535-582, 1063-1092
@@ -66,6 +69,10 @@ class RegionOutOfBoundsError(Error):
     pass
 
 
+class IoError(Error):
+    """patchdb::IoError (unreadable / malformed store file)."""
+
+
 class DeviceError(Error):
     """CUDA failure, missing sm_100 device or out-of-memory (no CPU path)."""
 
@@ -76,6 +83,7 @@ _STATUS_EXC = {
     capi.PDB_ERR_MIXED_DIMENSION: MixedDimensionError,
     capi.PDB_ERR_DIMENSION_MISMATCH: DimensionMismatchError,
     capi.PDB_ERR_DUPLICATE_ID: DuplicatePatchIdError,
+    capi.PDB_ERR_IO: IoError,
 }
 
 
@@ -772,3 +780,96 @@ def q1_duplicate_frames(frames: np.ndarray, bins: int, tau: float):
     b = np.concatenate([j, i])
     order = np.lexsort((a, b))
     return a[order], b[order]
+
+
+# ---------------------------------------------------------------------------
+# Frame source: the reference's VideoStore files.
+
+
+class VideoStore:
+    """VideoStore::open / scan (include/patchdb/storage.hpp:60-89) over the
+    reference's store files, decoded by libpdb_cuda's reader (parallel zlib
+    clip decode on host threads); ``featurize`` feeds the frames to K1."""
+
+    def __init__(self, handle, info):
+        self._h = handle
+        self.info = info
+
+    @classmethod
+    def open(cls, path: str) -> "VideoStore":
+        h = C.c_void_p()
+        _check(capi.lib().pdb_store_open(str(path).encode(), C.byref(h)))
+        info = capi.StoreInfo()
+        _check(capi.lib().pdb_store_describe(h, C.byref(info)))
+        return cls(h, info)
+
+    def close(self) -> None:
+        if self._h:
+            capi.lib().pdb_store_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def frame_count(self) -> int:
+        return int(self.info.frame_count)
+
+    @property
+    def width(self) -> int:
+        return int(self.info.width)
+
+    @property
+    def height(self) -> int:
+        return int(self.info.height)
+
+    @property
+    def video_id(self) -> str:
+        return self.info.video_id.decode()
+
+    def _range(self, rng):
+        if rng is None:
+            return -1, -1, self.frame_count
+        lo, hi = int(rng[0]), int(rng[1])
+        if lo >= hi:
+            raise ConfigError("scan range low bound must be below high bound")
+        n = max(min(hi, self.frame_count) - min(lo, self.frame_count), 0)
+        return lo, hi, n  # the library clamps both ends
+
+    def scan_array(self, rng: Optional[Tuple[int, int]] = None, threads: int = 0) -> np.ndarray:
+        """Frames [lo, hi) as a [n, H, W, 3] uint8 array (scan's frames)."""
+        lo, hi, n = self._range(rng)
+        out = np.empty((max(n, 1), self.height, self.width, 3), np.uint8)
+        got = C.c_int64()
+        _check(capi.lib().pdb_store_read(self._h, lo, hi, capi.ptr(out), C.byref(got),
+                                         threads or _host_threads()))
+        return out[:got.value]
+
+    def scan(self, rng: Optional[Tuple[int, int]] = None) -> Iterator[Frame]:
+        """VideoStore::scan: Frame objects in ascending frame order."""
+        arr = self.scan_array(rng)
+        first = 0 if rng is None else min(int(rng[0]), self.frame_count)
+        for k in range(arr.shape[0]):
+            yield Frame(self.video_id, first + k, arr[k])
+
+    def featurize(self, tile_h: int, tile_w: int, bins: int = 8, mode="per_channel",
+                  rng: Optional[Tuple[int, int]] = None, threads: int = 0, stream=None):
+        """Decode + K1 chunk by chunk: device features [frames * tiles, D]."""
+        import torch
+        m = _mode(mode)
+        lo, hi, n = self._range(rng)
+        D = hist_dim(bins, m)
+        tiles = (self.width // tile_w) * (self.height // tile_h)
+        out = torch.empty((max(n, 1) * tiles, D), dtype=torch.float32, device="cuda")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        got = C.c_int64()
+        _check(capi.lib().pdb_store_featurize(self._h, lo, hi, tile_h, tile_w, bins, m,
+                                              out.data_ptr(), C.byref(got),
+                                              threads or _host_threads(),
+                                              C.c_void_p(s.cuda_stream)))
+        return out[:got.value * tiles]
+
+
+def _host_threads() -> int:
+    import os
+    return max(1, min(os.cpu_count() or 1, 64))

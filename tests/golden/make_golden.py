@@ -193,9 +193,30 @@ def nlj_fixtures():
     np.savez_compressed(os.path.join(HERE, "nlj_golden.npz"), **res)
 
 
+def store_fixtures():
+    """VideoStore files written by the reference (VideoStore::ingest) for
+    every layout, lossless and lossy, and the frames its own scan decodes."""
+    sdir = os.path.join(HERE, "stores")
+    os.makedirs(sdir, exist_ok=True)
+    fr, _ = workloads.frames(16, 32, 48, seed=7, block=8, noise=2, period=6)
+    res = {}
+    for name, layout, q, cl in [("frame_file", 0, 0, 64), ("encoded_lossless", 1, 0, 64),
+                                ("encoded_lossy16", 1, 16, 64), ("segmented_lossless_c5", 2, 0, 5),
+                                ("segmented_lossy4_c8", 2, 4, 8)]:
+        path = os.path.join(sdir, f"{name}.pdb")
+        assert oracle.ref_store_write(fr, path, layout, q, cl) == 0
+        full = oracle.ref_store_scan(path, 16, 32, 48)
+        part = oracle.ref_store_scan(path, 16, 32, 48, 3, 13)
+        res[f"{name}__full_sha"] = np.frombuffer(hashlib.sha256(full.tobytes()).digest(), np.uint8)
+        res[f"{name}__part_sha"] = np.frombuffer(hashlib.sha256(part.tobytes()).digest(), np.uint8)
+        res[f"{name}__lossless"] = np.array([int(np.array_equal(full, fr))])
+        print(name, os.path.getsize(path))
+    np.savez_compressed(os.path.join(sdir, "stores_golden.npz"), **res)
+
+
 if __name__ == "__main__":
     assert oracle.ref() is not None, "build oracle/_ref first: make -C oracle ref"
-    which = sys.argv[1:] or ["hist", "join", "dedup", "nlj"]
+    which = sys.argv[1:] or ["hist", "join", "dedup", "nlj", "stores"]
     if "hist" in which:
         hist_fixtures()
     if "join" in which:
@@ -204,3 +225,5 @@ if __name__ == "__main__":
         dedup_fixtures()
     if "nlj" in which:
         nlj_fixtures()
+    if "stores" in which:
+        store_fixtures()

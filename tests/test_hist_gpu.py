@@ -141,3 +141,20 @@ def test_joint_tma_kernel_offset_frames():
     got = patchdb.featurize_tiles(view, 60, 80, 4, "joint").cpu().numpy()
     want = oracle.featurize_tiles(fr, 60, 80, 4, 1)
     assert np.array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.parametrize("name", ["frame_file", "encoded_lossy16", "segmented_lossy4_c8"])
+def test_store_featurize_matches_featurizing_the_decoded_frames(name):
+    """pdb_store_featurize (decode chunk by chunk + K1) equals K1 on the
+    frames the reference's scan decodes, and the restatement on them."""
+    import os
+    sdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "stores")
+    st = patchdb.VideoStore.open(os.path.join(sdir, f"{name}.pdb"))
+    fr = st.scan_array()
+    for bins, mode, th, tw in [(4, "joint", 8, 16), (8, "per_channel", 16, 16), (2, "joint", 32, 48)]:
+        got = st.featurize(th, tw, bins, mode).cpu().numpy()
+        want = oracle.featurize_tiles(fr, th, tw, bins, 1 if mode == "joint" else 0)
+        assert np.array_equal(_bits(got), _bits(want)), (name, bins, mode)
+        part = st.featurize(th, tw, bins, mode, rng=(3, 13)).cpu().numpy()
+        want_p = oracle.featurize_tiles(fr[3:13], th, tw, bins, 1 if mode == "joint" else 0)
+        assert np.array_equal(_bits(part), _bits(want_p))
