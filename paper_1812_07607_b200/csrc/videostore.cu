@@ -60,6 +60,13 @@ struct Store {
     uint32_t clip_len = 0, width = 0, height = 0;
     uint64_t frames = 0;
     std::string video_id;
+    // pinned staging of pdb_store_featurize, kept between calls
+    mutable uint8_t* pin[2] = {nullptr, nullptr};
+    mutable size_t pin_bytes = 0;
+    ~Store() {
+        if (pin[0]) cudaFreeHost(pin[0]);
+        if (pin[1]) cudaFreeHost(pin[1]);
+    }
 
     std::string read(uint64_t off, uint64_t len) const {
         File fh;
@@ -356,11 +363,14 @@ PDB_API int pdb_store_featurize(const pdb_store* s, int64_t lo, int64_t hi, int3
         const size_t fb = static_cast<size_t>(H) * W * 3;
         const int64_t tpf = static_cast<int64_t>(W / tile_w) * (H / tile_h);
         const int D = pdb::hist_dim(bins, mode);
-        // chunks of whole clips (segmented) or 64 frames: decode chunk k+1 on
-        // the host while chunk k is copied and featurized
-        const int64_t chunk = st.layout == 2 ? std::max<int64_t>(st.clip_len, 1) *
-                                                   std::max<int64_t>(1, 64 / std::max<int64_t>(st.clip_len, 1))
-                                             : 64;
+        // Decoding (zlib, host) is the bound: give it every thread.  Ranges up
+        // to 2 GB decode in one parallel pass into cached pinned memory;
+        // longer ones go in chunks of one clip per thread, chunk k+1
+        // decoding while chunk k is copied and featurized.
+        const int64_t cl = std::max<int64_t>(st.clip_len, 1);
+        const int64_t per_thread = st.layout == 2 ? cl : 8;
+        int64_t chunk = per_thread * std::max(threads, 1);
+        if (static_cast<size_t>(n) * fb <= (size_t{2} << 30)) chunk = n;
         if (st.layout == 1) {  // sequential codec: decode once, then stream
             pdb::DevBuf<uint8_t> dF(static_cast<size_t>(n) * fb, cs);
             std::vector<uint8_t> host(static_cast<size_t>(n) * fb);
@@ -370,20 +380,22 @@ PDB_API int pdb_store_featurize(const pdb_store* s, int64_t lo, int64_t hi, int3
             PDB_CUDA(cudaStreamSynchronize(cs));
             return;
         }
-        uint8_t* pin[2] = {nullptr, nullptr};
-        for (auto& p : pin)
-            if (cudaHostAlloc(reinterpret_cast<void**>(&p), static_cast<size_t>(chunk) * fb,
-                              cudaHostAllocDefault) != cudaSuccess) {
-                cudaGetLastError();
-                pdb::fail(PDB_ERR_OUT_OF_MEMORY, "pinned staging allocation failed");
+        const size_t need = static_cast<size_t>(chunk) * fb;
+        if (st.pin_bytes < need) {
+            for (auto& p : st.pin) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
             }
-        struct PinGuard {
-            uint8_t** p;
-            ~PinGuard() {
-                cudaFreeHost(p[0]);
-                cudaFreeHost(p[1]);
-            }
-        } pg{pin};
+            st.pin_bytes = 0;
+            for (auto& p : st.pin)
+                if (cudaHostAlloc(reinterpret_cast<void**>(&p), need, cudaHostAllocDefault) !=
+                    cudaSuccess) {
+                    cudaGetLastError();
+                    pdb::fail(PDB_ERR_OUT_OF_MEMORY, "pinned staging allocation failed");
+                }
+            st.pin_bytes = need;
+        }
+        uint8_t* const* pin = st.pin;
         pdb::DevBuf<uint8_t> dF(static_cast<size_t>(chunk) * fb * 2, cs);
         cudaEvent_t done[2];
         PDB_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));

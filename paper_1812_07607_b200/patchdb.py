@@ -804,7 +804,7 @@ class VideoStore:
         return cls(h, info)
 
     def close(self) -> None:
-        if self._h:
+        if getattr(self, "_h", None) and capi is not None:
             capi.lib().pdb_store_close(self._h)
             self._h = None
 
