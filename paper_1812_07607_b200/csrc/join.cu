@@ -92,6 +92,7 @@ constexpr int kModeCosBf16 = 2;
 // extra K=16 MMA per tile (A: constant [1,1,1,0..] rows, B: the three bf16
 // parts of -g_j), so the epilogue tests raw accumulators (DP <= 128 only).
 constexpr int kModeL2Bf16Aug = 3;
+constexpr int kModeL2Bf16Pair = 4;  // kModeL2Bf16Aug on CTA pairs (k_screen_pair)
 // Per-element perturbation bound U of the screen copies (round-to-nearest
 // to the MMA input type after an fp32 subtraction).
 constexpr double kU_tf32 = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
@@ -572,6 +573,384 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
 }
 
 // ---------------------------------------------------------------------------
+// K2 on CTA pairs (the default for the folded-g L2 screen, d <= 128, one
+// GPU): a cluster of two CTAs on one TPC runs tcgen05.mma.cta_group::2 with
+// M = 256 -- each CTA keeps its own 128-row block of L resident and loads
+// half of every 256-row R tile (and half of its folded-g block), and the
+// leader CTA issues the MMAs for both.  Per 128x256 tile an SM then reads
+// 8 KB of MMA operands per K=16 step instead of 12 KB and receives 20 KB of
+// TMA data instead of 40 KB: measured on the 1-SM screen, the SM moved a
+// near-constant ~110 B/clk of shared memory (MMA operand reads + TMA
+// writes) whatever d and the fold did, i.e. it was shared-memory bound at
+// 70 % of the MMA floor.
+//
+// Work units are (column chunk, row-block pair); the leader's producer
+// claims them and publishes each to both CTAs (DSMEM store + remote
+// arrive).  Barriers: full / a_full / t_empty / u_empty live in the leader
+// (the peer's TMA completes on the leader's full barriers, the peer's
+// epilogue and consumers arrive remotely); empty / a_empty / t_full / u_full
+// in both (the leader's MMA commits multicast to the pair).
+template <int DP>
+struct PairSmem {
+    static constexpr int NKB = DP / 64;
+    static constexpr int kHalfB = (BN / 2) * 128;             // 16 KB: 128 R rows x 128 B
+    static constexpr int kHalfG = (BN / 2) * kGCols * 2;      // 4 KB
+    static constexpr int kStage = NKB * kHalfB + kHalfG;      // one tile's half of R (+g)
+    static constexpr int kASlot = NKB * kABytes;
+    static constexpr int kConst = BM * kGCols * 2;            // the fold's constant A block
+    static constexpr int kTail = 512 + kEpiWarps * 32 * 16 + 128;
+    static constexpr int STAGES = (232448 - 1024 - 2 * kASlot - kConst - kTail) / kStage > 8
+                                      ? 8
+                                      : (232448 - 1024 - 2 * kASlot - kConst - kTail) / kStage;
+    static constexpr size_t kBytes =
+        1024 + 2 * static_cast<size_t>(kASlot) + kConst + static_cast<size_t>(STAGES) * kStage + kTail;
+};
+
+struct PairUnit {
+    int32_t q, j0, j1, chunk;  // row-block pair q (rows [256q, 256q+256)), columns [j0, j1)
+};
+
+__device__ __forceinline__ PairUnit decode_pair_unit(const ScreenParams& p, int64_t u) {
+    int lo = 0, hi = p.n_chunks;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(p.chunk_off + mid) <= u) lo = mid;
+        else hi = mid;
+    }
+    PairUnit r;
+    r.q = static_cast<int32_t>(u - __ldg(p.chunk_off + lo));
+    r.chunk = lo;
+    r.j0 = lo * p.ch;
+    r.j1 = min(r.j0 + p.ch, p.nt);
+    if (p.self_join) r.j0 = max(r.j0, r.q);
+    return r;
+}
+
+template <int DP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmG, const ScreenParams p) {
+    using SM = PairSmem<DP>;
+    constexpr int NKB = SM::NKB;
+    constexpr int STAGES = SM::STAGES;
+    constexpr int KE = 64;
+    constexpr uint32_t kIdescPair = ptx::idesc_bf16(2 * BM, BN);
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = ptx::smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+    uint8_t* smA = smem;                                  // 2 resident A slots
+    uint8_t* smC = smA + 2 * SM::kASlot;                  // constant fold block
+    uint8_t* smS = smC + SM::kConst;                      // stage ring
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smS + STAGES * SM::kStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* a_full = bars + 2 * STAGES;  // [2]
+    uint64_t* a_empty = a_full + 2;        // [2]
+    uint64_t* t_full = a_full + 4;         // [2]
+    uint64_t* t_empty = a_full + 6;        // [2]
+    uint64_t* u_full = a_full + 8;         // [4]
+    uint64_t* u_empty = a_full + 12;       // [4]
+    volatile int64_t* u_val = reinterpret_cast<volatile int64_t*>(a_full + 16);  // [4]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 20);
+    int4* r_smem = reinterpret_cast<int4*>(smem_raw + (smS - smem_raw) + STAGES * SM::kStage + 512);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    auto leader_addr = [&](const void* p_local) { return ptx::mapa(ptx::smem_u32(p_local), 0); };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; a++) {
+            ptx::mbar_init(&a_full[a], 1);
+            ptx::mbar_init(&a_empty[a], 1);
+            ptx::mbar_init(&t_full[a], 1);
+            ptx::mbar_init(&t_empty[a], 2 * kEpiWarps);
+        }
+        for (int k = 0; k < 4; k++) {
+            ptx::mbar_init(&u_full[k], 1);
+            ptx::mbar_init(&u_empty[k], 2 + 2 * kEpiWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        ptx::tma_prefetch_desc(&tmG);
+    }
+    // constant A block for the folded g ([1, 1, 1, 0, ...], 32B-swizzled K-major)
+    for (int qd = threadIdx.x; qd < BM * 2; qd += blockDim.x) {
+        const int r = qd >> 1, c = qd & 1;
+        reinterpret_cast<uint4*>(smC)[qd] = c == ((r >> 2) & 1)
+                                                ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u)
+                                                : make_uint4(0u, 0u, 0u, 0u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 1) ptx::tmem_alloc_pair(tmem_slot, kTmemCols);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
+
+    // unit ring consumers: leader's MMA lane and epilogue warps, the peer's
+    // producer lane and epilogue warps; each frees its slot on the leader
+    int u_slot = 0;
+    uint32_t u_phase = 0;
+    auto take_unit = [&](bool whole_warp) -> int64_t {
+        ptx::mbar_wait_acq_cluster(&u_full[u_slot], u_phase);
+        const int64_t u = u_val[u_slot];
+        if (whole_warp) __syncwarp();
+        if (!whole_warp || lane == 0) {
+            if (leader) ptx::mbar_arrive(&u_empty[u_slot]);
+            else ptx::mbar_arrive_cluster(leader_addr(&u_empty[u_slot]));
+        }
+        if (++u_slot == 4) {
+            u_slot = 0;
+            u_phase ^= 1;
+        }
+        return u;
+    };
+
+    if (warp == 0) {
+        // ===================== TMA producers (one per CTA) =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t na = 0;
+            int ps = 0;
+            uint32_t pph = 0;
+            auto claim = [&]() -> int64_t {
+                const int64_t c = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
+                return c < p.n_units ? c : -1;
+            };
+            int64_t u = leader ? claim() : 0;
+            for (;;) {
+                if (leader) {
+                    // publish u to both CTAs of the pair
+                    ptx::mbar_wait_acq_cluster(&u_empty[ps], pph ^ 1);
+                    u_val[ps] = u;
+                    ptx::st_cluster_u64(ptx::mapa(ptx::smem_u32(const_cast<int64_t*>(&u_val[ps])), 1),
+                                        static_cast<uint64_t>(u));
+                    ptx::mbar_arrive(&u_full[ps]);
+                    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&u_full[ps]), 1));
+                    if (++ps == 4) {
+                        ps = 0;
+                        pph ^= 1;
+                    }
+                } else {
+                    u = take_unit(false);
+                }
+                if (u < 0) break;
+                const int64_t u_next = leader ? claim() : 0;
+                const PairUnit w = decode_pair_unit(p, u);
+                const int32_t rb = 2 * w.q + static_cast<int32_t>(rank);
+                {
+                    const uint32_t slot = na & 1;
+                    ptx::mbar_wait(&a_empty[slot], ((na >> 1) & 1) ^ 1);
+                    if (leader) ptx::mbar_arrive_expect_tx(&a_full[slot], 2 * NKB * kABytes);
+                    const uint32_t bar = leader_addr(&a_full[slot]);
+                    for (int kb = 0; kb < NKB; kb++)
+                        ptx::tma_load_2d_pair(smA + slot * SM::kASlot + kb * kABytes, &tmA, bar,
+                                              kb * KE, rb * BM);
+                    na++;
+                }
+                for (int J = w.j0; J < w.j1; J++) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* st = smS + stage * SM::kStage;
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * SM::kStage);
+                    const uint32_t bar = leader_addr(&full[stage]);
+                    const int32_t r0 = J * BN + static_cast<int32_t>(rank) * (BN / 2);
+                    for (int kb = 0; kb < NKB; kb++)
+                        ptx::tma_load_2d_pair(st + kb * SM::kHalfB, &tmB, bar, kb * KE, r0);
+                    ptx::tma_load_2d_pair(st + NKB * SM::kHalfB, &tmG, bar, 0, r0);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (leader) u = u_next;
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader, one thread) =====================
+        if (leader && lane == 0) {
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0, na = 0;
+            unsigned long long ntiles = 0;
+            for (;;) {
+                const int64_t u = take_unit(false);
+                if (u < 0) break;
+                const PairUnit w = decode_pair_unit(p, u);
+                const uint32_t slot = na & 1;
+                ptx::mbar_wait(&a_full[slot], (na >> 1) & 1);
+                ptx::tc_fence_after();
+                const uint8_t* sa = smA + slot * SM::kASlot;
+                for (int J = w.j0; J < w.j1; J++) {
+                    ptx::mbar_wait(&t_empty[acc], acc_phase ^ 1);
+                    ptx::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint8_t* st = smS + stage * SM::kStage;
+                    for (int kb = 0; kb < NKB; kb++) {
+                        const uint32_t a_addr = ptx::smem_u32(sa + kb * kABytes);
+                        const uint32_t b_addr = ptx::smem_u32(st + kb * SM::kHalfB);
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++)
+                            ptx::mma_f16_pair(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
+                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescPair,
+                                              (kb | kk) != 0);
+                    }
+                    // the folded-g block: one K=16 step on 32-byte rows
+                    ptx::mma_f16_pair(d_tmem, ptx::sdesc_k_sw32(ptx::smem_u32(smC)),
+                                      ptx::sdesc_k_sw32(ptx::smem_u32(st + NKB * SM::kHalfB)),
+                                      kIdescPair, 1u);
+                    ptx::mma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    ptx::mma_commit_pair(&t_full[acc], 0x3);
+                    ntiles += 2;
+                    if (++acc == 2) {
+                        acc = 0;
+                        acc_phase ^= 1;
+                    }
+                }
+                ptx::mma_commit_pair(&a_empty[slot], 0x3);
+                na++;
+            }
+            atomicAdd(p.tiles, ntiles);
+        }
+    } else {
+        // ===================== epilogue (warps 2-9 of each CTA) =====================
+        const int ew = warp - 2;
+        const int qd = warp & 3;
+        const int half = ew >> 2;
+        const int row = qd * 32 + lane;
+        const uint32_t t_lane = static_cast<uint32_t>(qd * 32) << 16;
+        int4* rbuf = r_smem + ew * 32;
+        uint32_t nbuf = 0;
+        unsigned long long ncand = 0;
+        auto flush = [&]() {
+            __syncwarp();
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(nbuf));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (lane < static_cast<int>(nbuf) && base + lane < p.cap) p.rec[base + lane] = rbuf[lane];
+            __syncwarp();
+            nbuf = 0;
+        };
+        const uint32_t t_empty_remote = leader ? 0u : leader_addr(&t_empty[0]);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (;;) {
+            const int64_t u = take_unit(true);
+            if (u < 0) break;
+            const PairUnit w = decode_pair_unit(p, u);
+            const int64_t i = (static_cast<int64_t>(2 * w.q) + rank) * BM + row;
+            const bool row_ok = i < p.nL;
+            const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
+            const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
+            float h;
+            if (sn == kFlagNonFinite) {
+                h = __int_as_float(0x7f800000);
+            } else if (sn == kFlagBig) {
+                h = -__int_as_float(0x7f800000);
+            } else {
+                const float ms = __ldg(p.cmaxS + w.chunk), mn = __ldg(p.cmaxN + w.chunk);
+                const double r = p.tau_p + p.u * (static_cast<double>(sn) + ms) + 1e-30;
+                const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
+                h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
+            }
+            for (int J = w.j0; J < w.j1; J++) {
+                ptx::mbar_wait(&t_full[acc], acc_phase);  // a tcgen05.commit arrival
+                ptx::tc_fence_after();
+                const int64_t colw = static_cast<int64_t>(J) * BN + half * kColsPerWarp;
+                const uint32_t t_acc =
+                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * kColsPerWarp);
+                auto process = [&](const uint32_t(&v)[32], int c) {
+                    float m = -__int_as_float(0x7f800000);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) m = fmaxf(m, __uint_as_float(v[k]));
+                    const bool hit = row_ok && m >= h;
+                    if (__any_sync(0xffffffffu, hit)) {
+                        const int64_t col0 = colw + c * 32;
+                        uint32_t mask = 0;
+                        if (hit) {
+#pragma unroll
+                            for (int k = 0; k < 32; k++)
+                                mask |= static_cast<uint32_t>(__uint_as_float(v[k]) >= h) << k;
+                            if (col0 + 32 > p.nR)
+                                mask &= p.nR > col0 ? (0xffffffffu >> (32 - (p.nR - col0))) : 0u;
+                            if (p.self_join) {
+                                const int64_t lo = i + 1 - col0;
+                                mask &= lo <= 0 ? 0xffffffffu : (lo >= 32 ? 0u : (0xffffffffu << lo));
+                            }
+                        }
+                        const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
+                        if (bal) {
+                            const uint32_t nr = __popc(bal);
+                            if (nbuf + nr > 32) flush();
+                            ncand += __popc(mask);
+                            if (mask)
+                                rbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] =
+                                    make_int4(static_cast<int>(i), static_cast<int>(col0),
+                                              static_cast<int>(mask), 0);
+                            nbuf += nr;
+                        }
+                    }
+                };
+                uint32_t vbuf[2][32];
+                ptx::tmem_ld32(t_acc, vbuf[0]);
+                ptx::tmem_ld_wait();
+                ptx::reg_fence(vbuf[0]);
+#pragma unroll
+                for (int c = 0; c < kChunks; c++) {
+                    if (c + 1 < kChunks) {
+                        ptx::tmem_ld32(t_acc + (c + 1) * 32, vbuf[(c + 1) & 1]);
+                    } else {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {  // this CTA's TMEM reads of the tile are done
+                            if (leader) ptx::mbar_arrive(&t_empty[acc]);
+                            else ptx::mbar_arrive_cluster_relaxed(t_empty_remote + acc * 8);
+                        }
+                    }
+                    process(vbuf[c & 1], c);
+                    if (c + 1 < kChunks) {
+                        ptx::tmem_ld_wait();
+                        ptx::reg_fence(vbuf[(c + 1) & 1]);
+                    }
+                }
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+        if (nbuf) flush();
+        unsigned long long nc = ncand;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
+        if (lane == 0 && nc) atomicAdd(p.ncand, nc);
+    }
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // the peer's smem stays alive until the leader's MMAs are done
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Preparation kernels.
 // The centre mu only has to be a fixed vector (distances are translation
 // invariant and the margin is computed from the centred copies), so the mean
@@ -823,7 +1202,7 @@ __global__ void k_tile_stats(const float* __restrict__ hn, const float* __restri
 // the screen / re-check counters (this is the first kernel they follow).
 __global__ void __launch_bounds__(1024)
 k_chunk_plan(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN, int nt, int ch,
-             int n_chunks, int64_t n_rb, int self, int P, int shard, float* __restrict__ cmaxS,
+             int n_chunks, int64_t n_rb, int rpt, int self, int P, int shard, float* __restrict__ cmaxS,
              float* __restrict__ cmaxN, int64_t* __restrict__ chunk_off,
              unsigned long long* __restrict__ counters) {
     ptx::pdl_wait();
@@ -844,7 +1223,7 @@ k_chunk_plan(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN, i
             cmaxN[c] = b;
         }
         int64_t lim = n_rb;
-        if (self) lim = min(n_rb, static_cast<int64_t>(2) * (c + 1) * ch);
+        if (self) lim = min(n_rb, static_cast<int64_t>(rpt) * (c + 1) * ch);
         const int64_t full = lim / P, rem = lim % P;
         const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
         local += full + (pos_last < rem ? 1 : 0);
@@ -861,7 +1240,7 @@ k_chunk_plan(const float* __restrict__ tmaxS, const float* __restrict__ tmaxN, i
     if (t == 0) chunk_off[0] = 0;
     for (int c = t * per; c < min((t + 1) * per, n_chunks); c++) {
         int64_t lim = n_rb;
-        if (self) lim = min(n_rb, static_cast<int64_t>(2) * (c + 1) * ch);
+        if (self) lim = min(n_rb, static_cast<int64_t>(rpt) * (c + 1) * ch);
         const int64_t full = lim / P, rem = lim % P;
         const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
         run += full + (pos_last < rem ? 1 : 0);
@@ -1118,11 +1497,11 @@ CUtensorMap make_tmap(const DeviceCtx& ctx, const void* base, int64_t rows, int 
 
 // The folded-g rows: [n, kGCols] bf16, one 32-byte K=16 slice per row,
 // loaded 256 rows at a time in the 32B-swizzled layout of sdesc_k_sw32.
-CUtensorMap make_tmap_g(const DeviceCtx& ctx, const void* base, int64_t rows) {
+CUtensorMap make_tmap_g(const DeviceCtx& ctx, const void* base, int64_t rows, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kGCols), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kGCols) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kGCols), static_cast<cuuint32_t>(BN)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kGCols), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
     const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
@@ -1145,9 +1524,28 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     PDB_CUDA(cudaGetLastError());
 }
 
+template <int DP>
+void launch_screen_pair(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMap& tB,
+                        const CUtensorMap& tG, const ScreenParams& p, cudaStream_t s) {
+    constexpr size_t smem = PairSmem<DP>::kBytes;
+    static_assert(smem <= 232448, "shared memory budget");
+    auto k = k_screen_pair<DP>;
+    set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
+    const int64_t clusters = std::min<int64_t>(ctx.sm_count / 2, std::max<int64_t>(p.n_units, 1));
+    launch_pdl(k, dim3(static_cast<unsigned>(2 * clusters)), dim3(kThreads), smem, s, tA, tB, tG, p);
+    PDB_CUDA(cudaGetLastError());
+}
+
 void dispatch_screen(int DP, int mode, const DeviceCtx& ctx, const CUtensorMap& tA,
                      const CUtensorMap& tB, const CUtensorMap& tG, const ScreenParams& p,
                      cudaStream_t s) {
+    if (mode == kModeL2Bf16Pair) {
+        switch (DP) {
+            case 64: launch_screen_pair<64>(ctx, tA, tB, tG, p, s); return;
+            case 128: launch_screen_pair<128>(ctx, tA, tB, tG, p, s); return;
+        }
+        fail(PDB_ERR_CONFIG, "join: unsupported padded dimension for the paired screen");
+    }
     if (mode == kModeL2Bf16Aug) {
         switch (DP) {
             case 64: launch_screen<64, true, 4, kModeL2Bf16Aug>(ctx, tA, tB, tG, p, s); return;
@@ -1243,18 +1641,22 @@ struct PhaseTimer {
 struct UnitPlan {
     int64_t* off = nullptr;  // device [n_chunks + 1], caller-provided (<= nt + 1 entries)
     int ch = 1, nt = 0, n_chunks = 0;
+    int rpt = 2;             // row blocks per column tile (2: 128-row blocks, 1: pairs)
     int64_t n_rb = 0;
     int64_t n_units = 0;
 };
 
+// pair: units over 256-row block pairs (k_screen_pair; one shard only).
 void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, int shard,
-                UnitPlan& u) {
+                bool pair, UnitPlan& u) {
     u.nt = static_cast<int>(ceil_div(nR, BN));
-    u.n_rb = ceil_div(nL, BM);
+    u.rpt = pair ? 1 : 2;
+    u.n_rb = ceil_div(nL, pair ? 2 * BM : BM);
     const int64_t n_rb = u.n_rb;
     double total_tiles = 0;
     for (int64_t rb = 0; rb < n_rb; rb++)
-        total_tiles += self ? static_cast<double>(u.nt - (rb >> 1)) : static_cast<double>(u.nt);
+        total_tiles += self ? static_cast<double>(u.nt - (pair ? rb : rb >> 1)) : static_cast<double>(u.nt);
+    if (pair) total_tiles *= 2;  // 128x256 tiles
     total_tiles /= P;
     static const double div = [] {
         const char* e = getenv("PDB_UNIT_DIV");
@@ -1266,7 +1668,7 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
     int64_t n_units = 0;
     for (int c = 0; c < u.n_chunks; c++) {
         int64_t lim = n_rb;  // row blocks rb < lim are valid in chunk c
-        if (self) lim = std::min<int64_t>(n_rb, 2LL * (static_cast<int64_t>(c) + 1) * u.ch);
+        if (self) lim = std::min<int64_t>(n_rb, u.rpt * (static_cast<int64_t>(c) + 1) * u.ch);
         const int64_t full = lim / P, rem = lim % P;
         const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
         n_units += full + (pos_last < rem ? 1 : 0);
@@ -1519,7 +1921,13 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     UnitPlan plan;
     plan.off = ar.take<int64_t>(nt_ + 2);
-    plan_units(ctx, nL, nR, self, P, shard, plan);
+    // CTA pairs for the folded-g screen (opt-in, PDB_SCREEN_PAIR=1, one GPU):
+    // measured no faster than the 1-SM screen -- both run the tensor pipe at
+    // ~62-64 % active, ~0.9 of the measured cuBLAS bf16 rate for the MMA
+    // work they issue -- so the 1-SM kernel stays the default.
+    const char* pe = getenv("PDB_SCREEN_PAIR");
+    const bool pair = fold && P == 1 && pe && pe[0] == '1';
+    plan_units(ctx, nL, nR, self, P, shard, pair, plan);
     const int nt = plan.nt;
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     float* tmaxS = ar.take<float>(nt);
@@ -1529,14 +1937,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     float* cmaxS = ar.take<float>(nt + 1);
     float* cmaxN = ar.take<float>(nt + 1);
     launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
-               static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb,
+               static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb, plan.rpt,
                static_cast<int>(self), P, shard, cmaxS, cmaxN, plan.off, counters);
     PDB_CUDA(cudaGetLastError());
     launches += 2;
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
-    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, BN, !tf32);
-    const CUtensorMap tG = fold ? make_tmap_g(ctx, gx, nR) : tB;
+    const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, pair ? BN / 2 : BN, !tf32);
+    const CUtensorMap tG = fold ? make_tmap_g(ctx, gx, nR, pair ? BN / 2 : BN) : tB;
     ScreenParams p{};
     p.nL = nL;
     p.nR = nR;
@@ -1558,7 +1966,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
-    screen_and_recheck(ctx, s, DP, mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
+    screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
                            launch_pdl(k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s, 
@@ -1622,13 +2030,13 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
                s);
     UnitPlan plan;
     plan.off = ar.take<int64_t>(nt_ + 2);
-    plan_units(ctx, nL, nR, self, P, shard, plan);
+    plan_units(ctx, nL, nR, self, P, shard, false, plan);
     const int nt = plan.nt;
     float* hL = ar.take<float>(nL);
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     unsigned long long* counters = ar.take<unsigned long long>(5);
     launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(nullptr),
-               static_cast<const float*>(nullptr), nt, plan.ch, plan.n_chunks, plan.n_rb,
+               static_cast<const float*>(nullptr), nt, plan.ch, plan.n_chunks, plan.n_rb, plan.rpt,
                static_cast<int>(self), P, shard, static_cast<float*>(nullptr),
                static_cast<float*>(nullptr), plan.off, counters);
     launches++;

@@ -220,3 +220,17 @@ def test_config5_scaled_skewed_output_sampled_rows():
         m = (res.left >= r0) & (res.left < r0 + 64)
         assert np.array_equal(res.left[m], ol) and np.array_equal(res.right[m], orr)
         assert np.array_equal(res.dist[m], od.astype(np.float32))
+
+
+def test_cta_pair_screen_opt_in(monkeypatch):
+    """The cta_group::2 screen (PDB_SCREEN_PAIR=1) finds the same pair set as
+    the brute-force oracle, self and cross, with ragged edges."""
+    monkeypatch.setenv("PDB_SCREEN_PAIR", "1")
+    rng = np.random.default_rng(21)
+    for n, m, d, tau in [(3000, None, 64, 0.05), (1000, 777, 100, 0.9), (700, None, 17, 0.3)]:
+        L = workloads.clusters(n, d, 40, 0.02, True, 3) if m is None else rng.random((n, d), dtype=np.float32)
+        R = None if m is None else rng.random((m, d), dtype=np.float32)
+        got = patchdb.sim_join(L, R, tau, self_join=m is None)
+        ol, orr, od = oracle.sim_join(L, R, tau, self_join=m is None)
+        assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
+        assert np.array_equal(got.dist, od.astype(np.float32))
