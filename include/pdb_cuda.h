@@ -229,6 +229,13 @@ int pdb_dedup(const float* X, int64_t n, int32_t d, double tau, const pdb_join_o
 int pdb_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, const pdb_join_opts* opts,
                   int64_t* d_rep_of, int64_t* n_reps);
 
+/* Row-pair `within`: out[k] = euclidean(A[k], B[k]) <= radius (fp64,
+ * src/index.cpp:69-76) for k < n, A/B host fp32 [n, d].  Replaces the
+ * per-tuple within evaluation of eval_view (src/query.cpp:142-151) when both
+ * slots lie in one input; the plan layer batches every tuple into one call. */
+int pdb_rows_within(const float* A, const float* B, int64_t n, int32_t d, double radius,
+                    uint8_t* out);
+
 /* Frame source -- reads the reference's VideoStore files (record store +
  * descriptor + frame_file / encoded_file / segmented_file layouts with the
  * zlib delta clip codec; src/record_store.cpp, src/storage.cpp:170-501).

@@ -88,6 +88,8 @@ def ref():
         L.ref_store_write.argtypes = [vp, i64, i32, i32, i32, i32, i32, C.c_char_p]
         L.ref_store_scan.argtypes = [C.c_char_p, i64, i64, vp]
         L.ref_store_scan.restype = i64
+        L.ref_run_query.argtypes = [C.c_char_p, i32, i64]
+        L.ref_run_query.restype = vp
         _ref = L
     return _ref
 
@@ -316,3 +318,21 @@ def ref_store_scan(path, F, H, W, lo=-1, hi=-1):
     if k < 0:
         return int(-k)
     return out[:k]
+
+
+def ref_run_query(plan, with_data=False, reset_ids=1):
+    """patchdb.run_query on the reference (bindings/py_module.cpp:168-213):
+    the plan file's ETL section materialized, its plan executed.  Returns
+    {"tuples": [[patch, ...], ...]} (patch: id, shape, meta, lineage, data)
+    or raises RuntimeError with the reference's message."""
+    import json
+    if not isinstance(plan, str):
+        plan = json.dumps(plan)
+    L = ref()
+    ptr = L.ref_run_query(plan.encode(), int(bool(with_data)), int(reset_ids))
+    if not ptr:
+        raise RuntimeError(L.ref_last_error().decode())
+    try:
+        return json.loads(C.string_at(ptr).decode())
+    finally:
+        L.ref_free(C.c_void_p(ptr))

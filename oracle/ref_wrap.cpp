@@ -33,6 +33,7 @@
 #include "patchdb/index.hpp"
 #include "patchdb/query.hpp"
 #include "patchdb/storage.hpp"
+#include "patchdb/planfile.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -428,5 +429,95 @@ REF_API int64_t ref_store_scan(const char* path, int64_t lo, int64_t hi, uint8_t
     } catch (const std::exception& e) {
         g_err = e.what();
         return -code_of(e);
+    }
+}
+
+#include "json.hpp"
+
+namespace {
+nlohmann::json patch_json(const Patch& p, bool with_data) {
+    using nlohmann::json;
+    json d;
+    d["id"] = p.patch_id;
+    d["shape"] = p.shape;
+    json meta = json::object();
+    for (const auto& [k, v] : p.meta) {
+        if (const auto* i = std::get_if<int64_t>(&v)) meta[k] = *i;
+        else if (const auto* f = std::get_if<double>(&v)) meta[k] = *f;
+        else if (const auto* s = std::get_if<std::string>(&v)) meta[k] = *s;
+        else if (const auto* b = std::get_if<BoundingBox>(&v)) meta[k] = {b->x1, b->y1, b->x2, b->y2};
+        else meta[k] = std::get<std::vector<std::string>>(v);
+    }
+    d["meta"] = meta;
+    json lin = json::array();
+    for (const auto& s : p.lineage) {
+        json st;
+        st["op"] = s.op_name;
+        if (s.kind() == SourceKind::base_frame) st["frame"] = {s.frame().video_id, s.frame().frame_no};
+        else st["parent"] = s.parent_id();
+        st["digest"] = s.params_digest;
+        if (s.region) st["region"] = {s.region->x1, s.region->y1, s.region->x2, s.region->y2};
+        lin.push_back(st);
+    }
+    d["lineage"] = lin;
+    if (with_data) d["data"] = p.data;
+    return d;
+}
+}  // namespace
+
+// patchdb.run_query (bindings/py_module.cpp:168-213) on the reference: parse
+// the plan file, materialize its ETL section (materialize_etl, py_module.cpp:
+// 68-76), execute the plan.  Returns a malloc'd JSON document
+// {"tuples": [[patch, ...], ...]} (patch: id, shape, meta, lineage, data),
+// or NULL with ref_last_error set.  reset_ids: restart the patch-id counter.
+REF_API char* ref_run_query(const char* plan_json, int32_t with_data, int64_t reset_ids) {
+    try {
+        if (reset_ids > 0) reset_patch_ids(static_cast<uint64_t>(reset_ids));
+        PlanFile pf = PlanFile::parse(plan_json);
+        if (!pf.plan) throw ValidationError("plan file has no plan section");
+        auto stages = plan_stages(pf);
+        if (!stages.empty()) {
+            auto violations = validate_pipeline(stages);
+            // check_stages (bindings/py_module.cpp:54-66): every violation
+            std::string msg;
+            for (const auto& v : violations) {
+                if (!msg.empty()) msg += "; ";
+                msg += "stage " + std::to_string(v.stage) + ": " + v.message;
+            }
+            if (!msg.empty()) throw ValidationError(msg);
+        }
+        std::map<std::string, PatchCollection> cols;
+        if (pf.etl) {
+            const EtlSection& etl = *pf.etl;
+            auto it = pf.stores.find(etl.store);
+            std::string store_path = it == pf.stores.end() ? etl.store : it->second;
+            VideoStore vs = VideoStore::open(store_path);
+            IoCounters io;
+            auto stream = generate(vs.scan(std::nullopt, io), etl.generator);
+            for (const auto& t : etl.transformers) stream = transform(std::move(stream), t);
+            cols.emplace(etl.name, PatchCollection::materialize(*stream, etl.output));
+        }
+        for (const auto& [alias, path] : pf.collections)
+            cols.emplace(alias, PatchCollection::open(path, false));
+        std::map<std::string, VideoStore> stores;
+        for (const auto& [alias, path] : pf.stores) stores.emplace(alias, VideoStore::open(path));
+        ExecContext ctx;
+        for (const auto& [alias, col] : cols) ctx.collections[alias] = &col;
+        for (const auto& [alias, vs] : stores) ctx.videos[vs.video_id()] = &vs;
+        ExecResult res = execute(*pf.plan, ctx);
+        nlohmann::json out;
+        out["tuples"] = nlohmann::json::array();
+        for (const auto& t : res.tuples) {
+            nlohmann::json slots = nlohmann::json::array();
+            for (const auto& p : t) slots.push_back(patch_json(p, with_data != 0));
+            out["tuples"].push_back(slots);
+        }
+        const std::string s = out.dump();
+        char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+        return buf;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
     }
 }

@@ -47,7 +47,7 @@ EXPORTS = (
     "pdb_featurize_join", "pdb_host_alloc", "pdb_host_free",
     "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
     "pdb_store_open", "pdb_store_close", "pdb_store_describe", "pdb_store_read",
-    "pdb_store_featurize",
+    "pdb_store_featurize", "pdb_rows_within",
 )
 
 
@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
         L.pdb_store_read.argtypes = [vp, i64, i64, vp, C.POINTER(i64), i32]
         L.pdb_store_featurize.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, C.POINTER(i64),
                                           i32, vp]
+        L.pdb_rows_within.argtypes = [vp, vp, i64, i32, f64, vp]
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

@@ -516,6 +516,28 @@ PDB_API int pdb_dedup(const float* X, int64_t n, int32_t d, double tau, const pd
     });
 }
 
+PDB_API int pdb_rows_within(const float* A, const float* B, int64_t n, int32_t d, double radius,
+                            uint8_t* out) {
+    return guarded([&] {
+        if (n < 0 || d < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative size");
+        if (n > 0 && (!A || !B || !out)) fail(PDB_ERR_INVALID_ARGUMENT, "null rows");
+        if (n == 0) return;
+        device_ctx();
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t bytes = static_cast<size_t>(n) * d * sizeof(float);
+        DevBuf<float> dA(std::max<size_t>(bytes / sizeof(float), 1), s),
+            dB(std::max<size_t>(bytes / sizeof(float), 1), s);
+        DevBuf<uint8_t> dO(static_cast<size_t>(n), s);
+        if (bytes) {
+            PDB_CUDA(cudaMemcpyAsync(dA.p, A, bytes, cudaMemcpyHostToDevice, s));
+            PDB_CUDA(cudaMemcpyAsync(dB.p, B, bytes, cudaMemcpyHostToDevice, s));
+        }
+        run_rows_within(dA.p, dB.p, n, d, radius, dO.p, s);
+        PDB_CUDA(cudaMemcpyAsync(out, dO.p, static_cast<size_t>(n), cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 PDB_API void* pdb_host_alloc(int64_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, static_cast<size_t>(std::max<int64_t>(bytes, 1)), cudaHostAllocDefault) !=

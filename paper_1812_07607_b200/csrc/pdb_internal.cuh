@@ -131,6 +131,9 @@ PDB_HIDDEN void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R,
                                  pdb_dev_pairs* out, pdb_join_stats* stats);
 PDB_HIDDEN void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStream_t s,
                               int64_t* d_rep_of, int64_t* n_reps);
+// out[k] = euclidean(A[k], B[k]) <= radius (rows.cu)
+PDB_HIDDEN void run_rows_within(const float* d_A, const float* d_B, int64_t n, int32_t d,
+                                double radius, uint8_t* d_out, cudaStream_t s);
 PDB_HIDDEN void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int64_t nR,
                                  int32_t d, double min_cos, const pdb_join_opts& o,
                                  pdb_dev_pairs* out, pdb_join_stats* stats);

@@ -73,6 +73,22 @@ class IoError(Error):
     """patchdb::IoError (unreadable / malformed store file)."""
 
 
+class ValidationError(Error):
+    """patchdb::ValidationError (plan files, pipeline checks, tuple widths)."""
+
+
+class TagMismatchError(Error):
+    pass
+
+
+class MissingKeyError(Error):
+    pass
+
+
+class MalformedLineageError(Error):
+    pass
+
+
 class DeviceError(Error):
     """CUDA failure, missing sm_100 device or out-of-memory (no CPU path)."""
 
@@ -446,7 +462,8 @@ def next_patch_id() -> int:
 def _fnv_digest(name: str, items: Sequence[Tuple[str, object]]) -> int:
     """ParamsDigest (include/patchdb/core.hpp:155-196): FNV-1a-64 over the
     big-endian byte record str8(op_name) then, per param, str8(key) and
-    either tag 0 + i64 (int) or tag 1 + the f64 bit pattern (float)."""
+    either tag 0 + i64 (int), tag 1 + the f64 bit pattern (float) or tag 2
+    + str16 (string)."""
     import struct
     buf = bytearray()
     nb = name.encode()
@@ -455,6 +472,9 @@ def _fnv_digest(name: str, items: Sequence[Tuple[str, object]]) -> int:
         kb = k.encode()
         if isinstance(v, float):
             buf += bytes([len(kb)]) + kb + b"\x01" + struct.pack(">d", v)
+        elif isinstance(v, str):
+            vb = v.encode()
+            buf += bytes([len(kb)]) + kb + b"\x02" + struct.pack(">H", len(vb)) + vb
         else:
             buf += bytes([len(kb)]) + kb + b"\x00" + int(v & 0xFFFFFFFFFFFFFFFF).to_bytes(8, "big")
     h = 0xCBF29CE484222325

@@ -9,9 +9,12 @@ stored alongside outputs, so nothing needs the reference at test time.
 
 from __future__ import annotations
 
+import gzip
 import hashlib
+import json
 import os
 import sys
+import tempfile
 
 import numpy as np
 
@@ -214,9 +217,183 @@ def store_fixtures():
     np.savez_compressed(os.path.join(sdir, "stores_golden.npz"), **res)
 
 
+# ---- plan files (run_query / run_etl, bindings/py_module.cpp:139-213) -------
+
+def _tiles(bins=None, w=16, h=16, depth=False):
+    t = [{"kind": "depth_proxy"}] if depth else []
+    if bins:
+        t.append({"kind": "color_histogram", "bins": bins})
+    return {"kind": "tiles", "tile_w": w, "tile_h": h}, t
+
+
+def _cmp(op, lhs, rhs, offset=None):
+    d = {"kind": "cmp", "op": op, "lhs": lhs, "rhs": rhs}
+    if offset is not None:
+        d["offset"] = offset
+    return d
+
+
+def _within(a, b, r):
+    return {"kind": "within", "slot_a": a, "slot_b": b, "radius": r}
+
+
+def _fno(slot):
+    return {"slot": slot, "key": "frameno"}
+
+
+PLAN_ETLS = {
+    # name: (store fixture, generator, transformers)
+    "A": ("segmented_lossless_c5", *_tiles(4)),
+    "B": ("encoded_lossy16", {"kind": "whole_image"}, [{"kind": "color_histogram", "bins": 8}]),
+    "C": ("frame_file", *_tiles(4, depth=True)),
+    "P": ("segmented_lossy4_c8", *_tiles(None, 20, 7, depth=True)),
+}
+PLAN_COLLECTIONS = {
+    # reference-materialized collections the plans open by alias
+    "r4": ("encoded_lossless", *_tiles(4)),
+    "r8": ("frame_file", *_tiles(8)),
+}
+
+
+def plan_cases():
+    """(name, etl key, plan, with_data, gpu) -- every case's expected tuples
+    (ids, shape, meta, lineage, data) or error message come from the
+    reference's run_query."""
+    S = {"op": "scan", "collection": "etl"}
+    R4 = {"op": "scan", "collection": "r4"}
+    R8 = {"op": "scan", "collection": "r8"}
+    dd = lambda x, t: {"op": "dedup", "input": x, "tau": t}
+    sj = lambda l, r, t, side=None: dict({"op": "sim_join", "left": l, "right": r, "tau": t},
+                                         **({"build_side": side} if side else {}))
+    nl = lambda l, r, on: {"op": "nl_join", "left": l, "right": r, "on": on}
+    sel = lambda x, p: {"op": "select", "input": x, "pred": p}
+    return [
+        ("scan_A", "A", S, True, True),
+        ("simjoin_self_A", "A", sj(S, S, 0.05), False, True),
+        ("simjoin_A_r4_right", "A", sj(S, R4, 0.1, "right"), False, True),
+        ("simjoin_A_r4_left", "A", sj(S, R4, 0.1, "left"), False, True),
+        ("q1_select_A", "A", sel(sj(S, S, 0.1), _cmp("ne", _fno(0), _fno(1))), False, True),
+        ("dedup_A", "A", dd(S, 0.05), True, True),
+        ("dedup_A_tau0", "A", dd(S, 0.0), False, True),
+        ("dedup_A_neg", "A", dd(S, -1.0), False, True),
+        ("nlj_within_A_r4", "A", nl(S, R4, _within(0, 1, 0.1)), False, True),
+        ("nlj_and_A_r4", "A", nl(S, R4, {"kind": "and", "parts": [
+            _within(1, 0, 0.1), _cmp("ne", _fno(0), _fno(1))]}), False, True),
+        ("nlj_or_A_r4", "A", nl(sel(S, _cmp("lt", _fno(0), {"lit": 6})), R4, {"kind": "or", "parts": [
+            _within(0, 1, 0.05), _cmp("eq", {"slot": 1, "key": "bbox.x1"}, {"lit": 32})]}),
+         False, True),
+        ("select_within_pairs", "A", sel(sj(S, R4, 0.2), _within(0, 1, 0.1)), False, True),
+        ("countby_dedup_A", "A", {"op": "count_by", "input": dd(S, 0.1), "key": "frameno"},
+         False, True),
+        ("simjoin_dim_mismatch", "A", sj(S, R8, 0.1), False, True),
+        ("nlj_dim_mismatch", "A", nl(S, R8, _within(0, 1, 0.1)), False, True),
+        ("dedup_B", "B", dd(S, 0.02), True, True),
+        ("simjoin_B", "B", sj(S, S, 0.05), False, True),
+        ("scan_C", "C", S, True, True),
+        ("simjoin_dedups", "A", sj(dd(S, 0.05), dd(R4, 0.05), 0.1), False, True),
+        ("nlj_dedups", "A", nl(dd(S, 0.05), dd(R4, 0.05), _within(0, 1, 0.1)), False, True),
+        ("scan_P", "P", S, True, False),
+        ("countby_P", "P", {"op": "count_by", "input": S, "key": "depth"}, False, False),
+        ("select_P", "P", sel(S, {"kind": "and", "parts": [
+            _cmp("ge", {"slot": 0, "key": "bbox.y1"}, {"lit": 14}),
+            {"kind": "not", "part": _cmp("eq", _fno(0), {"lit": 3}, 1)}]}), False, False),
+        ("nlj_cmp_P", "P", nl(sel(S, _cmp("lt", _fno(0), {"lit": 2})), R4,
+                              _cmp("eq", _fno(0), _fno(1), 1)), False, False),
+        ("select_box_order_P", "P", sel(S, _cmp("lt", {"slot": 0, "key": "bbox"},
+                                                {"lit": [0, 0, 1, 1]})), False, False),
+        ("select_slot_P", "P", sel(S, _cmp("eq", {"slot": 2, "key": "frameno"}, {"lit": 1})),
+         False, False),
+    ]
+
+
+def plan_error_docs():
+    """Malformed plan files: the reference's ValidationError / ConfigError
+    messages ("@STORES@" / "@OUT@" are substituted at test time)."""
+    etl = {"name": "etl", "store": "@STORES@/frame_file.pdb",
+           "generator": {"kind": "tiles", "tile_w": 16, "tile_h": 16},
+           "transformers": [{"kind": "color_histogram", "bins": 4}], "output": "@OUT@/e.pdbc"}
+    S = {"op": "scan", "collection": "etl"}
+    bad = [
+        {"etl": etl, "plan": S, "extra": 1},
+        {"etl": etl},
+        {"etl": etl, "plan": {"op": "frobnicate"}},
+        {"etl": etl, "plan": {"op": "sim_join", "left": S, "right": S}},
+        {"etl": etl, "plan": {"op": "sim_join", "left": S, "right": S, "tau": "x"}},
+        {"etl": etl, "plan": {"op": "sim_join", "left": S, "right": S, "tau": 1, "build_side": "up"}},
+        {"etl": etl, "plan": {"op": "select", "input": S, "pred": {"kind": "near"}}},
+        {"etl": etl, "plan": {"op": "select", "input": S, "pred": _cmp("approx", _fno(0), _fno(0))}},
+        {"etl": etl, "plan": {"op": "select", "input": S, "pred": _cmp("eq", {"slot": -1, "key": "a"},
+                                                                         {"lit": 1})}},
+        {"etl": etl, "plan": {"op": "select", "input": S, "pred": _cmp("eq", _fno(0), {"lit": {}})}},
+        {"etl": etl, "plan": {"op": "dedup", "input": S}},
+        {"etl": etl, "plan": {"op": "scan"}},
+        {"etl": etl, "plan": {"op": "nl_join", "left": S, "right": S}},
+        {"etl": etl, "plan": {"op": "count_by", "input": S}},
+        {"etl": dict(etl, generator={"kind": "tiles", "tile_w": 0, "tile_h": 16}), "plan": S},
+        {"etl": dict(etl, generator={"kind": "mosaic"}), "plan": S},
+        {"etl": dict(etl, transformers=[{"kind": "color_histogram", "bins": 1}]), "plan": S},
+        {"etl": dict(etl, transformers=[{"kind": "color_histogram", "bins": 4},
+                                        {"kind": "color_histogram", "bins": 4}]), "plan": S},
+        {"etl": dict(etl, transformers=[{"kind": "color_histogram", "bins": 4},
+                                        {"kind": "depth_proxy"}]), "plan": S},
+        {"etl": dict(etl, transformers=[{"kind": "sharpen"}]), "plan": S},
+        {"etl": dict(etl, transformers={"kind": "depth_proxy"}), "plan": S},
+        {"etl": {k: v for k, v in etl.items() if k != "output"}, "plan": S},
+        {"etl": dict(etl, store="@STORES@/missing.pdb"), "plan": S},
+        {"etl": etl, "plan": {"op": "scan", "collection": "nope"}},
+        {"etl": etl, "plan": {"op": "select", "input": S, "pred": {"kind": "and", "parts": 3}}},
+        {"etl": etl, "stores": {"v": 3}, "plan": S},
+    ]
+    return [json.dumps(d) for d in bad] + ["{not json", "[]"]
+
+
+def _sub(doc: str, stores: str, out: str) -> str:
+    return doc.replace("@STORES@", stores).replace("@OUT@", out)
+
+
+def plan_doc(etl_key, plan, stores, out):
+    store, gen, trans = PLAN_ETLS[etl_key]
+    return json.dumps({"etl": {"name": "etl", "store": f"{stores}/{store}.pdb", "generator": gen,
+                               "transformers": trans, "output": f"{out}/etl_{etl_key}.pdbc"},
+                       "collections": {k: f"{stores}/{k}.pdbc" for k in PLAN_COLLECTIONS},
+                       "plan": plan})
+
+
+def plan_fixtures():
+    sdir = os.path.join(HERE, "stores")
+    tmp = tempfile.mkdtemp()
+    for name, (store, gen, trans) in PLAN_COLLECTIONS.items():
+        doc = json.dumps({"etl": {"name": "x", "store": f"{sdir}/{store}.pdb", "generator": gen,
+                                  "transformers": trans, "output": f"{sdir}/{name}.pdbc"},
+                          "plan": {"op": "scan", "collection": "x"}})
+        oracle.ref_run_query(doc, reset_ids=1000)
+    res = {"cases": [], "errors": [], "etl_sha": {}}
+    for name, key, plan, with_data, gpu in plan_cases():
+        doc = plan_doc(key, plan, sdir, tmp)
+        try:
+            r = oracle.ref_run_query(doc, with_data=with_data, reset_ids=1)
+            exp = {"tuples": r["tuples"]}
+        except RuntimeError as e:
+            exp = {"error": str(e)}
+        res["cases"].append({"name": name, "etl": key, "with_data": with_data, "gpu": gpu,
+                             "doc": plan_doc(key, plan, "@STORES@", "@OUT@"), **exp})
+        res["etl_sha"][key] = hashlib.sha256(open(f"{tmp}/etl_{key}.pdbc", "rb").read()).hexdigest()
+        print(name, len(exp.get("tuples", [])), exp.get("error", ""))
+    for doc in plan_error_docs():
+        try:
+            oracle.ref_run_query(_sub(doc, sdir, tmp), reset_ids=1)
+            msg = None
+        except RuntimeError as e:
+            msg = str(e).replace(sdir, "@STORES@").replace(tmp, "@OUT@")
+        res["errors"].append({"doc": doc, "error": msg})
+        print("error:", msg)
+    with gzip.open(os.path.join(HERE, "plans_golden.json.gz"), "wt") as f:
+        json.dump(res, f, separators=(",", ":"))
+
+
 if __name__ == "__main__":
     assert oracle.ref() is not None, "build oracle/_ref first: make -C oracle ref"
-    which = sys.argv[1:] or ["hist", "join", "dedup", "nlj", "stores"]
+    which = sys.argv[1:] or ["hist", "join", "dedup", "nlj", "stores", "plans"]
     if "hist" in which:
         hist_fixtures()
     if "join" in which:
@@ -227,3 +404,5 @@ if __name__ == "__main__":
         nlj_fixtures()
     if "stores" in which:
         store_fixtures()
+    if "plans" in which:
+        plan_fixtures()
