@@ -37,6 +37,7 @@ PDB_JOIN_SELF = 1
 PDB_JOIN_SORTED = 2
 PDB_JOIN_TF32 = 4
 PDB_JOIN_PHASE_TIMES = 8
+PDB_JOIN_DENSE = 16
 
 # Every symbol include/pdb_cuda.h declares (checked by tests/test_capi.py).
 EXPORTS = (

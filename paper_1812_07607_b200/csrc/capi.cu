@@ -158,7 +158,8 @@ void check_join_args(const void* L, int64_t nL, const void* R, int64_t nR, int32
         fail(PDB_ERR_SHAPE, "similarity join needs non-empty patch data");
     if (nL > 0 && !L) fail(PDB_ERR_INVALID_ARGUMENT, "null L");
     if (!self && nR > 0 && !R) fail(PDB_ERR_INVALID_ARGUMENT, "null R");
-    if (o && (o->flags & ~(PDB_JOIN_SELF | PDB_JOIN_SORTED | PDB_JOIN_TF32 | PDB_JOIN_PHASE_TIMES)))
+    if (o && (o->flags & ~(PDB_JOIN_SELF | PDB_JOIN_SORTED | PDB_JOIN_TF32 | PDB_JOIN_PHASE_TIMES |
+                           PDB_JOIN_DENSE)))
         fail(PDB_ERR_INVALID_ARGUMENT, "unknown join flags");
     if (o && o->shard_count > 1 && (o->shard_index < 0 || o->shard_index >= o->shard_count))
         fail(PDB_ERR_INVALID_ARGUMENT, "shard_index out of range");

@@ -125,13 +125,45 @@ struct ScreenParams {
     unsigned long long* ncand;    // candidate pairs (popc of the masks)
     unsigned long long* tiles;
     unsigned long long* next_unit;  // dynamic work-unit counter (zeroed per launch)
+    // banded plan (tile_list != nullptr): units are segments of dev_ch tiles
+    // of each row slot's surviving column tiles; cmaxS / cmaxN are per slot
+    const int32_t* tile_list;      // surviving column tiles, slot-major, ascending
+    const int64_t* slot_list_off;  // [n_slots + 1]
+    const int64_t* slot_unit_off;  // [n_slots + 1]
+    const int64_t* dev_n_units;    // unit count (device)
+    const int32_t* dev_ch;         // tiles per unit (device)
+    int32_t n_slots;
 };
 
 struct Unit {
     int32_t rb, j0, j1, chunk;
 };
 
+__device__ __forceinline__ int tile_at(const ScreenParams& p, int o) {
+    return p.tile_list ? __ldg(p.tile_list + o) : o;
+}
+
 __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
+    if (p.tile_list) {
+        // banded: slot_unit_off[lo] <= u < slot_unit_off[lo + 1]
+        int lo = 0, hi = p.n_slots;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(p.slot_unit_off + mid) <= u) lo = mid;
+            else hi = mid;
+        }
+        const int64_t seg = u - __ldg(p.slot_unit_off + lo);
+        const int ch = __ldg(p.dev_ch);
+        const int P = p.shard_count;
+        const int pos = (lo & 1) ? P - 1 - p.shard_index : p.shard_index;
+        Unit r;
+        r.rb = lo * P + pos;
+        const int64_t o0 = __ldg(p.slot_list_off + lo) + seg * ch;
+        r.j0 = static_cast<int32_t>(o0);
+        r.j1 = static_cast<int32_t>(min(o0 + ch, __ldg(p.slot_list_off + lo + 1)));
+        r.chunk = lo;  // per-slot norm maxima
+        return r;
+    }
     int lo = 0, hi = p.n_chunks;  // chunk_off[lo] <= u < chunk_off[hi]
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -290,9 +322,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             int ps = 0;
             uint32_t pph = 0;
             uint32_t na = 0;  // units whose A has been loaded
+            const int64_t n_units = p.dev_n_units ? *p.dev_n_units : p.n_units;
             auto claim = [&]() -> int64_t {
                 const int64_t c = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
-                return c < p.n_units ? c : -1;
+                return c < n_units ? c : -1;
             };
             int64_t u = claim();
             for (;;) {
@@ -317,7 +350,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                                          kb * KE, w.rb * BM);
                     na++;
                 }
-                for (int J = w.j0; J < w.j1; J++) {
+                for (int o = w.j0; o < w.j1; o++) {
+                    const int J = tile_at(p, o);
                     for (int kb = 0; kb < NKB; kb++) {
                         const bool with_g = AUG && kb == NKB - 1;
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -441,7 +475,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             GV gnext{};
             if (!AUG)
                 gnext = __ldg(reinterpret_cast<const GV*>(
-                    p.gR + static_cast<int64_t>(w.j0) * BN + half * kColsPerWarp) + lane);
+                    p.gR + static_cast<int64_t>(tile_at(p, w.j0)) * BN + half * kColsPerWarp) + lane);
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
@@ -458,14 +492,15 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
                 h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
             }
-            for (int J = w.j0; J < w.j1; J++) {
+            for (int o = w.j0; o < w.j1; o++) {
+                const int J = tile_at(p, o);
                 __syncwarp();
                 if (!AUG) reinterpret_cast<GV*>(gs)[lane] = gnext;
                 // unconditional (clamped) prefetch: a predicated load would
                 // force a wait at the register move (none needed when g is folded)
                 if (!AUG)
                 gnext = __ldg(reinterpret_cast<const GV*>(
-                    p.gR + static_cast<int64_t>(min(J + 1, w.j1 - 1)) * BN + half * kColsPerWarp) + lane);
+                    p.gR + static_cast<int64_t>(tile_at(p, min(o + 1, w.j1 - 1))) * BN + half * kColsPerWarp) + lane);
                 __syncwarp();
                 ptx::mbar_wait(&t_full[acc], acc_phase);
                 ptx::tc_fence_after();
@@ -1075,7 +1110,7 @@ template <bool BF16, int NV>
 __global__ void __launch_bounds__(256)
 k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
        void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn,
-       uint16_t* __restrict__ gx) {
+       uint16_t* __restrict__ gx, const int32_t* __restrict__ perm) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1085,12 +1120,16 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
     float m[NV], x[kRowsPerWarp][NV];
 #pragma unroll
     for (int i = 0; i < NV; i++) m[i] = lane + 32 * i < d ? mu[lane + 32 * i] : 0.0f;
+    int64_t src[kRowsPerWarp];  // row r0 + r of the (sorted) copy is input row src[r]
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; r++)
+        src[r] = r0 + r < n ? (perm ? static_cast<int64_t>(__ldg(perm + r0 + r)) : r0 + r) : 0;
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; r++)
 #pragma unroll
         for (int i = 0; i < NV; i++) {
             const int k = lane + 32 * i;
-            x[r][i] = (r0 + r < n && k < d) ? __ldg(X + (r0 + r) * d + k) : 0.0f;
+            x[r][i] = (r0 + r < n && k < d) ? __ldg(X + src[r] * d + k) : 0.0f;
         }
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; r++)
@@ -1257,6 +1296,569 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 }
 
 // ---------------------------------------------------------------------------
+// The band plan: exact tile pruning on two principal projections.
+//
+// For any d x 2 matrix U, ||U^T (x - y)|| <= s ||x - y|| with s^2 the largest
+// eigenvalue of U^T U.  So a 128-row block of L and a 256-row tile of R whose
+// projected bounding boxes lie further apart than s * tau (plus the fp64
+// projection error) hold no pair within tau, and the screen skips that tile.
+// Rows are sorted by a Morton key of their projections onto the two leading
+// principal directions of a row sample, so blocks and tiles are compact in
+// that plane and most block / tile pairs of a large join separate.  Only
+// surviving tiles are screened; the pair set is unchanged (the test never
+// drops a pair whose exact distance is <= tau).  Every step is
+// deterministic, so all shards of a join build the same plan.
+
+constexpr int kPcaRows = 32;    // sample rows per partial block
+constexpr int kPcaBlocks = 128; // 4096 sample rows
+constexpr int kPcaMaxD = 128;
+constexpr int64_t kBandMinRows = 32768;  // smaller joins: the plan costs more than it saves
+constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
+constexpr int kPcaIters = 6;   // subspace iterations for the top-2 principal plane
+
+struct BandInfo {
+    float u[2][kPcaMaxD];   // the two directions (zero past d)
+    double lo[2], inv[2];   // key quantisation q = (p - lo) * inv, clamped to [0, 2^bits - 1]
+    double s;               // sqrt(lambda_max(U^T U)), rounded up
+    unsigned long long bmax;  // fp64 bits of max_rows sum_k |u_k x_k| (projection error scale)
+};
+
+// Partial sums over kPcaRows sample rows, centred by mu: the d x d products
+// (a T x T register tile per thread, 16 x 16 threads), column sums and the
+// count of usable rows (finite, |x - mu| <= 1e15).
+template <int T>
+__global__ void __launch_bounds__(256)
+k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
+              float* __restrict__ part) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ float xs[kPcaRows][16 * T];
+    __shared__ int ok[kPcaRows];
+    const int64_t S = static_cast<int64_t>(kPcaBlocks) * kPcaRows;
+    for (int q = threadIdx.x; q < kPcaRows * 16 * T; q += blockDim.x) {
+        const int k = q / (16 * T), c = q % (16 * T);
+        const int64_t r = (static_cast<int64_t>(blockIdx.x * kPcaRows + k) * n) / S;
+        xs[k][c] = c < d ? X[r * d + c] - mu[c] : 0.0f;
+    }
+    __syncthreads();
+    if (threadIdx.x < kPcaRows) {
+        bool good = true;
+        for (int c = 0; c < d; c++)
+            if (!(fabsf(xs[threadIdx.x][c]) <= 1e15f)) good = false;
+        ok[threadIdx.x] = good;
+    }
+    __syncthreads();
+    const int ta = threadIdx.x >> 4, tb = threadIdx.x & 15;
+    float acc[T][T], cs[T];
+#pragma unroll
+    for (int i = 0; i < T; i++) {
+        cs[i] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < T; j++) acc[i][j] = 0.0f;
+    }
+    int cnt = 0;
+    for (int k = 0; k < kPcaRows; k++) {
+        if (!ok[k]) continue;  // block-uniform
+        cnt++;
+        float xa[T], xb[T];
+#pragma unroll
+        for (int i = 0; i < T; i++) {
+            xa[i] = xs[k][ta * T + i];
+            xb[i] = xs[k][tb * T + i];
+        }
+#pragma unroll
+        for (int i = 0; i < T; i++) {
+            cs[i] += xa[i];
+#pragma unroll
+            for (int j = 0; j < T; j++) acc[i][j] = fmaf(xa[i], xb[j], acc[i][j]);
+        }
+    }
+    const int E = d + d * d + 1;
+    float* out = part + static_cast<size_t>(blockIdx.x) * E;
+#pragma unroll
+    for (int i = 0; i < T; i++) {
+        const int a = ta * T + i;
+        if (a >= d) continue;
+        if (tb == 0) out[a] = cs[i];
+#pragma unroll
+        for (int j = 0; j < T; j++) {
+            const int b = tb * T + j;
+            if (b < d) out[d + a * d + b] = acc[i][j];
+        }
+    }
+    if (threadIdx.x == 0) out[E - 1] = static_cast<float>(cnt);
+}
+
+// Fixed-order fp64 reduction of the partials (deterministic).
+__global__ void __launch_bounds__(128)
+k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double acc = 0.0;
+    for (int b = 0; b < kPcaBlocks; b += 8) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = part[static_cast<size_t>(b + q) * E + e];
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc += static_cast<double>(v[q]);
+    }
+    sum[e] = acc;
+}
+
+// One block: the covariance (fp32, symmetric, read by columns so lanes hit
+// distinct banks), kPcaIters subspace iterations on two vectors with
+// Gram-Schmidt (a few suffice: any plane near the leading one prunes about
+// as well), then the key quantisation and the bound's scale s of the fp32
+// directions (fp64).
+__global__ void __launch_bounds__(256)
+k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
+          BandInfo* __restrict__ info) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    extern __shared__ float Cs[];  // [d][d]
+    __shared__ float v[2][kPcaMaxD];
+    __shared__ float wpart[2][8][kPcaMaxD];
+    __shared__ double mean[kPcaMaxD];
+    __shared__ float fred[3][8];
+    __shared__ double dred[5][8];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const double m = sum[d + d * d];
+    const double im = m > 0 ? 1.0 / m : 0.0;
+    for (int c = t; c < d; c += blockDim.x) mean[c] = sum[c] * im;
+    for (int c = t; c < kPcaMaxD; c += blockDim.x) {
+        v[0][c] = c < d ? 1.0f + 0.001f * c : 0.0f;
+        v[1][c] = c < d ? ((c & 1) ? 1.0f : -1.0f) * (1.0f + 0.002f * c) : 0.0f;
+    }
+    __syncthreads();
+    for (int e = t; e < d * d; e += blockDim.x) {
+        const int a = e / d, b = e - a * d;
+        Cs[e] = static_cast<float>(m > 0 ? sum[d + e] * im - mean[a] * mean[b] : (a == b ? 1.0 : 0.0));
+    }
+    __syncthreads();
+    const int np = min(8, max(1, static_cast<int>(blockDim.x) / d));  // column groups
+    const int a = t % d, pg = t / d;
+    const int bw = (d + np - 1) / np;
+    const int b0 = pg * bw, b1 = min(d, b0 + bw);
+    float l0 = 0.0f, l1 = 0.0f;
+    for (int it = 0; it < kPcaIters; it++) {
+        if (pg < np) {
+            float w0 = 0.0f, w1 = 0.0f;
+            for (int b = b0; b < b1; b++) {
+                const float c = Cs[b * d + a];  // = C[a][b]
+                w0 = fmaf(c, v[0][b], w0);
+                w1 = fmaf(c, v[1][b], w1);
+            }
+            wpart[0][pg][a] = w0;
+            wpart[1][pg][a] = w1;
+        }
+        __syncthreads();
+        float w0 = 0.0f, w1 = 0.0f, q0 = 0.0f, q1 = 0.0f, q2 = 0.0f;
+        if (t < d) {
+            for (int g = 0; g < np; g++) {
+                w0 += wpart[0][g][t];
+                w1 += wpart[1][g][t];
+            }
+            q0 = w0 * w0;
+            q1 = w0 * w1;
+            q2 = w1 * w1;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+            q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+            q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+        }
+        if (lane == 0) {
+            fred[0][wid] = q0;
+            fred[1][wid] = q1;
+            fred[2][wid] = q2;
+        }
+        __syncthreads();
+        q0 = q1 = q2 = 0.0f;
+        for (int w = 0; w < 8; w++) {
+            q0 += fred[0][w];
+            q1 += fred[1][w];
+            q2 += fred[2][w];
+        }
+        // v0 = w0 / |w0|; v1 = (w1 - (w0.w1 / |w0|^2) w0) / |..|
+        const float r0 = q0 > 0.0f ? rsqrtf(q0) : 0.0f;
+        const float c01 = q0 > 0.0f ? q1 * r0 * r0 : 0.0f;
+        const float e2 = q2 - c01 * q1;
+        const float r1 = e2 > 0.0f ? rsqrtf(e2) : 0.0f;
+        l0 = q0 * r0;
+        l1 = e2 * r1;
+        if (t < d) {
+            v[0][t] = r0 > 0.0f ? w0 * r0 : (t == 0 ? 1.0f : 0.0f);
+            v[1][t] = r1 > 0.0f ? (w1 - c01 * w0) * r1 : (t == 1 ? 1.0f : 0.0f);
+        }
+        __syncthreads();
+    }
+    for (int c = t; c < kPcaMaxD; c += blockDim.x) {
+        info->u[0][c] = c < d ? v[0][c] : 0.0f;
+        info->u[1][c] = c < d ? v[1][c] : 0.0f;
+    }
+    double g[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // u0.u0, u1.u1, u0.u1, u0.centre, u1.centre
+    if (t < d) {
+        const double x0 = v[0][t], x1 = v[1][t];
+        const double centre = static_cast<double>(mu[t]) + mean[t];
+        g[0] = x0 * x0;
+        g[1] = x1 * x1;
+        g[2] = x0 * x1;
+        g[3] = x0 * centre;
+        g[4] = x1 * centre;
+    }
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+        for (int o = 16; o > 0; o >>= 1) g[q] += __shfl_xor_sync(0xffffffffu, g[q], o);
+        if (lane == 0) dred[q][wid] = g[q];
+    }
+    __syncthreads();
+    if (t == 0) {
+        for (int q = 0; q < 5; q++) {
+            g[q] = 0.0;
+            for (int w = 0; w < 8; w++) g[q] += dred[q][w];
+        }
+        const double h = 0.5 * (g[0] + g[1]), q = 0.5 * (g[0] - g[1]);
+        info->s = sqrt(h + sqrt(q * q + g[2] * g[2])) * (1.0 + 1e-12);
+        const double cen[2] = {g[3], g[4]}, lam[2] = {l0, l1};
+        for (int k = 0; k < 2; k++) {
+            const double sd = sqrt(fmax(lam[k], 0.0));
+            info->lo[k] = cen[k] - 3.0 * sd;
+            info->inv[k] = sd > 0 ? static_cast<double>(1 << kMortonBits) / (6.0 * sd) : 0.0;
+        }
+        info->bmax = 0ull;
+    }
+}
+
+__device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> even positions
+    x &= 0xffu;
+    x = (x | (x << 4)) & 0x0f0fu;
+    x = (x | (x << 2)) & 0x3333u;
+    x = (x | (x << 1)) & 0x5555u;
+    return x;
+}
+
+// One thread per row: fp64 projections, the Morton sort key and the
+// projection-error scale sum_k |u_k x_k|, max-reduced per block (one
+// atomicMax per block).
+__global__ void __launch_bounds__(256)
+k_band_keys(const float* __restrict__ X, int64_t n, int d, BandInfo* __restrict__ info,
+            double2* __restrict__ proj, uint32_t* __restrict__ key, int32_t* __restrict__ val,
+            int32_t* __restrict__ zero_bins) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (zero_bins && blockIdx.x == 0)  // the counting sort's bin counts
+        for (int b = threadIdx.x; b < (1 << (2 * kMortonBits)); b += blockDim.x) zero_bins[b] = 0;
+    __shared__ float us[2][kPcaMaxD];
+    __shared__ double bred[8];
+    for (int c = threadIdx.x; c < kPcaMaxD; c += blockDim.x) {
+        us[0][c] = info->u[0][c];
+        us[1][c] = info->u[1][c];
+    }
+    const double lo0 = info->lo[0], lo1 = info->lo[1], inv0 = info->inv[0], inv1 = info->inv[1];
+    __syncthreads();
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double bm = 0.0;
+    if (row < n) {
+        const float* x = X + row * d;
+        double p0 = 0.0, p1 = 0.0, b = 0.0;
+        const bool v4 = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+        if (v4) {
+            for (int k = 0; k < d; k += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(x + k));
+                const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const double a0 = static_cast<double>(us[0][k + i]) * e[i];
+                    const double a1 = static_cast<double>(us[1][k + i]) * e[i];
+                    p0 += a0;
+                    p1 += a1;
+                    b += fabs(a0) + fabs(a1);
+                }
+            }
+        } else {
+            for (int k = 0; k < d; k++) {
+                const double e = __ldg(x + k);
+                const double a0 = us[0][k] * e, a1 = us[1][k] * e;
+                p0 += a0;
+                p1 += a1;
+                b += fabs(a0) + fabs(a1);
+            }
+        }
+        uint32_t kk = (1u << (2 * kMortonBits)) - 1;  // non-finite rows sort last
+        if (isfinite(p0) && isfinite(p1)) {
+            const double lim = static_cast<double>((1 << kMortonBits) - 1);
+            const uint32_t q0 = static_cast<uint32_t>(fmin(fmax((p0 - lo0) * inv0, 0.0), lim));
+            const uint32_t q1 = static_cast<uint32_t>(fmin(fmax((p1 - lo1) * inv1, 0.0), lim));
+            kk = spread_bits(q0) | (spread_bits(q1) << 1);
+            if (isfinite(b)) bm = b;
+        } else {
+            p0 = p1 = __longlong_as_double(0x7ff8000000000000ll);  // NaN: in no box
+        }
+        proj[row] = make_double2(p0, p1);
+        key[row] = kk;
+        val[row] = static_cast<int32_t>(row);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if ((threadIdx.x & 31) == 0) bred[threadIdx.x >> 5] = bm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) m = fmax(m, bred[w]);
+        if (m > 0) atomicMax(&info->bmax, static_cast<unsigned long long>(__double_as_longlong(m)));
+    }
+}
+
+// Counting sort of the 12-bit keys for single-GPU joins: block-aggregated
+// bin counts, one exclusive scan, atomic scatter (the order inside a bin is
+// arbitrary -- harmless, since the tile test is exact for any order).
+// Sharded joins need every rank to build the same order and use a stable
+// radix sort instead.
+constexpr int kBins = 1 << (2 * kMortonBits);
+
+__global__ void __launch_bounds__(256)
+k_bin_count(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ count) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int32_t h[kBins];
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride)
+        atomicAdd(&h[__ldg(key + r)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+        if (h[b]) atomicAdd(count + b, h[b]);
+}
+
+// One block: exclusive scan of the bin counts into running positions.
+__global__ void __launch_bounds__(1024)
+k_bin_scan(const int32_t* __restrict__ count, int32_t* __restrict__ pos) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int32_t part[1024];
+    constexpr int per = kBins / 1024;
+    const int t = threadIdx.x;
+    int32_t v[per], local = 0;
+#pragma unroll
+    for (int i = 0; i < per; i++) {
+        v[i] = count[t * per + i];
+        local += v[i];
+    }
+    part[t] = local;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int32_t x = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += x;
+        __syncthreads();
+    }
+    int32_t run = part[t] - local;
+#pragma unroll
+    for (int i = 0; i < per; i++) {
+        pos[t * per + i] = run;
+        run += v[i];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ pos,
+              int32_t* __restrict__ perm) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t k = r < n ? __ldg(key + r) : 0xffffffffu;
+    // one atomic per distinct key in the warp
+    const uint32_t peers = __match_any_sync(0xffffffffu, k);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    int32_t base = 0;
+    if (r < n && lane == leader) base = atomicAdd(pos + k, __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (r < n) perm[base + __popc(peers & ((1u << lane) - 1u))] = static_cast<int32_t>(r);
+}
+
+// One warp per block of `blk` sorted rows: the projected bounding box
+// (min0, max0, min1, max1); NaN projections (rows that match nothing) are
+// left out, an all-NaN block gets an empty box.
+__global__ void __launch_bounds__(256)
+k_band_boxes(const double2* __restrict__ proj, const int32_t* __restrict__ perm, int64_t n, int blk,
+             int64_t n_blk, double4* __restrict__ box) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t b = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (b >= n_blk) return;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double lo0 = inf, hi0 = -inf, lo1 = inf, hi1 = -inf;
+    const int64_t r1 = min(n, (b + 1) * blk);
+    for (int64_t r = b * blk + lane; r < r1; r += 32) {
+        const double2 q = proj[__ldg(perm + r)];
+        lo0 = fmin(lo0, q.x);
+        hi0 = fmax(hi0, q.x);
+        lo1 = fmin(lo1, q.y);
+        hi1 = fmax(hi1, q.y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo0 = fmin(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
+        hi0 = fmax(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+        lo1 = fmin(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
+        hi1 = fmax(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+    }
+    if (lane == 0) box[b] = make_double4(lo0, hi0, lo1, hi1);
+}
+
+struct BandPlan {
+    const double4* boxL;
+    const double4* boxR;  // nullptr for a self-join: tile J = row blocks 2J, 2J + 1
+    const BandInfo* info;
+    double tau;
+    int d, nt, self, P, shard, n_slots, nbl;
+};
+
+__device__ __forceinline__ double4 box_r(const BandPlan& q, int J) {
+    if (q.boxR) return q.boxR[J];
+    const double4 a = q.boxL[2 * J];
+    if (2 * J + 1 >= q.nbl) return a;
+    const double4 b = q.boxL[2 * J + 1];
+    return make_double4(fmin(a.x, b.x), fmax(a.y, b.y), fmin(a.z, b.z), fmax(a.w, b.w));
+}
+
+// Squared threshold of the box test: (s tau + projection error)^2, widened.
+__device__ __forceinline__ double band_thr2(const BandPlan& q) {
+    const double bmax = __longlong_as_double(static_cast<long long>(q.info->bmax));
+    const double err = 4.0 * (q.d + 2) * 1.1102230246251565e-16 * bmax;  // 4 (d+2) 2^-53 bmax
+    const double t = (q.tau * q.info->s + err) * (1.0 + 1e-9);
+    return t * t;
+}
+
+__device__ __forceinline__ bool band_keep(const double4& a, const double4& b, double thr2) {
+    const double g0 = fmax(0.0, fmax(b.x - a.y, a.x - b.y));
+    const double g1 = fmax(0.0, fmax(b.z - a.w, a.z - b.w));
+    return !(g0 * g0 + g1 * g1 > thr2);  // NaN-safe: keeps the tile
+}
+
+__device__ __forceinline__ int slot_rb(const BandPlan& q, int k) {
+    const int pos = (k & 1) ? q.P - 1 - q.shard : q.shard;
+    return k * q.P + pos;
+}
+
+// One warp per row slot of this shard: surviving column tiles.
+__global__ void __launch_bounds__(256)
+k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int k = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= q.n_slots) return;
+    const int rb = slot_rb(q, k);
+    const double thr2 = band_thr2(q);
+    const double4 a = q.boxL[rb];
+    int c = 0;
+    for (int J = (q.self ? rb >> 1 : 0) + lane; J < q.nt; J += 32) c += band_keep(a, box_r(q, J), thr2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[k] = c;
+}
+
+// One block: list offsets, tiles per unit, unit offsets; zeroes the screen /
+// re-check counters (the first kernel they follow).
+__global__ void __launch_bounds__(1024)
+k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int sm_count, int64_t* __restrict__ list_off,
+            int64_t* __restrict__ unit_off, int64_t* __restrict__ n_units, int32_t* __restrict__ dev_ch,
+            unsigned long long* __restrict__ counters) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int64_t part[1024];
+    __shared__ int ch_s;
+    const int t = threadIdx.x;
+    if (t < 5) counters[t] = 0;
+    const int per = (n_slots + 1023) / 1024;
+    const int k0 = min(t * per, n_slots), k1 = min((t + 1) * per, n_slots);
+    auto scan = [&](int64_t local) -> int64_t {  // exclusive prefix of this thread's range
+        part[t] = local;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            const int64_t v = t >= o ? part[t - o] : 0;
+            __syncthreads();
+            part[t] += v;
+            __syncthreads();
+        }
+        const int64_t r = part[t] - local;
+        __syncthreads();
+        return r;
+    };
+    int64_t local = 0;
+    for (int k = k0; k < k1; k++) local += cnt[k];
+    int64_t run = scan(local);
+    if (t == 1023) {
+        const int64_t total = run + local;
+        int64_t c = total / (16 * static_cast<int64_t>(sm_count));
+        c = c < 1 ? 1 : (c > 64 ? 64 : c);
+        ch_s = static_cast<int>(c);
+        *dev_ch = ch_s;
+    }
+    if (t == 0) list_off[0] = 0;
+    for (int k = k0; k < k1; k++) {
+        run += cnt[k];
+        list_off[k + 1] = run;
+    }
+    __syncthreads();
+    const int ch = ch_s;
+    local = 0;
+    for (int k = k0; k < k1; k++) local += (cnt[k] + ch - 1) / ch;
+    run = scan(local);
+    if (t == 0) unit_off[0] = 0;
+    for (int k = k0; k < k1; k++) {
+        run += (cnt[k] + ch - 1) / ch;
+        unit_off[k + 1] = run;
+    }
+    if (t == 1023) *n_units = run;
+}
+
+// One warp per row slot: the surviving tiles in ascending order and the
+// slot's norm maxima over them (the screen's margin for the whole slot).
+__global__ void __launch_bounds__(256)
+k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __restrict__ list,
+             const float* __restrict__ tmaxS, const float* __restrict__ tmaxN,
+             float* __restrict__ smaxS, float* __restrict__ smaxN) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int k = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= q.n_slots) return;
+    const int rb = slot_rb(q, k);
+    const double thr2 = band_thr2(q);
+    const double4 a = q.boxL[rb];
+    int64_t w = list_off[k];
+    float ms = 0.0f, mn = 0.0f;
+    for (int J0 = q.self ? rb >> 1 : 0; J0 < q.nt; J0 += 32) {
+        const int J = J0 + lane;
+        const bool keep = J < q.nt && band_keep(a, box_r(q, J), thr2);
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            list[w + __popc(bal & ((1u << lane) - 1u))] = J;
+            ms = fmaxf(ms, tmaxS[J]);
+            mn = fmaxf(mn, tmaxN[J]);
+        }
+        w += __popc(bal);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+        mn = fmaxf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+        smaxS[k] = ms;
+        smaxN[k] = mn;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: exact re-check.  The fp64 chain is written with explicit _rn
 // intrinsics so it can never be contracted into FMAs: diff = a - b,
 // acc = acc + diff * diff, sequential in k, then sqrt -- src/index.cpp:69-76.
@@ -1268,7 +1870,8 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
           unsigned long long cap, const float* __restrict__ L, const float* __restrict__ R,
           int d, double tau, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
           float* __restrict__ out_d, unsigned long long out_cap,
-          unsigned long long* __restrict__ out_count) {
+          unsigned long long* __restrict__ out_count, const int32_t* __restrict__ permL,
+          const int32_t* __restrict__ permR, int self_join) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const unsigned long long n = min(*n_rec, cap);
@@ -1283,17 +1886,28 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
         int4 rc = make_int4(0, 0, 0, 0);
         if (idx < n) rc = rec[idx];
         uint32_t mask = static_cast<uint32_t>(rc.z);
+        // banded plans screen row-sorted copies: map back to input rows
+        int i = rc.x;
+        if (permL && mask) i = __ldg(permL + rc.x);
         while (__any_sync(0xffffffffu, mask != 0)) {
             bool ok = false;
             double dist = 0.0;
-            int j = 0;
+            int j = 0, a = i;
             if (mask) {
                 const int k = __ffs(mask) - 1;
                 mask &= mask - 1;
                 j = rc.y + k;
-                dist = exact_dist(L + static_cast<int64_t>(rc.x) * d,
+                if (permR) j = __ldg(permR + j);
+                // euclidean(L_i, R_j); bitwise symmetric, so a self-join pair
+                // can be reported as (min, max)
+                dist = exact_dist(L + static_cast<int64_t>(i) * d,
                                   R + static_cast<int64_t>(j) * d, d, vec8);
                 ok = dist <= tau;
+                if (self_join && a > j) {
+                    const int t = a;
+                    a = j;
+                    j = t;
+                }
             }
             const uint32_t ball = __ballot_sync(0xffffffffu, ok);
             if (!ball) continue;
@@ -1303,7 +1917,7 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
             if (ok) {
                 const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
                 if (pos < out_cap) {
-                    out_l[pos] = rc.x;
+                    out_l[pos] = a;
                     out_r[pos] = j;
                     out_d[pos] = static_cast<float>(dist);
                 }
@@ -1867,15 +2481,59 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         fail(PDB_ERR_CONFIG, "similarity join: d is larger than this build supports");
     const size_t es = tf32 ? 4 : 2;
 
+    // CTA pairs for the folded-g screen (opt-in, PDB_SCREEN_PAIR=1, one GPU):
+    // measured no faster than the 1-SM screen -- both run the tensor pipe at
+    // ~62-64 % active, ~0.9 of the measured cuBLAS bf16 rate for the MMA
+    // work they issue -- so the 1-SM kernel stays the default.
+    const char* pe = getenv("PDB_SCREEN_PAIR");
+    const bool pair = fold && P == 1 && pe && pe[0] == '1';
+    // The band plan (exact tile pruning, see k_pca_partial) for resident-A
+    // L2 joins of at least kBandMinRows rows per side; PDB_JOIN_DENSE or
+    // PDB_JOIN_BAND=0 turn it off, PDB_JOIN_BAND=1 forces it.
+    const char* be = getenv("PDB_JOIN_BAND");
+    const int band_env = be ? atoi(be) : -1;
+    const bool band = !pair && DP <= 128 && d <= kPcaMaxD && (o.flags & PDB_JOIN_DENSE) == 0 &&
+                      band_env != 0 && (band_env == 1 || (nL >= kBandMinRows && nR >= kBandMinRows));
+
     // ---- scratch: one pool allocation for every small buffer ---------------
     const int64_t nt_ = ceil_div(nR, BN);
+    const int64_t nbl = ceil_div(nL, BM);
+    int n_slots = 0;
+    int64_t list_cap = 0;
+    size_t sort_tmp = 0;
+    const int E = d + d * d + 1;
+    if (band) {
+        const int64_t full = nbl / P, rem = nbl % P;
+        const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
+        n_slots = static_cast<int>(full + (pos_last < rem ? 1 : 0));
+        for (int k = 0; k < n_slots; k++) {
+            const int64_t rb = static_cast<int64_t>(k) * P + ((k & 1) ? P - 1 - shard : shard);
+            list_cap += nt_ - (self ? rb >> 1 : 0);
+        }
+        if (P > 1)
+            PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint32_t*>(nullptr),
+                                                     static_cast<uint32_t*>(nullptr),
+                                                     static_cast<int32_t*>(nullptr),
+                                                     static_cast<int32_t*>(nullptr),
+                                                     std::max(nL, nR), 0, 2 * kMortonBits, s));
+        sort_tmp = std::max(sort_tmp, static_cast<size_t>(2 * kBins * 4));
+    }
+    const size_t band_bytes =
+        !band ? 0
+              : Arena::need(static_cast<size_t>(kPcaBlocks) * E, 4) + Arena::need(E, 8) +
+                    Arena::need(1, sizeof(BandInfo)) +
+                    Arena::need(nL, 16) + 4 * Arena::need(nL, 4) + Arena::need(sort_tmp, 1) +
+                    (self ? 0 : Arena::need(nR, 16) + 4 * Arena::need(nR, 4) + Arena::need(sort_tmp, 1)) +
+                    Arena::need(nbl, 32) + Arena::need(nt_, 32) +
+                    Arena::need(n_slots, 4) + 2 * Arena::need(n_slots + 1, 8) + Arena::need(2, 8) +
+                    Arena::need(std::max<int64_t>(list_cap, 1), 4) + 2 * Arena::need(n_slots, 4);
     Arena ar;
     ar.reserve(Arena::need(DP, 4) + Arena::need(static_cast<size_t>(nL) * DP, es) +
                    2 * Arena::need(nL, 4) +
                    (self ? 0 : Arena::need(static_cast<size_t>(nR) * DP, es) + 2 * Arena::need(nR, 4)) +
                    Arena::need(static_cast<size_t>(nt_) * BN, 4) + 4 * Arena::need(nt_ + 1, 4) +
                    Arena::need(nt_ + 2, 8) + Arena::need(5, 8) +
-                   (fold ? Arena::need(static_cast<size_t>(nR) * kGCols, 2) : 0),
+                   (fold ? Arena::need(static_cast<size_t>(nR) * kGCols, 2) : 0) + band_bytes,
                s);
     float* mu = ar.take<float>(DP);
     uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * kGCols) : nullptr;
@@ -1885,14 +2543,15 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                nL, d, DP, mu);
     PDB_CUDA(cudaGetLastError());
     launches++;
-    auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out) {
+    auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out,
+                    const int32_t* perm) {
         if (DP <= 128) {  // g_out (the folded block) only exists for DP <= 128
             const unsigned g = static_cast<unsigned>(ceil_div(ceil_div(n, kRowsPerWarp) * 32, 256));
             auto pick = [&](auto k32, auto k64, auto k96, auto k128) {
                 const int nv = DP / 32;
                 auto k = nv == 1 ? k32 : nv == 2 ? k64 : nv == 3 ? k96 : k128;
                 launch_pdl(k, dim3(g), dim3(256), 0, s, X, n, d, DP, static_cast<const float*>(mu),
-                           static_cast<void*>(Xp), hn, sn, g_out);
+                           static_cast<void*>(Xp), hn, sn, g_out, perm);
             };
             if (tf32) pick(k_prep<false, 1>, k_prep<false, 2>, k_prep<false, 3>, k_prep<false, 4>);
             else pick(k_prep<true, 1>, k_prep<true, 2>, k_prep<true, 3>, k_prep<true, 4>);
@@ -1904,29 +2563,84 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         PDB_CUDA(cudaGetLastError());
         launches++;
     };
+    // ---- band plan, part 1: directions, sort keys, row permutations ------
+    int32_t* permL = nullptr;
+    int32_t* permR = nullptr;
+    BandInfo* info = nullptr;
+    double2 *projL = nullptr, *projR = nullptr;
+    if (band) {
+        float* part = ar.take<float>(static_cast<size_t>(kPcaBlocks) * E);
+        double* sum = ar.take<double>(E);
+        info = ar.take<BandInfo>(1);
+        auto kp = d <= 16 ? k_pca_partial<1> : d <= 32 ? k_pca_partial<2> : d <= 64 ? k_pca_partial<4>
+                                                                                  : k_pca_partial<8>;
+        launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, s, d_L, nL, d, static_cast<const float*>(mu),
+                   part);
+        launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
+                   static_cast<const float*>(part), E, sum);
+        const int eig_smem = d * d * 4;
+        static bool eig_attr = false;
+        if (!eig_attr) {
+            set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
+            eig_attr = true;
+        }
+        launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
+                   static_cast<const float*>(mu), info);
+        launches += 3;
+        auto keys_and_sort = [&](const float* X, int64_t n, double2*& proj, int32_t*& perm) {
+            proj = ar.take<double2>(n);
+            uint32_t* k_in = ar.take<uint32_t>(n);
+            int32_t* v_in = ar.take<int32_t>(n);
+            perm = ar.take<int32_t>(n);
+            uint8_t* tmp = ar.take<uint8_t>(sort_tmp);
+            launch_pdl(k_band_keys, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, s, X,
+                       n, d, info, proj, k_in, v_in, P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
+            if (P > 1) {
+                // every rank must build the same order: stable radix sort
+                uint32_t* k_out = ar.take<uint32_t>(n);
+                size_t tb = sort_tmp;
+                PDB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, perm, n, 0,
+                                                         2 * kMortonBits, s));
+                launches += 5;
+            } else {
+                int32_t* count = reinterpret_cast<int32_t*>(tmp);
+                int32_t* pos = count + kBins;
+                const unsigned gc = static_cast<unsigned>(
+                    std::min<int64_t>(ceil_div(n, 256), int64_t{ctx.sm_count} * 2));
+                launch_pdl(k_bin_count, dim3(gc), dim3(256), 0, s, static_cast<const uint32_t*>(k_in), n,
+                           count);
+                launch_pdl(k_bin_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(count), pos);
+                launch_pdl(k_bin_scatter, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, s,
+                           static_cast<const uint32_t*>(k_in), n, pos, perm);
+                launches += 4;
+            }
+        };
+        keys_and_sort(d_L, nL, projL, permL);
+        if (self) {
+            permR = permL;
+            projR = projL;
+        } else {
+            keys_and_sort(d_R, nR, projR, permR);
+        }
+    }
+
     uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
     float* hnL = ar.take<float>(nL);
     float* snL = ar.take<float>(nL);
-    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr);
+    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL);
     const uint8_t* XpR = XpL;
     const float *hnR = hnL, *snR = snL;
     if (!self) {
         uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
         float* hr = ar.take<float>(nR);
         float* sr = ar.take<float>(nR);
-        prep(d_R, nR, xr, hr, sr, gx);
+        prep(d_R, nR, xr, hr, sr, gx, permR);
         XpR = xr;
         hnR = hr;
         snR = sr;
     }
     UnitPlan plan;
     plan.off = ar.take<int64_t>(nt_ + 2);
-    // CTA pairs for the folded-g screen (opt-in, PDB_SCREEN_PAIR=1, one GPU):
-    // measured no faster than the 1-SM screen -- both run the tensor pipe at
-    // ~62-64 % active, ~0.9 of the measured cuBLAS bf16 rate for the MMA
-    // work they issue -- so the 1-SM kernel stays the default.
-    const char* pe = getenv("PDB_SCREEN_PAIR");
-    const bool pair = fold && P == 1 && pe && pe[0] == '1';
     plan_units(ctx, nL, nR, self, P, shard, pair, plan);
     const int nt = plan.nt;
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
@@ -1936,11 +2650,47 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
     float* cmaxS = ar.take<float>(nt + 1);
     float* cmaxN = ar.take<float>(nt + 1);
-    launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
-               static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb, plan.rpt,
-               static_cast<int>(self), P, shard, cmaxS, cmaxN, plan.off, counters);
+    // ---- band plan, part 2: boxes, surviving tiles, units -----------------
+    int32_t* list = nullptr;
+    int64_t *list_off = nullptr, *unit_off = nullptr, *dev_n_units = nullptr;
+    int32_t* dev_ch = nullptr;
+    if (band) {
+        double4* boxL = ar.take<double4>(nbl);
+        double4* boxR = ar.take<double4>(nt);
+        int32_t* cnt = ar.take<int32_t>(n_slots);
+        list_off = ar.take<int64_t>(n_slots + 1);
+        unit_off = ar.take<int64_t>(n_slots + 1);
+        dev_n_units = ar.take<int64_t>(1);
+        dev_ch = ar.take<int32_t>(1);
+        list = ar.take<int32_t>(std::max<int64_t>(list_cap, 1));
+        cmaxS = ar.take<float>(n_slots);
+        cmaxN = ar.take<float>(n_slots);
+        launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))), dim3(256), 0, s,
+                   static_cast<const double2*>(projL), static_cast<const int32_t*>(permL), nL, BM,
+                   nbl, boxL);
+        if (!self)
+            launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(int64_t{nt} * 32, 256))),
+                       dim3(256), 0, s, static_cast<const double2*>(projR),
+                       static_cast<const int32_t*>(permR), nR, BN, static_cast<int64_t>(nt), boxR);
+        BandPlan bp{boxL, self ? nullptr : boxR, info, tau, d, nt, static_cast<int>(self), P, shard,
+                    n_slots, static_cast<int>(nbl)};
+        const unsigned gs = static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256));
+        if (n_slots > 0) launch_pdl(k_band_count, dim3(gs), dim3(256), 0, s, bp, cnt);
+        launch_pdl(k_band_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(cnt), n_slots,
+                   ctx.sm_count, list_off, unit_off, dev_n_units, dev_ch, counters);
+        if (n_slots > 0)
+            launch_pdl(k_band_write, dim3(gs), dim3(256), 0, s, bp,
+                       static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
+                       static_cast<const float*>(tmaxN), cmaxS, cmaxN);
+        launches += 5;
+    } else {
+        launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
+                   static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb, plan.rpt,
+                   static_cast<int>(self), P, shard, cmaxS, cmaxN, plan.off, counters);
+        launches++;
+    }
     PDB_CUDA(cudaGetLastError());
-    launches += 2;
+    launches++;
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, pair ? BN / 2 : BN, !tf32);
@@ -1966,13 +2716,22 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
+    if (band) {
+        p.tile_list = list;
+        p.slot_list_off = list_off;
+        p.slot_unit_off = unit_off;
+        p.dev_n_units = dev_n_units;
+        p.dev_ch = dev_ch;
+        p.n_slots = n_slots;
+    }
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2) {
-                           launch_pdl(k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s, 
+                           launch_pdl(k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
-                               counters + 2);
+                               counters + 2, static_cast<const int32_t*>(permL),
+                               static_cast<const int32_t*>(permR), static_cast<int>(self));
                            PDB_CUDA(cudaGetLastError());
                        });
 }

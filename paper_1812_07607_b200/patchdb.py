@@ -188,22 +188,25 @@ class JoinResult:
 
 
 def _opts(self_join: bool, sort: bool, shard: Tuple[int, int], stream=None,
-          tf32: bool = False, phase_times: bool = False) -> capi.JoinOpts:
+          tf32: bool = False, phase_times: bool = False, dense: bool = False) -> capi.JoinOpts:
     o = capi.JoinOpts()
     o.flags = ((capi.PDB_JOIN_SELF if self_join else 0) | (capi.PDB_JOIN_SORTED if sort else 0) |
                (capi.PDB_JOIN_TF32 if tf32 else 0) |
-               (capi.PDB_JOIN_PHASE_TIMES if phase_times else 0))
+               (capi.PDB_JOIN_PHASE_TIMES if phase_times else 0) |
+               (capi.PDB_JOIN_DENSE if dense else 0))
     o.shard_index, o.shard_count = int(shard[0]), int(shard[1])
     o.stream = stream
     return o
 
 
 def sim_join(L: np.ndarray, R: Optional[np.ndarray], tau: float, *, self_join: bool = False,
-             sort: bool = True, shard: Tuple[int, int] = (0, 1), tf32: bool = False) -> JoinResult:
+             sort: bool = True, shard: Tuple[int, int] = (0, 1), tf32: bool = False,
+             dense: bool = False) -> JoinResult:
     """Host threshold join (K2 + K3): every (i, j) with euclidean(L_i, R_j) <= tau.
 
     ``self_join=True`` joins L with itself and keeps i < j.  ``tf32`` screens
     on tf32 instead of bf16 copies (same result, tighter candidate band).
+    ``dense`` screens every tile (no band plan; same result).
     """
     L = np.ascontiguousarray(L, dtype=np.float32)
     if L.ndim != 2:
@@ -219,7 +222,7 @@ def sim_join(L: np.ndarray, R: Optional[np.ndarray], tau: float, *, self_join: b
             raise DimensionMismatchError(
                 f"similarity join over {L.shape[1]} and {R_.shape[1]} dimensional sides")
     d = L.shape[1] if L.shape[0] else (R_.shape[1] if nR else L.shape[1])
-    o = _opts(self_join, sort, shard, tf32=tf32)
+    o = _opts(self_join, sort, shard, tf32=tf32, dense=dense)
     pr = capi.Pairs()
     _check(capi.lib().pdb_sim_join(capi.ptr(L), L.shape[0], capi.ptr(R_), nR, d, float(tau),
                                    C.byref(o), C.byref(pr)))
@@ -336,9 +339,11 @@ def cosine_join_bf16_device(L, R, min_cos: float, *, self_join: bool = False, so
 
 def sim_join_device(L, R, tau: float, *, self_join: bool = False, sort: bool = False,
                     shard: Tuple[int, int] = (0, 1), out: Optional[DevicePairs] = None,
-                    stream=None, tf32: bool = False, phase_times: bool = False) -> DevicePairs:
+                    stream=None, tf32: bool = False, phase_times: bool = False,
+                    dense: bool = False) -> DevicePairs:
     """Device threshold join on CUDA torch tensors; the result stays in HBM.
-    ``phase_times`` fills ``stats.*_ms`` (CUDA events between the phases)."""
+    ``phase_times`` fills ``stats.*_ms`` (CUDA events between the phases);
+    ``dense`` screens every tile (no band plan)."""
     import torch
     assert L.is_cuda and L.dtype == torch.float32 and L.is_contiguous()
     nL, d = int(L.shape[0]), int(L.shape[1])
@@ -349,7 +354,7 @@ def sim_join_device(L, R, tau: float, *, self_join: bool = False, sort: bool = F
         Rp, nR = R.data_ptr(), int(R.shape[0])
     s = stream if stream is not None else torch.cuda.current_stream(L.device)
     o = _opts(self_join, sort, shard, C.c_void_p(s.cuda_stream), tf32=tf32,
-              phase_times=phase_times)
+              phase_times=phase_times, dense=dense)
     res = out if out is not None else DevicePairs()
     _check(capi.lib().pdb_sim_join_dev(L.data_ptr(), nL, Rp, nR, d, float(tau), C.byref(o),
                                        C.byref(res._p), C.byref(res.stats)))

@@ -1,0 +1,122 @@
+"""The band plan (exact tile pruning on two principal projections, join.cu
+k_pca_* / k_band_*): the pair set must be identical to the dense screen's
+and to the brute-force oracle's, for self and cross joins, every padding
+class, shards, degenerate data and non-finite rows.  PDB_JOIN_BAND=1 forces
+the plan below its default size threshold; PDB_JOIN_DENSE (dense=True)
+disables it."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1812_07607_b200 import patchdb, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _pairs(res):
+    return set(zip(res.left.tolist(), res.right.tolist()))
+
+
+def _check_vs_oracle(L, R, tau, self_join):
+    got = patchdb.sim_join(L, R, tau, self_join=self_join)
+    ol, orr, od = oracle.sim_join(L, R, tau, self_join=self_join)
+    assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
+    assert np.array_equal(got.dist, od.astype(np.float32))
+    return got
+
+
+@pytest.fixture
+def forced(monkeypatch):
+    monkeypatch.setenv("PDB_JOIN_BAND", "1")
+
+
+@pytest.mark.parametrize("d", [1, 3, 17, 64, 100, 128])
+def test_forced_band_self_matches_oracle(forced, d):
+    x = workloads.clusters(5000 + 37 * d, d, 60, 0.02, True, d)
+    _check_vs_oracle(x, None, 0.05 if d > 3 else 0.002, True)
+
+
+@pytest.mark.parametrize("n,m,d,tau", [(3000, 4100, 64, 0.3), (777, 2000, 128, 0.6),
+                                       (2048, 257, 5, 0.05), (1, 5000, 64, 2.0)])
+def test_forced_band_cross_matches_oracle(forced, n, m, d, tau):
+    rng = np.random.default_rng(n + m)
+    L = rng.random((n, d), dtype=np.float32)
+    R = np.concatenate([L[: min(n, m) // 2] + 1e-3 * rng.standard_normal((min(n, m) // 2, d),
+                                                                         dtype=np.float32),
+                        rng.random((m - min(n, m) // 2, d), dtype=np.float32)])
+    _check_vs_oracle(L, R, tau, False)
+
+
+def test_forced_band_degenerate_data(forced):
+    # identical rows (zero covariance), a single distinct direction, tau = 0
+    x = np.zeros((3000, 64), np.float32)
+    _check_vs_oracle(x, None, 0.0, True)
+    x[::3, 5] = 1.0
+    _check_vs_oracle(x, None, 0.0, True)
+    _check_vs_oracle(x, None, 0.999, True)
+    # everything within tau: no tile may be pruned
+    y = workloads.uniform(2500, 64, 4)
+    got = _check_vs_oracle(y, None, 100.0, True)
+    assert len(got) == 2500 * 2499 // 2
+
+
+def test_forced_band_nonfinite_and_huge_rows(forced):
+    rng = np.random.default_rng(7)
+    x = rng.random((4000, 64), dtype=np.float32)
+    x[10] = np.nan
+    x[11, 3] = np.inf
+    x[12] = -np.inf
+    x[13] = 3e30            # beyond the screen's range: always a candidate
+    x[14] = 3e30
+    x[15] = x[13]
+    x[16:40] = x[100:124] + 1e-4
+    got = _check_vs_oracle(x, None, 0.05, True)
+    assert (13, 15) in _pairs(got) and (13, 14) in _pairs(got)
+
+
+def test_forced_band_shards_partition(forced):
+    x = workloads.clusters(9000, 64, 80, 0.02, True, 11)
+    full = patchdb.sim_join(x, None, 0.05, self_join=True)
+    parts = [patchdb.sim_join(x, None, 0.05, self_join=True, shard=(k, 3)) for k in range(3)]
+    sets = [_pairs(p) for p in parts]
+    assert sum(len(s) for s in sets) == len(full)
+    assert set().union(*sets) == _pairs(full)
+
+
+def _band_vs_dense(L, R, tau, self_join):
+    import torch
+    Lt = torch.from_numpy(L).cuda()
+    Rt = None if R is None else torch.from_numpy(R).cuda()
+    b = patchdb.sim_join_device(Lt, Rt, tau, self_join=self_join, sort=True)
+    bl, br, bd = (t.cpu().numpy() for t in b.to_torch(Lt.device))
+    tiles_b = b.stats.tiles
+    dn = patchdb.sim_join_device(Lt, Rt, tau, self_join=self_join, sort=True, dense=True)
+    dl, dr, dd = (t.cpu().numpy() for t in dn.to_torch(Lt.device))
+    assert np.array_equal(bl, dl) and np.array_equal(br, dr) and np.array_equal(bd, dd)
+    return tiles_b, dn.stats.tiles, len(bl)
+
+
+def test_default_band_config2_features():
+    fr, _ = workloads.frames(600, 480, 640, seed=2)
+    h = patchdb.featurize_tiles(fr, 60, 80, 4, "joint")
+    tb, td, n = _band_vs_dense(h, None, 0.05, True)
+    assert n > 0 and tb < 0.7 * td
+    # sampled rows against the brute-force oracle
+    res = patchdb.sim_join(h, None, 0.05, self_join=True)
+    for r0 in (0, 20_000, 38_300):
+        ol, orr, od = oracle.sim_join(h, None, 0.05, self_join=True, rows=(r0, r0 + 100))
+        m = (res.left >= r0) & (res.left < r0 + 100)
+        assert np.array_equal(res.left[m], ol) and np.array_equal(res.right[m], orr)
+
+
+def test_default_band_cross_d128_planted():
+    L, R, _, _ = workloads.config3(n=65_536)
+    tb, td, n = _band_vs_dense(L, R, 0.02, False)
+    assert n > 0 and tb < 0.5 * td
+
+
+def test_default_band_skewed_self():
+    x = workloads.config5(131_072)
+    tb, td, n = _band_vs_dense(x, None, 0.01, True)
+    assert n > 100_000 and tb < td
