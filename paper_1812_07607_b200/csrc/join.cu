@@ -1031,81 +1031,36 @@ __device__ __forceinline__ uint16_t to_bf16_bits(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
-// Row epilogue shared by both prep kernels: lane holds the raw values x[k]
-// of columns k = lane + 32*i (i < NV, NV*32 == DP), writes the centred,
-// rounded copy, the norms / row class and the folded-g block.
-template <bool BF16, int NV>
-__device__ __forceinline__ void prep_row(int64_t row, int lane, int d, int DP,
-                                         const float (&x)[NV], const float (&m)[NV],
-                                         void* __restrict__ Xp_, float* __restrict__ hn,
-                                         float* __restrict__ sn, uint16_t* __restrict__ gx) {
-    float* xpf = static_cast<float*>(Xp_) + row * DP;
-    uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
-    double acc = 0.0;
-    bool finite = true, big = false;
-    float t[NV];
+// Sum over the 32 lanes of eight per-row partials v[0..7] with 9 shuffles
+// (a transposing butterfly): afterwards lanes 4r .. 4r+3 hold row r's total.
+__device__ __forceinline__ double sum8_transpose(const double (&v)[8], int lane) {
+    double k4[4], k2[2];
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-    for (int i = 0; i < NV; i++) {
-        const int k = lane + 32 * i;
-        t[i] = 0.0f;
-        if (k < d) {
-            if (!isfinite(x[i])) finite = false;
-            const float c = __fsub_rn(x[i], m[i]);
-            t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
-                        : round_tf32(c);
-            if (!(fabsf(t[i]) <= kBigLimit)) big = true;
-        }
-        acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
+    for (int i = 0; i < 4; i++) {
+        const double send = b4 ? v[i] : v[i + 4];
+        k4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    finite = __all_sync(0xffffffffu, finite);
-    big = __any_sync(0xffffffffu, big);
-#pragma unroll
-    for (int i = 0; i < NV; i++) {
-        const float v = (!finite || big) ? 0.0f : t[i];
-        if (BF16) xpb[lane + 32 * i] = static_cast<uint16_t>(__float_as_uint(v) >> 16);
-        else xpf[lane + 32 * i] = v;
+    for (int i = 0; i < 2; i++) {
+        const double send = b3 ? k4[i] : k4[i + 2];
+        k2[i] = (b3 ? k4[i + 2] : k4[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-    if (lane == 0) {
-        if (!finite) {
-            hn[row] = 0.0f;
-            sn[row] = kFlagNonFinite;
-        } else if (big) {
-            hn[row] = 0.0f;
-            sn[row] = kFlagBig;
-        } else {
-            hn[row] = static_cast<float>(acc);
-            sn[row] = __double2float_ru(sqrt(acc));
-        }
-    }
-    if (gx) {
-        // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
-        // parts (24 significant bits), zeros elsewhere; -inf never matches,
-        // +inf is always a candidate (rows too large for the screen)
-        uint16_t part[3] = {0, 0, 0};
-        if (!finite) {
-            part[0] = 0xFF80u;
-        } else if (big) {
-            part[0] = 0x7F80u;
-        } else {
-            double r = -0.5 * acc;
-            for (int q = 0; q < 3; q++) {
-                const uint16_t b = to_bf16_bits(static_cast<float>(r));
-                part[q] = b;
-                r -= static_cast<double>(__uint_as_float(static_cast<uint32_t>(b) << 16));
-            }
-        }
-        uint32_t* gw = reinterpret_cast<uint32_t*>(gx + row * kGCols);
-        const uint32_t w = lane == 0 ? (static_cast<uint32_t>(part[1]) << 16) | part[0]
-                         : lane == 1 ? part[2] : 0u;
-        if (lane < kGCols / 2) gw[lane] = w;
-    }
+    const double send = b2 ? k2[0] : k2[1];
+    double t = (b2 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    return t;
 }
 
-// DP <= 128: each warp loads kRowsPerWarp rows up front (all loads in
-// flight together), then finishes them one by one.
-constexpr int kRowsPerWarp = 4;
+// DP <= 128: a warp prepares kRowsPerWarp = 8 rows at once.  Lane owns the
+// NV contiguous columns k = lane*NV + i of each row (one coalesced vector
+// load and one vector store per lane and row).  The centred copy is rounded
+// to the MMA input type; the per-row epilogue (norms / row class, the
+// folded-g block) runs on lane 4r for row r after one transposing fp64
+// reduction, so no lane serialises the eight rows.  perm: row r of the copy
+// is input row perm[r] (band plan).
+constexpr int kRowsPerWarp = 8;
 template <bool BF16, int NV>
 __global__ void __launch_bounds__(256)
 k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
@@ -1117,23 +1072,121 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
     const int lane = threadIdx.x & 31;
     const int64_t r0 = w * kRowsPerWarp;
     if (r0 >= n) return;
-    float m[NV], x[kRowsPerWarp][NV];
+    float m[NV];
 #pragma unroll
-    for (int i = 0; i < NV; i++) m[i] = lane + 32 * i < d ? mu[lane + 32 * i] : 0.0f;
-    int64_t src[kRowsPerWarp];  // row r0 + r of the (sorted) copy is input row src[r]
+    for (int i = 0; i < NV; i++) m[i] = lane * NV + i < d ? mu[lane * NV + i] : 0.0f;
+    // vector loads need every column of the lane in range and aligned rows
+    const bool vec = (NV == 2 || NV == 4) && d == DP && (reinterpret_cast<uintptr_t>(X) % (4 * NV) == 0);
+    float x[kRowsPerWarp][NV];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; r++)
-        src[r] = r0 + r < n ? (perm ? static_cast<int64_t>(__ldg(perm + r0 + r)) : r0 + r) : 0;
+    for (int r = 0; r < kRowsPerWarp; r++) {
+        const int64_t src = r0 + r < n ? (perm ? static_cast<int64_t>(__ldg(perm + r0 + r)) : r0 + r) : -1;
+        const float* xr = X + (src >= 0 ? src : 0) * d + lane * NV;
+        if (src >= 0 && vec) {
+            if (NV == 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(xr));
+                x[r][0] = q.x;
+                x[r][1 % NV] = q.y;
+                x[r][2 % NV] = q.z;
+                x[r][3 % NV] = q.w;
+            } else {
+                const float2 q = __ldg(reinterpret_cast<const float2*>(xr));
+                x[r][0] = q.x;
+                x[r][1 % NV] = q.y;
+            }
+        } else {
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; r++)
+            for (int i = 0; i < NV; i++)
+                x[r][i] = (src >= 0 && lane * NV + i < d) ? __ldg(xr + i) : 0.0f;
+        }
+    }
+    double part[kRowsPerWarp];
+    uint32_t fin_mask = 0, big_mask = 0;
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; r++) {
+        double acc = 0.0;
+        bool finite = true, big = false;
+        float t[NV];
 #pragma unroll
         for (int i = 0; i < NV; i++) {
-            const int k = lane + 32 * i;
-            x[r][i] = (r0 + r < n && k < d) ? __ldg(X + src[r] * d + k) : 0.0f;
+            const int k = lane * NV + i;
+            t[i] = 0.0f;
+            if (k < d) {
+                if (!isfinite(x[r][i])) finite = false;
+                const float c = __fsub_rn(x[r][i], m[i]);
+                t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
+                            : round_tf32(c);
+                if (!(fabsf(t[i]) <= kBigLimit)) big = true;
+            }
+            acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
         }
+        part[r] = acc;
+        finite = __all_sync(0xffffffffu, finite);
+        big = __any_sync(0xffffffffu, big);
+        fin_mask |= static_cast<uint32_t>(finite) << r;
+        big_mask |= static_cast<uint32_t>(big) << r;
+        if (r0 + r < n) {
+            const bool zero = !finite || big;
+            const int64_t row = r0 + r;
+            if (BF16) {
+                uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP + lane * NV;
+                uint16_t b[NV];
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; r++)
-        if (r0 + r < n) prep_row<BF16, NV>(r0 + r, lane, d, DP, x[r], m, Xp_, hn, sn, gx);
+                for (int i = 0; i < NV; i++)
+                    b[i] = zero ? 0 : static_cast<uint16_t>(__float_as_uint(t[i]) >> 16);
+                if (NV == 4) {
+                    *reinterpret_cast<uint2*>(xpb) =
+                        make_uint2(b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16),
+                                   b[2 % NV] | (static_cast<uint32_t>(b[3 % NV]) << 16));
+                } else if (NV == 2) {
+                    *reinterpret_cast<uint32_t*>(xpb) = b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NV; i++) xpb[i] = b[i];
+                }
+            } else {
+                float* xpf = static_cast<float*>(Xp_) + row * DP + lane * NV;
+#pragma unroll
+                for (int i = 0; i < NV; i++) xpf[i] = zero ? 0.0f : t[i];
+            }
+        }
+    }
+    const double acc = sum8_transpose(part, lane);
+    const int r = (lane >> 2) & 7;
+    if ((lane & 3) != 0 || r0 + r >= n) return;
+    const int64_t row = r0 + r;
+    const bool finite = (fin_mask >> r) & 1, big = (big_mask >> r) & 1;
+    if (!finite) {
+        hn[row] = 0.0f;
+        sn[row] = kFlagNonFinite;
+    } else if (big) {
+        hn[row] = 0.0f;
+        sn[row] = kFlagBig;
+    } else {
+        hn[row] = static_cast<float>(acc);
+        sn[row] = __double2float_ru(sqrt(acc));
+    }
+    if (gx) {
+        // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
+        // parts (24 significant bits), zeros elsewhere; -inf never matches,
+        // +inf is always a candidate (rows too large for the screen)
+        uint16_t pt[3] = {0, 0, 0};
+        if (!finite) {
+            pt[0] = 0xFF80u;
+        } else if (big) {
+            pt[0] = 0x7F80u;
+        } else {
+            double rr = -0.5 * acc;
+            for (int q = 0; q < 3; q++) {
+                const uint16_t b = to_bf16_bits(static_cast<float>(rr));
+                pt[q] = b;
+                rr -= static_cast<double>(__uint_as_float(static_cast<uint32_t>(b) << 16));
+            }
+        }
+        uint4* gw = reinterpret_cast<uint4*>(gx + row * kGCols);
+        gw[0] = make_uint4((static_cast<uint32_t>(pt[1]) << 16) | pt[0], pt[2], 0u, 0u);
+        gw[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
 }
 
 // Any DP: one warp per row, 32 columns at a time.
@@ -1502,7 +1555,7 @@ k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
     double g[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // u0.u0, u1.u1, u0.u1, u0.centre, u1.centre
     if (t < d) {
         const double x0 = v[0][t], x1 = v[1][t];
-        const double centre = static_cast<double>(mu[t]) + mean[t];
+        const double centre = mean[t];  // projections are of x - mu
         g[0] = x0 * x0;
         g[1] = x1 * x1;
         g[2] = x0 * x1;
@@ -1540,75 +1593,105 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> 
     return x;
 }
 
-// One thread per row: fp64 projections, the Morton sort key and the
-// projection-error scale sum_k |u_k x_k|, max-reduced per block (one
-// atomicMax per block).
-__global__ void __launch_bounds__(256)
-k_band_keys(const float* __restrict__ X, int64_t n, int d, BandInfo* __restrict__ info,
-            double2* __restrict__ proj, uint32_t* __restrict__ key, int32_t* __restrict__ val,
-            int32_t* __restrict__ zero_bins) {
+// Eight lanes per row, four rows per warp step: lane sub = lane % 8 owns
+// columns 32 i + 4 sub + j (i < NV, j < 4), so each group reads its row in
+// coalesced 128-byte float4 runs.  Projections of the centred row x - mu in
+// fp32 FMA chains with the error scale b = sum_k |u_k| |x_k - mu_k|: the
+// computed projection is within (d + 2) 2^-24 b of the exact one (the
+// centring cancels in every difference of two rows).  Outputs: the
+// projections, the Morton sort key, and b max-reduced per block (one
+// atomicMax per block).  Block 0 also zeroes the counting sort's bins.
+template <int NV>
+__global__ void __launch_bounds__(256, 4)
+k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
+            BandInfo* __restrict__ info, float2* __restrict__ proj, uint32_t* __restrict__ key,
+            int32_t* __restrict__ val, int32_t* __restrict__ zero_bins) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    if (zero_bins && blockIdx.x == 0)  // the counting sort's bin counts
+    if (zero_bins && blockIdx.x == 0)
         for (int b = threadIdx.x; b < (1 << (2 * kMortonBits)); b += blockDim.x) zero_bins[b] = 0;
-    __shared__ float us[2][kPcaMaxD];
-    __shared__ double bred[8];
-    for (int c = threadIdx.x; c < kPcaMaxD; c += blockDim.x) {
-        us[0][c] = info->u[0][c];
-        us[1][c] = info->u[1][c];
+    __shared__ float bred[8];
+    __shared__ float4 us[3][32 * NV / 4];  // u0, u1, mu
+    for (int c = threadIdx.x; c < 32 * NV / 4; c += blockDim.x) {
+        us[0][c] = reinterpret_cast<const float4*>(info->u[0])[c];
+        us[1][c] = reinterpret_cast<const float4*>(info->u[1])[c];
+        float4 m;
+        m.x = 4 * c < d ? mu[4 * c] : 0.0f;
+        m.y = 4 * c + 1 < d ? mu[4 * c + 1] : 0.0f;
+        m.z = 4 * c + 2 < d ? mu[4 * c + 2] : 0.0f;
+        m.w = 4 * c + 3 < d ? mu[4 * c + 3] : 0.0f;
+        us[2][c] = m;
     }
-    const double lo0 = info->lo[0], lo1 = info->lo[1], inv0 = info->inv[0], inv1 = info->inv[1];
     __syncthreads();
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    double bm = 0.0;
-    if (row < n) {
-        const float* x = X + row * d;
-        double p0 = 0.0, p1 = 0.0, b = 0.0;
-        const bool v4 = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-        if (v4) {
-            for (int k = 0; k < d; k += 4) {
-                const float4 q = __ldg(reinterpret_cast<const float4*>(x + k));
-                const float e[4] = {q.x, q.y, q.z, q.w};
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane >> 3, sub = lane & 7;
+    const float lo0 = static_cast<float>(info->lo[0]), lo1 = static_cast<float>(info->lo[1]);
+    const float inv0 = static_cast<float>(info->inv[0]), inv1 = static_cast<float>(info->inv[1]);
+    const bool vec = d == 32 * NV && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+    const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
+    float bm = 0.0f;
+    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * 4; r0 < n; r0 += step) {
+        const int64_t row = r0 + grp;
+        const bool on = row < n;
+        const float* xr = X + (on ? row : 0) * d;
+        float p0 = 0.0f, p1 = 0.0f, b = 0.0f;
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const double a0 = static_cast<double>(us[0][k + i]) * e[i];
-                    const double a1 = static_cast<double>(us[1][k + i]) * e[i];
-                    p0 += a0;
-                    p1 += a1;
-                    b += fabs(a0) + fabs(a1);
-                }
+        for (int i = 0; i < NV; i++) {
+            float x[4];
+            const int c0 = 32 * i + 4 * sub;
+            if (vec) {
+                const float4 q = on ? __ldg(reinterpret_cast<const float4*>(xr + c0)) : make_float4(0, 0, 0, 0);
+                x[0] = q.x;
+                x[1] = q.y;
+                x[2] = q.z;
+                x[3] = q.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) x[j] = (on && c0 + j < d) ? __ldg(xr + c0 + j) : 0.0f;
             }
-        } else {
-            for (int k = 0; k < d; k++) {
-                const double e = __ldg(x + k);
-                const double a0 = us[0][k] * e, a1 = us[1][k] * e;
-                p0 += a0;
-                p1 += a1;
-                b += fabs(a0) + fabs(a1);
+            const float4 w0 = us[0][8 * i + sub], w1 = us[1][8 * i + sub], mm = us[2][8 * i + sub];
+            const float ua[4] = {w0.x, w0.y, w0.z, w0.w}, ub[4] = {w1.x, w1.y, w1.z, w1.w};
+            const float mc[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float xc = x[j] - mc[j];
+                p0 = fmaf(ua[j], xc, p0);
+                p1 = fmaf(ub[j], xc, p1);
+                b = fmaf(fabsf(ua[j]) + fabsf(ub[j]), fabsf(xc), b);
             }
         }
-        uint32_t kk = (1u << (2 * kMortonBits)) - 1;  // non-finite rows sort last
-        if (isfinite(p0) && isfinite(p1)) {
-            const double lim = static_cast<double>((1 << kMortonBits) - 1);
-            const uint32_t q0 = static_cast<uint32_t>(fmin(fmax((p0 - lo0) * inv0, 0.0), lim));
-            const uint32_t q1 = static_cast<uint32_t>(fmin(fmax((p1 - lo1) * inv1, 0.0), lim));
-            kk = spread_bits(q0) | (spread_bits(q1) << 1);
-            if (isfinite(b)) bm = b;
-        } else {
-            p0 = p1 = __longlong_as_double(0x7ff8000000000000ll);  // NaN: in no box
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
         }
-        proj[row] = make_double2(p0, p1);
-        key[row] = kk;
-        val[row] = static_cast<int32_t>(row);
+        if (on && sub == 0) {
+            uint32_t kk = (1u << (2 * kMortonBits)) - 1;  // non-finite rows sort last
+            if (isfinite(p0) && isfinite(p1) && isfinite(b)) {
+                const float lim = static_cast<float>((1 << kMortonBits) - 1);
+                const uint32_t q0 = static_cast<uint32_t>(fminf(fmaxf((p0 - lo0) * inv0, 0.0f), lim));
+                const uint32_t q1 = static_cast<uint32_t>(fminf(fmaxf((p1 - lo1) * inv1, 0.0f), lim));
+                kk = spread_bits(q0) | (spread_bits(q1) << 1);
+                bm = fmaxf(bm, b);
+            } else {
+                // rows whose projections overflow fp32 are left in every box's
+                // way (NaN boxes keep every tile); truly non-finite rows match nothing
+                p0 = p1 = __int_as_float(0x7fc00000);
+            }
+            proj[row] = make_float2(p0, p1);
+            key[row] = kk;
+            val[row] = static_cast<int32_t>(row);
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-    if ((threadIdx.x & 31) == 0) bred[threadIdx.x >> 5] = bm;
+    for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    if (lane == 0) bred[wib] = bm;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) m = fmax(m, bred[w]);
-        if (m > 0) atomicMax(&info->bmax, static_cast<unsigned long long>(__double_as_longlong(m)));
+        float m = 0.0f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) m = fmaxf(m, bred[w]);
+        if (m > 0) atomicMax(&info->bmax, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(m))));
     }
 }
 
@@ -1664,57 +1747,78 @@ k_bin_scan(const int32_t* __restrict__ count, int32_t* __restrict__ pos) {
     }
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kScatterRows = 4;  // rows per thread (4096 per 1024-thread block)
+__global__ void __launch_bounds__(1024)
 k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ pos,
               int32_t* __restrict__ perm) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint32_t k = r < n ? __ldg(key + r) : 0xffffffffu;
-    // one atomic per distinct key in the warp
-    const uint32_t peers = __match_any_sync(0xffffffffu, k);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    int32_t base = 0;
-    if (r < n && lane == leader) base = atomicAdd(pos + k, __popc(peers));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (r < n) perm[base + __popc(peers & ((1u << lane) - 1u))] = static_cast<int32_t>(r);
+    __shared__ int32_t cnt[kBins], base[kBins];
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kScatterRows;
+    uint32_t k[kScatterRows];
+    int32_t local[kScatterRows];
+#pragma unroll
+    for (int i = 0; i < kScatterRows; i++) {
+        const int64_t r = r0 + i * blockDim.x + threadIdx.x;
+        k[i] = r < n ? __ldg(key + r) : 0xffffffffu;
+        local[i] = r < n ? atomicAdd(&cnt[k[i]], 1) : 0;
+    }
+    __syncthreads();
+    // one global reservation per (block, bin)
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+        base[b] = cnt[b] ? atomicAdd(pos + b, cnt[b]) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kScatterRows; i++) {
+        const int64_t r = r0 + i * blockDim.x + threadIdx.x;
+        if (r < n) perm[base[k[i]] + local[i]] = static_cast<int32_t>(r);
+    }
 }
 
 // One warp per block of `blk` sorted rows: the projected bounding box
-// (min0, max0, min1, max1); NaN projections (rows that match nothing) are
-// left out, an all-NaN block gets an empty box.
+// (min0, max0, min1, max1).  A row without finite projections (non-finite
+// data, or fp32 overflow of a huge row) makes its block's box the whole
+// plane, so no tile of that block is ever pruned.
 __global__ void __launch_bounds__(256)
-k_band_boxes(const double2* __restrict__ proj, const int32_t* __restrict__ perm, int64_t n, int blk,
+k_band_boxes(const float2* __restrict__ proj, const int32_t* __restrict__ perm, int64_t n, int blk,
              int64_t n_blk, double4* __restrict__ box) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int64_t b = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (b >= n_blk) return;
-    const double inf = __longlong_as_double(0x7ff0000000000000ll);
-    double lo0 = inf, hi0 = -inf, lo1 = inf, hi1 = -inf;
+    const float inf = __int_as_float(0x7f800000);
+    float lo0 = inf, hi0 = -inf, lo1 = inf, hi1 = -inf;
+    bool wild = false;
     const int64_t r1 = min(n, (b + 1) * blk);
     for (int64_t r = b * blk + lane; r < r1; r += 32) {
-        const double2 q = proj[__ldg(perm + r)];
-        lo0 = fmin(lo0, q.x);
-        hi0 = fmax(hi0, q.x);
-        lo1 = fmin(lo1, q.y);
-        hi1 = fmax(hi1, q.y);
+        const float2 q = proj[__ldg(perm + r)];
+        if (!(isfinite(q.x) && isfinite(q.y))) wild = true;
+        lo0 = fminf(lo0, q.x);
+        hi0 = fmaxf(hi0, q.x);
+        lo1 = fminf(lo1, q.y);
+        hi1 = fmaxf(hi1, q.y);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        lo0 = fmin(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
-        hi0 = fmax(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
-        lo1 = fmin(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
-        hi1 = fmax(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+        lo0 = fminf(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
+        hi0 = fmaxf(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+        lo1 = fminf(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
+        hi1 = fmaxf(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
     }
-    if (lane == 0) box[b] = make_double4(lo0, hi0, lo1, hi1);
+    wild = __any_sync(0xffffffffu, wild);
+    if (lane == 0) {
+        const double dinf = __longlong_as_double(0x7ff0000000000000ll);
+        box[b] = wild ? make_double4(-dinf, dinf, -dinf, dinf) : make_double4(lo0, hi0, lo1, hi1);
+    }
 }
 
 struct BandPlan {
     const double4* boxL;
     const double4* boxR;  // nullptr for a self-join: tile J = row blocks 2J, 2J + 1
+    const double4* sup;   // union box of each group of 32 consecutive tiles
     const BandInfo* info;
     double tau;
     int d, nt, self, P, shard, n_slots, nbl;
@@ -1731,9 +1835,33 @@ __device__ __forceinline__ double4 box_r(const BandPlan& q, int J) {
 // Squared threshold of the box test: (s tau + projection error)^2, widened.
 __device__ __forceinline__ double band_thr2(const BandPlan& q) {
     const double bmax = __longlong_as_double(static_cast<long long>(q.info->bmax));
-    const double err = 4.0 * (q.d + 2) * 1.1102230246251565e-16 * bmax;  // 4 (d+2) 2^-53 bmax
+    const double err = 4.0 * (q.d + 8) * 5.9604644775390625e-08 * bmax;  // 4 (d+8) 2^-24 bmax
     const double t = (q.tau * q.info->s + err) * (1.0 + 1e-9);
     return t * t;
+}
+
+// One warp per group of 32 consecutive column tiles: their union box (the
+// tiles are Morton-ordered, so a group is compact and most groups fail the
+// test as a whole).
+__global__ void __launch_bounds__(256)
+k_band_groups(const BandPlan q, double4* __restrict__ sup) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int g = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= (q.nt + 31) / 32) return;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double4 u = make_double4(inf, -inf, inf, -inf);
+    const int J = g * 32 + lane;
+    if (J < q.nt) u = box_r(q, J);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        u.x = fmin(u.x, __shfl_xor_sync(0xffffffffu, u.x, o));
+        u.y = fmax(u.y, __shfl_xor_sync(0xffffffffu, u.y, o));
+        u.z = fmin(u.z, __shfl_xor_sync(0xffffffffu, u.z, o));
+        u.w = fmax(u.w, __shfl_xor_sync(0xffffffffu, u.w, o));
+    }
+    if (lane == 0) sup[g] = u;
 }
 
 __device__ __forceinline__ bool band_keep(const double4& a, const double4& b, double thr2) {
@@ -1759,7 +1887,12 @@ k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
     const double thr2 = band_thr2(q);
     const double4 a = q.boxL[rb];
     int c = 0;
-    for (int J = (q.self ? rb >> 1 : 0) + lane; J < q.nt; J += 32) c += band_keep(a, box_r(q, J), thr2);
+    const int j0 = q.self ? rb >> 1 : 0;
+    for (int g = j0 >> 5; g * 32 < q.nt; g++) {
+        if (!band_keep(a, q.sup[g], thr2)) continue;  // warp-uniform: the whole group is out
+        const int J = g * 32 + lane;
+        if (J >= j0 && J < q.nt) c += band_keep(a, box_r(q, J), thr2);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) cnt[k] = c;
@@ -1768,7 +1901,7 @@ k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
 // One block: list offsets, tiles per unit, unit offsets; zeroes the screen /
 // re-check counters (the first kernel they follow).
 __global__ void __launch_bounds__(1024)
-k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int sm_count, int64_t* __restrict__ list_off,
+k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int units_target, int64_t* __restrict__ list_off,
             int64_t* __restrict__ unit_off, int64_t* __restrict__ n_units, int32_t* __restrict__ dev_ch,
             unsigned long long* __restrict__ counters) {
     ptx::pdl_wait();
@@ -1797,7 +1930,7 @@ k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int sm_count, int64_t*
     int64_t run = scan(local);
     if (t == 1023) {
         const int64_t total = run + local;
-        int64_t c = total / (16 * static_cast<int64_t>(sm_count));
+        int64_t c = total / units_target;
         c = c < 1 ? 1 : (c > 64 ? 64 : c);
         ch_s = static_cast<int>(c);
         *dev_ch = ch_s;
@@ -1836,9 +1969,11 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     const double4 a = q.boxL[rb];
     int64_t w = list_off[k];
     float ms = 0.0f, mn = 0.0f;
-    for (int J0 = q.self ? rb >> 1 : 0; J0 < q.nt; J0 += 32) {
-        const int J = J0 + lane;
-        const bool keep = J < q.nt && band_keep(a, box_r(q, J), thr2);
+    const int j0 = q.self ? rb >> 1 : 0;
+    for (int g = j0 >> 5; g * 32 < q.nt; g++) {
+        if (!band_keep(a, q.sup[g], thr2)) continue;  // warp-uniform
+        const int J = g * 32 + lane;
+        const bool keep = J >= j0 && J < q.nt && band_keep(a, box_r(q, J), thr2);
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             list[w + __popc(bal & ((1u << lane) - 1u))] = J;
@@ -2367,7 +2502,12 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     // and output buffers from that sample, so a heavy output (config 5:
     // ~1.4e9 candidates) does not cost a second full screen pass.
     constexpr int64_t kSampleStep = 64;
-    if (p.n_units >= kSampleStep * ctx.sm_count) {
+    int64_t units = p.n_units;  // dense estimate; a band plan's real count is on the device
+    if (p.tile_list && units >= kSampleStep * ctx.sm_count) {
+        PDB_CUDA(cudaMemcpyAsync(&units, p.dev_n_units, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PDB_CUDA(cudaStreamSynchronize(s));
+    }
+    if (units >= kSampleStep * ctx.sm_count) {
         recs.reset(cap, s);
         arm();
         p.unit_step = kSampleStep;
@@ -2524,7 +2664,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                     Arena::need(1, sizeof(BandInfo)) +
                     Arena::need(nL, 16) + 4 * Arena::need(nL, 4) + Arena::need(sort_tmp, 1) +
                     (self ? 0 : Arena::need(nR, 16) + 4 * Arena::need(nR, 4) + Arena::need(sort_tmp, 1)) +
-                    Arena::need(nbl, 32) + Arena::need(nt_, 32) +
+                    Arena::need(nbl, 32) + Arena::need(nt_, 32) + Arena::need(ceil_div(nt_, 32), 32) +
                     Arena::need(n_slots, 4) + 2 * Arena::need(n_slots + 1, 8) + Arena::need(2, 8) +
                     Arena::need(std::max<int64_t>(list_cap, 1), 4) + 2 * Arena::need(n_slots, 4);
     Arena ar;
@@ -2567,7 +2707,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     int32_t* permL = nullptr;
     int32_t* permR = nullptr;
     BandInfo* info = nullptr;
-    double2 *projL = nullptr, *projR = nullptr;
+    float2 *projL = nullptr, *projR = nullptr;
     if (band) {
         float* part = ar.take<float>(static_cast<size_t>(kPcaBlocks) * E);
         double* sum = ar.take<double>(E);
@@ -2587,14 +2727,20 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
                    static_cast<const float*>(mu), info);
         launches += 3;
-        auto keys_and_sort = [&](const float* X, int64_t n, double2*& proj, int32_t*& perm) {
-            proj = ar.take<double2>(n);
+        auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm) {
+            proj = ar.take<float2>(n);
             uint32_t* k_in = ar.take<uint32_t>(n);
             int32_t* v_in = ar.take<int32_t>(n);
             perm = ar.take<int32_t>(n);
             uint8_t* tmp = ar.take<uint8_t>(sort_tmp);
-            launch_pdl(k_band_keys, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, s, X,
-                       n, d, info, proj, k_in, v_in, P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
+            const int nv = (d + 31) / 32;
+            auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
+                                                                                      : k_band_keys<4>;
+            const unsigned gk = static_cast<unsigned>(
+                std::min<int64_t>(ceil_div(n, 32), int64_t{ctx.sm_count} * 16));
+            launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
+                       proj, k_in, v_in,
+                       P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
             if (P > 1) {
                 // every rank must build the same order: stable radix sort
                 uint32_t* k_out = ar.take<uint32_t>(n);
@@ -2610,8 +2756,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                 launch_pdl(k_bin_count, dim3(gc), dim3(256), 0, s, static_cast<const uint32_t*>(k_in), n,
                            count);
                 launch_pdl(k_bin_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(count), pos);
-                launch_pdl(k_bin_scatter, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, s,
-                           static_cast<const uint32_t*>(k_in), n, pos, perm);
+                launch_pdl(k_bin_scatter, dim3(static_cast<unsigned>(ceil_div(n, 1024 * kScatterRows))),
+                           dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n, pos, perm);
                 launches += 4;
             }
         };
@@ -2666,18 +2812,23 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         cmaxS = ar.take<float>(n_slots);
         cmaxN = ar.take<float>(n_slots);
         launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))), dim3(256), 0, s,
-                   static_cast<const double2*>(projL), static_cast<const int32_t*>(permL), nL, BM,
+                   static_cast<const float2*>(projL), static_cast<const int32_t*>(permL), nL, BM,
                    nbl, boxL);
         if (!self)
             launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(int64_t{nt} * 32, 256))),
-                       dim3(256), 0, s, static_cast<const double2*>(projR),
+                       dim3(256), 0, s, static_cast<const float2*>(projR),
                        static_cast<const int32_t*>(permR), nR, BN, static_cast<int64_t>(nt), boxR);
-        BandPlan bp{boxL, self ? nullptr : boxR, info, tau, d, nt, static_cast<int>(self), P, shard,
-                    n_slots, static_cast<int>(nbl)};
+        double4* sup = ar.take<double4>(ceil_div(int64_t{nt}, 32));
+        BandPlan bp{boxL, self ? nullptr : boxR, sup, info, tau, d, nt, static_cast<int>(self), P,
+                    shard, n_slots, static_cast<int>(nbl)};
+        launch_pdl(k_band_groups, dim3(static_cast<unsigned>(ceil_div(ceil_div(int64_t{nt}, 32) * 32, 256))),
+                   dim3(256), 0, s, bp, sup);
         const unsigned gs = static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256));
         if (n_slots > 0) launch_pdl(k_band_count, dim3(gs), dim3(256), 0, s, bp, cnt);
+        const char* bd = getenv("PDB_BAND_DIV");
+        const int units_target = (bd ? std::max(1, atoi(bd)) : 8) * ctx.sm_count;
         launch_pdl(k_band_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(cnt), n_slots,
-                   ctx.sm_count, list_off, unit_off, dev_n_units, dev_ch, counters);
+                   units_target, list_off, unit_off, dev_n_units, dev_ch, counters);
         if (n_slots > 0)
             launch_pdl(k_band_write, dim3(gs), dim3(256), 0, s, bp,
                        static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),

@@ -1,0 +1,52 @@
+"""GPU activity timeline (CUPTI via torch.profiler) of one join-only bench
+workload (default c3): every kernel of the last call with start offsets and
+durations.  Diagnostic only.  Usage: python tools/timeline_join.py [c3|c5|c1]"""
+import ctypes as C
+import os
+import sys
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench_join import JOINS, _gen  # noqa: E402
+from paper_1812_07607_b200 import _capi as capi  # noqa: E402
+from paper_1812_07607_b200 import patchdb  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "c3"
+plain = "--plain" in sys.argv  # no profiler (for ncu)
+cfg = JOINS[which]
+L, R = _gen(which)
+Ld = torch.from_numpy(L).cuda()
+Rd = Ld if R is None else torch.from_numpy(R).cuda()
+lib = capi.lib()
+stream = torch.cuda.current_stream()
+opts = capi.JoinOpts()
+opts.flags = capi.PDB_JOIN_SELF if cfg["self_join"] else 0
+opts.stream = C.c_void_p(stream.cuda_stream)
+pairs = patchdb.DevicePairs()
+
+
+def call():
+    assert lib.pdb_sim_join_dev(Ld.data_ptr(), Ld.shape[0], Rd.data_ptr(), Rd.shape[0], Ld.shape[1],
+                                float(cfg["tau"]), C.byref(opts), C.byref(pairs._p),
+                                C.byref(pairs.stats)) == 0
+
+
+for _ in range(2):
+    call()
+torch.cuda.synchronize()
+if plain:
+    sys.exit(0)
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    call()
+    torch.cuda.synchronize()
+evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+             key=lambda e: e.time_range.start)
+t0 = evs[0].time_range.start
+prev = t0
+for e in evs:
+    s, t = e.time_range.start, e.time_range.end
+    print(f"{s - t0:10.1f} us  gap {s - prev:8.1f}  dur {t - s:9.1f}  {e.name[:80]}")
+    prev = t
+print("tiles", pairs.stats.tiles, "pairs", pairs.count, "candidates", pairs.stats.candidates)
