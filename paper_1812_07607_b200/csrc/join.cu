@@ -1997,9 +1997,13 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
 // K3: exact re-check.  The fp64 chain is written with explicit _rn
 // intrinsics so it can never be contracted into FMAs: diff = a - b,
 // acc = acc + diff * diff, sequential in k, then sqrt -- src/index.cpp:69-76.
-// One thread per candidate record: each lane walks the set bits of its
-// record's mask (warp-uniform loop, so every iteration compacts survivors
-// with a ballot and one atomic per warp).
+// A warp loads 32 candidate records (row i, first column j0, 32-bit mask)
+// and flattens their set bits into one queue: the c-th candidate belongs to
+// the lane whose exclusive popcount prefix covers c, and is that lane's
+// (c - prefix)-th set bit.  Every batch of 32 candidates keeps all lanes
+// busy whatever the masks' skew (records of tight clusters carry ~30 bits,
+// scattered ones 1-2), and lanes of one record share their row of L.
+// Survivors are compacted with a ballot and one atomic per batch.
 __global__ void __launch_bounds__(256)
 k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n_rec,
           unsigned long long cap, const float* __restrict__ L, const float* __restrict__ R,
@@ -2020,23 +2024,42 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
         const unsigned long long idx = base + lane;
         int4 rc = make_int4(0, 0, 0, 0);
         if (idx < n) rc = rec[idx];
-        uint32_t mask = static_cast<uint32_t>(rc.z);
+        const uint32_t mask = static_cast<uint32_t>(rc.z);
         // banded plans screen row-sorted copies: map back to input rows
-        int i = rc.x;
-        if (permL && mask) i = __ldg(permL + rc.x);
-        while (__any_sync(0xffffffffu, mask != 0)) {
+        const int my_i = (permL && mask) ? __ldg(permL + rc.x) : rc.x;
+        // exclusive prefix of the popcounts over the warp
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int c0 = 0; c0 < total; c0 += 32) {
+            const int c = c0 + lane;
+            // source lane: the last lane whose exclusive prefix is <= c
+            int src = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int e = __shfl_sync(0xffffffffu, excl, src + step);
+                if (e <= c) src += step;
+            }
+            const int s_excl = __shfl_sync(0xffffffffu, excl, src);
+            const uint32_t s_mask = __shfl_sync(0xffffffffu, mask, src);
+            const int s_j0 = __shfl_sync(0xffffffffu, rc.y, src);
+            int a = __shfl_sync(0xffffffffu, my_i, src);
             bool ok = false;
             double dist = 0.0;
-            int j = 0, a = i;
-            if (mask) {
-                const int k = __ffs(mask) - 1;
-                mask &= mask - 1;
-                j = rc.y + k;
+            int j = 0;
+            if (c < total) {
+                const int k = __fns(s_mask, 0, c - s_excl + 1);  // that lane's (c - excl)-th set bit
+                j = s_j0 + k;
                 if (permR) j = __ldg(permR + j);
                 // euclidean(L_i, R_j); bitwise symmetric, so a self-join pair
                 // can be reported as (min, max)
-                dist = exact_dist(L + static_cast<int64_t>(i) * d,
-                                  R + static_cast<int64_t>(j) * d, d, vec8);
+                dist = exact_dist(L + static_cast<int64_t>(a) * d, R + static_cast<int64_t>(j) * d, d, vec8);
                 ok = dist <= tau;
                 if (self_join && a > j) {
                     const int t = a;
