@@ -132,6 +132,7 @@ struct ScreenParams {
     const int64_t* slot_unit_off;  // [n_slots + 1]
     const int64_t* dev_n_units;    // unit count (device)
     const int32_t* dev_ch;         // tiles per unit (device)
+    const int4* unit_info;         // decoded units (rb, first, end, slot), one load per unit
     int32_t n_slots;
 };
 
@@ -144,6 +145,15 @@ __device__ __forceinline__ int tile_at(const ScreenParams& p, int o) {
 }
 
 __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
+    if (p.unit_info) {
+        const int4 q = __ldg(p.unit_info + u);
+        Unit r;
+        r.rb = q.x;
+        r.j0 = q.y;
+        r.j1 = q.z;
+        r.chunk = q.w;
+        return r;
+    }
     if (p.tile_list) {
         // banded: slot_unit_off[lo] <= u < slot_unit_off[lo + 1]
         int lo = 0, hi = p.n_slots;
@@ -251,7 +261,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     // atomic and hands them to the MMA and epilogue warps through a 4-slot ring
     uint64_t* u_full = reinterpret_cast<uint64_t*>(r_smem + kEpiWarps * 32);
     uint64_t* u_empty = u_full + 4;
-    volatile int64_t* u_val = reinterpret_cast<volatile int64_t*>(u_full + 8);
+    // the producer publishes decoded units {rb, first tile, end, chunk}; rb < 0 ends
+    volatile int4* u_dec = reinterpret_cast<volatile int4*>(u_full + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -302,16 +313,21 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     // consumer side of the unit ring (MMA warp: lane 0 only; epilogue: whole warp)
     int u_slot = 0;
     uint32_t u_phase = 0;
-    auto take_unit = [&](bool whole_warp) -> int64_t {
+    auto take_unit = [&](bool whole_warp) -> Unit {
         ptx::mbar_wait(&u_full[u_slot], u_phase);
-        const int64_t u = u_val[u_slot];
+        const int4 q = const_cast<const int4&>(u_dec[u_slot]);
         if (whole_warp) __syncwarp();
         if (!whole_warp || lane == 0) ptx::mbar_arrive(&u_empty[u_slot]);
         if (++u_slot == 4) {
             u_slot = 0;
             u_phase ^= 1;
         }
-        return u;
+        Unit w;
+        w.rb = q.x;
+        w.j0 = q.y;
+        w.j1 = q.z;
+        w.chunk = q.w;
+        return w;
     };
 
     if (warp == 0) {
@@ -327,20 +343,26 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 const int64_t c = static_cast<int64_t>(atomicAdd(p.next_unit, 1ull)) * p.unit_step;
                 return c < n_units ? c : -1;
             };
-            int64_t u = claim();
+            auto decode = [&](int64_t u) -> Unit {
+                if (u >= 0) return decode_unit(p, u);
+                Unit e;
+                e.rb = -1;
+                e.j0 = e.j1 = e.chunk = 0;
+                return e;
+            };
+            Unit w = decode(claim());
             for (;;) {
                 ptx::mbar_wait(&u_empty[ps], pph ^ 1);
-                u_val[ps] = u;
+                const_cast<int4&>(u_dec[ps]) = make_int4(w.rb, w.j0, w.j1, w.chunk);
                 ptx::mbar_arrive(&u_full[ps]);
                 if (++ps == 4) {
                     ps = 0;
                     pph ^= 1;
                 }
-                if (u < 0) break;
-                // claim the next unit now: the atomic's round trip overlaps
+                if (w.rb < 0) break;
+                // claim and decode the next unit now: the round trips overlap
                 // this unit's loads instead of stalling between units
-                const int64_t u_next = claim();
-                const Unit w = decode_unit(p, u);
+                const Unit w_next = decode(claim());
                 if (A_RES) {
                     const uint32_t slot = na % kASlots, use = na / kASlots;
                     ptx::mbar_wait(&a_empty[slot], (use & 1) ^ 1);
@@ -370,7 +392,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         }
                     }
                 }
-                u = u_next;
+                w = w_next;
             }
         }
     } else if (warp == 1) {
@@ -381,9 +403,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             uint32_t na = 0;  // units consumed
             unsigned long long ntiles = 0;
             for (;;) {
-                const int64_t u = take_unit(false);
-                if (u < 0) break;
-                const Unit w = decode_unit(p, u);
+                const Unit w = take_unit(false);
+                if (w.rb < 0) break;
                 const uint32_t slot = na % kASlots;
                 uint8_t* smAu = smA + slot * kASlot;
                 if (A_RES) {
@@ -464,9 +485,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         int acc = 0;
         uint32_t acc_phase = 0;
         for (;;) {
-            const int64_t u = take_unit(true);
-            if (u < 0) break;
-            const Unit w = decode_unit(p, u);
+            const Unit w = take_unit(true);
+            if (w.rb < 0) break;
             const int64_t i = static_cast<int64_t>(w.rb) * BM + row;
             const bool row_ok = i < p.nL;
             const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
@@ -1958,7 +1978,9 @@ k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int units_target, int6
 __global__ void __launch_bounds__(256)
 k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __restrict__ list,
              const float* __restrict__ tmaxS, const float* __restrict__ tmaxN,
-             float* __restrict__ smaxS, float* __restrict__ smaxN) {
+             float* __restrict__ smaxS, float* __restrict__ smaxN,
+             const int64_t* __restrict__ unit_off, const int32_t* __restrict__ dev_ch,
+             int4* __restrict__ unit_info) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int k = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
@@ -1990,6 +2012,13 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     if (lane == 0) {
         smaxS[k] = ms;
         smaxN[k] = mn;
+    }
+    // the slot's work units, decoded once for the screen
+    const int ch = *dev_ch;
+    const int64_t l0 = list_off[k], l1 = list_off[k + 1], u0 = unit_off[k], u1 = unit_off[k + 1];
+    for (int64_t u = u0 + lane; u < u1; u += 32) {
+        const int64_t o0 = l0 + (u - u0) * ch;
+        unit_info[u] = make_int4(rb, static_cast<int>(o0), static_cast<int>(min(o0 + ch, l1)), k);
     }
 }
 
@@ -2665,6 +2694,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     int64_t list_cap = 0;
     size_t sort_tmp = 0;
     const int E = d + d * d + 1;
+    const char* bd = getenv("PDB_BAND_DIV");
+    const int units_target = (bd ? std::max(1, atoi(bd)) : 8) * ctx.sm_count;
+    int64_t units_cap = 0;
     if (band) {
         const int64_t full = nbl / P, rem = nbl % P;
         const int64_t pos_last = (full & 1) ? P - 1 - shard : shard;
@@ -2673,6 +2705,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             const int64_t rb = static_cast<int64_t>(k) * P + ((k & 1) ? P - 1 - shard : shard);
             list_cap += nt_ - (self ? rb >> 1 : 0);
         }
+        // units <= total / ch + n_slots with ch = clamp(total / units_target, 1, 64)
+        units_cap = 2 * static_cast<int64_t>(units_target) + list_cap / 64 + n_slots + 1;
         if (P > 1)
             PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint32_t*>(nullptr),
                                                      static_cast<uint32_t*>(nullptr),
@@ -2689,7 +2723,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                     (self ? 0 : Arena::need(nR, 16) + 4 * Arena::need(nR, 4) + Arena::need(sort_tmp, 1)) +
                     Arena::need(nbl, 32) + Arena::need(nt_, 32) + Arena::need(ceil_div(nt_, 32), 32) +
                     Arena::need(n_slots, 4) + 2 * Arena::need(n_slots + 1, 8) + Arena::need(2, 8) +
-                    Arena::need(std::max<int64_t>(list_cap, 1), 4) + 2 * Arena::need(n_slots, 4);
+                    Arena::need(std::max<int64_t>(list_cap, 1), 4) + 2 * Arena::need(n_slots, 4) +
+                    Arena::need(units_cap, 16);
     Arena ar;
     ar.reserve(Arena::need(DP, 4) + Arena::need(static_cast<size_t>(nL) * DP, es) +
                    2 * Arena::need(nL, 4) +
@@ -2821,6 +2856,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     float* cmaxN = ar.take<float>(nt + 1);
     // ---- band plan, part 2: boxes, surviving tiles, units -----------------
     int32_t* list = nullptr;
+    int4* unit_info = nullptr;
     int64_t *list_off = nullptr, *unit_off = nullptr, *dev_n_units = nullptr;
     int32_t* dev_ch = nullptr;
     if (band) {
@@ -2832,6 +2868,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         dev_n_units = ar.take<int64_t>(1);
         dev_ch = ar.take<int32_t>(1);
         list = ar.take<int32_t>(std::max<int64_t>(list_cap, 1));
+        unit_info = ar.take<int4>(units_cap);
         cmaxS = ar.take<float>(n_slots);
         cmaxN = ar.take<float>(n_slots);
         launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))), dim3(256), 0, s,
@@ -2848,14 +2885,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                    dim3(256), 0, s, bp, sup);
         const unsigned gs = static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256));
         if (n_slots > 0) launch_pdl(k_band_count, dim3(gs), dim3(256), 0, s, bp, cnt);
-        const char* bd = getenv("PDB_BAND_DIV");
-        const int units_target = (bd ? std::max(1, atoi(bd)) : 8) * ctx.sm_count;
         launch_pdl(k_band_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(cnt), n_slots,
                    units_target, list_off, unit_off, dev_n_units, dev_ch, counters);
         if (n_slots > 0)
             launch_pdl(k_band_write, dim3(gs), dim3(256), 0, s, bp,
                        static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
-                       static_cast<const float*>(tmaxN), cmaxS, cmaxN);
+                       static_cast<const float*>(tmaxN), cmaxS, cmaxN,
+                       static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
+                       unit_info);
         launches += 5;
     } else {
         launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
@@ -2891,6 +2928,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
     if (band) {
+        p.unit_info = unit_info;
         p.tile_list = list;
         p.slot_list_off = list_off;
         p.slot_unit_off = unit_off;
