@@ -169,7 +169,8 @@ typedef struct pdb_join_stats {
     int64_t candidate_capacity;
     int32_t launches;        /* kernels this call launched */
     int32_t screen_passes;   /* 1, or 2 after a candidate-buffer overflow */
-    float prep_ms;           /* centring, tf32 copies, norms, tile stats */
+    float prep_ms;           /* centring, screen copies, norms, tile stats, band plan, and the
+                                sampled output-size screen pass when one is taken */
     float screen_ms;         /* K2, the tcgen05 screen */
     float recheck_ms;        /* K3, exact re-check + compaction */
     float sort_ms;           /* optional canonical ordering */

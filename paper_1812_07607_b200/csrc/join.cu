@@ -2549,7 +2549,6 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         zeroed = false;
     };
     p.unit_step = 1;
-    tm.mark(1);
     // Large problems: screen every 64th work unit first and size the record
     // and output buffers from that sample, so a heavy output (config 5:
     // ~1.4e9 candidates) does not cost a second full screen pass.
@@ -2571,6 +2570,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         cap = std::max(cap, static_cast<unsigned long long>(h_cnt[0] * scale) + (1 << 20));
         out_need = std::max(out_need, static_cast<unsigned long long>(h_cnt[3] * scale) + (1 << 20));
     }
+    // (the sampled pass, when taken, counts as preparation in the phase times)
+    tm.mark(1);
     // Screen and re-check run back to back and the host reads the counters
     // once.  A record overflow re-runs the screen with the exact record
     // count; an output overflow re-runs only the re-check.
