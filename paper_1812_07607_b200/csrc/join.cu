@@ -372,8 +372,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                                          kb * KE, w.rb * BM);
                     na++;
                 }
+                // banded: the next tile's index loads while this one is issued
+                int J_next = w.j0 < w.j1 ? tile_at(p, w.j0) : 0;
                 for (int o = w.j0; o < w.j1; o++) {
-                    const int J = tile_at(p, o);
+                    const int J = J_next;
+                    if (o + 1 < w.j1) J_next = tile_at(p, o + 1);
                     for (int kb = 0; kb < NKB; kb++) {
                         const bool with_g = AUG && kb == NKB - 1;
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -512,8 +515,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 const double T = r * r + p.gam * (static_cast<double>(hn) + mn);
                 h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
             }
+            int J_next = w.j0 < w.j1 ? tile_at(p, w.j0) : 0;
             for (int o = w.j0; o < w.j1; o++) {
-                const int J = tile_at(p, o);
+                const int J = J_next;
+                if (o + 1 < w.j1) J_next = tile_at(p, o + 1);
                 __syncwarp();
                 if (!AUG) reinterpret_cast<GV*>(gs)[lane] = gnext;
                 // unconditional (clamped) prefetch: a predicated load would
@@ -1385,7 +1390,11 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 constexpr int kPcaRows = 32;    // sample rows per partial block
 constexpr int kPcaBlocks = 128; // 4096 sample rows
 constexpr int kPcaMaxD = 128;
-constexpr int64_t kBandMinRows = 32768;  // smaller joins: the plan costs more than it saves
+// The plan costs ~60-90 us (config-2 size) whatever the shard count; it pays
+// when this shard's dense screen would visit at least kBandMinTiles tiles
+// (~60 us of dense screen at d = 64) and both sides have kBandMinRows rows.
+constexpr int64_t kBandMinRows = 8192;
+constexpr int64_t kBandMinTiles = 16384;
 constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
 constexpr int kPcaIters = 6;   // subspace iterations for the top-2 principal plane
 
@@ -2685,8 +2694,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     // PDB_JOIN_BAND=0 turn it off, PDB_JOIN_BAND=1 forces it.
     const char* be = getenv("PDB_JOIN_BAND");
     const int band_env = be ? atoi(be) : -1;
-    const bool band = !pair && DP <= 128 && d <= kPcaMaxD && (o.flags & PDB_JOIN_DENSE) == 0 &&
-                      band_env != 0 && (band_env == 1 || (nL >= kBandMinRows && nR >= kBandMinRows));
+    bool band = !pair && DP <= 128 && d <= kPcaMaxD && (o.flags & PDB_JOIN_DENSE) == 0 &&
+                band_env != 0 && (band_env == 1 || (nL >= kBandMinRows && nR >= kBandMinRows));
 
     // ---- scratch: one pool allocation for every small buffer ---------------
     const int64_t nt_ = ceil_div(nR, BN);
@@ -2708,6 +2717,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         }
         // units <= total / ch + n_slots with ch = clamp(total / units_target, 1, 64)
         units_cap = 2 * static_cast<int64_t>(units_target) + list_cap / 64 + n_slots + 1;
+        if (band_env != 1 && list_cap < kBandMinTiles) band = false;  // too little screen to save
+    }
+    if (band) {
         if (P > 1)
             PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint32_t*>(nullptr),
                                                      static_cast<uint32_t*>(nullptr),

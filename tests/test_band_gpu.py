@@ -120,3 +120,18 @@ def test_default_band_skewed_self():
     x = workloads.config5(131_072)
     tb, td, n = _band_vs_dense(x, None, 0.01, True)
     assert n > 100_000 and tb < td
+
+
+def test_forced_band_tf32_copies(forced):
+    x = workloads.clusters(6000, 64, 70, 0.02, True, 5)
+    got = patchdb.sim_join(x, None, 0.05, self_join=True, tf32=True)
+    ol, orr, od = oracle.sim_join(x, None, 0.05, self_join=True)
+    assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
+
+
+def test_band_rule_keeps_small_joins_dense():
+    import torch
+    x = torch.from_numpy(workloads.config1(20_000, seed=1)).cuda()
+    r = patchdb.sim_join_device(x, None, 0.05, self_join=True)
+    nb = -(-20_000 // 128)
+    assert r.stats.tiles == sum(-(-20_000 // 256) - rb // 2 for rb in range(nb))
