@@ -1387,8 +1387,8 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 // drops a pair whose exact distance is <= tau).  Every step is
 // deterministic, so all shards of a join build the same plan.
 
-constexpr int kPcaRows = 32;    // sample rows per partial block
-constexpr int kPcaBlocks = 128; // 4096 sample rows
+constexpr int kPcaRows = 64;    // sample rows per partial block
+constexpr int kPcaBlocks = 64;  // 4096 sample rows
 constexpr int kPcaMaxD = 128;
 // The plan costs ~60-90 us (config-2 size) whatever the shard count; it pays
 // when this shard's dense screen would visit at least kBandMinTiles tiles
@@ -1396,7 +1396,7 @@ constexpr int kPcaMaxD = 128;
 constexpr int64_t kBandMinRows = 8192;
 constexpr int64_t kBandMinTiles = 16384;
 constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
-constexpr int kPcaIters = 6;   // subspace iterations for the top-2 principal plane
+constexpr int kPcaIters = 4;   // subspace iterations for the top-2 principal plane
 
 struct BandInfo {
     float u[2][kPcaMaxD];   // the two directions (zero past d)
@@ -1416,11 +1416,14 @@ k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __rest
     ptx::pdl_trigger();
     __shared__ float xs[kPcaRows][16 * T];
     __shared__ int ok[kPcaRows];
+    __shared__ int64_t rows[kPcaRows];
     const int64_t S = static_cast<int64_t>(kPcaBlocks) * kPcaRows;
+    if (threadIdx.x < kPcaRows)
+        rows[threadIdx.x] = (static_cast<int64_t>(blockIdx.x * kPcaRows + threadIdx.x) * n) / S;
+    __syncthreads();
     for (int q = threadIdx.x; q < kPcaRows * 16 * T; q += blockDim.x) {
         const int k = q / (16 * T), c = q % (16 * T);
-        const int64_t r = (static_cast<int64_t>(blockIdx.x * kPcaRows + k) * n) / S;
-        xs[k][c] = c < d ? X[r * d + c] - mu[c] : 0.0f;
+        xs[k][c] = c < d ? X[rows[k] * d + c] - mu[c] : 0.0f;
     }
     __syncthreads();
     if (threadIdx.x < kPcaRows) {
