@@ -1634,7 +1634,7 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> 
 // projections, the Morton sort key, and b max-reduced per block (one
 // atomicMax per block).  Block 0 also zeroes the counting sort's bins.
 template <int NV>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 3)
 k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
             BandInfo* __restrict__ info, float2* __restrict__ proj, uint32_t* __restrict__ key,
             int32_t* __restrict__ val, int32_t* __restrict__ zero_bins) {
@@ -1660,60 +1660,74 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
     const float lo0 = static_cast<float>(info->lo[0]), lo1 = static_cast<float>(info->lo[1]);
     const float inv0 = static_cast<float>(info->inv[0]), inv1 = static_cast<float>(info->inv[1]);
     const bool vec = d == 32 * NV && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-    const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
+    // eight rows per warp step (two per lane group), all loads issued first
+    constexpr int RPG = NV >= 3 ? 2 : 1;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4 * RPG;
     float bm = 0.0f;
-    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * 4; r0 < n; r0 += step) {
-        const int64_t row = r0 + grp;
-        const bool on = row < n;
-        const float* xr = X + (on ? row : 0) * d;
-        float p0 = 0.0f, p1 = 0.0f, b = 0.0f;
+    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * 4 * RPG; r0 < n;
+         r0 += step) {
+        float x[RPG][NV][4];
 #pragma unroll
-        for (int i = 0; i < NV; i++) {
-            float x[4];
-            const int c0 = 32 * i + 4 * sub;
-            if (vec) {
-                const float4 q = on ? __ldg(reinterpret_cast<const float4*>(xr + c0)) : make_float4(0, 0, 0, 0);
-                x[0] = q.x;
-                x[1] = q.y;
-                x[2] = q.z;
-                x[3] = q.w;
-            } else {
+        for (int h = 0; h < RPG; h++) {
+            const int64_t row = r0 + 4 * h + grp;
+            const bool on = row < n;
+            const float* xr = X + (on ? row : 0) * d;
 #pragma unroll
-                for (int j = 0; j < 4; j++) x[j] = (on && c0 + j < d) ? __ldg(xr + c0 + j) : 0.0f;
-            }
-            const float4 w0 = us[0][8 * i + sub], w1 = us[1][8 * i + sub], mm = us[2][8 * i + sub];
-            const float ua[4] = {w0.x, w0.y, w0.z, w0.w}, ub[4] = {w1.x, w1.y, w1.z, w1.w};
-            const float mc[4] = {mm.x, mm.y, mm.z, mm.w};
+            for (int i = 0; i < NV; i++) {
+                const int c0 = 32 * i + 4 * sub;
+                if (vec) {
+                    const float4 q = on ? __ldg(reinterpret_cast<const float4*>(xr + c0)) : make_float4(0, 0, 0, 0);
+                    x[h][i][0] = q.x;
+                    x[h][i][1] = q.y;
+                    x[h][i][2] = q.z;
+                    x[h][i][3] = q.w;
+                } else {
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const float xc = x[j] - mc[j];
-                p0 = fmaf(ua[j], xc, p0);
-                p1 = fmaf(ub[j], xc, p1);
-                b = fmaf(fabsf(ua[j]) + fabsf(ub[j]), fabsf(xc), b);
+                    for (int j = 0; j < 4; j++) x[h][i][j] = (on && c0 + j < d) ? __ldg(xr + c0 + j) : 0.0f;
+                }
             }
         }
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
-            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (on && sub == 0) {
-            uint32_t kk = (1u << (2 * kMortonBits)) - 1;  // non-finite rows sort last
-            if (isfinite(p0) && isfinite(p1) && isfinite(b)) {
-                const float lim = static_cast<float>((1 << kMortonBits) - 1);
-                const uint32_t q0 = static_cast<uint32_t>(fminf(fmaxf((p0 - lo0) * inv0, 0.0f), lim));
-                const uint32_t q1 = static_cast<uint32_t>(fminf(fmaxf((p1 - lo1) * inv1, 0.0f), lim));
-                kk = spread_bits(q0) | (spread_bits(q1) << 1);
-                bm = fmaxf(bm, b);
-            } else {
-                // rows whose projections overflow fp32 are left in every box's
-                // way (NaN boxes keep every tile); truly non-finite rows match nothing
-                p0 = p1 = __int_as_float(0x7fc00000);
+        for (int h = 0; h < RPG; h++) {
+            const int64_t row = r0 + 4 * h + grp;
+            const bool on = row < n;
+            float p0 = 0.0f, p1 = 0.0f, b = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NV; i++) {
+                const float4 w0 = us[0][8 * i + sub], w1 = us[1][8 * i + sub], mm = us[2][8 * i + sub];
+                const float ua[4] = {w0.x, w0.y, w0.z, w0.w}, ub[4] = {w1.x, w1.y, w1.z, w1.w};
+                const float mc[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float xc = x[h][i][j] - mc[j];
+                    p0 = fmaf(ua[j], xc, p0);
+                    p1 = fmaf(ub[j], xc, p1);
+                    b = fmaf(fabsf(ua[j]) + fabsf(ub[j]), fabsf(xc), b);
+                }
             }
-            proj[row] = make_float2(p0, p1);
-            key[row] = kk;
-            val[row] = static_cast<int32_t>(row);
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+                p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+            }
+            if (on && sub == 0) {
+                uint32_t kk = (1u << (2 * kMortonBits)) - 1;  // non-finite rows sort last
+                if (isfinite(p0) && isfinite(p1) && isfinite(b)) {
+                    const float lim = static_cast<float>((1 << kMortonBits) - 1);
+                    const uint32_t q0 = static_cast<uint32_t>(fminf(fmaxf((p0 - lo0) * inv0, 0.0f), lim));
+                    const uint32_t q1 = static_cast<uint32_t>(fminf(fmaxf((p1 - lo1) * inv1, 0.0f), lim));
+                    kk = spread_bits(q0) | (spread_bits(q1) << 1);
+                    bm = fmaxf(bm, b);
+                } else {
+                    // rows whose projections overflow fp32 are left in every box's
+                    // way (NaN boxes keep every tile); truly non-finite rows match nothing
+                    p0 = p1 = __int_as_float(0x7fc00000);
+                }
+                proj[row] = make_float2(p0, p1);
+                key[row] = kk;
+                val[row] = static_cast<int32_t>(row);
+            }
         }
     }
 #pragma unroll
@@ -2811,7 +2825,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
                                                                                       : k_band_keys<4>;
             const unsigned gk = static_cast<unsigned>(
-                std::min<int64_t>(ceil_div(n, 32), int64_t{ctx.sm_count} * 16));
+                std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
             launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
                        proj, k_in, v_in,
                        P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
