@@ -1634,7 +1634,7 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> 
 // projections, the Morton sort key, and b max-reduced per block (one
 // atomicMax per block).  Block 0 also zeroes the counting sort's bins.
 template <int NV>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 2)
 k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
             BandInfo* __restrict__ info, float2* __restrict__ proj, uint32_t* __restrict__ key,
             int32_t* __restrict__ val, int32_t* __restrict__ zero_bins) {
