@@ -2592,9 +2592,12 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         launches++;
         read_counters();
         p.unit_step = 1;
-        const double scale = static_cast<double>(kSampleStep) * 1.3;
-        cap = std::max(cap, static_cast<unsigned long long>(h_cnt[0] * scale) + (1 << 20));
-        out_need = std::max(out_need, static_cast<unsigned long long>(h_cnt[3] * scale) + (1 << 20));
+        // Generous margins: the per-unit output of clustered data is heavily
+        // skewed, so the 1/64 sample is a noisy estimate, and a miss costs a
+        // second full screen (records) or re-check (pairs).  16 B per record,
+        // 12 B per pair: a 4x record margin on config 5 is ~13 GB of 180.
+        cap = std::max(cap, static_cast<unsigned long long>(h_cnt[0] * kSampleStep * 4.0) + (1 << 20));
+        out_need = std::max(out_need, static_cast<unsigned long long>(h_cnt[3] * kSampleStep * 2.0) + (1 << 20));
     }
     // (the sampled pass, when taken, counts as preparation in the phase times)
     tm.mark(1);
