@@ -2539,7 +2539,37 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         d_pin = nullptr;
     }
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
-    DevBuf<int4> recs;
+    // Candidate records live in a per-thread, per-device buffer that only
+    // grows (plain cudaMalloc: usable from any stream): a multi-GB record
+    // buffer is mapped once, not on every call.
+    struct RecCache {
+        int4* p = nullptr;
+        unsigned long long cap = 0;
+    };
+    thread_local RecCache rec_cache[64];
+    int dev_id = 0;
+    PDB_CUDA(cudaGetDevice(&dev_id));
+    RecCache& rcache = rec_cache[dev_id & 63];
+    struct {
+        int4* p = nullptr;
+    } recs;
+    auto recs_reset = [&](unsigned long long need) {
+        if (rcache.cap < need) {
+            PDB_CUDA(cudaStreamSynchronize(s));
+            if (rcache.p) PDB_CUDA(cudaFree(rcache.p));
+            rcache.p = nullptr;
+            rcache.cap = 0;
+            void* q = nullptr;
+            const cudaError_t e = cudaMalloc(&q, static_cast<size_t>(need) * sizeof(int4));
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                fail(PDB_ERR_OUT_OF_MEMORY, "cannot allocate the candidate record buffer");
+            }
+            rcache.p = static_cast<int4*>(q);
+            rcache.cap = need;
+        }
+        recs.p = rcache.p;
+    };
     int passes = 0;
     auto ensure_out = [&](unsigned long long need) {
         if (static_cast<unsigned long long>(out->capacity) >= need && out->left) return;
@@ -2584,8 +2614,12 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         PDB_CUDA(cudaMemcpyAsync(&units, p.dev_n_units, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
     }
-    if (units >= kSampleStep * ctx.sm_count) {
-        recs.reset(cap, s);
+    // Short joins chain the re-check to the screen with programmatic
+    // dependent launch; for long ones (config 5: 0.16 s screen) the early-
+    // resident re-check CTAs measured ~20 % slower than a plain launch.
+    const bool small = units < kSampleStep * ctx.sm_count;
+    if (!small) {
+        recs_reset(cap);
         arm();
         p.unit_step = kSampleStep;
         dispatch_screen(DP, mode, ctx, tA, tB, tG, p, s);
@@ -2594,10 +2628,17 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         p.unit_step = 1;
         // Generous margins: the per-unit output of clustered data is heavily
         // skewed, so the 1/64 sample is a noisy estimate, and a miss costs a
-        // second full screen (records) or re-check (pairs).  16 B per record,
-        // 12 B per pair: a 4x record margin on config 5 is ~13 GB of 180.
-        cap = std::max(cap, static_cast<unsigned long long>(h_cnt[0] * kSampleStep * 4.0) + (1 << 20));
-        out_need = std::max(out_need, static_cast<unsigned long long>(h_cnt[3] * kSampleStep * 2.0) + (1 << 20));
+        // second full screen (records) or re-check (pairs).
+        // Sizes snap to a 2^(1/4) grid so that repeated calls with slightly
+        // different estimates reuse the stream-ordered pool's blocks instead
+        // of mapping new multi-GB ones.
+        auto snap = [](double x) {
+            double v = 1 << 20;
+            while (v < x) v *= 1.189207115002721;  // 2^(1/4)
+            return static_cast<unsigned long long>(v);
+        };
+        cap = std::max(cap, snap(h_cnt[0] * kSampleStep * 2.0));
+        out_need = std::max(out_need, snap(h_cnt[3] * kSampleStep * 1.5));
     }
     // (the sampled pass, when taken, counts as preparation in the phase times)
     tm.mark(1);
@@ -2605,7 +2646,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     // once.  A record overflow re-runs the screen with the exact record
     // count; an output overflow re-runs only the re-check.
     for (int attempt = 0; attempt < 2; attempt++) {
-        recs.reset(cap, s);
+        recs_reset(cap);
         ensure_out(out_need);
         arm();
         if (p.n_units > 0) {
@@ -2613,7 +2654,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
             launches++;
         }
         tm.mark(2);
-        recheck(recs.p, counters.p, cap, out);
+        recheck(recs.p, counters.p, cap, out, small);
         launches++;
         tm.mark(3);
         passes++;
@@ -2625,7 +2666,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
         ensure_out(h_cnt[2]);
         PDB_CUDA(cudaMemsetAsync(counters.p + 2, 0, sizeof(unsigned long long), s));
-        recheck(recs.p, counters.p, cap, out);
+        recheck(recs.p, counters.p, cap, out, small);
         launches++;
         tm.mark(3);
         read_counters();
@@ -2971,8 +3012,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2) {
-                           launch_pdl(k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
+                           launch_pdl_if(pdl, k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2, static_cast<const int32_t*>(permL),
@@ -3068,8 +3109,8 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, tB, p, nL, nR, o, out, stats, tm, launches,
                        counters,
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2) {
-                           launch_pdl(k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
+                           launch_pdl_if(pdl, k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, min_cos, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2);

@@ -22,7 +22,8 @@ Rd = Ld if R is None else torch.from_numpy(R).cuda()
 lib = capi.lib()
 stream = torch.cuda.current_stream()
 opts = capi.JoinOpts()
-opts.flags = capi.PDB_JOIN_SELF if cfg["self_join"] else 0
+opts.flags = (capi.PDB_JOIN_SELF if cfg["self_join"] else 0) | \
+    (capi.PDB_JOIN_PHASE_TIMES if "--phase" in sys.argv else 0)
 opts.stream = C.c_void_p(stream.cuda_stream)
 pairs = patchdb.DevicePairs()
 
@@ -49,4 +50,5 @@ for e in evs:
     s, t = e.time_range.start, e.time_range.end
     print(f"{s - t0:10.1f} us  gap {s - prev:8.1f}  dur {t - s:9.1f}  {e.name[:80]}")
     prev = t
-print("tiles", pairs.stats.tiles, "pairs", pairs.count, "candidates", pairs.stats.candidates)
+print("tiles", pairs.stats.tiles, "pairs", pairs.count, "candidates", pairs.stats.candidates,
+      "ms", pairs.stats.prep_ms, pairs.stats.screen_ms, pairs.stats.recheck_ms)
