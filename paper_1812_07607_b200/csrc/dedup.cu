@@ -41,11 +41,17 @@ __global__ void k_graph_keys(const int32_t* __restrict__ left, const int32_t* __
                   static_cast<uint32_t>(left[k]);
 }
 
-// off[i] = first key with upper word >= i (keys sorted), i = 0..n.
+// off[i] = first key with upper word >= i (keys sorted), i = 0..n; also
+// clears the item statuses and the round / representative counters.
 __global__ void k_csr_offsets(const unsigned long long* __restrict__ keys, int64_t m, int64_t n,
-                              int64_t* __restrict__ off) {
+                              int64_t* __restrict__ off, uint8_t* __restrict__ status,
+                              unsigned long long* __restrict__ cnt) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (blockIdx.x == 0 && threadIdx.x < 3) cnt[threadIdx.x] = 0;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < n) status[i] = 0;
         const unsigned long long t = static_cast<unsigned long long>(i) << 32;
         int64_t lo = 0, hi = m;
         while (lo < hi) {
@@ -60,9 +66,16 @@ __global__ void k_csr_offsets(const unsigned long long* __restrict__ keys, int64
 constexpr uint8_t kUndecided = 0, kRep = 1, kMember = 2;
 
 // One round of the greedy scan over the still undecided items.
+// Round counters are double-buffered: a round counts into cnt[r & 1] and
+// clears cnt[(r + 1) & 1] for the next one (the previous round, which used
+// it, has completed), so rounds chain without host memsets.
 __global__ void k_dedup_round(const unsigned long long* __restrict__ keys,
                               const int64_t* __restrict__ off, int64_t n,
-                              uint8_t* status, unsigned int* undecided) {
+                              uint8_t* status, unsigned long long* cnt, int r) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    unsigned int* undecided = reinterpret_cast<unsigned int*>(cnt + (r & 1));
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(r + 1) & 1] = 0;
     unsigned int left = 0;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -94,6 +107,8 @@ __global__ void k_dedup_attach(const unsigned long long* __restrict__ keys,
                                const uint8_t* __restrict__ status, const float* __restrict__ X,
                                int d, int64_t* __restrict__ rep_of,
                                unsigned long long* __restrict__ n_reps) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const bool vec8 = (d % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 32 == 0);
     unsigned int reps = 0;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -155,13 +170,12 @@ void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStrea
         DevBuf<uint8_t> tmp(tmp_bytes, s);
         PDB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, k_in.p, keys.p, m, 0, 32 + bits, s));
     }
-    k_csr_offsets<<<grid, 256, 0, s>>>(keys.p, m, n, off.p);
-    PDB_CUDA(cudaGetLastError());
-
     // 3. greedy rounds until every item is decided
     DevBuf<uint8_t> status(static_cast<size_t>(n), s);
-    DevBuf<unsigned long long> cnt(2, s);
-    PDB_CUDA(cudaMemsetAsync(status.p, 0, static_cast<size_t>(n), s));
+    DevBuf<unsigned long long> cnt(3, s);  // [0], [1] round counters, [2] representatives
+    launch_pdl(k_csr_offsets, dim3(grid), dim3(256), 0, s, static_cast<const unsigned long long*>(keys.p),
+               m, n, off.p, status.p, cnt.p);
+    PDB_CUDA(cudaGetLastError());
     thread_local unsigned long long* h_cnt = [] {
         void* q = nullptr;
         if (cudaHostAlloc(&q, 16, cudaHostAllocDefault) != cudaSuccess) {
@@ -172,24 +186,27 @@ void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStrea
     }();
     unsigned long long local[2];
     unsigned long long* hc = h_cnt ? h_cnt : local;
-    for (int round = 0;; round++) {
+    int r = 0;
+    for (int check = 0;; check++) {
         // a few rounds per host check: most items settle in the first two
-        for (int r = 0; r < 4; r++) {
-            PDB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
-            k_dedup_round<<<grid, 256, 0, s>>>(keys.p, off.p, n, status.p,
-                                               reinterpret_cast<unsigned int*>(cnt.p));
-        }
-        PDB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        for (int k = 0; k < 4; k++, r++)
+            launch_pdl(k_dedup_round, dim3(grid), dim3(256), 0, s,
+                       static_cast<const unsigned long long*>(keys.p),
+                       static_cast<const int64_t*>(off.p), n, status.p, cnt.p, r);
+        // the last round's count (it cleared the other counter)
+        PDB_CUDA(cudaMemcpyAsync(hc, cnt.p + ((r - 1) & 1), sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
         if (static_cast<unsigned int>(hc[0]) == 0) break;
-        if (round > n) fail(PDB_ERR_CUDA, "dedup rounds did not converge");  // unreachable
+        if (check > n) fail(PDB_ERR_CUDA, "dedup rounds did not converge");  // unreachable
     }
 
     // 4. attach members to their nearest representative
-    PDB_CUDA(cudaMemsetAsync(cnt.p + 1, 0, sizeof(unsigned long long), s));
-    k_dedup_attach<<<grid, 256, 0, s>>>(keys.p, off.p, n, status.p, d_X, d, d_rep_of, cnt.p + 1);
+    launch_pdl(k_dedup_attach, dim3(grid), dim3(256), 0, s, static_cast<const unsigned long long*>(keys.p),
+               static_cast<const int64_t*>(off.p), n, static_cast<const uint8_t*>(status.p), d_X, d,
+               d_rep_of, cnt.p + 2);
     PDB_CUDA(cudaGetLastError());
-    PDB_CUDA(cudaMemcpyAsync(hc + 1, cnt.p + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PDB_CUDA(cudaMemcpyAsync(hc + 1, cnt.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     PDB_CUDA(cudaStreamSynchronize(s));
     *n_reps = static_cast<int64_t>(hc[1]);
 }
