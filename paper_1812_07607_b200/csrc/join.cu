@@ -2855,11 +2855,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
                    static_cast<const float*>(part), E, sum);
         const int eig_smem = d * d * 4;
-        static bool eig_attr = false;
-        if (!eig_attr) {
-            set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
-            eig_attr = true;
-        }
+        // (set_max_smem caches per function and device)
+        set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
         launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
                    static_cast<const float*>(mu), info);
         launches += 3;
