@@ -133,7 +133,7 @@ int pdb_color_histogram_f32_dev(const float* d_patches, int64_t n, int32_t h, in
 #define PDB_JOIN_TF32 4u   /* screen on tf32 copies (tighter candidate band) instead of bf16;
                               the result is identical either way */
 #define PDB_JOIN_DENSE 16u  /* screen every tile: no band plan.  By default, joins with
-                               d <= 128, >= 8192 rows per side and >= 16384 dense tiles in
+                               d <= 128, >= 8192 rows per side and >= 16384 dense tiles (32768 when sharded) in
                                this shard first sort the rows
                                by two principal projections and skip the 128x256 tiles whose
                                projected bounding boxes are further apart than tau (an exact

@@ -2778,7 +2778,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         }
         // units <= total / ch + n_slots with ch = clamp(total / units_target, 1, 64)
         units_cap = 2 * static_cast<int64_t>(units_target) + list_cap / 64 + n_slots + 1;
-        if (band_env != 1 && list_cap < kBandMinTiles) band = false;  // too little screen to save
+        // too little screen to save (sharded joins also pay a stable radix sort)
+        if (band_env != 1 && list_cap < kBandMinTiles * (P > 1 ? 2 : 1)) band = false;
         // tile-list positions travel as int32 (unit_info, Unit): beyond 2^31
         // dense tiles per shard (> ~11.8 M rows self-joined on one GPU) the
         // join keeps the dense plan
