@@ -251,13 +251,43 @@ def run_ours(args, rank, world, local_rank):
     opts.shard_index, opts.shard_count = rank, world
     opts.stream = sptr
 
+    # Sharded steps fuse the feature all-gather into K1 (P2P stores into every
+    # rank's matrix over NVLink, shard.PeerFeatures); PDB_P2P_FEATURES=0 keeps
+    # the NCCL all-gather.
+    p2p = None
+    if world > 1 and os.environ.get("PDB_P2P_FEATURES", "1") != "0":
+        from paper_1812_07607_b200 import shard
+        try:
+            p2p = shard.PeerFeatures(feats)
+        except Exception as e:  # no IPC between these processes: NCCL path
+            if rank == 0:
+                print(f"P2P feature exchange unavailable ({e}); using all_gather", file=sys.stderr)
+            p2p = None
+    out_ptrs = None
+    if p2p is not None:
+        ptrs = p2p.ptrs(f0 * tpf * D)
+        out_ptrs = (C.c_void_p * len(ptrs))(*ptrs)
+    barrier_t = torch.zeros(1, dtype=torch.int32, device=dev)
+
     def featurize():
-        rc = lib.pdb_featurize_tiles_dev(d_frames.data_ptr(), nf, H, W, th, tw, B, mode,
-                                         my_feats.data_ptr(), sptr)
+        if p2p is not None:
+            rc = lib.pdb_featurize_tiles_dev_multi(d_frames.data_ptr(), nf, H, W, th, tw, B, mode,
+                                                   out_ptrs, len(out_ptrs), sptr)
+        else:
+            rc = lib.pdb_featurize_tiles_dev(d_frames.data_ptr(), nf, H, W, th, tw, B, mode,
+                                             my_feats.data_ptr(), sptr)
         assert rc == 0, capi.last_error()
 
     def gather():
-        if world > 1:
+        if world > 1 and p2p is not None:
+            # every rank's K1 has stored into our matrix once all have passed
+            # this point (K1 ends with a system-scope fence)
+            if dist.get_backend() == "nccl":
+                dist.all_reduce(barrier_t)
+            else:
+                torch.cuda.current_stream(dev).synchronize()
+                dist.barrier()
+        elif world > 1:
             if dist.get_backend() == "nccl":
                 dist.all_gather_into_tensor(feats, my_feats)
             else:  # gloo (multi-rank smoke on one GPU): list all-gather
@@ -474,7 +504,10 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "u8 hist / bf16 screen / f64 exact", "data": "synthetic",
             "config": {"workload": WORKLOAD, "frames": F, "tiles": n_tiles, "d": D, "tau": tau,
                        "candidate_pairs": pairs_cand, "l2": "flushed (256 MB write) before each step",
-                       "parallelism": f"frames sharded x{world}, features all-gathered, join row-blocks cyclic x{world}"},
+                       "parallelism": f"frames sharded x{world}, "
+                       + ("features P2P-stored by K1 into every rank's matrix (fused all-gather)"
+                          if p2p is not None else "features all-gathered")
+                       + f", join row-blocks cyclic x{world}"},
             "join_gpairs_per_s": pairs_cand / (ms_join * 1e-3) / 1e9,
             "featurize_frames_per_s": F / (ms_feat * 1e-3),
             "phase_ms": {"featurize": ms_feat, "gather": ms_gather,

@@ -70,6 +70,17 @@ int pdb_device_count(void);
 #define PDB_HIST_PER_CHANNEL 0
 #define PDB_HIST_JOINT 1
 
+/* pdb_featurize_tiles_dev with every tile's features written to n_outs
+ * (1..8) device buffers at the same offset: the local one first, then
+ * peers' buffers mapped over NVLink (CUDA IPC).  This fuses a sharded
+ * step's feature all-gather into K1: each rank featurizes its frame range
+ * straight into every rank's feature matrix with P2P stores that overlap
+ * the counting, then one on-stream barrier replaces the collective.  Shapes
+ * without the multi-output kernel copy the local slice to the peers. */
+int pdb_featurize_tiles_dev_multi(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W,
+                                  int32_t tile_h, int32_t tile_w, int32_t bins, int32_t mode,
+                                  float* const* d_outs, int32_t n_outs, void* stream);
+
 /* Feature dimension D for (bins, mode), or -1 if the pair is invalid. */
 int pdb_hist_dim(int32_t bins, int32_t mode);
 

@@ -48,7 +48,7 @@ EXPORTS = (
     "pdb_featurize_join", "pdb_host_alloc", "pdb_host_free",
     "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
     "pdb_store_open", "pdb_store_close", "pdb_store_describe", "pdb_store_read",
-    "pdb_store_featurize", "pdb_rows_within",
+    "pdb_store_featurize", "pdb_rows_within", "pdb_featurize_tiles_dev_multi",
 )
 
 
@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
         L.pdb_store_featurize.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, C.POINTER(i64),
                                           i32, vp]
         L.pdb_rows_within.argtypes = [vp, vp, i64, i32, f64, vp]
+        L.pdb_featurize_tiles_dev_multi.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, vp, i32,
+                                                    vp]
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

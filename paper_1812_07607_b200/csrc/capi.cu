@@ -235,6 +235,23 @@ PDB_API int pdb_featurize_tiles_dev(const uint8_t* d_frames, int64_t n, int32_t 
     });
 }
 
+PDB_API int pdb_featurize_tiles_dev_multi(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W,
+                                          int32_t th, int32_t tw, int32_t bins, int32_t mode,
+                                          float* const* d_outs, int32_t n_outs, void* stream) {
+    return guarded([&] {
+        if (!d_outs || n_outs < 1 || n_outs > kMaxFeatOuts)
+            fail(PDB_ERR_INVALID_ARGUMENT, "n_outs must be 1..8 output pointers");
+        for (int k = 0; k < n_outs; k++)
+            if (!d_outs[k]) fail(PDB_ERR_INVALID_ARGUMENT, "null output pointer");
+        check_featurize_args(d_frames, n, H, W, th, tw, bins, mode, d_outs[0]);
+        device_ctx();
+        FeatOuts o{};
+        for (int k = 0; k < n_outs; k++) o.p[k] = d_outs[k];
+        o.n = n_outs;
+        launch_featurize_tiles_multi(d_frames, n, H, W, th, tw, bins, mode, o, stream_of(stream));
+    });
+}
+
 PDB_API int pdb_featurize_tiles(const uint8_t* frames, int64_t n, int32_t H, int32_t W,
                                 int32_t th, int32_t tw, int32_t bins, int32_t mode, float* out) {
     return guarded([&] {

@@ -319,7 +319,7 @@ __device__ __forceinline__ uint32_t pix_offset(uint32_t p) {
 template <int LB, int S>
 __global__ void __launch_bounds__(17 * 32, 1)
 k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty, int H, int th,
-                   int tw, int ntx, uint32_t stage_bytes, float npix, float* __restrict__ out) {
+                   int tw, int ntx, uint32_t stage_bytes, float npix, const FeatOuts outs) {
     constexpr int NB = 1 << (3 * LB);
     constexpr int B = 1 << LB;
     constexpr int NWD = PixMap<LB>::kWords;        // counter words per lane
@@ -430,10 +430,18 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
         }
         __syncwarp();
         const int f = tr / nty, ty = tr - f * nty;
-        float* o = out + ((static_cast<int64_t>(f) * nty + ty) * ntx + warp) * NB;
-        if (lane < NB) o[lane] = normalise(mine0, npix);
-        if (NB > 32) o[lane + 32] = normalise(mine1, npix);
+        const int64_t ofs = ((static_cast<int64_t>(f) * nty + ty) * ntx + warp) * NB;
+        const float v0 = normalise(mine0, npix), v1 = normalise(mine1, npix);
+        // every output: the local features and, for a sharded step, each
+        // peer's copy over NVLink (P2P stores overlapping the counting)
+        for (int k = 0; k < outs.n; k++) {
+            float* o = outs.p[k] + ofs;
+            if (lane < NB) o[lane] = v0;
+            if (NB > 32) o[lane + 32] = v1;
+        }
     }
+    // peer stores become visible before anything the host orders after us
+    if (outs.n > 1) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -584,6 +592,16 @@ int hist_dim(int32_t bins, int32_t mode) {
 void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H, int32_t W,
                             int32_t th, int32_t tw, int32_t bins, int32_t mode, float* d_out,
                             cudaStream_t s) {
+    FeatOuts one{};
+    one.p[0] = d_out;
+    one.n = 1;
+    launch_featurize_tiles_multi(d_frames, n_frames, H, W, th, tw, bins, mode, one, s);
+}
+
+void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int32_t H, int32_t W,
+                                  int32_t th, int32_t tw, int32_t bins, int32_t mode,
+                                  const FeatOuts& outs, cudaStream_t s) {
+    float* d_out = outs.p[0];
     const int D = hist_dim(bins, mode);
     const int ntx = W / tw, nty = H / th;
     const int tpf = ntx * nty;
@@ -642,7 +660,9 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
         const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * ctx.sm_count;
         const dim3 g(static_cast<unsigned>(std::min(n_rows, cap)));
         kern<<<g, threads, smem, s>>>(m, static_cast<int>(n_rows), nty, H, th, tw, ntx,
-                                      static_cast<uint32_t>(row_smem), npix_h, d_out);
+                                      static_cast<uint32_t>(row_smem), npix_h, outs);
+        PDB_CUDA(cudaGetLastError());
+        return;  // every output written by the kernel
     } else if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {
         const int lb = bins == 4 ? 2 : 1;
         // 32-bit lane-private counters, 4 warps per CTA, one batch of
@@ -688,6 +708,11 @@ void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H
         }
     }
     PDB_CUDA(cudaGetLastError());
+    // kernels without multi-output stores: copy the local features to the
+    // peers (copy engines over NVLink)
+    for (int k = 1; k < outs.n; k++)
+        PDB_CUDA(cudaMemcpyAsync(outs.p[k], d_out, static_cast<size_t>(n_tiles) * D * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
 }
 
 void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t w, int32_t bins,

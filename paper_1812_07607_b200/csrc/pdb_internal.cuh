@@ -124,6 +124,16 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 }
 
 // ---- K1 launchers (histogram.cu) -----------------------------------------
+// Feature outputs of one featurization: the local buffer first, then (a
+// sharded step) peers' buffers mapped over NVLink, all at the same offset.
+constexpr int kMaxFeatOuts = 8;
+struct FeatOuts {
+    float* p[kMaxFeatOuts];
+    int n;
+};
+PDB_HIDDEN void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int32_t H,
+                                             int32_t W, int32_t th, int32_t tw, int32_t bins,
+                                             int32_t mode, const FeatOuts& outs, cudaStream_t s);
 PDB_HIDDEN int hist_dim(int32_t bins, int32_t mode);
 PDB_HIDDEN void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H,
                                        int32_t W, int32_t th, int32_t tw, int32_t bins,

@@ -4,9 +4,12 @@ torch.distributed over NCCL on the box, gloo in the CPU tests).
 The reference is single-threaded with no distributed backend (SPEC.md:495,
 565); the sharding here is the B200 build's own:
 
-* featurization: frames are independent -> contiguous frame ranges per rank,
-  no exchange; the features are then all-gathered (config 2: 64,000 x 64 x 4
-  = 16 MB) because every rank joins against all of them;
+* featurization: frames are independent -> contiguous frame ranges per rank;
+  every rank joins against all the features (config 2: 64,000 x 64 x 4 =
+  16 MB).  With PeerFeatures the exchange is fused into K1: each rank maps
+  every rank's feature matrix over CUDA IPC and writes its slice into all of
+  them with P2P stores over NVLink while it counts, so one on-stream barrier
+  replaces the all-gather (all_gather_rows is the NCCL fallback);
 * join: the 128-row blocks of L in boustrophedon rounds -- block
   k*world + (rank if k even else world-1-rank) (pdb_join_opts
   shard_index/shard_count) -- which balances the triangular self-join and
@@ -44,6 +47,37 @@ def selfjoin_tiles(rank: int, world: int, n_rows: int, bn: int = 256) -> int:
     """Screen tiles rank executes in a self-join (upper triangle by 256-col tiles)."""
     nt = (n_rows + bn - 1) // bn
     return int(sum(nt - (b >> 1) for b in row_blocks(rank, world, n_rows)))
+
+
+class PeerFeatures:
+    """Every rank's feature matrix mapped into this process (CUDA IPC), for
+    pdb_featurize_tiles_dev_multi: `ptrs(offset_elems)` lists the local
+    buffer first, then each peer's, all shifted by `offset_elems` floats.
+    The mapped storages stay referenced for the object's lifetime."""
+
+    def __init__(self, feats, group=None):
+        import torch.distributed as dist
+        import torch
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.elem = feats.element_size()
+        mine = (feats.untyped_storage()._share_cuda_(), feats.storage_offset())
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._keep = []
+        self._base = []
+        for r, (h, off) in enumerate(allh):
+            if r == self.rank:
+                self._base.append(feats.data_ptr())
+                continue
+            st = torch.UntypedStorage._new_shared_cuda(*h)
+            self._keep.append(st)
+            self._base.append(st.data_ptr() + off * self.elem)
+        # local first
+        self._order = [self.rank] + [r for r in range(self.world) if r != self.rank]
+
+    def ptrs(self, offset_elems: int):
+        return [self._base[r] + offset_elems * self.elem for r in self._order]
 
 
 def all_gather_rows(local, world: int, group=None):

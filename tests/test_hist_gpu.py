@@ -158,3 +158,31 @@ def test_store_featurize_matches_featurizing_the_decoded_frames(name):
         part = st.featurize(th, tw, bins, mode, rng=(3, 13)).cpu().numpy()
         want_p = oracle.featurize_tiles(fr[3:13], th, tw, bins, 1 if mode == "joint" else 0)
         assert np.array_equal(_bits(part), _bits(want_p))
+
+
+@pytest.mark.parametrize("shape", [(60, 80, 4, 1), (16, 16, 4, 1), (60, 80, 8, 0)])
+def test_featurize_multi_output_writes_every_buffer(shape):
+    """pdb_featurize_tiles_dev_multi (the fused feature all-gather): every
+    output buffer holds the single-output features, at the given offset --
+    the TMA kernel's multi-output stores (60x80 joint B=4) and the
+    copy-to-peers fallback (other shapes)."""
+    import ctypes as C
+    import torch
+    from paper_1812_07607_b200 import _capi as capi
+    th, tw, bins, mode = shape
+    fr, _ = workloads.frames(12, 480, 640, seed=9)
+    d_fr = torch.from_numpy(fr).cuda()
+    D = capi.lib().pdb_hist_dim(bins, mode)
+    n = 12 * (480 // th) * (640 // tw)
+    want = patchdb.featurize_tiles(fr, th, tw, bins, "joint" if mode else "per_channel")
+    bufs = [torch.full((n + 7, D), -1.0, device="cuda") for _ in range(3)]
+    ptrs = (C.c_void_p * 3)(*[b.data_ptr() + 7 * D * 4 for b in bufs])
+    s = torch.cuda.current_stream()
+    rc = capi.lib().pdb_featurize_tiles_dev_multi(d_fr.data_ptr(), 12, 480, 640, th, tw, bins, mode,
+                                                  ptrs, 3, C.c_void_p(s.cuda_stream))
+    assert rc == 0, capi.last_error()
+    torch.cuda.synchronize()
+    for b in bufs:
+        got = b[7:].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.reshape(n, D).view(np.uint32))
+        assert (b[:7].cpu().numpy() == -1.0).all()
