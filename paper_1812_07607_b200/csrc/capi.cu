@@ -449,32 +449,39 @@ PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int3
         DevBuf<uint8_t> dF(static_cast<size_t>(n) * fb, s);
         DevBuf<float> dX(static_cast<size_t>(std::max<int64_t>(nt, 1)) * D, s);
         // Copy frames in chunks on a second stream so K1 on chunk k overlaps
-        // the H2D copy of chunk k+1.
-        cudaStream_t cs;
-        PDB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        // the H2D copy of chunk k+1.  The copy stream and the chunk events
+        // are created once per host thread and device (creating a stream
+        // measured ~1 ms per call).
+        struct CopyCtx {
+            cudaStream_t cs = nullptr;
+            std::vector<cudaEvent_t> evs;
+        };
+        thread_local CopyCtx copy_ctx[64];
+        int dev = 0;
+        PDB_CUDA(cudaGetDevice(&dev));
+        CopyCtx& cc = copy_ctx[dev & 63];
+        if (!cc.cs) PDB_CUDA(cudaStreamCreateWithFlags(&cc.cs, cudaStreamNonBlocking));
+        cudaStream_t cs = cc.cs;
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 64));
-        std::vector<cudaEvent_t> evs;
-        const int64_t tpf = static_cast<int64_t>(W / tw) * (H / th);
-        try {
-            for (int64_t f0 = 0; f0 < n; f0 += chunk) {
-                const int64_t cnt = std::min(chunk, n - f0);
-                cudaEvent_t e;
-                PDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                evs.push_back(e);
-                PDB_CUDA(cudaMemcpyAsync(dF.p + f0 * fb, frames + f0 * fb, cnt * fb,
-                                         cudaMemcpyHostToDevice, cs));
-                PDB_CUDA(cudaEventRecord(e, cs));
-                PDB_CUDA(cudaStreamWaitEvent(s, e, 0));
-                launch_featurize_tiles(dF.p + f0 * fb, cnt, H, W, th, tw, bins, mode,
-                                       dX.p + f0 * tpf * D, s);
-            }
-        } catch (...) {
-            for (auto e : evs) cudaEventDestroy(e);
-            cudaStreamDestroy(cs);
-            throw;
+        const int64_t n_chunks = ceil_div(n, chunk);
+        while (static_cast<int64_t>(cc.evs.size()) < n_chunks) {
+            cudaEvent_t e;
+            PDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            cc.evs.push_back(e);
         }
-        for (auto e : evs) cudaEventDestroy(e);
-        cudaStreamDestroy(cs);
+        // the copy stream must not overwrite frames a previous call's K1 still reads
+        PDB_CUDA(cudaStreamSynchronize(s));
+        const int64_t tpf = static_cast<int64_t>(W / tw) * (H / th);
+        for (int64_t f0 = 0, k = 0; f0 < n; f0 += chunk, k++) {
+            const int64_t cnt = std::min(chunk, n - f0);
+            cudaEvent_t e = cc.evs[static_cast<size_t>(k)];
+            PDB_CUDA(cudaMemcpyAsync(dF.p + f0 * fb, frames + f0 * fb, cnt * fb,
+                                     cudaMemcpyHostToDevice, cs));
+            PDB_CUDA(cudaEventRecord(e, cs));
+            PDB_CUDA(cudaStreamWaitEvent(s, e, 0));
+            launch_featurize_tiles(dF.p + f0 * fb, cnt, H, W, th, tw, bins, mode,
+                                   dX.p + f0 * tpf * D, s);
+        }
         pdb_join_opts o = opts ? *opts : pdb_join_opts{};
         o.flags |= PDB_JOIN_SELF;
         o.stream = s;
