@@ -415,19 +415,25 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
         __syncwarp();
         // sum bytes 0,2 and 1,3 of every counter word over lanes in 16-bit
         // halves; lane l keeps the totals of bins l and l+32.
-        uint32_t mine0 = 0, mine1 = 0;
+        // Lane 0 parks the two half-sums of word wd in counter words 2wd and
+        // 2wd+1 (already read by every lane: the warp reads word wd before
+        // any store of iteration wd), then each lane fetches its two bins.
 #pragma unroll
         for (int wd = 0; wd < NWD; wd++) {
             const uint32_t v = wcnt32[wd * 32 + lane];
             const uint32_t s02 = __reduce_add_sync(0xffffffffu, v & 0x00FF00FFu);
             const uint32_t s13 = __reduce_add_sync(0xffffffffu, (v >> 8) & 0x00FF00FFu);
-            auto pick = [&](uint32_t o) {
-                const uint32_t v2 = (o & 1) ? s13 : s02;
-                return (o & 2) ? v2 >> 16 : v2 & 0xFFFFu;
-            };
-            if ((o0 >> 7) == static_cast<uint32_t>(wd)) mine0 = pick(o0);
-            if ((o1 >> 7) == static_cast<uint32_t>(wd)) mine1 = pick(o1);
+            if (lane == 0) {
+                wcnt32[2 * wd] = s02;
+                wcnt32[2 * wd + 1] = s13;
+            }
         }
+        __syncwarp();
+        auto fetch = [&](uint32_t o) {
+            const uint32_t v2 = wcnt32[2 * (o >> 7) + (o & 1)];
+            return (o & 2) ? v2 >> 16 : v2 & 0xFFFFu;
+        };
+        const uint32_t mine0 = fetch(o0), mine1 = NB > 32 ? fetch(o1) : 0u;
         __syncwarp();
         const int f = tr / nty, ty = tr - f * nty;
         const int64_t ofs = ((static_cast<int64_t>(f) * nty + ty) * ntx + warp) * NB;
