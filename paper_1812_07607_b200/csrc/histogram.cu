@@ -375,8 +375,10 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
     const uint32_t o0 = bin_word(lane & (NB - 1)), o1 = bin_word((lane + 32) & (NB - 1));
     uint32_t it = 0;
     for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
+        // zero the warp's counters with 16-byte stores (any lane may clear
+        // any word: the block belongs to the warp)
 #pragma unroll
-        for (int wd = 0; wd < NWD; wd++) wcnt32[wd * 32 + lane] = 0;
+        for (int k = lane; k < NWD * 8; k += 32) reinterpret_cast<uint4*>(wcnt32)[k] = make_uint4(0, 0, 0, 0);
         __syncwarp();
         for (int bt = 0; bt < nb; bt++, it++) {
             const uint32_t s = it % S;
