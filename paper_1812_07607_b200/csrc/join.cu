@@ -134,6 +134,7 @@ struct ScreenParams {
     const int32_t* dev_ch;         // tiles per unit (device)
     const int4* unit_info;         // decoded units (rb, first, end, slot), one load per unit
     int32_t n_slots;
+    const float* hrow;             // banded: each row's screen threshold h_i (k_band_write)
 };
 
 struct Unit {
@@ -492,8 +493,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             if (w.rb < 0) break;
             const int64_t i = static_cast<int64_t>(w.rb) * BM + row;
             const bool row_ok = i < p.nL;
-            const float hn = row_ok ? __ldg(p.hnL + i) : 0.0f;
-            const float sn = row_ok ? __ldg(p.snL + i) : kFlagNonFinite;
+            const float hn = (row_ok && !p.hrow) ? __ldg(p.hnL + i) : 0.0f;
+            const float sn = (row_ok && !p.hrow) ? __ldg(p.snL + i) : kFlagNonFinite;
             using GV = typename std::conditional<kColsPerWarp == 128, float4, float2>::type;
             GV gnext{};
             if (!AUG)
@@ -502,7 +503,9 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
-            if (COS) {
+            if (p.hrow) {
+                h = row_ok ? __ldg(p.hrow + i) : __int_as_float(0x7f800000);  // precomputed per row
+            } else if (COS) {
                 h = row_ok ? hn : __int_as_float(0x7f800000);  // prep stored h_i itself
             } else if (sn == kFlagNonFinite) {
                 h = __int_as_float(0x7f800000);  // +inf: never a candidate
@@ -2006,7 +2009,9 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
              const float* __restrict__ tmaxS, const float* __restrict__ tmaxN,
              float* __restrict__ smaxS, float* __restrict__ smaxN,
              const int64_t* __restrict__ unit_off, const int32_t* __restrict__ dev_ch,
-             int4* __restrict__ unit_info) {
+             int4* __restrict__ unit_info, const float* __restrict__ hnL,
+             const float* __restrict__ snL, int64_t nL, double tau_p, double uu, double gam,
+             float* __restrict__ hrow) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int k = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
@@ -2038,6 +2043,23 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     if (lane == 0) {
         smaxS[k] = ms;
         smaxN[k] = mn;
+    }
+    // each row's screen threshold, exactly as k_screen's epilogue would
+    // compute it from the slot maxima (one load per unit there instead)
+    for (int64_t i = static_cast<int64_t>(rb) * BM + lane; i < min(nL, static_cast<int64_t>(rb + 1) * BM);
+         i += 32) {
+        const float hn = hnL[i], sn = snL[i];
+        float h;
+        if (sn == kFlagNonFinite) {
+            h = __int_as_float(0x7f800000);
+        } else if (sn == kFlagBig) {
+            h = -__int_as_float(0x7f800000);
+        } else {
+            const double r = tau_p + uu * (static_cast<double>(sn) + ms) + 1e-30;
+            const double T = r * r + gam * (static_cast<double>(hn) + mn);
+            h = __double2float_rd((static_cast<double>(hn) - T) * 0.5);
+        }
+        hrow[i] = h;
     }
     // the slot's work units, decoded once for the screen
     const int ch = *dev_ch;
@@ -2803,7 +2825,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                     Arena::need(nbl, 32) + Arena::need(nt_, 32) + Arena::need(ceil_div(nt_, 32), 32) +
                     Arena::need(n_slots, 4) + 2 * Arena::need(n_slots + 1, 8) + Arena::need(2, 8) +
                     Arena::need(std::max<int64_t>(list_cap, 1), 4) + 2 * Arena::need(n_slots, 4) +
-                    Arena::need(units_cap, 16);
+                    Arena::need(units_cap, 16) + Arena::need(nL, 4);
     Arena ar;
     ar.reserve(Arena::need(DP, 4) + Arena::need(static_cast<size_t>(nL) * DP, es) +
                    2 * Arena::need(nL, 4) +
@@ -2933,6 +2955,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     // ---- band plan, part 2: boxes, surviving tiles, units -----------------
     int32_t* list = nullptr;
     int4* unit_info = nullptr;
+    float* hrow = nullptr;
     int64_t *list_off = nullptr, *unit_off = nullptr, *dev_n_units = nullptr;
     int32_t* dev_ch = nullptr;
     if (band) {
@@ -2945,6 +2968,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         dev_ch = ar.take<int32_t>(1);
         list = ar.take<int32_t>(std::max<int64_t>(list_cap, 1));
         unit_info = ar.take<int4>(units_cap);
+        hrow = ar.take<float>(nL);
         cmaxS = ar.take<float>(n_slots);
         cmaxN = ar.take<float>(n_slots);
         launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))), dim3(256), 0, s,
@@ -2968,7 +2992,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                        static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
                        static_cast<const float*>(tmaxN), cmaxS, cmaxN,
                        static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
-                       unit_info);
+                       unit_info, static_cast<const float*>(hnL), static_cast<const float*>(snL), nL,
+                       tau * (1.0 + 1e-9), tf32 ? kU_tf32 : kU_bf16,
+                       (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow);
         launches += 5;
     } else {
         launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
@@ -3004,6 +3030,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.u = tf32 ? kU_tf32 : kU_bf16;
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
     if (band) {
+        p.hrow = hrow;
         p.unit_info = unit_info;
         p.tile_list = list;
         p.slot_list_off = list_off;
