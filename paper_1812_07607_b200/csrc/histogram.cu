@@ -373,30 +373,43 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
         return pix_offset<LB>((r << (8 - LB)) | (g << (16 - LB)) | (b << (24 - LB)));
     };
     const uint32_t o0 = bin_word(lane & (NB - 1)), o1 = bin_word((lane + 32) & (NB - 1));
-    uint32_t it = 0;
+    // stage ring position, carried across tile rows (the producer's order);
+    // the full-band and last-band group counts are fixed per launch
+    uint32_t s = 0, ph = 0;
+    const int ng_full = RB * segs, ng_last = (th - (nb - 1) * RB) * segs;
+    const uint8_t* my_stage = stages + warp * tile_bytes + lane * 48;
     for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
         // zero the warp's counters with 16-byte stores (any lane may clear
         // any word: the block belongs to the warp)
 #pragma unroll
         for (int k = lane; k < NWD * 8; k += 32) reinterpret_cast<uint4*>(wcnt32)[k] = make_uint4(0, 0, 0, 0);
         __syncwarp();
-        for (int bt = 0; bt < nb; bt++, it++) {
-            const uint32_t s = it % S;
-            ptx::mbar_wait_sleep(&full[s], (it / S) & 1);
-            const int ngroups = min(RB, th - bt * RB) * segs;
-            uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a;
+        for (int bt = 0; bt < nb; bt++) {
+            ptx::mbar_wait_sleep(&full[s], ph);
+            const int ngroups = bt == nb - 1 ? ng_last : ng_full;
+            uint32_t w[12];
             if (lane < ngroups) {
-                const uint4* g = reinterpret_cast<const uint4*>(stages + s * stage_bytes +
-                                                                warp * tile_bytes + lane * 48);
-                a = g[0];
-                b = g[1];
-                c = g[2];
+                const uint4* g = reinterpret_cast<const uint4*>(my_stage + s * stage_bytes);
+                const uint4 a = g[0], b = g[1], c = g[2];
+                w[0] = a.x & kTop;
+                w[1] = a.y & kTop;
+                w[2] = a.z & kTop;
+                w[3] = a.w & kTop;
+                w[4] = b.x & kTop;
+                w[5] = b.y & kTop;
+                w[6] = b.z & kTop;
+                w[7] = b.w & kTop;
+                w[8] = c.x & kTop;
+                w[9] = c.y & kTop;
+                w[10] = c.z & kTop;
+                w[11] = c.w & kTop;
             }
-            const uint32_t w[12] = {a.x & kTop, a.y & kTop, a.z & kTop, a.w & kTop,
-                                    b.x & kTop, b.y & kTop, b.z & kTop, b.w & kTop,
-                                    c.x & kTop, c.y & kTop, c.z & kTop, c.w & kTop};
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
             if (lane < ngroups) {
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
