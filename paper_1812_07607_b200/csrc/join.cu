@@ -1421,19 +1421,25 @@ k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __rest
     __shared__ int ok[kPcaRows];
     __shared__ int64_t rows[kPcaRows];
     const int64_t S = static_cast<int64_t>(kPcaBlocks) * kPcaRows;
-    if (threadIdx.x < kPcaRows)
+    if (threadIdx.x < kPcaRows) {
         rows[threadIdx.x] = (static_cast<int64_t>(blockIdx.x * kPcaRows + threadIdx.x) * n) / S;
-    __syncthreads();
-    for (int q = threadIdx.x; q < kPcaRows * 16 * T; q += blockDim.x) {
-        const int k = q / (16 * T), c = q % (16 * T);
-        xs[k][c] = c < d ? X[rows[k] * d + c] - mu[c] : 0.0f;
+        ok[threadIdx.x] = 1;
     }
     __syncthreads();
-    if (threadIdx.x < kPcaRows) {
-        bool good = true;
-        for (int c = 0; c < d; c++)
-            if (!(fabsf(xs[threadIdx.x][c]) <= 1e15f)) good = false;
-        ok[threadIdx.x] = good;
+    // all of this thread's loads in flight at once (256 threads per block)
+    constexpr int NQ = kPcaRows * 16 * T / 256;
+    float v[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; i++) {
+        const int q = threadIdx.x + 256 * i, k = q / (16 * T), c = q % (16 * T);
+        v[i] = c < d ? __ldg(X + rows[k] * d + c) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < NQ; i++) {
+        const int q = threadIdx.x + 256 * i, k = q / (16 * T), c = q % (16 * T);
+        const float x = c < d ? v[i] - __ldg(mu + c) : 0.0f;
+        xs[k][c] = x;
+        if (!(fabsf(x) <= 1e15f)) ok[k] = 0;  // rows with huge or non-finite values sit out
     }
     __syncthreads();
     const int ta = threadIdx.x >> 4, tb = threadIdx.x & 15;
@@ -1924,6 +1930,41 @@ __device__ __forceinline__ int slot_rb(const BandPlan& q, int k) {
     return k * q.P + pos;
 }
 
+// Walks row slot `a`'s candidate column tiles J >= j0 in ascending order:
+// one load per lane tests 32 groups' union boxes at once, then the tile
+// boxes of up to four surviving groups are loaded together, so a slot costs
+// a few dependent load latencies instead of one per group.  f(J, keep) is
+// called by the whole warp (J differs per lane) once per surviving group.
+template <class F>
+__device__ __forceinline__ void band_walk(const BandPlan& q, const double4& a, double thr2, int j0,
+                                          int lane, F&& f) {
+    const int g_end = (q.nt + 31) >> 5;
+    for (int gb = j0 >> 5; gb < g_end; gb += 32) {
+        const int g = gb + lane;
+        uint32_t gm = __ballot_sync(0xffffffffu, g < g_end && band_keep(a, q.sup[g], thr2));
+        while (gm) {
+            int gs[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                gs[i] = gm ? gb + __ffs(gm) - 1 : -1;
+                gm &= gm - 1;
+            }
+            double4 bx[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int J = gs[i] * 32 + lane;
+                bx[i] = (gs[i] >= 0 && J >= j0 && J < q.nt) ? box_r(q, J) : make_double4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                if (gs[i] < 0) break;  // warp-uniform
+                const int J = gs[i] * 32 + lane;
+                f(J, J >= j0 && J < q.nt && band_keep(a, bx[i], thr2));
+            }
+        }
+    }
+}
+
 // One warp per row slot of this shard: surviving column tiles.
 __global__ void __launch_bounds__(256)
 k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
@@ -1936,12 +1977,7 @@ k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
     const double thr2 = band_thr2(q);
     const double4 a = q.boxL[rb];
     int c = 0;
-    const int j0 = q.self ? rb >> 1 : 0;
-    for (int g = j0 >> 5; g * 32 < q.nt; g++) {
-        if (!band_keep(a, q.sup[g], thr2)) continue;  // warp-uniform: the whole group is out
-        const int J = g * 32 + lane;
-        if (J >= j0 && J < q.nt) c += band_keep(a, box_r(q, J), thr2);
-    }
+    band_walk(q, a, thr2, q.self ? rb >> 1 : 0, lane, [&](int, bool keep) { c += keep; });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) cnt[k] = c;
@@ -1952,7 +1988,7 @@ k_band_count(const BandPlan q, int32_t* __restrict__ cnt) {
 __global__ void __launch_bounds__(1024)
 k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int units_target, int64_t* __restrict__ list_off,
             int64_t* __restrict__ unit_off, int64_t* __restrict__ n_units, int32_t* __restrict__ dev_ch,
-            unsigned long long* __restrict__ counters) {
+            unsigned long long* __restrict__ counters, unsigned long long* host_units) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     __shared__ int64_t part[1024];
@@ -1999,7 +2035,13 @@ k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int units_target, int6
         run += (cnt[k] + ch - 1) / ch;
         unit_off[k + 1] = run;
     }
-    if (t == 1023) *n_units = run;
+    if (t == 1023) {
+        *n_units = run;
+        if (host_units) {  // mapped pinned slot: the host reads it after an event
+            *reinterpret_cast<volatile unsigned long long*>(host_units) = static_cast<unsigned long long>(run);
+            __threadfence_system();
+        }
+    }
 }
 
 // One warp per row slot: the surviving tiles in ascending order and the
@@ -2022,11 +2064,7 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     const double4 a = q.boxL[rb];
     int64_t w = list_off[k];
     float ms = 0.0f, mn = 0.0f;
-    const int j0 = q.self ? rb >> 1 : 0;
-    for (int g = j0 >> 5; g * 32 < q.nt; g++) {
-        if (!band_keep(a, q.sup[g], thr2)) continue;  // warp-uniform
-        const int J = g * 32 + lane;
-        const bool keep = J >= j0 && J < q.nt && band_keep(a, box_r(q, J), thr2);
+    band_walk(q, a, thr2, q.self ? rb >> 1 : 0, lane, [&](int J, bool keep) {
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             list[w + __popc(bal & ((1u << lane) - 1u))] = J;
@@ -2034,7 +2072,7 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
             mn = fmaxf(mn, tmaxN[J]);
         }
         w += __popc(bal);
-    }
+    });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
@@ -2525,6 +2563,62 @@ void plan_units(const DeviceCtx& ctx, int64_t nL, int64_t nR, bool self, int P, 
     u.n_units = n_units;
 }
 
+// A per-thread mapped pinned slot of 8 words: [0, 4) the counter read-back,
+// [4] the band plan's unit count.  Null when mapped memory is unavailable.
+struct PinSlot {
+    unsigned long long* h = nullptr;
+    unsigned long long* d = nullptr;
+};
+PinSlot pinned_slot() {
+    thread_local unsigned long long* h_pin = [] {
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            q = nullptr;
+        }
+        return static_cast<unsigned long long*>(q);
+    }();
+    PinSlot r;
+    if (h_pin && cudaHostGetDevicePointer(reinterpret_cast<void**>(&r.d), h_pin, 0) == cudaSuccess)
+        r.h = h_pin;
+    else
+        cudaGetLastError(), r.d = nullptr;
+    return r;
+}
+
+// Second stream of the band plan (per thread and device): the box / count /
+// scan chain runs on it beside the bf16 preparation, and its scan's unit
+// count reaches the host while the main stream still writes the tile lists.
+struct PlanAux {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+PlanAux* plan_aux() {
+    thread_local PlanAux cache[64];
+    thread_local bool made[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    PlanAux& a = cache[dev & 63];
+    if (!made[dev & 63]) {
+        if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        made[dev & 63] = true;
+    }
+    return &a;
+}
+
+// Where the host can read a band plan's unit count early (null ev: read
+// p.dev_n_units on the main stream).
+struct UnitsReady {
+    cudaEvent_t ev = nullptr;
+    const unsigned long long* h = nullptr;
+};
+constexpr unsigned long long kUnitsUnset = ~0ull;
+
 // The shared back half of both joins: screen (with a sampled output-size
 // estimate for large problems), exact re-check, one counter read-back,
 // overflow handling, optional sort, stats.  `recheck(recs, cap, out)`
@@ -2535,7 +2629,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
                         ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
                         pdb_join_stats* stats, PhaseTimer& tm, int launches,
-                        unsigned long long* counters_p, Recheck&& recheck) {
+                        unsigned long long* counters_p, UnitsReady ready, Recheck&& recheck) {
     struct {
         unsigned long long* p;
     } counters{counters_p};  // [records, tiles, pairs, candidates, next unit]
@@ -2547,19 +2641,9 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     // staging copy to the one synchronisation of the call)
     // (mapped: a one-warp kernel stores the counters straight into it, no
     // copy-engine round trip)
-    thread_local unsigned long long* h_pin = [] {
-        void* q = nullptr;
-        if (cudaHostAlloc(&q, 64, cudaHostAllocMapped) != cudaSuccess) {
-            cudaGetLastError();
-            q = nullptr;
-        }
-        return static_cast<unsigned long long*>(q);
-    }();
-    unsigned long long* d_pin = nullptr;
-    if (h_pin && cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pin), h_pin, 0) != cudaSuccess) {
-        cudaGetLastError();
-        d_pin = nullptr;
-    }
+    const PinSlot pin = pinned_slot();
+    unsigned long long* h_pin = pin.h;
+    unsigned long long* d_pin = pin.d;
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
     // Candidate records live in a per-thread, per-device buffer that only
     // grows (plain cudaMalloc: usable from any stream): a multi-GB record
@@ -2633,8 +2717,25 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     constexpr int64_t kSampleStep = 64;
     int64_t units = p.n_units;  // dense estimate; a band plan's real count is on the device
     if (p.tile_list && units >= kSampleStep * ctx.sm_count) {
-        PDB_CUDA(cudaMemcpyAsync(&units, p.dev_n_units, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        PDB_CUDA(cudaStreamSynchronize(s));
+        const volatile unsigned long long* hv = ready.h;
+        if (hv && ready.ev) {
+            PDB_CUDA(cudaEventSynchronize(ready.ev));
+        } else if (hv) {
+            // spin on the mapped slot: the host learns the count as soon as
+            // k_band_scan stores it, while the stream still writes the tile lists
+            while (*hv == kUnitsUnset) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q == cudaErrorNotReady) continue;
+                PDB_CUDA(q);
+                break;
+            }
+        }
+        if (hv && *hv != kUnitsUnset) {
+            units = static_cast<int64_t>(*hv);
+        } else {
+            PDB_CUDA(cudaMemcpyAsync(&units, p.dev_n_units, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            PDB_CUDA(cudaStreamSynchronize(s));
+        }
     }
     // Short joins chain the re-check to the screen with programmatic
     // dependent launch; for long ones (config 5: 0.16 s screen) the early-
@@ -2926,6 +3027,73 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         }
     }
 
+    UnitPlan plan;
+    plan.off = ar.take<int64_t>(nt_ + 2);
+    plan_units(ctx, nL, nR, self, P, shard, pair, plan);
+    const int nt = plan.nt;
+    unsigned long long* counters = ar.take<unsigned long long>(5);
+    // ---- band plan, part 2: boxes, surviving tiles, units -----------------
+    // Boxes, groups, counts and the scan need only the projections and the
+    // permutation: they run on the aux stream beside the bf16 preparation.
+    int32_t* list = nullptr;
+    int4* unit_info = nullptr;
+    float* hrow = nullptr;
+    int64_t *list_off = nullptr, *unit_off = nullptr, *dev_n_units = nullptr;
+    int32_t* dev_ch = nullptr;
+    float *cmaxS = nullptr, *cmaxN = nullptr;
+    BandPlan bp{};
+    UnitsReady ready;
+    // (PDB_PLAN_AUX=0: one PDL-chained stream, the host spinning on the
+    // mapped unit count instead -- ~2 us slower on config 2)
+    static const bool use_aux = [] {
+        const char* e = std::getenv("PDB_PLAN_AUX");
+        return !(e && e[0] == '0');
+    }();
+    PlanAux* aux = band && use_aux ? plan_aux() : nullptr;
+    if (band) {
+        double4* boxL = ar.take<double4>(nbl);
+        double4* boxR = ar.take<double4>(nt);
+        int32_t* cnt = ar.take<int32_t>(n_slots);
+        list_off = ar.take<int64_t>(n_slots + 1);
+        unit_off = ar.take<int64_t>(n_slots + 1);
+        dev_n_units = ar.take<int64_t>(1);
+        dev_ch = ar.take<int32_t>(1);
+        list = ar.take<int32_t>(std::max<int64_t>(list_cap, 1));
+        unit_info = ar.take<int4>(units_cap);
+        hrow = ar.take<float>(nL);
+        cmaxS = ar.take<float>(n_slots);
+        cmaxN = ar.take<float>(n_slots);
+        double4* sup = ar.take<double4>(ceil_div(int64_t{nt}, 32));
+        cudaStream_t sa = s;
+        const PinSlot pin = pinned_slot();
+        if (pin.h) *reinterpret_cast<volatile unsigned long long*>(pin.h + 4) = kUnitsUnset;
+        if (aux) {
+            PDB_CUDA(cudaEventRecord(aux->fork, s));
+            PDB_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+            sa = aux->s;
+        }
+        // (the first kernel after a cross-stream wait launches without PDL)
+        launch_pdl_if(!aux, k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))),
+                      dim3(256), 0, sa, static_cast<const float2*>(projL),
+                      static_cast<const int32_t*>(permL), nL, BM, nbl, boxL);
+        if (!self)
+            launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(int64_t{nt} * 32, 256))),
+                       dim3(256), 0, sa, static_cast<const float2*>(projR),
+                       static_cast<const int32_t*>(permR), nR, BN, static_cast<int64_t>(nt), boxR);
+        bp = BandPlan{boxL, self ? nullptr : boxR, sup, info, tau, d, nt, static_cast<int>(self), P,
+                      shard, n_slots, static_cast<int>(nbl)};
+        launch_pdl(k_band_groups, dim3(static_cast<unsigned>(ceil_div(ceil_div(int64_t{nt}, 32) * 32, 256))),
+                   dim3(256), 0, sa, bp, sup);
+        const unsigned gs = static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256));
+        if (n_slots > 0) launch_pdl(k_band_count, dim3(gs), dim3(256), 0, sa, bp, cnt);
+        launch_pdl(k_band_scan, dim3(1), dim3(1024), 0, sa, static_cast<const int32_t*>(cnt), n_slots,
+                   units_target, list_off, unit_off, dev_n_units, dev_ch, counters,
+                   pin.d ? pin.d + 4 : nullptr);
+        launches += 4 + (self ? 0 : 1);
+        if (aux) PDB_CUDA(cudaEventRecord(aux->join, sa));
+        if (pin.h) ready = UnitsReady{aux ? aux->join : nullptr, pin.h + 4};
+    }
+
     uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
     float* hnL = ar.take<float>(nL);
     float* snL = ar.take<float>(nL);
@@ -2941,62 +3109,25 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         hnR = hr;
         snR = sr;
     }
-    UnitPlan plan;
-    plan.off = ar.take<int64_t>(nt_ + 2);
-    plan_units(ctx, nL, nR, self, P, shard, pair, plan);
-    const int nt = plan.nt;
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     float* tmaxS = ar.take<float>(nt);
     float* tmaxN = ar.take<float>(nt);
-    unsigned long long* counters = ar.take<unsigned long long>(5);
     launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
-    float* cmaxS = ar.take<float>(nt + 1);
-    float* cmaxN = ar.take<float>(nt + 1);
-    // ---- band plan, part 2: boxes, surviving tiles, units -----------------
-    int32_t* list = nullptr;
-    int4* unit_info = nullptr;
-    float* hrow = nullptr;
-    int64_t *list_off = nullptr, *unit_off = nullptr, *dev_n_units = nullptr;
-    int32_t* dev_ch = nullptr;
     if (band) {
-        double4* boxL = ar.take<double4>(nbl);
-        double4* boxR = ar.take<double4>(nt);
-        int32_t* cnt = ar.take<int32_t>(n_slots);
-        list_off = ar.take<int64_t>(n_slots + 1);
-        unit_off = ar.take<int64_t>(n_slots + 1);
-        dev_n_units = ar.take<int64_t>(1);
-        dev_ch = ar.take<int32_t>(1);
-        list = ar.take<int32_t>(std::max<int64_t>(list_cap, 1));
-        unit_info = ar.take<int4>(units_cap);
-        hrow = ar.take<float>(nL);
-        cmaxS = ar.take<float>(n_slots);
-        cmaxN = ar.take<float>(n_slots);
-        launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))), dim3(256), 0, s,
-                   static_cast<const float2*>(projL), static_cast<const int32_t*>(permL), nL, BM,
-                   nbl, boxL);
-        if (!self)
-            launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(int64_t{nt} * 32, 256))),
-                       dim3(256), 0, s, static_cast<const float2*>(projR),
-                       static_cast<const int32_t*>(permR), nR, BN, static_cast<int64_t>(nt), boxR);
-        double4* sup = ar.take<double4>(ceil_div(int64_t{nt}, 32));
-        BandPlan bp{boxL, self ? nullptr : boxR, sup, info, tau, d, nt, static_cast<int>(self), P,
-                    shard, n_slots, static_cast<int>(nbl)};
-        launch_pdl(k_band_groups, dim3(static_cast<unsigned>(ceil_div(ceil_div(int64_t{nt}, 32) * 32, 256))),
-                   dim3(256), 0, s, bp, sup);
-        const unsigned gs = static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256));
-        if (n_slots > 0) launch_pdl(k_band_count, dim3(gs), dim3(256), 0, s, bp, cnt);
-        launch_pdl(k_band_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(cnt), n_slots,
-                   units_target, list_off, unit_off, dev_n_units, dev_ch, counters);
+        if (aux) PDB_CUDA(cudaStreamWaitEvent(s, aux->join, 0));
         if (n_slots > 0)
-            launch_pdl(k_band_write, dim3(gs), dim3(256), 0, s, bp,
-                       static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
-                       static_cast<const float*>(tmaxN), cmaxS, cmaxN,
-                       static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
-                       unit_info, static_cast<const float*>(hnL), static_cast<const float*>(snL), nL,
-                       tau * (1.0 + 1e-9), tf32 ? kU_tf32 : kU_bf16,
-                       (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow);
-        launches += 5;
+            launch_pdl_if(!aux, k_band_write, dim3(static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256))),
+                          dim3(256), 0, s, bp,
+                          static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
+                          static_cast<const float*>(tmaxN), cmaxS, cmaxN,
+                          static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
+                          unit_info, static_cast<const float*>(hnL), static_cast<const float*>(snL), nL,
+                          tau * (1.0 + 1e-9), tf32 ? kU_tf32 : kU_bf16,
+                          (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow);
+        launches++;
     } else {
+        cmaxS = ar.take<float>(nt + 1);
+        cmaxN = ar.take<float>(nt + 1);
         launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
                    static_cast<const float*>(tmaxN), nt, plan.ch, plan.n_chunks, plan.n_rb, plan.rpt,
                    static_cast<int>(self), P, shard, cmaxS, cmaxN, plan.off, counters);
@@ -3039,7 +3170,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         p.dev_ch = dev_ch;
         p.n_slots = n_slots;
     }
-    screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters,
+    screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters, ready,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
                            launch_pdl_if(pdl, k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
@@ -3136,7 +3267,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     p.hnL = hL;
     p.gR = gR;
     screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, tB, p, nL, nR, o, out, stats, tm, launches,
-                       counters,
+                       counters, UnitsReady{},
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
                            launch_pdl_if(pdl, k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 

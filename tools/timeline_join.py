@@ -1,5 +1,5 @@
 """GPU activity timeline (CUPTI via torch.profiler) of one join-only bench
-workload (default c3): every kernel of the last call with start offsets and
+workload (default c3; c2 = the config-2 tile histograms): every kernel of the last call with start offsets and
 durations.  Diagnostic only.  Usage: python tools/timeline_join.py [c3|c5|c1]"""
 import ctypes as C
 import os
@@ -15,8 +15,14 @@ from paper_1812_07607_b200 import patchdb  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c3"
 plain = "--plain" in sys.argv  # no profiler (for ncu)
-cfg = JOINS[which]
-L, R = _gen(which)
+if which == "c2":  # the config-2 tile histograms (bench.py's join)
+    from paper_1812_07607_b200 import workloads  # noqa: E402
+    fr, _ = workloads.frames(1000, 480, 640, seed=2)
+    cfg = dict(self_join=True, tau=0.05)
+    L, R = patchdb.featurize_tiles(fr, 60, 80, 4, "joint"), None
+else:
+    cfg = JOINS[which]
+    L, R = _gen(which)
 Ld = torch.from_numpy(L).cuda()
 Rd = Ld if R is None else torch.from_numpy(R).cuda()
 lib = capi.lib()
