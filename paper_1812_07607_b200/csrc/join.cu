@@ -1508,9 +1508,14 @@ k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum) {
 // directions (fp64).
 __global__ void __launch_bounds__(256)
 k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
-          BandInfo* __restrict__ info) {
+          BandInfo* __restrict__ info, int32_t* __restrict__ bins0, int32_t* __restrict__ bins1) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    // the counting sorts' bin counts and fill cursors (2 x 4096 per side)
+    for (int b = threadIdx.x; b < 2 * (1 << (2 * kMortonBits)); b += blockDim.x) {
+        if (bins0) bins0[b] = 0;
+        if (bins1) bins1[b] = 0;
+    }
     extern __shared__ float Cs[];  // [d][d]
     __shared__ float v[2][kPcaMaxD];
     __shared__ float wpart[2][8][kPcaMaxD];
@@ -1641,16 +1646,15 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> 
 // computed projection is within (d + 2) 2^-24 b of the exact one (the
 // centring cancels in every difference of two rows).  Outputs: the
 // projections, the Morton sort key, and b max-reduced per block (one
-// atomicMax per block).  Block 0 also zeroes the counting sort's bins.
+// atomicMax per block), and (single-GPU joins) the counting sort's bin
+// counts, zeroed by k_pca_eig.
 template <int NV>
 __global__ void __launch_bounds__(256, 2)
 k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
             BandInfo* __restrict__ info, float2* __restrict__ proj, uint32_t* __restrict__ key,
-            int32_t* __restrict__ val, int32_t* __restrict__ zero_bins) {
+            int32_t* __restrict__ val, int32_t* __restrict__ bin_count) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    if (zero_bins && blockIdx.x == 0)
-        for (int b = threadIdx.x; b < (1 << (2 * kMortonBits)); b += blockDim.x) zero_bins[b] = 0;
     __shared__ float bred[8];
     __shared__ float4 us[3][32 * NV / 4];  // u0, u1, mu
     for (int c = threadIdx.x; c < 32 * NV / 4; c += blockDim.x) {
@@ -1736,6 +1740,7 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
                 proj[row] = make_float2(p0, p1);
                 key[row] = kk;
                 val[row] = static_cast<int32_t>(row);
+                if (bin_count) atomicAdd(bin_count + kk, 1);
             }
         }
     }
@@ -1750,66 +1755,57 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
     }
 }
 
-// Counting sort of the 12-bit keys for single-GPU joins: block-aggregated
-// bin counts, one exclusive scan, atomic scatter (the order inside a bin is
-// arbitrary -- harmless, since the tile test is exact for any order).
+// Counting sort of the 12-bit keys for single-GPU joins: k_band_keys counts
+// the bins, each scatter block scans them and reserves its slots per bin
+// with one atomic (the order inside a bin is arbitrary -- harmless, since
+// the tile test is exact for any order).
 // Sharded joins need every rank to build the same order and use a stable
 // radix sort instead.
 constexpr int kBins = 1 << (2 * kMortonBits);
 
-__global__ void __launch_bounds__(256)
-k_bin_count(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ count) {
-    ptx::pdl_wait();
-    ptx::pdl_trigger();
-    __shared__ int32_t h[kBins];
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
-    __syncthreads();
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride)
-        atomicAdd(&h[__ldg(key + r)], 1);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-        if (h[b]) atomicAdd(count + b, h[b]);
-}
-
-// One block: exclusive scan of the bin counts into running positions.
-__global__ void __launch_bounds__(1024)
-k_bin_scan(const int32_t* __restrict__ count, int32_t* __restrict__ pos) {
-    ptx::pdl_wait();
-    ptx::pdl_trigger();
-    __shared__ int32_t part[1024];
-    constexpr int per = kBins / 1024;
-    const int t = threadIdx.x;
-    int32_t v[per], local = 0;
-#pragma unroll
-    for (int i = 0; i < per; i++) {
-        v[i] = count[t * per + i];
-        local += v[i];
-    }
-    part[t] = local;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        const int32_t x = t >= o ? part[t - o] : 0;
-        __syncthreads();
-        part[t] += x;
-        __syncthreads();
-    }
-    int32_t run = part[t] - local;
-#pragma unroll
-    for (int i = 0; i < per; i++) {
-        pos[t * per + i] = run;
-        run += v[i];
-    }
-}
-
 constexpr int kScatterRows = 4;  // rows per thread (4096 per 1024-thread block)
 __global__ void __launch_bounds__(1024)
-k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ pos,
-              int32_t* __restrict__ perm) {
+k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __restrict__ count,
+              int32_t* __restrict__ fill, int32_t* __restrict__ perm) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     __shared__ int32_t cnt[kBins], base[kBins];
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+    __shared__ int32_t wsum[32];
+    // every block scans the 4096 bin counts itself (16 KB from L2): the bin
+    // offsets need no kernel of their own
+    constexpr int per = kBins / 1024;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    int32_t v[per], lsum = 0;
+#pragma unroll
+    for (int i = 0; i < per; i++) {
+        v[i] = __ldcg(count + t * per + i);
+        lsum += v[i];
+        cnt[t * per + i] = 0;
+    }
+    int32_t incl = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int32_t x = wsum[lane], xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    int32_t run = wsum[wid] + incl - lsum;
+#pragma unroll
+    for (int i = 0; i < per; i++) {
+        base[t * per + i] = run;
+        run += v[i];
+    }
     __syncthreads();
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kScatterRows;
     uint32_t k[kScatterRows];
@@ -1823,7 +1819,7 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__
     __syncthreads();
     // one global reservation per (block, bin)
     for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-        base[b] = cnt[b] ? atomicAdd(pos + b, cnt[b]) : 0;
+        if (cnt[b]) base[b] += atomicAdd(fill + b, cnt[b]);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kScatterRows; i++) {
@@ -2665,14 +2661,20 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
             if (rcache.p) PDB_CUDA(cudaFree(rcache.p));
             rcache.p = nullptr;
             rcache.cap = 0;
+            // a quarter of headroom: the sampled estimate wobbles between
+            // calls, and each growth re-maps a multi-GB buffer
             void* q = nullptr;
-            const cudaError_t e = cudaMalloc(&q, static_cast<size_t>(need) * sizeof(int4));
-            if (e != cudaSuccess) {
+            unsigned long long got = need + need / 4;
+            if (cudaMalloc(&q, static_cast<size_t>(got) * sizeof(int4)) != cudaSuccess) {
                 cudaGetLastError();
-                fail(PDB_ERR_OUT_OF_MEMORY, "cannot allocate the candidate record buffer");
+                got = need;
+                if (cudaMalloc(&q, static_cast<size_t>(got) * sizeof(int4)) != cudaSuccess) {
+                    cudaGetLastError();
+                    fail(PDB_ERR_OUT_OF_MEMORY, "cannot allocate the candidate record buffer");
+                }
             }
             rcache.p = static_cast<int4*>(q);
-            rcache.cap = need;
+            rcache.cap = got;
         }
         recs.p = rcache.p;
     };
@@ -2680,7 +2682,9 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     auto ensure_out = [&](unsigned long long need) {
         if (static_cast<unsigned long long>(out->capacity) >= need && out->left) return;
         if (out->left) pdb_dev_pairs_free(out);
-        const int64_t c = static_cast<int64_t>(need);
+        // headroom for large outputs, as for the records (the pool keeps
+        // the blocks, so only growth maps new memory)
+        const int64_t c = static_cast<int64_t>(need > (1ull << 24) ? need + need / 4 : need);
         out->left = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
         out->right = static_cast<int32_t*>(dev_alloc(c * sizeof(int32_t), s));
         out->dist = static_cast<float*>(dev_alloc(c * sizeof(float), s));
@@ -2981,15 +2985,19 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         const int eig_smem = d * d * 4;
         // (set_max_smem caches per function and device)
         set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
+        uint8_t* tmpL = ar.take<uint8_t>(sort_tmp);
+        uint8_t* tmpR = self ? nullptr : ar.take<uint8_t>(sort_tmp);
         launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
-                   static_cast<const float*>(mu), info);
+                   static_cast<const float*>(mu), info,
+                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpL),
+                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpR));
         launches += 3;
-        auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm) {
+        auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm,
+                                 uint8_t* tmp) {
             proj = ar.take<float2>(n);
             uint32_t* k_in = ar.take<uint32_t>(n);
             int32_t* v_in = ar.take<int32_t>(n);
             perm = ar.take<int32_t>(n);
-            uint8_t* tmp = ar.take<uint8_t>(sort_tmp);
             const int nv = (d + 31) / 32;
             auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
                                                                                       : k_band_keys<4>;
@@ -3006,24 +3014,19 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                                          2 * kMortonBits, s));
                 launches += 5;
             } else {
-                int32_t* count = reinterpret_cast<int32_t*>(tmp);
-                int32_t* pos = count + kBins;
-                const unsigned gc = static_cast<unsigned>(
-                    std::min<int64_t>(ceil_div(n, 256), int64_t{ctx.sm_count} * 2));
-                launch_pdl(k_bin_count, dim3(gc), dim3(256), 0, s, static_cast<const uint32_t*>(k_in), n,
-                           count);
-                launch_pdl(k_bin_scan, dim3(1), dim3(1024), 0, s, static_cast<const int32_t*>(count), pos);
+                int32_t* count = reinterpret_cast<int32_t*>(tmp);  // counted by k_band_keys
                 launch_pdl(k_bin_scatter, dim3(static_cast<unsigned>(ceil_div(n, 1024 * kScatterRows))),
-                           dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n, pos, perm);
-                launches += 4;
+                           dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n,
+                           static_cast<const int32_t*>(count), count + kBins, perm);
+                launches += 2;
             }
         };
-        keys_and_sort(d_L, nL, projL, permL);
+        keys_and_sort(d_L, nL, projL, permL, tmpL);
         if (self) {
             permR = permL;
             projR = projL;
         } else {
-            keys_and_sort(d_R, nR, projR, permR);
+            keys_and_sort(d_R, nR, projR, permR, tmpR);
         }
     }
 
