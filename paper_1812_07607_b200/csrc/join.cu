@@ -1485,10 +1485,16 @@ k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __rest
 
 // Fixed-order fp64 reduction of the partials (deterministic).
 __global__ void __launch_bounds__(128)
-k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum) {
+k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum,
+             int32_t* __restrict__ bins0, int32_t* __restrict__ bins1) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    // the counting sorts' bin counts and fill cursors (2 x 4096 per side)
+    for (int b = e; b < 2 * (1 << (2 * kMortonBits)); b += gridDim.x * blockDim.x) {
+        if (bins0) bins0[b] = 0;
+        if (bins1) bins1[b] = 0;
+    }
     if (e >= E) return;
     double acc = 0.0;
     for (int b = 0; b < kPcaBlocks; b += 8) {
@@ -1508,14 +1514,9 @@ k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum) {
 // directions (fp64).
 __global__ void __launch_bounds__(256)
 k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
-          BandInfo* __restrict__ info, int32_t* __restrict__ bins0, int32_t* __restrict__ bins1) {
+          BandInfo* __restrict__ info) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    // the counting sorts' bin counts and fill cursors (2 x 4096 per side)
-    for (int b = threadIdx.x; b < 2 * (1 << (2 * kMortonBits)); b += blockDim.x) {
-        if (bins0) bins0[b] = 0;
-        if (bins1) bins1[b] = 0;
-    }
     extern __shared__ float Cs[];  // [d][d]
     __shared__ float v[2][kPcaMaxD];
     __shared__ float wpart[2][8][kPcaMaxD];
@@ -1531,6 +1532,7 @@ k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
         v[1][c] = c < d ? ((c & 1) ? 1.0f : -1.0f) * (1.0f + 0.002f * c) : 0.0f;
     }
     __syncthreads();
+#pragma unroll 8
     for (int e = t; e < d * d; e += blockDim.x) {
         const int a = e / d, b = e - a * d;
         Cs[e] = static_cast<float>(m > 0 ? sum[d + e] * im - mean[a] * mean[b] : (a == b ? 1.0 : 0.0));
@@ -1647,7 +1649,7 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // low 8 bits -> 
 // centring cancels in every difference of two rows).  Outputs: the
 // projections, the Morton sort key, and b max-reduced per block (one
 // atomicMax per block), and (single-GPU joins) the counting sort's bin
-// counts, zeroed by k_pca_eig.
+// counts, zeroed by k_pca_reduce.
 template <int NV>
 __global__ void __launch_bounds__(256, 2)
 k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ mu,
@@ -2980,17 +2982,17 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                                                                   : k_pca_partial<8>;
         launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, s, d_L, nL, d, static_cast<const float*>(mu),
                    part);
+        uint8_t* tmpL = ar.take<uint8_t>(sort_tmp);
+        uint8_t* tmpR = self ? nullptr : ar.take<uint8_t>(sort_tmp);
         launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
-                   static_cast<const float*>(part), E, sum);
+                   static_cast<const float*>(part), E, sum,
+                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpL),
+                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpR));
         const int eig_smem = d * d * 4;
         // (set_max_smem caches per function and device)
         set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
-        uint8_t* tmpL = ar.take<uint8_t>(sort_tmp);
-        uint8_t* tmpR = self ? nullptr : ar.take<uint8_t>(sort_tmp);
         launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
-                   static_cast<const float*>(mu), info,
-                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpL),
-                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpR));
+                   static_cast<const float*>(mu), info);
         launches += 3;
         auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm,
                                  uint8_t* tmp) {
