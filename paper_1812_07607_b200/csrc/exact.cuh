@@ -42,4 +42,32 @@ __device__ __forceinline__ double exact_dist(const float* __restrict__ a,
     return __dsqrt_rn(acc);
 }
 
+// The same chain with b read from the grouped copy (k_group_copy): 8-column
+// groups of consecutive rows, group stride gs floats.  Lanes whose
+// candidates are neighbouring rows then share 128-byte lines, where the
+// row-major gather costs one wavefront per lane per 32 bytes.
+__device__ __forceinline__ double exact_dist_grouped(const float* __restrict__ a,
+                                                     const float* __restrict__ bg, int64_t gs, int d,
+                                                     bool vec8a) {
+    double acc = 0.0;
+    for (int k = 0; k < d; k += 8) {
+        float x[8], y[8];
+        if (vec8a) {
+            ldg256(a + k, x);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; q++) x[q] = k + q < d ? __ldg(a + k + q) : 0.0f;
+        }
+        ldg256(bg + (k >> 3) * gs, y);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (k + q < d) {
+                const double t = __dsub_rn(static_cast<double>(x[q]), static_cast<double>(y[q]));
+                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            }
+        }
+    }
+    return __dsqrt_rn(acc);
+}
+
 }  // namespace pdb

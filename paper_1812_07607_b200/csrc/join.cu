@@ -2106,6 +2106,31 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     }
 }
 
+// Grouped copy of R for dense re-checks: XT[(g * ldt + p) * 8 + c] =
+// R[perm[p]][8 g + c] (zero past d), p the column position.  Consecutive
+// threads take consecutive positions of one group, so the writes coalesce.
+__global__ void __launch_bounds__(256)
+k_group_copy(const float* __restrict__ R, int64_t n, int d, const int32_t* __restrict__ perm,
+             float* __restrict__ XT) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int G = (d + 7) / 8;
+    const int64_t total = n * G;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t / n);
+        const int64_t p = t - static_cast<int64_t>(g) * n;
+        const int64_t src = perm ? __ldg(perm + p) : p;
+        const float* r = R + src * d + 8 * g;
+        float v[8];
+#pragma unroll
+        for (int c = 0; c < 8; c++) v[c] = 8 * g + c < d ? __ldg(r + c) : 0.0f;
+        float4* o = reinterpret_cast<float4*>(XT + (static_cast<int64_t>(g) * n + p) * 8);
+        o[0] = make_float4(v[0], v[1], v[2], v[3]);
+        o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: exact re-check.  The fp64 chain is written with explicit _rn
 // intrinsics so it can never be contracted into FMAs: diff = a - b,
@@ -2123,7 +2148,8 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
           int d, double tau, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
           float* __restrict__ out_d, unsigned long long out_cap,
           unsigned long long* __restrict__ out_count, const int32_t* __restrict__ permL,
-          const int32_t* __restrict__ permR, int self_join) {
+          const int32_t* __restrict__ permR, int self_join, const float* __restrict__ XT,
+          int64_t ldt) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const unsigned long long n = min(*n_rec, cap);
@@ -2169,10 +2195,13 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
             if (c < total) {
                 const int k = __fns(s_mask, 0, c - s_excl + 1);  // that lane's (c - excl)-th set bit
                 j = s_j0 + k;
+                const int jp = j;  // column position (sorted under a band plan)
                 if (permR) j = __ldg(permR + j);
                 // euclidean(L_i, R_j); bitwise symmetric, so a self-join pair
                 // can be reported as (min, max)
-                dist = exact_dist(L + static_cast<int64_t>(a) * d, R + static_cast<int64_t>(j) * d, d, vec8);
+                dist = XT ? exact_dist_grouped(L + static_cast<int64_t>(a) * d,
+                                               XT + static_cast<int64_t>(jp) * 8, ldt * 8, d, vec8)
+                          : exact_dist(L + static_cast<int64_t>(a) * d, R + static_cast<int64_t>(j) * d, d, vec8);
                 ok = dist <= tau;
                 if (self_join && a > j) {
                     const int t = a;
@@ -2769,6 +2798,15 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         cap = std::max(cap, snap(h_cnt[0] * kSampleStep * 2.0));
         out_need = std::max(out_need, snap(h_cnt[3] * kSampleStep * 1.5));
     }
+    // Re-check over a grouped copy of R when the output is candidate-heavy:
+    // small dense joins (cheap to copy), or a sample of >= 4 candidates per
+    // column row (PDB_K3_GROUPED=0 disables it)
+    static const bool grouped_ok = [] {
+        const char* e = std::getenv("PDB_K3_GROUPED");
+        return !(e && e[0] == '0');
+    }();
+    const bool grouped = grouped_ok && (small ? p.tile_list == nullptr
+                                              : h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR));
     // (the sampled pass, when taken, counts as preparation in the phase times)
     tm.mark(1);
     // Screen and re-check run back to back and the host reads the counters
@@ -2783,7 +2821,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
             launches++;
         }
         tm.mark(2);
-        recheck(recs.p, counters.p, cap, out, small);
+        recheck(recs.p, counters.p, cap, out, small, grouped);
         launches++;
         tm.mark(3);
         passes++;
@@ -2795,7 +2833,7 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
         ensure_out(h_cnt[2]);
         PDB_CUDA(cudaMemsetAsync(counters.p + 2, 0, sizeof(unsigned long long), s));
-        recheck(recs.p, counters.p, cap, out, small);
+        recheck(recs.p, counters.p, cap, out, small, grouped);
         launches++;
         tm.mark(3);
         read_counters();
@@ -3175,14 +3213,23 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         p.dev_ch = dev_ch;
         p.n_slots = n_slots;
     }
+    DevBuf<float> XT;  // grouped copy of R for candidate-heavy re-checks
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters, ready,
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool grouped) {
+                           if (grouped && !XT.p) {
+                               XT.reset(static_cast<size_t>(nR) * ((d + 7) / 8) * 8, s);
+                               // (PDL like the re-check: early-resident CTAs slow a long screen)
+                               launch_pdl_if(pdl, k_group_copy, dim3(ctx.sm_count * 8), dim3(256), 0, s, d_R,
+                                             nR, d, static_cast<const int32_t*>(permR), XT.p);
+                               PDB_CUDA(cudaGetLastError());
+                           }
                            launch_pdl_if(pdl, k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2, static_cast<const int32_t*>(permL),
-                               static_cast<const int32_t*>(permR), static_cast<int>(self));
+                               static_cast<const int32_t*>(permR), static_cast<int>(self),
+                               static_cast<const float*>(grouped ? XT.p : nullptr), nR);
                            PDB_CUDA(cudaGetLastError());
                        });
 }
@@ -3274,7 +3321,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, tB, p, nL, nR, o, out, stats, tm, launches,
                        counters, UnitsReady{},
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl) {
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool) {
                            launch_pdl_if(pdl, k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, min_cos, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
