@@ -2142,6 +2142,7 @@ k_group_copy(const float* __restrict__ R, int64_t n, int d, const int32_t* __res
 // busy whatever the masks' skew (records of tight clusters carry ~30 bits,
 // scattered ones 1-2), and lanes of one record share their row of L.
 // Survivors are compacted with a ballot and one atomic per batch.
+template <bool GROUPED>
 __global__ void __launch_bounds__(256)
 k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n_rec,
           unsigned long long cap, const float* __restrict__ L, const float* __restrict__ R,
@@ -2199,7 +2200,7 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
                 if (permR) j = __ldg(permR + j);
                 // euclidean(L_i, R_j); bitwise symmetric, so a self-join pair
                 // can be reported as (min, max)
-                dist = XT ? exact_dist_grouped(L + static_cast<int64_t>(a) * d,
+                dist = GROUPED ? exact_dist_grouped(L + static_cast<int64_t>(a) * d,
                                                XT + static_cast<int64_t>(jp) * 8, ldt * 8, d, vec8)
                           : exact_dist(L + static_cast<int64_t>(a) * d, R + static_cast<int64_t>(j) * d, d, vec8);
                 ok = dist <= tau;
@@ -2798,15 +2799,15 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         cap = std::max(cap, snap(h_cnt[0] * kSampleStep * 2.0));
         out_need = std::max(out_need, snap(h_cnt[3] * kSampleStep * 1.5));
     }
-    // Re-check over a grouped copy of R when the output is candidate-heavy:
-    // small dense joins (cheap to copy), or a sample of >= 4 candidates per
-    // column row (PDB_K3_GROUPED=0 disables it)
+    // Re-check over a grouped copy of R when the sampled output is
+    // candidate-heavy: >= 4 candidates per column row (config 5).  Sparse
+    // records (config 1) gain nothing from it.  PDB_K3_GROUPED=0 disables it.
     static const bool grouped_ok = [] {
         const char* e = std::getenv("PDB_K3_GROUPED");
         return !(e && e[0] == '0');
     }();
-    const bool grouped = grouped_ok && (small ? p.tile_list == nullptr
-                                              : h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR));
+    const bool grouped = grouped_ok && !small &&
+                         h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR);
     // (the sampled pass, when taken, counts as preparation in the phase times)
     tm.mark(1);
     // Screen and re-check run back to back and the host reads the counters
@@ -3224,7 +3225,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                              nR, d, static_cast<const int32_t*>(permR), XT.p);
                                PDB_CUDA(cudaGetLastError());
                            }
-                           launch_pdl_if(pdl, k_recheck, dim3(ctx.sm_count * 8), dim3(256), 0, s,
+                           // (separate instantiations: the grouped path's registers
+                           // would otherwise spill in the row-major one)
+                           launch_pdl_if(pdl, grouped ? k_recheck<true> : k_recheck<false>,
+                               dim3(ctx.sm_count * 8), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2, static_cast<const int32_t*>(permL),
