@@ -283,6 +283,12 @@ int pdb_store_featurize(const pdb_store* s, int64_t lo, int64_t hi, int32_t tile
                         int32_t tile_w, int32_t bins, int32_t mode, float* d_features,
                         int64_t* n_frames, int32_t threads, void* stream);
 
+/* Returns the device memory the library keeps between calls on the calling
+ * thread (the grow-only candidate-record buffer of large joins) and trims the
+ * library's own stream-ordered pool to zero.  Synchronises the device.  No
+ * reference counterpart: the reference holds no device memory. */
+int pdb_release_caches(void);
+
 /* Pinned host memory helpers (the e2e path copies from pinned buffers). */
 void* pdb_host_alloc(int64_t bytes);
 void pdb_host_free(void* p);

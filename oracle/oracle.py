@@ -52,6 +52,10 @@ def port():
                                            C.POINTER(OrcPairs)]
         L.orc_cosine_bf16.argtypes = [vp, vp, i64]
         L.orc_cosine_bf16.restype = f64
+        L.orc_sim_join_rows.argtypes = [vp, i64, vp, i64, i64, f64, i32, vp, i64, i32,
+                                        C.POINTER(OrcPairs)]
+        L.orc_sim_join_pruned.argtypes = [vp, i64, vp, i64, i64, f64, i32, i32,
+                                          C.POINTER(OrcPairs)]
         L.orc_dedup.argtypes = [vp, i64, i64, f64, vp]
         L.orc_dedup.restype = i64
         _port = L
@@ -148,6 +152,52 @@ def sim_join(L: np.ndarray, R, tau: float, self_join: bool = False, rows=(0, -1)
     return res
 
 
+def _take(out):
+    n = out.count
+    try:
+        if n:
+            res = (np.ctypeslib.as_array(out.left, (n,)).copy(),
+                   np.ctypeslib.as_array(out.right, (n,)).copy(),
+                   np.ctypeslib.as_array(out.dist, (n,)).copy())
+        else:
+            res = (np.empty(0, np.int32), np.empty(0, np.int32), np.empty(0, np.float64))
+    finally:
+        port().orc_pairs_free(C.byref(out))
+    return res
+
+
+def sim_join_rows(L: np.ndarray, R, tau: float, rows, self_join: bool = False,
+                  threads: int | None = None):
+    """Brute force over a list of L rows (ascending, deduplicated here):
+    every (i, j) with euclidean <= tau for i in rows (j > i for self joins),
+    sorted by (i, j).  Exact early abandon only (pdb_oracle.c (1))."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = L if self_join else np.ascontiguousarray(R, dtype=np.float32)
+    rows = np.unique(np.asarray(rows, dtype=np.int64))
+    out = OrcPairs()
+    th = threads or max(1, os.cpu_count() or 1)
+    rc = port().orc_sim_join_rows(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
+                                  int(self_join), _p(rows), rows.shape[0], th, C.byref(out))
+    if rc:
+        raise RuntimeError(f"oracle join failed: {rc}")
+    return _take(out)
+
+
+def sim_join_pruned(L: np.ndarray, R, tau: float, self_join: bool = False,
+                    threads: int | None = None):
+    """The full join, all rows, with exact coordinate-window pruning
+    (pdb_oracle.c (2)); same result as sim_join()."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = L if self_join else np.ascontiguousarray(R, dtype=np.float32)
+    out = OrcPairs()
+    th = threads or max(1, os.cpu_count() or 1)
+    rc = port().orc_sim_join_pruned(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1],
+                                    float(tau), int(self_join), th, C.byref(out))
+    if rc:
+        raise RuntimeError(f"oracle join failed: {rc}")
+    return _take(out)
+
+
 def cosine_join_bf16(L: np.ndarray, R, min_cos: float, self_join: bool = False, rows=(0, -1),
                      threads: int | None = None):
     """RESTATED cosine join over bf16 bit patterns (uint16 [n, d]): pairs
@@ -172,6 +222,13 @@ def cosine_join_bf16(L: np.ndarray, R, min_cos: float, self_join: bool = False, 
     finally:
         port().orc_pairs_free(C.byref(out))
     return res
+
+
+def cosine_bf16(a: np.ndarray, b: np.ndarray) -> float:
+    """Restated fp64 cosine of two bf16 rows (uint16 bit patterns)."""
+    a = np.ascontiguousarray(a, dtype=np.uint16)
+    b = np.ascontiguousarray(b, dtype=np.uint16)
+    return port().orc_cosine_bf16(_p(a), _p(b), a.shape[0])
 
 
 def dedup(X: np.ndarray, tau: float):

@@ -396,3 +396,411 @@ int64_t orc_dedup(const float* X, int64_t n, int64_t d, double tau, int64_t* rep
     free(reps);
     return nr;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Faster exact restatements of the same contract, for full-size checks.
+ *
+ * Both return exactly the pair set {(i, j): euclidean(L_i, R_j) <= tau}
+ * (tests/oracles.hpp:77-85) with euclidean()'s value, sorted by (i, j); they
+ * only skip work that provably cannot change it:
+ *
+ * (1) Early abandon.  euclidean() accumulates non-negative terms with
+ *     round-to-nearest adds, so every partial sum is <= the final one
+ *     (fl(acc + t) >= acc for t >= 0) and sqrt is monotone.  Once a partial
+ *     sum exceeds T = tau^2 (1 + 1e-9), fl(sqrt(final)) >= fl(sqrt(T)) > tau
+ *     (sqrt(T) exceeds tau by 5e-10 relative, far above one rounding), so
+ *     the pair cannot be emitted.  Pairs that are not abandoned run the full
+ *     chain, whose result is the one emitted and compared.  Disabled (T =
+ *     inf) unless 1e-150 < tau < 1e150, where tau^2 could under/overflow.
+ *
+ * (2) Coordinate windows (orc_sim_join_pruned).  For any coordinate c, the
+ *     chain's final sum is >= fl(diff_c^2) (the sum before term c is >= 0),
+ *     so |(double)a_c - (double)b_c| > tau (1 + 1e-6) excludes the pair by
+ *     the argument in (1).  Each L row compares only the R rows within
+ *     w = tau (1 + 1e-6) of it on three coordinates k1, k2, k3, found
+ *     through a grid of cell width 2w (orc_sim_join_pruned).  Rows with any
+ *     non-finite value, and all rows when tau is outside (1e-150, 1e150),
+ *     bypass the windows and are compared against every row.
+ *
+ * tests/test_oracle.py checks both against orc_sim_join (plain brute
+ * force) and the reference itself. */
+
+static inline double orc_abandon_limit(double tau) {
+    if (!(tau > 1e-150 && tau < 1e150)) return INFINITY;
+    return tau * tau * (1.0 + 1e-9);
+}
+
+/* euclidean() with early abandon: returns +inf when the pair is provably
+ * above tau, otherwise the exact euclidean() value. */
+static inline double orc_euclidean_ea(const float* a, const float* b, int64_t d, double T) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < d; i++) {
+        double diff = (double)a[i] - (double)b[i];
+        acc += diff * diff;
+        if (acc > T) return INFINITY;
+    }
+    return sqrt(acc);
+}
+
+typedef struct {
+    int64_t n, cap;
+    int32_t* li;
+    int32_t* rj;
+    double* dist;
+    int oom;
+} orc_buf;
+
+static int orc_buf_push(orc_buf* b, int64_t i, int64_t j, double dd) {
+    if (b->n == b->cap) {
+        int64_t nc = b->cap ? b->cap * 2 : 1024;
+        int32_t* x = (int32_t*)realloc(b->li, nc * sizeof(int32_t));
+        if (x) b->li = x;
+        int32_t* y = (int32_t*)realloc(b->rj, nc * sizeof(int32_t));
+        if (y) b->rj = y;
+        double* z = (double*)realloc(b->dist, nc * sizeof(double));
+        if (z) b->dist = z;
+        if (!x || !y || !z) {
+            b->oom = 1;
+            return -1;
+        }
+        b->cap = nc;
+    }
+    b->li[b->n] = (int32_t)i;
+    b->rj[b->n] = (int32_t)j;
+    b->dist[b->n] = dd;
+    b->n++;
+    return 0;
+}
+
+/* Chunked work list: chunk k covers items [k*csz, (k+1)*csz) of the row
+ * list; threads take chunks in order from an atomic counter, each chunk has
+ * its own buffer, and the buffers are concatenated in chunk order, so the
+ * output is independent of the thread count. */
+typedef struct orc_sched orc_sched;
+typedef void (*orc_row_fn)(orc_sched* s, int64_t item, orc_buf* out);
+struct orc_sched {
+    int64_t n_items, csz, n_chunks;
+    int64_t next; /* atomic */
+    orc_buf* bufs;
+    orc_row_fn fn;
+    /* the join */
+    const float *L, *R;
+    int64_t nL, nR, d;
+    double tau, T, w;
+    int self_join;
+    const int64_t* rows; /* row list (NULL: 0..n_items-1) */
+    /* pruned join: the finite R rows sorted by grid cell */
+    int k1, k2, k3;
+    double cw;            /* cell width 2w */
+    const uint64_t* gk;   /* cell keys, ascending */
+    const float* gv;      /* their (k1, k2, k3) values, same order */
+    const int32_t* sidx;  /* their row indices */
+    int64_t n_fin;
+    const int32_t* wild;  /* R rows with a non-finite value */
+    int64_t n_wild;
+    const uint8_t* l_wild; /* per L row: non-finite */
+    /* scratch per thread is allocated inside the worker */
+};
+
+static void* orc_sched_worker(void* arg) {
+    orc_sched* s = (orc_sched*)arg;
+    for (;;) {
+        int64_t c = __atomic_fetch_add(&s->next, 1, __ATOMIC_RELAXED);
+        if (c >= s->n_chunks) break;
+        int64_t a = c * s->csz, e = a + s->csz;
+        if (e > s->n_items) e = s->n_items;
+        for (int64_t k = a; k < e && !s->bufs[c].oom; k++) s->fn(s, k, &s->bufs[c]);
+    }
+    return NULL;
+}
+
+static int orc_sched_run(orc_sched* s, int32_t threads, orc_pairs* out) {
+    s->n_chunks = (s->n_items + s->csz - 1) / s->csz;
+    s->next = 0;
+    s->bufs = (orc_buf*)calloc((size_t)(s->n_chunks > 0 ? s->n_chunks : 1), sizeof(orc_buf));
+    if (!s->bufs) return ORC_ERR_OOM;
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t th[256];
+    for (int32_t k = 0; k < threads; k++) pthread_create(&th[k], NULL, orc_sched_worker, s);
+    for (int32_t k = 0; k < threads; k++) pthread_join(th[k], NULL);
+    int64_t total = 0;
+    int oom = 0;
+    for (int64_t c = 0; c < s->n_chunks; c++) {
+        total += s->bufs[c].n;
+        oom |= s->bufs[c].oom;
+    }
+    if (!oom && total > 0) {
+        out->left = (int32_t*)malloc((size_t)total * sizeof(int32_t));
+        out->right = (int32_t*)malloc((size_t)total * sizeof(int32_t));
+        out->dist = (double*)malloc((size_t)total * sizeof(double));
+        if (!out->left || !out->right || !out->dist) {
+            oom = 1;
+        } else {
+            int64_t o = 0;
+            for (int64_t c = 0; c < s->n_chunks; c++) {
+                orc_buf* b = &s->bufs[c];
+                memcpy(out->left + o, b->li, (size_t)b->n * sizeof(int32_t));
+                memcpy(out->right + o, b->rj, (size_t)b->n * sizeof(int32_t));
+                memcpy(out->dist + o, b->dist, (size_t)b->n * sizeof(double));
+                o += b->n;
+            }
+            out->count = total;
+        }
+    }
+    for (int64_t c = 0; c < s->n_chunks; c++) {
+        free(s->bufs[c].li);
+        free(s->bufs[c].rj);
+        free(s->bufs[c].dist);
+    }
+    free(s->bufs);
+    if (oom) {
+        orc_pairs_free(out);
+        return ORC_ERR_OOM;
+    }
+    return ORC_OK;
+}
+
+static void orc_row_brute(orc_sched* s, int64_t k, orc_buf* out) {
+    int64_t i = s->rows ? s->rows[k] : k;
+    const float* a = s->L + (size_t)i * s->d;
+    int64_t j0 = s->self_join ? i + 1 : 0;
+    for (int64_t j = j0; j < s->nR; j++) {
+        double dd = orc_euclidean_ea(a, s->R + (size_t)j * s->d, s->d, s->T);
+        if (dd <= s->tau && orc_buf_push(out, i, j, dd)) return;
+    }
+}
+
+/* Brute force (early abandon only) over an ascending list of L rows.
+ * self_join keeps j > i.  Output sorted by (i, j). */
+int orc_sim_join_rows(const float* L, int64_t nL, const float* R, int64_t nR, int64_t d,
+                      double tau, int32_t self_join, const int64_t* rows, int64_t n_rows,
+                      int32_t threads, orc_pairs* out) {
+    memset(out, 0, sizeof(*out));
+    if (tau < 0.0) return ORC_ERR_CONFIG;
+    if (d < 1) return ORC_ERR_SHAPE;
+    for (int64_t k = 0; k < n_rows; k++)
+        if (rows[k] < 0 || rows[k] >= nL || (k && rows[k] <= rows[k - 1])) return ORC_ERR_SHAPE;
+    if (n_rows == 0 || nR == 0) return ORC_OK;
+    orc_sched s;
+    memset(&s, 0, sizeof(s));
+    s.L = L;
+    s.R = self_join ? L : R;
+    s.nL = nL;
+    s.nR = self_join ? nL : nR;
+    s.d = d;
+    s.tau = tau;
+    s.T = orc_abandon_limit(tau);
+    s.self_join = self_join;
+    s.rows = rows;
+    s.n_items = n_rows;
+    s.csz = 1;
+    s.fn = orc_row_brute;
+    return orc_sched_run(&s, threads, out);
+}
+
+static int orc_row_finite(const float* a, int64_t d) {
+    for (int64_t k = 0; k < d; k++)
+        if (!isfinite(a[k])) return 0;
+    return 1;
+}
+
+/* one L row of the pruned join: the 27 grid cells around the row's cell,
+ * each run of 3 consecutive g3 cells contiguous in the sorted order */
+static int64_t orc_lower(const uint64_t* k, int64_t n, uint64_t key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (k[m] < key) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+#define ORC_GBIAS ((int64_t)1 << 20)
+
+static inline int orc_cell(double v, double c, int64_t* g) {
+    double q = floor(v / c);
+    if (!(q > -(double)ORC_GBIAS + 2 && q < (double)ORC_GBIAS - 2)) return 0;
+    *g = (int64_t)q;
+    return 1;
+}
+
+static inline uint64_t orc_gkey(int64_t g1, int64_t g2, int64_t g3) {
+    return ((uint64_t)(g1 + ORC_GBIAS) << 42) | ((uint64_t)(g2 + ORC_GBIAS) << 21) |
+           (uint64_t)(g3 + ORC_GBIAS);
+}
+
+static void orc_row_pruned(orc_sched* s, int64_t i, orc_buf* out) {
+    const float* a = s->L + (size_t)i * s->d;
+    int64_t n0 = out->n;
+    int64_t g1, g2, g3;
+    double x1 = (double)a[s->k1], x2 = (double)a[s->k2], x3 = (double)a[s->k3], w = s->w;
+    if (s->l_wild[i] || s->w == INFINITY || !orc_cell(x1, s->cw, &g1) ||
+        !orc_cell(x2, s->cw, &g2) || !orc_cell(x3, s->cw, &g3)) {
+        int64_t j0 = s->self_join ? i + 1 : 0;
+        for (int64_t j = j0; j < s->nR; j++) {
+            double dd = orc_euclidean_ea(a, s->R + (size_t)j * s->d, s->d, s->T);
+            if (dd <= s->tau && orc_buf_push(out, i, j, dd)) return;
+        }
+        return;
+    }
+    for (int64_t e1 = -1; e1 <= 1; e1++)
+        for (int64_t e2 = -1; e2 <= 1; e2++) {
+            int64_t p = orc_lower(s->gk, s->n_fin, orc_gkey(g1 + e1, g2 + e2, g3 - 1));
+            uint64_t kend = orc_gkey(g1 + e1, g2 + e2, g3 + 1);
+            for (; p < s->n_fin && s->gk[p] <= kend; p++) {
+                /* the exact window tests: fl(x - b) is the chain's own
+                 * difference up to sign, so a row is skipped only when that
+                 * chain term alone exceeds w^2 > T */
+                const float* kb = s->gv + 3 * (size_t)p;
+                double f1 = x1 - (double)kb[0], f2 = x2 - (double)kb[1], f3 = x3 - (double)kb[2];
+                if (f1 > w || f1 < -w || f2 > w || f2 < -w || f3 > w || f3 < -w) continue;
+                int64_t j = s->sidx[p];
+                if (s->self_join && j <= i) continue;
+                double dd = orc_euclidean_ea(a, s->R + (size_t)j * s->d, s->d, s->T);
+                if (dd <= s->tau && orc_buf_push(out, i, j, dd)) return;
+            }
+        }
+    for (int64_t q = 0; q < s->n_wild; q++) {
+        int64_t j = s->wild[q];
+        if (s->self_join && j <= i) continue;
+        double dd = orc_euclidean_ea(a, s->R + (size_t)j * s->d, s->d, s->T);
+        if (dd <= s->tau && orc_buf_push(out, i, j, dd)) return;
+    }
+    /* restore ascending j within the row (insertion sort: rows are short) */
+    for (int64_t p = n0 + 1; p < out->n; p++) {
+        int32_t j = out->rj[p];
+        double dd = out->dist[p];
+        int64_t q = p;
+        while (q > n0 && out->rj[q - 1] > j) {
+            out->rj[q] = out->rj[q - 1];
+            out->dist[q] = out->dist[q - 1];
+            q--;
+        }
+        out->rj[q] = j;
+        out->dist[q] = dd;
+    }
+}
+
+typedef struct {
+    uint64_t k;
+    int32_t i;
+} orc_kv;
+
+static int orc_kv_cmp(const void* x, const void* y) {
+    const orc_kv* a = (const orc_kv*)x;
+    const orc_kv* b = (const orc_kv*)y;
+    if (a->k != b->k) return a->k < b->k ? -1 : 1;
+    return a->i < b->i ? -1 : a->i > b->i;
+}
+
+/* The full join with coordinate windows (see (2) above): the finite R rows
+ * are bucketed on a grid of cell width 2w over their three coordinates of
+ * largest spread (k1, k2, k3).  A row within w of an L row on all three lies
+ * in one of the 27 cells around the L row's cell (|b - a| <= w is half a
+ * cell; the rounding of v / (2w) is ~1e-16 relative), and every bucketed
+ * row is still passed through the exact window tests before the chain.
+ * Rows whose cell index would not fit (|v| > 2^19 cells) go to the
+ * compared-against-everything lists like non-finite rows. */
+int orc_sim_join_pruned(const float* L, int64_t nL, const float* R, int64_t nR, int64_t d,
+                        double tau, int32_t self_join, int32_t threads, orc_pairs* out) {
+    memset(out, 0, sizeof(*out));
+    if (tau < 0.0) return ORC_ERR_CONFIG;
+    if (d < 1) return ORC_ERR_SHAPE;
+    if (self_join) {
+        R = L;
+        nR = nL;
+    }
+    if (nL == 0 || nR == 0 || tau != tau) return ORC_OK; /* NaN tau: nothing is <= NaN */
+    orc_sched s;
+    memset(&s, 0, sizeof(s));
+    s.L = L;
+    s.R = R;
+    s.nL = nL;
+    s.nR = nR;
+    s.d = d;
+    s.tau = tau;
+    s.T = orc_abandon_limit(tau);
+    s.w = s.T == INFINITY ? INFINITY : tau * (1.0 + 1e-6);
+    s.cw = 2.0 * s.w;
+    s.self_join = self_join;
+    /* k1, k2, k3: the coordinates of largest spread over (a sample of) R */
+    int64_t step = nR > 65536 ? nR / 65536 : 1;
+    double var_k[3] = {-1.0, -1.0, -1.0};
+    int kk[3] = {0, 0, 0};
+    for (int64_t c = 0; c < d; c++) {
+        double m = 0, m2 = 0;
+        int64_t cnt = 0;
+        for (int64_t j = 0; j < nR; j += step) {
+            double v = R[(size_t)j * d + c];
+            if (!isfinite(v)) continue;
+            m += v;
+            m2 += v * v;
+            cnt++;
+        }
+        double var = cnt ? m2 / cnt - (m / cnt) * (m / cnt) : 0.0;
+        int pos = 3;
+        while (pos > 0 && var > var_k[pos - 1]) pos--;
+        if (pos < 3) {
+            for (int q = 2; q > pos; q--) {
+                var_k[q] = var_k[q - 1];
+                kk[q] = kk[q - 1];
+            }
+            var_k[pos] = var;
+            kk[pos] = (int)c;
+        }
+    }
+    s.k1 = kk[0];
+    s.k2 = d > 1 ? kk[1] : kk[0];
+    s.k3 = d > 2 ? kk[2] : s.k2;
+    orc_kv* kv = (orc_kv*)malloc((size_t)nR * sizeof(orc_kv));
+    int32_t* wild = (int32_t*)malloc((size_t)nR * sizeof(int32_t));
+    uint8_t* lw = (uint8_t*)malloc((size_t)nL);
+    uint64_t* gk = (uint64_t*)malloc((size_t)nR * sizeof(uint64_t));
+    float* gv = (float*)malloc((size_t)nR * 3 * sizeof(float));
+    int32_t* sidx = (int32_t*)malloc((size_t)nR * sizeof(int32_t));
+    int rc = ORC_ERR_OOM;
+    if (kv && wild && lw && gk && gv && sidx) {
+        int64_t nf = 0, nw = 0;
+        for (int64_t j = 0; j < nR; j++) {
+            const float* r = R + (size_t)j * d;
+            int64_t g1, g2, g3;
+            if (s.w != INFINITY && orc_row_finite(r, d) && orc_cell(r[s.k1], s.cw, &g1) &&
+                orc_cell(r[s.k2], s.cw, &g2) && orc_cell(r[s.k3], s.cw, &g3)) {
+                kv[nf].k = orc_gkey(g1, g2, g3);
+                kv[nf].i = (int32_t)j;
+                nf++;
+            } else {
+                wild[nw++] = (int32_t)j;
+            }
+        }
+        qsort(kv, (size_t)nf, sizeof(orc_kv), orc_kv_cmp);
+        for (int64_t p = 0; p < nf; p++) {
+            const float* r = R + (size_t)kv[p].i * d;
+            gk[p] = kv[p].k;
+            sidx[p] = kv[p].i;
+            gv[3 * p] = r[s.k1];
+            gv[3 * p + 1] = r[s.k2];
+            gv[3 * p + 2] = r[s.k3];
+        }
+        for (int64_t i = 0; i < nL; i++) lw[i] = (uint8_t)!orc_row_finite(L + (size_t)i * d, d);
+        s.gk = gk;
+        s.gv = gv;
+        s.sidx = sidx;
+        s.n_fin = nf;
+        s.wild = wild;
+        s.n_wild = nw;
+        s.l_wild = lw;
+        s.n_items = nL;
+        s.csz = 256;
+        s.fn = orc_row_pruned;
+        rc = orc_sched_run(&s, threads, out);
+    }
+    free(kv);
+    free(wild);
+    free(lw);
+    free(gk);
+    free(gv);
+    free(sidx);
+    return rc;
+}

@@ -64,19 +64,35 @@ const DeviceCtx& device_ctx() {
     if (!fn || q != cudaDriverEntryPointSuccess)
         fail(PDB_ERR_CUDA, "driver entry point cuTensorMapEncodeTiled unavailable");
     c.encode_tiled = fn;
-    // Keep freed scratch in the stream-ordered pool between calls.
-    cudaMemPool_t pool;
-    PDB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    // The library's own stream-ordered pool: freed scratch stays mapped
+    // between calls (release threshold raised on this pool only, not on the
+    // device's default pool other libraries in the process share);
+    // pdb_release_caches() trims it.
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    PDB_CUDA(cudaMemPoolCreate(&c.pool, &pp));
     uint64_t thr = UINT64_MAX;
-    PDB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    PDB_CUDA(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &thr));
     g_ctx[dev] = c;
     g_ctx_ok[dev] = true;
     return g_ctx[dev];
 }
 
+void* dev_try_alloc(size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 16), device_ctx().pool, s) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
-    const cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s);
+    const cudaError_t e = cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 16), device_ctx().pool, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         fail(PDB_ERR_OUT_OF_MEMORY, "device allocation of " + std::to_string(bytes) +
@@ -148,8 +164,9 @@ int64_t n_tiles_of(int64_t n, int32_t H, int32_t W, int32_t th, int32_t tw) {
 
 void check_join_args(const void* L, int64_t nL, const void* R, int64_t nR, int32_t d, double tau,
                      const pdb_join_opts* o) {
-    // run_sim_join order: tau (src/query.cpp:488), then dims (467-499).
-    if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
+    // run_sim_join order: tau (src/query.cpp:488), then dims (467-499).  The
+    // reference rejects only tau < 0.0: a NaN tau passes and matches nothing.
+    if (tau < 0.0) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
     if (nL < 0 || nR < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative row count");
     if (nL > INT32_MAX || nR > INT32_MAX)
         fail(PDB_ERR_INVALID_ARGUMENT, "row counts above 2^31-1 are not supported");
@@ -439,7 +456,7 @@ PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int3
     return guarded([&] {
         if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
         check_featurize_args(frames, n, H, W, th, tw, bins, mode, frames);
-        if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
+        if (tau < 0.0) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
         device_ctx();
         const int64_t nt = n_tiles_of(n, H, W, th, tw);
         const int D = hist_dim(bins, mode);
@@ -502,8 +519,10 @@ PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int3
 
 static void check_dedup_args(const void* X, int64_t n, int32_t d, double tau,
                              const pdb_join_opts* o) {
-    // run_dedup order: tau (src/query.cpp:536), then the dimension check
-    if (!(tau >= 0.0)) fail(PDB_ERR_CONFIG, "dedup needs tau >= 0");
+    // run_dedup order: tau (src/query.cpp:536), then the dimension check.
+    // As there, only tau < 0.0 is rejected: with a NaN tau nothing is within
+    // tau and every item is its own representative.
+    if (tau < 0.0) fail(PDB_ERR_CONFIG, "dedup needs tau >= 0");
     if (n < 0) fail(PDB_ERR_INVALID_ARGUMENT, "negative row count");
     if (n > INT32_MAX) fail(PDB_ERR_INVALID_ARGUMENT, "row counts above 2^31-1 are not supported");
     if (n > 0 && d < 1) fail(PDB_ERR_SHAPE, "dedup needs non-empty patch data");
@@ -560,6 +579,15 @@ PDB_API int pdb_rows_within(const float* A, const float* B, int64_t n, int32_t d
         run_rows_within(dA.p, dB.p, n, d, radius, dO.p, s);
         PDB_CUDA(cudaMemcpyAsync(out, dO.p, static_cast<size_t>(n), cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+PDB_API int pdb_release_caches(void) {
+    return guarded([&] {
+        device_ctx();
+        release_join_caches();
+        PDB_CUDA(cudaDeviceSynchronize());
+        PDB_CUDA(cudaMemPoolTrimTo(device_ctx().pool, 0));
     });
 }
 

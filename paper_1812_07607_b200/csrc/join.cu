@@ -2647,6 +2647,38 @@ struct UnitsReady {
 };
 constexpr unsigned long long kUnitsUnset = ~0ull;
 
+// Candidate records live in a per-thread, per-device buffer that only grows
+// (plain cudaMalloc: usable from any stream): a multi-GB record buffer is
+// mapped once, not on every call.  Freed at thread exit or by
+// pdb_release_caches().
+struct RecCache {
+    int4* p = nullptr;
+    unsigned long long cap = 0;
+    void release() {
+        if (p) cudaFree(p);  // (errors ignored: may run during process teardown)
+        p = nullptr;
+        cap = 0;
+    }
+};
+struct RecCaches {
+    RecCache c[64];
+    ~RecCaches() {
+        for (auto& r : c) r.release();
+    }
+};
+RecCaches& rec_caches() {
+    thread_local RecCaches caches;
+    return caches;
+}
+
+// PDB_K3_GROUPED, read on every call: 0 never re-check from the grouped copy
+// of R, 1 (default) when the sampled output is candidate-heavy, 2 always.
+int grouped_mode() {
+    const char* e = std::getenv("PDB_K3_GROUPED");
+    if (!e || !e[0]) return 1;
+    return std::clamp(atoi(e), 0, 2);
+}
+
 // The shared back half of both joins: screen (with a sampled output-size
 // estimate for large problems), exact re-check, one counter read-back,
 // overflow handling, optional sort, stats.  `recheck(recs, cap, out)`
@@ -2673,17 +2705,9 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     unsigned long long* h_pin = pin.h;
     unsigned long long* d_pin = pin.d;
     unsigned long long h_cnt[4] = {0, 0, 0, 0};
-    // Candidate records live in a per-thread, per-device buffer that only
-    // grows (plain cudaMalloc: usable from any stream): a multi-GB record
-    // buffer is mapped once, not on every call.
-    struct RecCache {
-        int4* p = nullptr;
-        unsigned long long cap = 0;
-    };
-    thread_local RecCache rec_cache[64];
     int dev_id = 0;
     PDB_CUDA(cudaGetDevice(&dev_id));
-    RecCache& rcache = rec_cache[dev_id & 63];
+    RecCache& rcache = rec_caches().c[dev_id & 63];
     struct {
         int4* p = nullptr;
     } recs;
@@ -2801,13 +2825,18 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     }
     // Re-check over a grouped copy of R when the sampled output is
     // candidate-heavy: >= 4 candidates per column row (config 5).  Sparse
-    // records (config 1) gain nothing from it.  PDB_K3_GROUPED=0 disables it.
-    static const bool grouped_ok = [] {
-        const char* e = std::getenv("PDB_K3_GROUPED");
-        return !(e && e[0] == '0');
-    }();
-    const bool grouped = grouped_ok && !small &&
-                         h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR);
+    // records (config 1) gain nothing from it.  PDB_K3_GROUPED: see
+    // grouped_mode().  The recheck callback may still fall back to the
+    // row-major gather when the copy cannot be allocated.
+    const int gmode = grouped_mode();
+    bool grouped = gmode == 2 || (gmode == 1 && !small &&
+                                  h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR));
+    // Test hooks: PDB_TEST_REC_CAP / PDB_TEST_OUT_CAP cap the first pass's
+    // record and pair buffers, forcing the overflow paths below.
+    if (const char* e = std::getenv("PDB_TEST_REC_CAP"))
+        cap = std::max<unsigned long long>(1, std::strtoull(e, nullptr, 10));
+    if (const char* e = std::getenv("PDB_TEST_OUT_CAP"))
+        out_need = std::max<unsigned long long>(1, std::strtoull(e, nullptr, 10));
     // (the sampled pass, when taken, counts as preparation in the phase times)
     tm.mark(1);
     // Screen and re-check run back to back and the host reads the counters
@@ -2877,6 +2906,13 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
 
 }  // namespace
 
+void release_join_caches() {
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    PDB_CUDA(cudaDeviceSynchronize());
+    rec_caches().c[dev & 63].release();
+}
+
 void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR, int32_t d,
                       double tau, const pdb_join_opts& o, pdb_dev_pairs* out,
                       pdb_join_stats* stats) {
@@ -2891,7 +2927,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     const int shard = o.shard_count > 1 ? o.shard_index : 0;
     if (stats) *stats = pdb_join_stats{};
     out->count = 0;
-    if (nL == 0 || nR == 0) return;
+    // (a NaN tau, which the reference accepts, matches nothing: every
+    // `euclidean <= tau` is false)
+    if (nL == 0 || nR == 0 || tau != tau) return;
     PhaseTimer tm(stats != nullptr && (o.flags & PDB_JOIN_PHASE_TIMES) != 0, s);
     int launches = 0;
     tm.mark(0);
@@ -3215,11 +3253,20 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         p.n_slots = n_slots;
     }
     DevBuf<float> XT;  // grouped copy of R for candidate-heavy re-checks
+    bool xt_filled = false;
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters, ready,
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool grouped) {
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool& grouped) {
                            if (grouped && !XT.p) {
-                               XT.reset(static_cast<size_t>(nR) * ((d + 7) / 8) * 8, s);
+                               // only a speed-up: without room for the copy
+                               // the re-check gathers R row-major
+                               XT.p = static_cast<float*>(dev_try_alloc(
+                                   static_cast<size_t>(nR) * ((d + 7) / 8) * 8 * sizeof(float), s));
+                               XT.s = s;
+                           }
+                           if (grouped && !XT.p) grouped = false;
+                           if (grouped && !xt_filled) {
+                               xt_filled = true;
                                // (PDL like the re-check: early-resident CTAs slow a long screen)
                                launch_pdl_if(pdl, k_group_copy, dim3(ctx.sm_count * 8), dim3(256), 0, s, d_R,
                                              nR, d, static_cast<const int32_t*>(permR), XT.p);
@@ -3325,7 +3372,7 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
     screen_and_recheck(ctx, s, DP, kModeCosBf16, tA, tB, tB, p, nL, nR, o, out, stats, tm, launches,
                        counters, UnitsReady{},
                        [&](const int4* recs, unsigned long long* counters,
-                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool) {
+                           unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool&) {
                            launch_pdl_if(pdl, k_recheck_cos, dim3(ctx.sm_count * 16), dim3(256), 0, s, 
                                recs, counters, cap, d_L, d_R, d, min_cos, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),

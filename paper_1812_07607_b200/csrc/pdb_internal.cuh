@@ -35,15 +35,20 @@ struct DeviceCtx {
     int cc_major = 0, cc_minor = 0;
     size_t smem_optin = 0;
     void* encode_tiled = nullptr;  // cuTensorMapEncodeTiled from the driver
+    cudaMemPool_t pool = nullptr;  // the library's stream-ordered pool
 };
 
 // Context of the calling thread's current device; fails with
 // PDB_ERR_NO_DEVICE when there is no sm_100 GPU (there is no CPU path).
 PDB_HIDDEN const DeviceCtx& device_ctx();
 
-// Stream-ordered scratch allocation from the device's default memory pool
+// Stream-ordered scratch allocation from the library's own memory pool
 // (release threshold raised once, so repeated calls reuse memory).
 PDB_HIDDEN void* dev_alloc(size_t bytes, cudaStream_t s);
+// The same, returning null instead of failing (optional speed-up buffers).
+PDB_HIDDEN void* dev_try_alloc(size_t bytes, cudaStream_t s);
+// Frees the calling thread's grow-only join buffers (pdb_release_caches).
+PDB_HIDDEN void release_join_caches();
 PDB_HIDDEN void dev_free(void* p, cudaStream_t s);
 
 template <class T>

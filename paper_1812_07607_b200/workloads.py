@@ -106,7 +106,7 @@ CONFIG2 = dict(frames=1000, H=480, W=640, tile_h=60, tile_w=80, bins=4, mode="jo
 
 
 def config4(n: int = 200_000, d: int = 2048, seed: int = 4, plant_frac: float = 0.005,
-            plant_sigma: float = 0.2, device: str = "cpu"):
+            plant_sigma: float = 0.2, device: str = "cpu", return_planted: bool = False):
     """Config 4: e = normalize(ReLU(P z)) stored as bf16, z ~ N(0,1)^d, P a
     fixed seeded d x d N(0,1)/sqrt(d) projection (torch's seeded CPU
     generator).  Independent ReLU'd projections sit near cosine ~0.3, so as
@@ -114,12 +114,14 @@ def config4(n: int = 200_000, d: int = 2048, seed: int = 4, plant_frac: float = 
     therefore near-duplicates (z_i = z_src + plant_sigma * N(0,1)) to make
     the cos >= 0.95 parity check non-vacuous.  Returns a [n, d] torch bf16
     tensor on `device` (the product reads it; the oracle reads its uint16
-    bits via .view(torch.int16))."""
+    bits via .view(torch.int16)); with ``return_planted`` also the planted
+    (row, source row) index pairs as int64 numpy arrays."""
     import torch
     g = torch.Generator(device="cpu").manual_seed(seed)
     P = torch.randn(d, d, generator=g) / d ** 0.5
     Z = torch.randn(n, d, generator=g)
     k = int(n * plant_frac)
+    dst = src = torch.empty(0, dtype=torch.int64)
     if k:
         dst = torch.randperm(n, generator=g)[:k]
         src = torch.randint(0, n, (k,), generator=g)
@@ -131,6 +133,8 @@ def config4(n: int = 200_000, d: int = 2048, seed: int = 4, plant_frac: float = 
         e = torch.relu(Z[a:a + step] @ P.T)
         e = e / e.norm(dim=1, keepdim=True).clamp_min(1e-30)
         out[a:a + step] = e.to(torch.bfloat16)
+    if return_planted:
+        return out, dst.numpy(), src.numpy()
     return out
 
 

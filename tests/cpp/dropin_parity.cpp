@@ -4,6 +4,7 @@
 // (proj/tests/oracles.hpp).  Built by `make -C oracle dropin` into
 // oracle/_ref/dropin_parity (test infrastructure); run on the GPU box by
 // tests/test_dropin_gpu.py.  Prints "DROPIN OK <checks>" and exits 0.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -82,6 +83,10 @@ int main() {
     std::vector<Patch> q{oracle::vec_patch(100, {1.0f, 1.0f})};
     join_case(dup, q, 1.0);
     join_case(dup, q, 0.999);
+    // NaN tau: the reference rejects only tau < 0.0 (src/query.cpp:488), so a
+    // NaN passes and matches nothing; the adapter must agree, not throw
+    join_case(lp, rp, std::nan(""));
+    join_case(x, x, std::nan(""));
     // errors
     EXPECT((throws_as<ConfigError>([&] { pdb::patchdb::sim_join_pairs(lp, rp, -1.0); })));
     auto bad = lp;
@@ -139,7 +144,7 @@ int main() {
     })));
     // dedup (src/query.cpp:535-582): group sizes and lineage parents of
     // PlanNode::dedup, kept set of dedup_stream
-    for (double tau : {0.05, 0.2, 0.6}) {
+    for (double tau : {0.05, 0.2, 0.6, std::nan("")}) {
         auto items = oracle::to_patches(oracle::clustered_points(11, 40, 12, 8, 0.02));
         std::vector<Tuple> tt;
         for (const auto& p : items) tt.push_back(Tuple{p});

@@ -111,9 +111,16 @@ def test_default_band_config2_features():
 
 
 def test_default_band_cross_d128_planted():
-    L, R, _, _ = workloads.config3(n=65_536)
+    """Config-3 distribution at 65,536 rows: band == dense, both == the exact
+    CPU join, and every planted pair present."""
+    L, R, pl, pr = workloads.config3(n=65_536)
     tb, td, n = _band_vs_dense(L, R, 0.02, False)
     assert n > 0 and tb < 0.5 * td
+    res = patchdb.sim_join(L, R, 0.02)
+    ol, orr, od = oracle.sim_join_pruned(L, R, 0.02)
+    assert np.array_equal(res.left, ol) and np.array_equal(res.right, orr)
+    got = set(zip(res.left.tolist(), res.right.tolist()))
+    assert all((a, b) in got for a, b in zip(pl.tolist(), pr.tolist()))
 
 
 def test_default_band_skewed_self():

@@ -65,7 +65,9 @@ def test_validation_errors_before_device():
     L = np.zeros((3, 2), np.float32)
     pr = capi.Pairs()
     assert lib.pdb_sim_join(capi.ptr(L), 3, capi.ptr(L), 3, 2, -1.0, None, C.byref(pr)) == capi.PDB_ERR_CONFIG
-    assert lib.pdb_sim_join(capi.ptr(L), 3, capi.ptr(L), 3, 2, float("nan"), None, C.byref(pr)) == capi.PDB_ERR_CONFIG
+    # NaN tau passes validation like the reference's `tau < 0.0` check (it then
+    # needs the device: no CPU path), so it is no ConfigError
+    assert lib.pdb_sim_join(capi.ptr(L), 3, capi.ptr(L), 3, 2, float("nan"), None, C.byref(pr)) != capi.PDB_ERR_CONFIG
     # d == 0 with rows -> ShapeError (src/query.cpp:467-477)
     assert lib.pdb_sim_join(capi.ptr(L), 3, capi.ptr(L), 3, 0, 1.0, None, C.byref(pr)) == capi.PDB_ERR_SHAPE
     o = capi.JoinOpts()

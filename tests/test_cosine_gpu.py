@@ -50,8 +50,8 @@ def test_cosine_edge_rows_and_thresholds():
 
 def test_config4_full_size_sampled_rows():
     """200,000 x 2048 bf16 (config 4): the device join, checked exactly on
-    sampled row blocks against the restated fp64 oracle, and every planted
-    near-duplicate found."""
+    sampled row blocks against the restated fp64 oracle (the planted
+    near-duplicates: test_fullsize_gpu.test_config4_planted_pairs_found)."""
     x = workloads.config4(device="cuda")
     out = patchdb.cosine_join_bf16_device(x, None, 0.95, self_join=True, sort=True)
     l, r, c = (t.cpu().numpy() for t in out.to_torch(x.device))

@@ -1,0 +1,216 @@
+"""Parity at BASELINE.json's full sizes, pinned to the CPU oracle (not to
+another GPU path):
+
+* config 3 (the north-star 1,048,576 x 1,048,576 x 128 cross join, tau 0.02):
+  the WHOLE pair set equals the exact CPU join (oracle.sim_join_pruned), for
+  the default band plan, the dense screen and the tf32 screen; that CPU join
+  itself equals plain brute force on 768 sampled rows at full size; and every
+  planted near-duplicate is in the output.
+* config 2 (1000 frames): all 64,000 joint 4x4x4 tile histograms bit-exact
+  against the restatement, the per-channel B=4 and B=8 histograms of all
+  64,000 tiles bit-exact against the reference itself (oracle/_ref), and the
+  whole 1000-frame pair set equal to plain brute force.
+* config 5 (4,194,304 x 64 self-join, tau 0.01): the full neighbourhood of
+  sampled rows (strided, a contiguous block, and the highest-degree rows of
+  the tight clusters) equals brute force; the grouped and row-major re-checks
+  agree on a checksum of all ~1e9 pairs.
+
+Contract: {(i, j): euclidean(L_i, R_j) <= tau}, /root/reference/proj/tests/
+oracles.hpp:77-85, distances fp32(euclidean) (src/index.cpp:69-76)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle
+from paper_1812_07607_b200 import patchdb, workloads
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def _assert_same(res, ol, orr, od):
+    """GPU JoinResult (sorted) == oracle (sorted), distances fp32(euclidean)."""
+    assert len(res) == len(ol)
+    assert np.array_equal(res.left, ol) and np.array_equal(res.right, orr)
+    assert np.array_equal(res.dist, od.astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# config 3
+
+@pytest.fixture(scope="module")
+def c3():
+    L, R, pl, pr = workloads.config3()
+    want = oracle.sim_join_pruned(L, R, 0.02, threads=THREADS)
+    return L, R, pl, pr, want
+
+
+def test_config3_oracle_pinned_to_brute_force_at_full_size(c3):
+    """The pruned CPU join equals plain brute force on 768 sampled rows
+    (512 strided over all of L, 256 planted rows) of the full relation."""
+    L, R, pl, pr, (wl, wr, wd) = c3
+    rows = np.unique(np.concatenate([np.arange(0, L.shape[0], L.shape[0] // 512),
+                                     pl[:: max(1, len(pl) // 256)]]))
+    bl, br, bd = oracle.sim_join_rows(L, R, 0.02, rows, threads=THREADS)
+    m = np.isin(wl, rows)
+    assert np.array_equal(wl[m], bl) and np.array_equal(wr[m], br) and np.array_equal(wd[m], bd)
+    assert len(bl) >= 200
+
+
+@pytest.mark.parametrize("variant", ["band", "dense", "tf32"])
+def test_config3_full_pair_set_equals_oracle(c3, variant):
+    L, R, pl, pr, (wl, wr, wd) = c3
+    res = patchdb.sim_join(L, R, 0.02, dense=variant == "dense", tf32=variant == "tf32")
+    _assert_same(res, wl, wr, wd)
+    got = set(zip(res.left.tolist(), res.right.tolist()))
+    missing = [(a, b) for a, b in zip(pl.tolist(), pr.tolist()) if (a, b) not in got]
+    assert not missing, f"{len(missing)} planted pairs missing, e.g. {missing[:5]}"
+    assert len(pl) > 5000
+
+
+def test_config3_device_entry_and_sharded_union(c3):
+    """The device entry on HBM-resident rows, and the union of 4 row shards
+    (the multi-GPU partition, run here one shard at a time), both equal the
+    oracle's pair set."""
+    L, R, pl, pr, (wl, wr, wd) = c3
+    dL, dR = torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda()
+    r = patchdb.sim_join_device(dL, dR, 0.02, sort=True)
+    l_, r_, d_ = (t.cpu().numpy() for t in r.to_torch(dL.device))
+    assert np.array_equal(l_, wl) and np.array_equal(r_, wr) and np.array_equal(d_, wd.astype(np.float32))
+    parts = []
+    for k in range(4):
+        s = patchdb.sim_join_device(dL, dR, 0.02, sort=True, shard=(k, 4))
+        parts.append(np.stack([t.cpu().numpy().view(np.int32) for t in s.to_torch(dL.device)], 1))
+    allp = np.concatenate(parts)
+    allp = allp[np.lexsort((allp[:, 1], allp[:, 0]))]
+    assert np.array_equal(allp[:, 0], wl) and np.array_equal(allp[:, 1], wr)
+
+
+# ---------------------------------------------------------------------------
+# config 2
+
+@pytest.fixture(scope="module")
+def c2():
+    fr, _ = workloads.frames(1000, 480, 640, seed=2)
+    return fr
+
+
+def test_config2_all_joint_tiles_bit_exact(c2):
+    dev = torch.from_numpy(c2).cuda()
+    got = patchdb.featurize_tiles(dev, 60, 80, 4, "joint").cpu().numpy()
+    want = oracle.featurize_tiles(c2, 60, 80, 4, 1)
+    assert got.shape == want.shape == (64000, 64)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.skipif(oracle.ref() is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("bins", [4, 8])
+def test_config2_all_per_channel_tiles_equal_reference(c2, bins):
+    """transform(generate(frames, tiles 80x60), color_histogram{B}) of the
+    reference itself, all 64,000 tiles."""
+    dev = torch.from_numpy(c2).cuda()
+    got = patchdb.featurize_tiles(dev, 60, 80, bins, "per_channel").cpu().numpy()
+    want = oracle.ref_featurize_tiles(c2, 60, 80, bins, threads=THREADS)
+    assert got.shape == want.shape == (64000, 3 * bins)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_config2_full_pair_set_equals_brute_force(c2):
+    """The 1000-frame pipeline through the public featurize_join call, and
+    the plain brute-force join (2.05e9 fp64 pair evaluations) of the
+    restatement's features."""
+    feats, res = patchdb.featurize_join(c2, 60, 80, 4, "joint", 0.05, want_features=True)
+    want_f = oracle.featurize_tiles(c2, 60, 80, 4, 1)
+    assert np.array_equal(_bits(feats), _bits(want_f))
+    ol, orr, od = oracle.sim_join(want_f, None, 0.05, self_join=True, threads=THREADS)
+    assert len(ol) > 500
+    _assert_same(res, ol, orr, od)
+
+
+# ---------------------------------------------------------------------------
+# config 5
+
+@pytest.fixture(scope="module")
+def c5():
+    return workloads.config5()
+
+
+def _pairs_of_rows(l, r, d, rows, n):
+    """Device pairs (i < j) touching `rows`, as the rows' full neighbourhoods:
+    sorted (row, other, dist) with other != row (both orientations)."""
+    flag = torch.zeros(n, dtype=torch.bool, device=l.device)
+    flag[torch.from_numpy(rows).to(l.device)] = True
+    a = flag[l.long()]
+    b = flag[r.long()]
+    out = torch.cat([torch.stack([l[a], r[a]], 1), torch.stack([r[b], l[b]], 1)]).cpu().numpy()
+    dist = torch.cat([d[a], d[b]]).cpu().numpy()
+    o = np.lexsort((out[:, 1], out[:, 0]))
+    return out[o, 0], out[o, 1], dist[o]
+
+
+def _checksum(l, r, d):
+    """Order-independent checksum of a pair set: count and two wrapping
+    int64 sums of mixed (left, right, dist bits)."""
+    l64, r64 = l.long(), r.long()
+    db = d.view(torch.int32).long()
+    h1 = (l64 * 0x9E3779B1 + r64 * 0x85EBCA77 + db * 0xC2B2AE3D) * 0x27D4EB2F
+    h2 = (l64 * 0x165667B1 ^ r64 * 0xD3A2646C) + db
+    return int(l.numel()), int(h1.sum()), int(h2.sum())
+
+
+def test_config5_full_size_sampled_neighbourhoods(c5, monkeypatch):
+    x = c5
+    n = x.shape[0]
+    dx = torch.from_numpy(x).cuda()
+    res = patchdb.sim_join_device(dx, None, 0.01, self_join=True)
+    l, r, d = res.to_torch(dx.device, copy=False)
+    assert res.count > 5e8
+    deg = torch.bincount(l.long(), minlength=n) + torch.bincount(r.long(), minlength=n)
+    heavy = torch.topk(deg, 128).indices.cpu().numpy()
+    rows = np.unique(np.concatenate([np.arange(0, n, n // 256), np.arange(2_000_000, 2_000_064),
+                                     heavy]))
+    gl, gr, gd = _pairs_of_rows(l, r, d, rows, n)
+    ol, orr, od = oracle.sim_join_rows(x, x, 0.01, rows, self_join=False, threads=THREADS)
+    keep = ol != orr
+    ol, orr, od = ol[keep], orr[keep], od[keep]
+    assert np.array_equal(gl, ol) and np.array_equal(gr, orr)
+    assert np.array_equal(gd, od.astype(np.float32))
+    assert deg[torch.from_numpy(heavy).cuda()].min().item() > 1000   # cluster rows
+    # grouped (default for this candidate-heavy join) vs row-major re-check:
+    # the same ~1e9 pairs
+    c_default = _checksum(l, r, d)
+    del l, r, d
+    res.free()
+    monkeypatch.setenv("PDB_K3_GROUPED", "0")
+    res2 = patchdb.sim_join_device(dx, None, 0.01, self_join=True)
+    c_rowmajor = _checksum(*res2.to_torch(dx.device, copy=False))
+    assert c_default == c_rowmajor
+    res2.free()
+
+
+# ---------------------------------------------------------------------------
+# config 4 (restated cosine): every planted near-duplicate found
+
+def test_config4_planted_pairs_found():
+    x, dst, src = workloads.config4(device="cuda", return_planted=True)
+    out = patchdb.cosine_join_bf16_device(x, None, 0.95, self_join=True, sort=True)
+    l, r, c = (t.cpu().numpy() for t in out.to_torch(x.device))
+    got = set(zip(l.tolist(), r.tolist()))
+    b = workloads.bf16_bits(x)
+    qualifying = 0
+    for a, s in zip(dst.tolist(), src.tolist()):
+        if a == s:
+            continue
+        cos = oracle.cosine_bf16(b[a], b[s])
+        if cos >= 0.95:
+            qualifying += 1
+            assert (min(a, s), max(a, s)) in got, (a, s, cos)
+    assert qualifying >= 0.9 * len(dst)

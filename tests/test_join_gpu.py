@@ -234,3 +234,98 @@ def test_cta_pair_screen_opt_in(monkeypatch):
         ol, orr, od = oracle.sim_join(L, R, tau, self_join=m is None)
         assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
         assert np.array_equal(got.dist, od.astype(np.float32))
+
+
+def test_record_overflow_rescreen(monkeypatch):
+    """PDB_TEST_REC_CAP caps the first pass's candidate-record buffer: the
+    join must detect the overflow, re-run the screen with the exact record
+    count (screen_passes == 2) and still return the oracle's pair set; the
+    same on a join large enough for the sampled sizing pass."""
+    x = workloads.config1()
+    ol, orr, od = oracle.sim_join(x, None, 0.05, self_join=True)
+    monkeypatch.setenv("PDB_TEST_REC_CAP", "1000")
+    xt = torch.from_numpy(x).cuda()
+    r = patchdb.sim_join_device(xt, None, 0.05, self_join=True, sort=True)
+    assert r.stats.screen_passes == 2 and r.stats.candidates > 1000
+    l_, r_, d_ = (t.cpu().numpy() for t in r.to_torch(xt.device))
+    assert np.array_equal(l_, ol) and np.array_equal(r_, orr)
+    assert np.array_equal(d_, od.astype(np.float32))
+    big = workloads.config5(262_144)
+    bt = torch.from_numpy(big).cuda()
+    monkeypatch.delenv("PDB_TEST_REC_CAP")
+    ref = patchdb.sim_join_device(bt, None, 0.01, self_join=True, sort=True)
+    want = [t.cpu().numpy() for t in ref.to_torch(bt.device)]
+    assert ref.stats.screen_passes == 1
+    monkeypatch.setenv("PDB_TEST_REC_CAP", "4096")
+    got = patchdb.sim_join_device(bt, None, 0.01, self_join=True, sort=True)
+    assert got.stats.screen_passes == 2
+    for a, b in zip(want, (t.cpu().numpy() for t in got.to_torch(bt.device))):
+        assert np.array_equal(a, b)
+    rows = np.arange(0, big.shape[0], 4096)
+    ol, orr, od = oracle.sim_join_rows(big, None, 0.01, rows, self_join=True)
+    m = np.isin(want[0], rows)
+    assert np.array_equal(want[0][m], ol) and np.array_equal(want[1][m], orr)
+
+
+def test_pair_overflow_rerun(monkeypatch):
+    """PDB_TEST_OUT_CAP caps the first pair buffer: only the re-check re-runs."""
+    x = workloads.config1(8000, seed=5)
+    ol, orr, od = oracle.sim_join(x, None, 0.05, self_join=True)
+    monkeypatch.setenv("PDB_TEST_OUT_CAP", "100")
+    res = patchdb.sim_join(x, None, 0.05, self_join=True)
+    assert len(ol) > 100
+    _check(res, ol, orr, od)
+
+
+@pytest.mark.parametrize("case", ["config5_self", "band_cross_permR", "odd_d61"])
+def test_grouped_recheck_bit_identical(monkeypatch, case):
+    """The grouped re-check (k_group_copy + k_recheck<true>, forced with
+    PDB_K3_GROUPED=2) and the row-major one (=0) return bit-identical sorted
+    output, equal to the oracle: self join, a band-plan cross join (column
+    permutation permR) and d % 8 != 0."""
+    rng = np.random.default_rng(61)
+    if case == "config5_self":
+        L, R, tau, self_join = workloads.config5(131_072), None, 0.01, True
+    elif case == "band_cross_permR":
+        L, R, _, _ = workloads.config3(n=65_536)
+        tau, self_join = 0.02, False
+    else:
+        L = workloads.clusters(20_000, 61, 150, 0.02, True, 61)
+        R = (L[rng.integers(0, 20_000, 9000)] + rng.normal(0, 2e-4, (9000, 61))).astype(np.float32)
+        tau, self_join = 0.01, False
+    Lt = torch.from_numpy(L).cuda()
+    Rt = None if R is None else torch.from_numpy(R).cuda()
+    outs = []
+    for mode in ("2", "0"):
+        monkeypatch.setenv("PDB_K3_GROUPED", mode)
+        r = patchdb.sim_join_device(Lt, Rt, tau, self_join=self_join, sort=True)
+        outs.append([t.cpu().numpy() for t in r.to_torch(Lt.device)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert len(outs[0][0]) > 300
+    rows = np.arange(0, L.shape[0], 97)
+    ol, orr, od = oracle.sim_join_rows(L, R, tau, rows, self_join=self_join)
+    m = np.isin(outs[0][0], rows)
+    assert np.array_equal(outs[0][0][m], ol) and np.array_equal(outs[0][1][m], orr)
+    assert np.array_equal(outs[0][2][m], od.astype(np.float32))
+
+
+def test_nan_tau_matches_nothing_like_the_reference():
+    """The reference rejects only tau < 0 (src/query.cpp:488); a NaN tau
+    passes and emits no pairs (every `euclidean <= NaN` is false)."""
+    x = workloads.config1(3000, seed=2)
+    assert len(patchdb.sim_join(x, None, float("nan"), self_join=True)) == 0
+    assert len(patchdb.sim_join(x, x, float("nan"))) == 0
+    g = patchdb.dedup(x, float("nan"))
+    assert len(g.reps) == 3000
+    with pytest.raises(patchdb.ConfigError):
+        patchdb.sim_join(x, None, -1e-300, self_join=True)
+
+
+def test_release_caches():
+    from paper_1812_07607_b200 import _capi as capi
+    x = workloads.config5(262_144)
+    a = patchdb.sim_join(x, None, 0.01, self_join=True)
+    assert capi.lib().pdb_release_caches() == 0
+    b = patchdb.sim_join(x, None, 0.01, self_join=True)
+    assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)

@@ -158,3 +158,61 @@ def test_nlj_within_and_q1_restatement_match_reference_golden():
         bj = np.concatenate([j, i]).astype(np.int64)
         order = np.lexsort((ai, bj))          # probe (right) order, then build id
         assert np.array_equal(ai[order], a) and np.array_equal(bj[order], b), name
+
+
+# ---- the faster exact restatements used at full size ----------------------
+
+def _same(a, b):
+    return all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 7, 64, 128])
+def test_pruned_and_rows_equal_plain_brute_force(d):
+    from paper_1812_07607_b200 import workloads
+    rng = np.random.default_rng(d)
+    L = workloads.clusters(1500, d, 30, 0.02, False, d)
+    R = np.concatenate([L[:400] + rng.normal(0, 0.01, (400, d)).astype(np.float32),
+                        workloads.clusters(900, d, 30, 0.02, False, d + 1)]).astype(np.float32)
+    for tau in (0.0, 0.02, 0.05, 0.3, 1e200):
+        want = oracle.sim_join(L, R, tau, threads=4)
+        assert _same(oracle.sim_join_pruned(L, R, tau, threads=3), want)
+        rows = np.arange(0, 1500, 7)
+        m = np.isin(want[0], rows)
+        assert _same(oracle.sim_join_rows(L, R, tau, rows, threads=5),
+                     (want[0][m], want[1][m], want[2][m]))
+        ws = oracle.sim_join(L, None, tau, self_join=True, threads=4)
+        assert _same(oracle.sim_join_pruned(L, None, tau, self_join=True), ws)
+
+
+def test_pruned_edge_rows_and_boundaries():
+    rng = np.random.default_rng(3)
+    L = rng.random((700, 24), dtype=np.float32)
+    R = L.copy()
+    R[:, 0] += np.float32(0.25)            # distance exactly 0.25 for many rows
+    L[5, 3] = np.nan
+    L[6, 0] = np.inf
+    R[7] = -np.inf
+    L[8] = 3e30
+    R[9] = 3e30
+    R[10] = 3e30
+    L[11] = 1e19
+    R[12] = 1e19
+    L[13, 2] = 7e12                          # beyond the grid: compared against all
+    R[14, 2] = 7e12
+    for tau in (0.25, np.nextafter(0.25, 0), 0.0, 1.5, float("inf")):
+        want = oracle.sim_join(L, R, tau, threads=4)
+        assert _same(oracle.sim_join_pruned(L, R, tau), want), tau
+        assert _same(oracle.sim_join_rows(L, R, tau, np.arange(700)), want), tau
+    assert len(oracle.sim_join_pruned(L, R, float("nan"))[0]) == 0
+    with pytest.raises(RuntimeError):
+        oracle.sim_join_pruned(L, R, -1.0)
+
+
+@pytest.mark.skipif(oracle.ref() is None, reason="oracle/_ref not built")
+def test_pruned_equals_reference_sim_join():
+    from paper_1812_07607_b200 import workloads
+    x = workloads.config1(4000, seed=9)
+    li, ri, _ = oracle.ref_sim_join(x, x, 0.05, 2)
+    m = li < ri
+    ol, orr, _ = oracle.sim_join_pruned(x, None, 0.05, self_join=True)
+    assert np.array_equal(golden_io.canonical(ol, orr), golden_io.canonical(li[m], ri[m]))
