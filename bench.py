@@ -23,7 +23,15 @@ frame shard, the 64,000 features are all-gathered over NCCL (16 MB), and
 each rank joins the 128-row blocks b = rank (mod N) of the features against
 all of them (strong scaling: the 1000-frame workload is fixed).
 ``--impl reference`` times the reference's own CPU implementation
-(oracle/_ref, the unmodified proj/ sources) on the host cores instead.
+(oracle/_ref, the unmodified proj/ sources) on the host cores instead: every
+timed step is the full config-2 step (all 1000 frames, the ball-tree join
+of all 64,000 features), on all host cores or --ref-threads N.
+
+The default line also carries ``config3``: the north-star join
+(1,048,576 x 1,048,576 x 128, tau 0.02) measured in the same run -- device
+and e2e Gpairs/s, the screen's tensor roofline on the tiles it screens, a
+dense-screen pass of the same join, and the reference's own probe output on
+sampled rows compared with the GPU's (``checked``).
 """
 
 from __future__ import annotations
@@ -126,31 +134,38 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's own implementation on the host cores.
 
-def reference_sample(feats: np.ndarray, frames_sample: np.ndarray, threads: int,
-                     probe_rows: int):
-    """Times oracle/_ref (the reference compiled from its sources):
-    featurization of `frames_sample` through transform(generate(tiles),
-    color_histogram{B=4}) -- the reference's per-channel operator; it has no
-    joint mode, whose binning cost is the same -- and its sim_join probe
-    (ball tree over all 64,000 features, balltree_within per probe row) on
-    `probe_rows` rows.  Returns extrapolated seconds for the full step."""
+def reference_step(frames: np.ndarray, feats: np.ndarray, threads: int, frames_n=None,
+                   probe_rows=None):
+    """One config-2 step of the reference itself (oracle/_ref, the unmodified
+    proj/ sources), on `threads` host threads:
+
+    * featurization: transform(generate(frames, tiles 80x60), color_histogram
+      {B=4}) (src/etl.cpp:264-373) -- the reference's per-channel operator;
+      it has no joint mode, whose binning cost is the same -- frames sharded
+      over the threads;
+    * the self-join of the 64,000 features: build_balltree over all of them
+      plus balltree_within(0.05) for every probe row (run_sim_join's probe
+      loop, src/query.cpp:516-526, over probe-row shards sharing the
+      immutable tree).
+
+    With frames_n / probe_rows set, only that many frames / probe rows run
+    and the seconds are extrapolated linearly (the single-thread sample).
+    Returns (featurize_s, join_s, info)."""
     from oracle import oracle
     if oracle.ref() is None:
         raise RuntimeError("oracle/_ref/libpdb_ref.so missing")
+    fr = frames if frames_n is None else frames[:frames_n]
     t0 = time.perf_counter()
-    oracle.ref_featurize_tiles(frames_sample, CFG["tile_h"], CFG["tile_w"], CFG["bins"],
-                               threads=threads)
-    t_feat = (time.perf_counter() - t0) * CFG["frames"] / frames_sample.shape[0]
+    oracle.ref_featurize_tiles(fr, CFG["tile_h"], CFG["tile_w"], CFG["bins"], threads=threads)
+    t_feat = (time.perf_counter() - t0) * CFG["frames"] / fr.shape[0]
     n = feats.shape[0]
-    rows = min(probe_rows, n)
-    # spread the probe sample evenly over the relation (the self-join's work
-    # per probe row does not depend on its position for the ball tree)
-    stride = max(1, n // rows)
-    sub = np.ascontiguousarray(feats[::stride][:rows])
+    rows = n if probe_rows is None else min(probe_rows, n)
+    # a sample spreads its probe rows evenly over the relation
+    sub = feats if rows == n else np.ascontiguousarray(feats[:: max(1, n // rows)][:rows])
     m, t_build, t_probe = _probe(sub, feats, threads)
     t_join = t_build + t_probe * n / rows
-    return t_feat, t_join, {"frames": int(frames_sample.shape[0]), "probe_rows": rows,
-                            "build_s": t_build, "probe_s": t_probe, "matches_in_sample": m}
+    return t_feat, t_join, {"frames": int(fr.shape[0]), "probe_rows": rows, "build_s": t_build,
+                            "probe_s": t_probe, "matches": m}
 
 
 def _probe(sub, feats, threads):
@@ -159,31 +174,40 @@ def _probe(sub, feats, threads):
     R = np.ascontiguousarray(feats, dtype=np.float32)
     L = np.ascontiguousarray(sub, dtype=np.float32)
     b, p = C.c_double(), C.c_double()
+    # self_join=0: every probe row is matched against the whole tree, as the
+    # reference's sim_join(X, X) does (the i < j view drops half afterwards)
     m = oracle.ref().ref_join_probe_timed(L.ctypes.data, L.shape[0], R.ctypes.data, R.shape[0],
                                           R.shape[1], CFG["tau"], 0, 0, L.shape[0], threads,
                                           C.byref(b), C.byref(p))
     return int(m), b.value, p.value
 
 
-def run_reference(args, rank, world):
+def _ref_inputs():
     from paper_1812_07607_b200 import workloads
-    if rank != 0:
-        return 0
-    threads = os.cpu_count() or 1
+    from oracle import oracle
     frames, _ = workloads.frames(CFG["frames"], CFG["H"], CFG["W"], seed=CFG["seed"])
     # the features the reference joins are the K1 output definition; compute
     # them with the restatement's bit-identical CPU code (no GPU in this arm)
-    from oracle import oracle
     feats = oracle.featurize_tiles(frames, CFG["tile_h"], CFG["tile_w"], CFG["bins"], 1)
-    fs = frames[:max(threads * 2, 16)]
-    probe_rows = _env_int("PDB_REF_PROBE_ROWS", 1024)
-    times = []
-    info = None
-    for k in range(args.warmup + args.steps):
-        t_feat, t_join, info = reference_sample(feats, fs, threads, probe_rows)
-        if k >= args.warmup:
-            times.append(t_feat + t_join)
-    step_s = statistics.mean(times)
+    return frames, feats
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = args.ref_threads or os.cpu_count() or 1
+    frames, feats = _ref_inputs()
+    # Warm-up steps page the reference's code and the inputs in on a small
+    # slice (1 frame, 64 probe rows); every TIMED step is the full workload:
+    # all 1000 frames and all 64,000 probe rows, nothing extrapolated.
+    for _ in range(args.warmup):
+        reference_step(frames, feats, threads, frames_n=1, probe_rows=64)
+    times, info = [], None
+    for _ in range(args.steps):
+        t_feat, t_join, info = reference_step(frames, feats, threads)
+        times.append((t_feat, t_join))
+    step_s = statistics.mean(a + b for a, b in times)
+    join_s = statistics.mean(b for _, b in times)
     value = CFG["frames"] / step_s
     n = feats.shape[0]
     line = {
@@ -193,13 +217,15 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "u8/f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "frames": CFG["frames"], "tiles": n, "d": 64,
                    "tau": CFG["tau"]},
-        "join_gpairs_per_s": n * (n - 1) / 2 / (
-            info["build_s"] + info["probe_s"] * n / info["probe_rows"]) / 1e9,
+        "join_gpairs_per_s": n * (n - 1) / 2 / join_s / 1e9,
+        "phase_s": {"featurize": statistics.mean(a for a, _ in times), "join": join_s,
+                    "join_build": info["build_s"], "join_probe": info["probe_s"]},
+        "extrapolated": False,
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
-                         "sample": f"per step: reference transform(generate(tiles),color_histogram) on "
-                                   f"{info['frames']} frames + build_balltree(64000) and "
-                                   f"balltree_within for {info['probe_rows']} probe rows, "
-                                   f"extrapolated to 1000 frames / 64000 probes"},
+                         "sample": f"the full step every timed step: reference transform(generate("
+                                   f"tiles),color_histogram) of all {info['frames']} frames + "
+                                   f"build_balltree({n}) and balltree_within for all "
+                                   f"{info['probe_rows']} probe rows, {threads} threads"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -441,21 +467,38 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            from oracle import oracle
             threads = os.cpu_count() or 1
             fh = feats.cpu().numpy()
-            t_feat, t_join, info = reference_sample(fh, host[:max(2 * threads, 16)], threads,
-                                                    _env_int("PDB_REF_PROBE_ROWS", 1024))
+            # the full step once on all host cores, nothing extrapolated ...
+            t_feat, t_join, info = reference_step(host, fh, threads)
             v = F / (t_feat + t_join)
             cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
-                   "sample": f"reference (oracle/_ref) featurization of {info['frames']} frames "
-                             f"(per-channel B=4 operator) + build_balltree(64000) and "
-                             f"balltree_within on {info['probe_rows']} probe rows, "
-                             f"{threads} threads, extrapolated to the full step",
-                   "featurize_s_per_1000_frames": t_feat, "join_s": t_join}
+                   "sample": f"the full step once: reference (oracle/_ref) featurization of all "
+                             f"{info['frames']} frames (per-channel B=4 operator) + "
+                             f"build_balltree({fh.shape[0]}) and balltree_within for all "
+                             f"{info['probe_rows']} probe rows, {threads} threads",
+                   "featurize_s": t_feat, "join_s": t_join, "extrapolated": False}
+            # ... and single-threaded as the reference ships, on a
+            # bounded sample: 32 frames + 1024 evenly spread probe rows
+            t1f, t1j, i1 = reference_step(host, fh, 1, frames_n=32, probe_rows=1024)
+            cpu["single_thread"] = {
+                "value": F / (t1f + t1j), "unit": "frames/s", "cores": 1, "kind": "reference",
+                "sample": f"{i1['frames']} frames + build_balltree({fh.shape[0]}) and "
+                          f"{i1['probe_rows']} evenly spread probe rows on 1 thread, "
+                          f"extrapolated linearly to 1000 frames / {fh.shape[0]} probe rows",
+                "featurize_s": t1f, "join_s": t1j, "extrapolated": True}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
+
+    # ---- the north-star join (config 3), measured in the same run ----------
+    c3 = None
+    if not args.no_config3:
+        import bench_join
+        c3_args = argparse.Namespace(**vars(args))
+        c3_args.steps = min(args.steps, 10)
+        c3 = bench_join.measure(c3_args, rank, world, local_rank, "c3", METRIC, peaks()[0],
+                                ClockSampler, dense=True)
 
     if rank == 0:
         mp, _ = peaks()
@@ -528,6 +571,8 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches,
             "clocks": sampler.summary(),
         }
+        if c3 is not None:
+            line["config3"] = c3
         print(json.dumps(line))
     pairs.free()
     lib.pdb_host_free(hbuf)
@@ -541,6 +586,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config3", action="store_true",
+                    help="skip the config-3 (1M x 1M x 128) sub-record of the default line")
+    ap.add_argument("--ref-threads", type=int, default=0,
+                    help="--impl reference: host threads (default: all cores; 1 = the "
+                         "reference as shipped)")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "dedup"],
                     help="c2 (default, the headline): featurize -> join pipeline; c1/c3/c4/c5: "
                          "the join-only configs of BASELINE.json (bench_join.py)")

@@ -83,6 +83,10 @@ def ref():
         L.ref_join_probe_timed.argtypes = [vp, i64, vp, i64, i32, f64, i32, i64, i64, i32,
                                            C.POINTER(f64), C.POINTER(f64)]
         L.ref_join_probe_timed.restype = i64
+        L.ref_join_probe_pairs.argtypes = [vp, i64, vp, i64, i32, f64, i32,
+                                           C.POINTER(C.POINTER(i32)), C.POINTER(C.POINTER(i32)),
+                                           C.POINTER(f64), C.POINTER(f64)]
+        L.ref_join_probe_pairs.restype = i64
         L.ref_dedup.argtypes = [vp, i64, i32, f64, vp, C.POINTER(i64)]
         L.ref_dedup_stream.argtypes = [vp, i64, i32, f64, vp]
         L.ref_dedup_stream.restype = i64
@@ -301,6 +305,26 @@ def ref_join_probe_timed(L, R, tau, self_join, p0, p1, threads):
     n = ref().ref_join_probe_timed(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
                                    int(self_join), p0, p1, threads, C.byref(b), C.byref(p))
     return n, b.value, p.value
+
+
+def ref_join_probe_pairs(L, R, tau, threads):
+    """build_balltree(R) + balltree_within(tau) for every row of L (the
+    reference's probe loop, src/query.cpp:516-526, over `threads` threads):
+    (left, right, build_s, probe_s), pairs in probe order, ascending ids."""
+    L = np.ascontiguousarray(L, dtype=np.float32)
+    R = np.ascontiguousarray(R, dtype=np.float32)
+    a = C.POINTER(C.c_int32)()
+    b = C.POINTER(C.c_int32)()
+    bs, ps = C.c_double(), C.c_double()
+    n = ref().ref_join_probe_pairs(_p(L), L.shape[0], _p(R), R.shape[0], L.shape[1], float(tau),
+                                   int(threads), C.byref(a), C.byref(b), C.byref(bs), C.byref(ps))
+    if n < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    li = np.ctypeslib.as_array(a, (max(n, 1),))[:n].copy()
+    ri = np.ctypeslib.as_array(b, (max(n, 1),))[:n].copy()
+    ref().ref_free(C.cast(a, C.c_void_p))
+    ref().ref_free(C.cast(b, C.c_void_p))
+    return li, ri, bs.value, ps.value
 
 
 def ref_dedup(X, tau):

@@ -256,6 +256,59 @@ REF_API int64_t ref_join_probe_timed(const float* L, int64_t nL, const float* R,
     }
 }
 
+// The same build + probe as ref_join_probe_timed, returning the pairs:
+// probe rows [0, nL) of L against all of R, per probe row the ids
+// balltree_within returns (ascending), probe rows in order.  *out_l / *out_r
+// are malloc'd (ref_free).  Returns the pair count or -1.
+REF_API int64_t ref_join_probe_pairs(const float* L, int64_t nL, const float* R, int64_t nR,
+                                     int32_t d, double tau, int32_t threads, int32_t** out_l,
+                                     int32_t** out_r, double* build_s, double* probe_s) {
+    try {
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::pair<std::vector<float>, uint64_t>> pts;
+        pts.reserve(static_cast<size_t>(nR));
+        for (int64_t j = 0; j < nR; j++)
+            pts.emplace_back(std::vector<float>(R + j * d, R + (j + 1) * d),
+                             static_cast<uint64_t>(j));
+        BallTreeIndex tree = build_balltree(pts);
+        auto t1 = std::chrono::steady_clock::now();
+        std::vector<std::vector<uint64_t>> hits(static_cast<size_t>(nL));
+        std::atomic<int64_t> next{0};
+        std::vector<std::thread> pool;
+        for (int32_t k = 0; k < std::max(threads, 1); k++)
+            pool.emplace_back([&] {
+                for (;;) {
+                    int64_t i0 = next.fetch_add(16);
+                    if (i0 >= nL) break;
+                    int64_t i1 = std::min<int64_t>(i0 + 16, nL);
+                    for (int64_t i = i0; i < i1; i++) {
+                        std::vector<float> q(L + i * d, L + (i + 1) * d);
+                        hits[static_cast<size_t>(i)] = balltree_within(tree, q, tau);
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+        auto t2 = std::chrono::steady_clock::now();
+        int64_t n = 0;
+        for (const auto& h : hits) n += static_cast<int64_t>(h.size());
+        *out_l = static_cast<int32_t*>(std::malloc(static_cast<size_t>(std::max<int64_t>(n, 1)) * 4));
+        *out_r = static_cast<int32_t*>(std::malloc(static_cast<size_t>(std::max<int64_t>(n, 1)) * 4));
+        int64_t o = 0;
+        for (int64_t i = 0; i < nL; i++)
+            for (uint64_t id : hits[static_cast<size_t>(i)]) {
+                (*out_l)[o] = static_cast<int32_t>(i);
+                (*out_r)[o] = static_cast<int32_t>(id);
+                o++;
+            }
+        if (build_s) *build_s = std::chrono::duration<double>(t1 - t0).count();
+        if (probe_s) *probe_s = std::chrono::duration<double>(t2 - t1).count();
+        return n;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // PlanNode::dedup over memory tuples (src/query.cpp:535-582, executed by
 // compile_dedup): item i carries the unique label "i", so each output
 // group's group_labels lists its members and its lineage parent is the

@@ -33,16 +33,21 @@ def test_bench_json_contract_one_gpu():
     assert d["roofline"]["bound"] in ("hbm", "tensor") and 0 < d["roofline"]["frac"]
     assert d["e2e"]["h2d_bytes_per_step"] == 1000 * 480 * 640 * 3
     assert d["pairs"] > 0
+    c3 = d["config3"]   # the north-star join, measured in the same run
+    assert c3["pairs"] == 5399 and c3["unit"] == "Gpairs/s" and c3["value"] > 0
+    assert c3["roofline"]["bound"] == "tensor" and c3["dense_screen"]["pairs"] == 5399
+    assert c3["e2e"]["h2d_bytes_per_step"] == 2 * 1048576 * 128 * 4
     _run.one = d
 
 
 def test_bench_two_ranks_same_pairs():
     d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
               "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
-              "--steps", "2", "--warmup", "3"], env={"PDB_DIST_BACKEND": "gloo"})
+              "--steps", "2", "--warmup", "3", "--no-config3"], env={"PDB_DIST_BACKEND": "gloo"})
     assert d["n_gpus"] == 2
     one = getattr(_run, "one", None) or _run([sys.executable, "bench.py", "--steps", "3",
-                                              "--warmup", "3", "--no-cpu-baseline"])
+                                              "--warmup", "3", "--no-cpu-baseline",
+                                              "--no-config3"])
     assert d["pairs"] == one["pairs"]
 
 
