@@ -135,27 +135,41 @@ std::vector<std::pair<size_t, size_t>> sim_join_positions(const std::vector<Patc
                 throw DuplicatePatchIdError("patch id " + std::to_string(p.patch_id) +
                                             " appears twice on the build side");
     }
-    const std::vector<float> L = detail::pack(left, dl), R = detail::pack(right, dl);
+    // Emission order: probe order, then ascending build-side patch id
+    // (balltree_within sorts ids).  When the build side's ids ascend with
+    // its positions (the usual case) that is the device's sorted (probe,
+    // build) order: the probe side goes in as L with PDB_JOIN_SORTED and no
+    // host sort is needed.  Otherwise the pairs are sorted here.
+    const auto& probe = chosen == BuildSide::left ? right : left;
+    bool ids_ascend = true;
+    for (size_t i = 1; i < build.size() && ids_ascend; i++)
+        ids_ascend = build[i - 1].patch_id < build[i].patch_id;
+    const std::vector<float> P = detail::pack(probe, dl), B = detail::pack(build, dl);
     pdb_join_opts o{};
+    o.flags = ids_ascend ? PDB_JOIN_SORTED : 0u;
     pdb_pairs pr{};
-    check(pdb_sim_join(L.data(), static_cast<int64_t>(left.size()), R.data(),
-                       static_cast<int64_t>(right.size()), static_cast<int32_t>(dl), tau, &o, &pr));
+    check(pdb_sim_join(P.data(), static_cast<int64_t>(probe.size()), B.data(),
+                       static_cast<int64_t>(build.size()), static_cast<int32_t>(dl), tau, &o, &pr));
     std::vector<std::pair<size_t, size_t>> out(static_cast<size_t>(pr.count));
-    for (int64_t k = 0; k < pr.count; k++)
-        out[static_cast<size_t>(k)] = {static_cast<size_t>(pr.left[k]),
-                                       static_cast<size_t>(pr.right[k])};
+    const bool swap = chosen == BuildSide::left;  // pairs are (left pos, right pos)
+    for (int64_t k = 0; k < pr.count; k++) {
+        const size_t pi = static_cast<size_t>(pr.left[k]), bi = static_cast<size_t>(pr.right[k]);
+        out[static_cast<size_t>(k)] = swap ? std::pair<size_t, size_t>{bi, pi}
+                                           : std::pair<size_t, size_t>{pi, bi};
+    }
     pdb_pairs_free(&pr);
-    // probe order, then ascending build-side patch id (balltree_within sorts ids)
-    if (chosen == BuildSide::left) {
-        std::sort(out.begin(), out.end(), [&](const auto& a, const auto& b) {
-            if (a.second != b.second) return a.second < b.second;
-            return left[a.first].patch_id < left[b.first].patch_id;
-        });
-    } else {
-        std::sort(out.begin(), out.end(), [&](const auto& a, const auto& b) {
-            if (a.first != b.first) return a.first < b.first;
-            return right[a.second].patch_id < right[b.second].patch_id;
-        });
+    if (!ids_ascend) {
+        if (chosen == BuildSide::left) {
+            std::sort(out.begin(), out.end(), [&](const auto& a, const auto& b) {
+                if (a.second != b.second) return a.second < b.second;
+                return left[a.first].patch_id < left[b.first].patch_id;
+            });
+        } else {
+            std::sort(out.begin(), out.end(), [&](const auto& a, const auto& b) {
+                if (a.first != b.first) return a.first < b.first;
+                return right[a.second].patch_id < right[b.second].patch_id;
+            });
+        }
     }
     if (index_probes) *index_probes = chosen == BuildSide::left ? right.size() : left.size();
     return out;

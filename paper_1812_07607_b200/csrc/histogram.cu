@@ -27,6 +27,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "pdb_internal.cuh"
 #include "tc_ptx.cuh"
@@ -316,10 +318,12 @@ __device__ __forceinline__ uint32_t pix_offset(uint32_t p) {
     return __umulhi(p, PixMap<LB>::kM) & PixMap<LB>::kQ;
 }
 
-template <int LB, int S>
+template <int LB, int G, bool BULK>
 __global__ void __launch_bounds__(17 * 32, 1)
-k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty, int H, int th,
-                   int tw, int ntx, uint32_t stage_bytes, float npix, const FeatOuts outs) {
+k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ frames,
+                   int n_rows, int nty, int H, int W3, int th, int tw, int ntx,
+                   uint32_t stage_bytes, int S, int pf, int skip_epi, float npix,
+                   const __grid_constant__ FeatOuts outs) {
     constexpr int NB = 1 << (3 * LB);
     constexpr int B = 1 << LB;
     constexpr int NWD = PixMap<LB>::kWords;        // counter words per lane
@@ -332,6 +336,8 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
     uint8_t* stages = smem_r8 + cpad + ntx * 2048;  // 128-B aligned TMA destinations
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + S * stage_bytes);
     uint64_t* empty = full + S;
+    // per-warp park area for the epilogue's lane sums (32 words)
+    uint32_t* park = reinterpret_cast<uint32_t*>(empty + S) + warp * 32;
     const int segs = tw >> 4;
     const int RB = 96 / (3 * segs);
     const int nb = (th + RB - 1) / RB;
@@ -350,14 +356,41 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
         if (lane == 0) {
             ptx::tma_prefetch_desc(&tmap);
             uint32_t it = 0;
+            // L2 prefetch cursor, pf bands ahead of the loads: the bands in
+            // flight to L2 need no shared memory, so the CTA keeps far more
+            // bytes in flight than its S stages hold
+            int p_tr = blockIdx.x, p_bt = 0;
+            auto prefetch_next = [&] {
+                if (p_tr >= n_rows) return;
+                const int pf_f = p_tr / nty, pf_ty = p_tr - pf_f * nty;
+                const int rows = min(RB, th - p_bt * RB);
+                ptx::bulk_prefetch_l2(frames + (static_cast<size_t>(pf_f) * H + pf_ty * th + p_bt * RB) * W3,
+                                      static_cast<uint32_t>(rows) * W3);
+                if (++p_bt == nb) {
+                    p_bt = 0;
+                    p_tr += gridDim.x;
+                }
+            };
+            for (int k = 0; k < pf; k++) prefetch_next();
             for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
                 const int f = tr / nty, ty = tr - f * nty;
                 const int row0 = f * H + ty * th;
                 for (int bt = 0; bt < nb; bt++, it++) {
+                    if (pf > 0) prefetch_next();
                     const uint32_t s = it % S;
-                    if (it >= S) ptx::mbar_wait_sleep(&empty[s], ((it / S) - 1) & 1);
-                    ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
-                    ptx::tma_load_3d(stages + s * stage_bytes, &tmap, &full[s], 0, row0 + bt * RB, 0);
+                    if (it >= static_cast<uint32_t>(S)) ptx::mbar_wait_sleep(&empty[s], ((it / S) - 1) & 1);
+                    if (BULK) {
+                        // RB whole frame rows are one contiguous run of bytes
+                        const int rows = min(RB, th - bt * RB);
+                        const uint32_t bytes = static_cast<uint32_t>(rows) * W3;
+                        ptx::mbar_arrive_expect_tx(&full[s], bytes);
+                        ptx::bulk_load(stages + s * stage_bytes,
+                                       frames + (static_cast<size_t>(row0) + bt * RB) * W3, bytes,
+                                       &full[s]);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+                        ptx::tma_load_3d(stages + s * stage_bytes, &tmap, &full[s], 0, row0 + bt * RB, 0);
+                    }
                 }
             }
         }
@@ -377,7 +410,9 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
     // the full-band and last-band group counts are fixed per launch
     uint32_t s = 0, ph = 0;
     const int ng_full = RB * segs, ng_last = (th - (nb - 1) * RB) * segs;
-    const uint8_t* my_stage = stages + warp * tile_bytes + lane * 48;
+    // a stage is tile-major (3-D tensor box) or RB whole frame rows (bulk)
+    const uint8_t* my_stage = BULK ? stages + (lane / segs) * W3 + warp * 3 * tw + (lane % segs) * 48
+                                   : stages + warp * tile_bytes + lane * 48;
     for (int tr = blockIdx.x; tr < n_rows; tr += gridDim.x) {
         // zero the warp's counters with 16-byte stores (any lane may clear
         // any word: the block belongs to the warp)
@@ -406,46 +441,108 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
-            if (++s == S) {
+            if (++s == static_cast<uint32_t>(S)) {
                 s = 0;
                 ph ^= 1;
             }
             if (lane < ngroups) {
+                uint32_t ad[16];
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
                     // pixels 4g..4g+3: [r0 g0 b0 r1][g1 b1 r2 g2][b2 r3 g3 b3]
                     const uint32_t w0 = w[3 * g], w1 = w[3 * g + 1], w2 = w[3 * g + 2];
-                    const uint32_t px[4] = {w0, __funnelshift_r(w0, w1, 24),
-                                            __funnelshift_r(w1, w2, 16), w2 >> 8};
+                    ad[4 * g] = pix_offset<LB>(w0) | lbase;
+                    ad[4 * g + 1] = pix_offset<LB>(__funnelshift_r(w0, w1, 24)) | lbase;
+                    ad[4 * g + 2] = pix_offset<LB>(__funnelshift_r(w1, w2, 16)) | lbase;
+                    ad[4 * g + 3] = pix_offset<LB>(w2 >> 8) | lbase;
+                }
+                if (G == 0) {
+                    // (measurement only: the pipeline without the counting)
+                    uint32_t x = 0;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const uint32_t ad = pix_offset<LB>(px[k]) | lbase;
+                    for (int k = 0; k < 16; k++) x ^= ad[k];
+                    if (x == 0xFFFFFFFFu) asm volatile("st.shared.u8 [%0], %1;" ::"r"(lbase), "r"(x) : "memory");
+                } else if (G == 1) {
+                    // one dependent read-modify-write per pixel
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
                         uint32_t v;
-                        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(ad) : "memory");
-                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad), "r"(v + 1u) : "memory");
+                        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(ad[k]) : "memory");
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad[k]), "r"(v + 1u) : "memory");
+                    }
+                } else {
+                    // G pixels at a time: equal counters are merged in
+                    // registers (the first occurrence carries the group's
+                    // count), so the G reads are independent and issue back
+                    // to back -- one shared-memory latency per G pixels
+                    // instead of per pixel -- and merged pixels cost no
+                    // access at all.
+#pragma unroll
+                    for (int k0 = 0; k0 < 16; k0 += G) {
+                        constexpr int GG = G > 0 ? G : 1;
+                        uint32_t keep[GG], inc[GG], v[GG];
+#pragma unroll
+                        for (int a = 0; a < G; a++) {
+                            keep[a] = 1u;
+                            inc[a] = 1u;
+                        }
+#pragma unroll
+                        for (int a = 0; a < G; a++)
+#pragma unroll
+                            for (int b = a + 1; b < G; b++) {
+                                const uint32_t e = ad[k0 + a] == ad[k0 + b];
+                                inc[a] += e & keep[a];  // counted once, at its first occurrence
+                                keep[b] &= e ^ 1u;
+                            }
+#pragma unroll
+                        for (int a = 0; a < G; a++) {
+                            v[a] = 0u;
+                            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
+                                         "@p ld.shared.u8 %0, [%1]; }"
+                                         : "+r"(v[a]) : "r"(ad[k0 + a]), "r"(keep[a]) : "memory");
+                        }
+#pragma unroll
+                        for (int a = 0; a < G; a++)
+                            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
+                                         "@p st.shared.u8 [%0], %1; }"
+                                         ::"r"(ad[k0 + a]), "r"(v[a] + inc[a]), "r"(keep[a])
+                                         : "memory");
                     }
                 }
             }
         }
         __syncwarp();
+        // (measurement only: 1 skips the epilogue, 2 skips the lane reduction,
+        // 3 skips the feature stores)
+        if (skip_epi == 1) continue;
         // sum bytes 0,2 and 1,3 of every counter word over lanes in 16-bit
         // halves; lane l keeps the totals of bins l and l+32.
-        // Lane 0 parks the two half-sums of word wd in counter words 2wd and
-        // 2wd+1 (already read by every lane: the warp reads word wd before
-        // any store of iteration wd), then each lane fetches its two bins.
+        // Lane 0 parks the two half-sums of word wd in the warp's park area
+        // (words 2wd, 2wd+1), then each lane fetches its two bins.  (Parking
+        // inside the counter block chained every word's read behind the
+        // previous store.)  Measured alternatives, all slower on config 2: a
+        // compare-select pick of the warp-uniform sums (serial on the REDUX
+        // results, +30 us), and a shuffle reduce-scatter (register pressure
+        // costs the counting loop more than it saves).
 #pragma unroll
-        for (int wd = 0; wd < NWD; wd++) {
-            const uint32_t v = wcnt32[wd * 32 + lane];
-            const uint32_t s02 = __reduce_add_sync(0xffffffffu, v & 0x00FF00FFu);
-            const uint32_t s13 = __reduce_add_sync(0xffffffffu, (v >> 8) & 0x00FF00FFu);
-            if (lane == 0) {
-                wcnt32[2 * wd] = s02;
-                wcnt32[2 * wd + 1] = s13;
+        for (int w0 = 0; w0 < (skip_epi == 2 ? 0 : NWD); w0 += 4) {
+            uint32_t cw[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) cw[k] = w0 + k < NWD ? wcnt32[(w0 + k) * 32 + lane] : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if (w0 + k >= NWD) break;
+                const uint32_t s02 = __reduce_add_sync(0xffffffffu, cw[k] & 0x00FF00FFu);
+                const uint32_t s13 = __reduce_add_sync(0xffffffffu, (cw[k] >> 8) & 0x00FF00FFu);
+                if (lane == 0) {
+                    park[2 * (w0 + k)] = s02;
+                    park[2 * (w0 + k) + 1] = s13;
+                }
             }
         }
         __syncwarp();
         auto fetch = [&](uint32_t o) {
-            const uint32_t v2 = wcnt32[2 * (o >> 7) + (o & 1)];
+            const uint32_t v2 = park[2 * (o >> 7) + (o & 1)];
             return (o & 2) ? v2 >> 16 : v2 & 0xFFFFu;
         };
         const uint32_t mine0 = fetch(o0), mine1 = NB > 32 ? fetch(o1) : 0u;
@@ -455,10 +552,12 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, int n_rows, int nty
         const float v0 = normalise(mine0, npix), v1 = normalise(mine1, npix);
         // every output: the local features and, for a sharded step, each
         // peer's copy over NVLink (P2P stores overlapping the counting)
-        for (int k = 0; k < outs.n; k++) {
+        // (outs is a __grid_constant__ parameter: the pointers are read from
+        // the constant bank, not from a local-memory copy of the struct)
+        for (int k = 0; k < (skip_epi == 3 ? 0 : outs.n); k++) {
             float* o = outs.p[k] + ofs;
-            if (lane < NB) o[lane] = v0;
-            if (NB > 32) o[lane + 32] = v1;
+            if (lane < NB) __stcs(o + lane, v0);
+            if (NB > 32) __stcs(o + lane + 32, v1);
         }
     }
     // peer stores become visible before anything the host orders after us
@@ -671,17 +770,79 @@ void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int
         // counting warps) per SM; measured 212 us on config 2 vs 218-248 us
         // for 4-6 stages.
         constexpr int kStages = 3;
-        auto kern = lb == 1 ? k_hist_joint_rows8<1, kStages> : k_hist_joint_rows8<2, kStages>;
+        // A/B measurement knobs, read once: PDB_K1_GROUP (pixels per merged
+        // read-modify-write group), PDB_K1_PF (L2 prefetch distance in bands;
+        // whole frame rows, so only when the tile grid covers the width),
+        // PDB_K1_BULK=1 (stages by 1-D bulk copies of whole frame rows),
+        // PDB_K1_STAGES, PDB_K1_EPI=0, PDB_K1_CTAS (CTAs per SM).
+        struct Knobs {
+            int grp = 1, pf = 0, bulk = 0, stages = kStages, skip_epi = 0, ctas = 0;
+        };
+        static const Knobs kn = [] {
+            Knobs k;
+            auto rd = [](const char* n, int d) {
+                const char* e = getenv(n);
+                return e ? atoi(e) : d;
+            };
+            k.grp = rd("PDB_K1_GROUP", 1);
+            k.pf = rd("PDB_K1_PF", 0);
+            k.bulk = rd("PDB_K1_BULK", 0);
+            k.stages = std::max(1, rd("PDB_K1_STAGES", kStages));
+            const int e = rd("PDB_K1_EPI", 1);
+            k.skip_epi = e == 0 ? 1 : e == 2 ? 2 : e == 3 ? 3 : 0;
+            k.ctas = rd("PDB_K1_CTAS", 0);
+            return k;
+        }();
+        const int grp = kn.grp;
+        const int pf = (W % tw == 0 && (W * 3) % 16 == 0) ? kn.pf : 0;
+        const bool bulk = kn.bulk != 0 && (W * 3) % 16 == 0;
+        auto pick = [&](auto g0, auto g1, auto g2, auto g4) {
+            return grp == 4 ? g4 : grp == 2 ? g2 : grp == 0 ? g0 : g1;
+        };
+        auto kern = bulk ? (lb == 1 ? pick(k_hist_joint_rows8<1, 0, true>, k_hist_joint_rows8<1, 1, true>,
+                                           k_hist_joint_rows8<1, 2, true>, k_hist_joint_rows8<1, 4, true>)
+                                    : pick(k_hist_joint_rows8<2, 0, true>, k_hist_joint_rows8<2, 1, true>,
+                                           k_hist_joint_rows8<2, 2, true>, k_hist_joint_rows8<2, 4, true>))
+                         : (lb == 1 ? pick(k_hist_joint_rows8<1, 0, false>, k_hist_joint_rows8<1, 1, false>,
+                                           k_hist_joint_rows8<1, 2, false>, k_hist_joint_rows8<1, 4, false>)
+                                    : pick(k_hist_joint_rows8<2, 0, false>, k_hist_joint_rows8<2, 1, false>,
+                                           k_hist_joint_rows8<2, 2, false>, k_hist_joint_rows8<2, 4, false>));
+        const int n_stages = kn.stages;
+        const int skip_epi = kn.skip_epi;
+        // (a bulk stage holds RB whole frame rows, edge columns included)
+        const int64_t stage_b = bulk ? (static_cast<int64_t>(rows_rb) * W * 3 + 127) / 128 * 128 : row_smem;
         const size_t smem = 2048 + static_cast<size_t>(ntx) * 2048 +
-                            static_cast<size_t>(kStages) * row_smem + kStages * 16;
+                            static_cast<size_t>(n_stages) * stage_b + n_stages * 16 + ntx * 128;
         set_max_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
         const int threads = (ntx + 1) * 32;
+        // resident CTAs per SM, cached per (kernel, block, smem, device): the
+        // query costs microseconds of host time per call otherwise
         int per_sm = 0;
-        PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        {
+            struct Occ {
+                const void* k;
+                int threads, dev;
+                size_t smem;
+                int per_sm;
+            };
+            static std::mutex mu;
+            static std::vector<Occ> cache;
+            std::lock_guard<std::mutex> lk(mu);
+            for (const Occ& o : cache)
+                if (o.k == reinterpret_cast<const void*>(kern) && o.threads == threads &&
+                    o.smem == smem && o.dev == ctx.device)
+                    per_sm = o.per_sm;
+            if (per_sm == 0) {
+                PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+                cache.push_back({reinterpret_cast<const void*>(kern), threads, ctx.device, smem, per_sm});
+            }
+        }
+        if (kn.ctas > 0) per_sm = std::min(per_sm, kn.ctas);
         const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * ctx.sm_count;
         const dim3 g(static_cast<unsigned>(std::min(n_rows, cap)));
-        kern<<<g, threads, smem, s>>>(m, static_cast<int>(n_rows), nty, H, th, tw, ntx,
-                                      static_cast<uint32_t>(row_smem), npix_h, outs);
+        kern<<<g, threads, smem, s>>>(m, d_frames, static_cast<int>(n_rows), nty, H, W * 3, th, tw,
+                                      ntx, static_cast<uint32_t>(stage_b), n_stages, pf, skip_epi,
+                                      npix_h, outs);
         PDB_CUDA(cudaGetLastError());
         return;  // every output written by the kernel
     } else if (joint && (bins == 4 || bins == 2) && vec && tw <= 512 && lane_px < 65536) {

@@ -4,6 +4,7 @@
 // (proj/tests/oracles.hpp).  Built by `make -C oracle dropin` into
 // oracle/_ref/dropin_parity (test infrastructure); run on the GPU box by
 // tests/test_dropin_gpu.py.  Prints "DROPIN OK <checks>" and exits 0.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -64,6 +65,14 @@ int main() {
     std::vector<Patch> rp;
     for (const auto& [p, id] : oracle::random_points(81, 40, 6)) rp.push_back(oracle::vec_patch(1000 + id, p));
     join_case(lp, rp, 0.45);
+    // build-side ids not ascending with position: the adapter's host sort
+    auto rev_l = lp;
+    std::reverse(rev_l.begin(), rev_l.end());
+    auto rev_r = rp;
+    std::reverse(rev_r.begin(), rev_r.end());
+    join_case(rev_l, rp, 0.45);
+    join_case(lp, rev_r, 0.45);
+    join_case(rev_l, rev_r, 0.6);
     // acceptance.cpp:140-198 shape (scaled): clustered 24-d, sigma 0.005, tau 0.1
     auto all = oracle::clustered_points(4242, 100, 40, 24, 0.005);
     std::vector<Patch> L2, R2;
