@@ -64,7 +64,9 @@ def launches(tag, path):
     lines = [f"# {tag}: ncu launch list (`gpu__time_duration.sum --clock-control none`)", "",
              "Command: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 2 --warmup 3 --no-cpu-baseline`.",
              "Cold-cache, serialised per-launch times (compare shares, not absolutes). The list covers",
-             "the device steps AND the e2e steps (whose K1 launches are 64-frame chunks).", "",
+             "the config-2 device steps, the e2e steps (whose K1 launches are 64-frame chunks) and the",
+             "config-3 sub-record (the 1M x 1M x 128 join: band-plan steps, e2e calls and the dense-screen",
+             "pass -- the `k_screen<128, ...>`, `k_band_keys<4>`, `k_prep<1, 4>` rows).", "",
              "| kernel | launches | avg us | total us | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} | {100*sum(v)/tot:.1f}% |")
