@@ -209,9 +209,18 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
     cos = cfg["kind"] == "cos"
     dt = torch.int16 if cos else torch.float32
 
-    # ---- data: generated on rank 0, broadcast once over NCCL --------------
+    # ---- data ----------------------------------------------------------------
+    # Cross joins (config 3): L is row-sharded -- rank k holds only its
+    # contiguous rows [l0, l1) and joins them against all of R as a plain
+    # cross join (so its band plan covers only its own L rows), and R is
+    # generated on rank 0 and broadcast once over NCCL.  The seeded generator
+    # is deterministic, so each rank slices its L rows from its own copy (a
+    # loader would read just that range).  Self-joins (configs 1, 4, 5): rank
+    # 0 generates X and broadcasts it; every rank scans its boustrophedon
+    # share of the 128-row blocks (pdb_join_opts.shard_*).
     planted = None
-    if rank == 0:
+    cross_shard = not cfg["self_join"] and world > 1
+    if rank == 0 or cross_shard:
         if which == "c3":
             from paper_1812_07607_b200 import workloads
             Lh, Rh, pl_, pr_ = workloads.config3()
@@ -227,8 +236,13 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
         box = [shape_L, shape_R]
         dist.broadcast_object_list(box, src=0)
         shape_L, shape_R = box
-    Ld = (torch.from_numpy(Lh.view(np.int16) if cos else Lh).to(dev) if rank == 0
-          else torch.empty(shape_L, dtype=dt, device=dev))
+    nL_all, d = shape_L
+    l0, l1 = (nL_all * rank // world, nL_all * (rank + 1) // world) if cross_shard else (0, nL_all)
+    if cross_shard:
+        Ld = torch.from_numpy(np.ascontiguousarray(Lh[l0:l1])).to(dev)
+    else:
+        Ld = (torch.from_numpy(Lh.view(np.int16) if cos else Lh).to(dev) if rank == 0
+              else torch.empty(shape_L, dtype=dt, device=dev))
     Rd = None
     if shape_R[0]:
         Rd = torch.from_numpy(Rh).to(dev) if rank == 0 else torch.empty(shape_R, dtype=dt,
@@ -238,15 +252,16 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        dist.broadcast(Ld, src=0)
+        if not cross_shard:
+            dist.broadcast(Ld, src=0)
         if Rd is not None:
-            dist.broadcast(Rd, src=0)
+            dist.broadcast(Rd, src=0)  # the right relation, once
         e1.record()
         torch.cuda.synchronize()
         setup_ms = e0.elapsed_time(e1)
-    nL, d = shape_L
+    nL = l1 - l0  # this rank's L rows
     nR = shape_R[0] if Rd is not None else nL
-    cand = nL * (nL - 1) / 2 if cfg["self_join"] else float(nL) * nR
+    cand = nL_all * (nL_all - 1) / 2 if cfg["self_join"] else float(nL_all) * nR
 
     stream = torch.cuda.current_stream(dev)
     sptr = C.c_void_p(stream.cuda_stream)
@@ -256,7 +271,8 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
         o = capi.JoinOpts()
         o.flags = ((capi.PDB_JOIN_SELF if cfg["self_join"] else 0) |
                    (capi.PDB_JOIN_PHASE_TIMES if phases else 0))
-        o.shard_index, o.shard_count = rank, world
+        # (a row-sharded cross join is a plain join of this rank's L rows)
+        o.shard_index, o.shard_count = (0, 1) if cross_shard else (rank, world)
         o.stream = sptr
         return o
 
@@ -325,7 +341,7 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
 
     # ---- e2e: pinned host relations -> host C-ABI call -> host pairs --------
     e2e_steps = 1 if which == "c5" else max(1, min(args.steps, 3))
-    Lhost = torch.empty(tuple(shape_L), dtype=dt, pin_memory=True)
+    Lhost = torch.empty(tuple(Ld.shape), dtype=dt, pin_memory=True)
     Lhost.copy_(Ld)
     Rhost = None
     if Rd is not None:
@@ -421,10 +437,13 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16 screen / f64 exact" if not cos else "bf16 screen / f64 exact (cosine)",
             "data": "synthetic",
-            "config": {"workload": cfg["workload"], "nL": nL, "nR": nR, "d": d,
+            "config": {"workload": cfg["workload"], "nL": nL_all, "nL_per_rank": nL, "nR": nR, "d": d,
                        "threshold": cfg["tau"], "candidate_pairs": cand,
                        "l2": "flushed (256 MB read) before each step",
-                       "parallelism": f"L row blocks boustrophedon x{world}, R broadcast once"},
+                       "parallelism": (f"L rows sharded contiguously x{world} (each rank's band plan "
+                                       f"covers its own L rows), R broadcast once over NCCL"
+                                       if cross_shard else
+                                       f"L row blocks boustrophedon x{world}, X broadcast once")},
             "pairs": n_pairs, "candidates": n_cand,
             "phase_ms": {"prep": ms_prep, "screen": ms_screen, "recheck": ms_recheck},
             "setup_ms": {"broadcast": setup_ms},

@@ -10,7 +10,11 @@ The reference is single-threaded with no distributed backend (SPEC.md:495,
   every rank's feature matrix over CUDA IPC and writes its slice into all of
   them with P2P stores over NVLink while it counts, so one on-stream barrier
   replaces the all-gather (all_gather_rows is the NCCL fallback);
-* join: the 128-row blocks of L in boustrophedon rounds -- block
+* cross join (config 3): L is row-sharded in contiguous ranges
+  (left_rows) and R is broadcast once over NCCL; each rank runs a plain
+  cross join of its rows, so the L side of the band plan is divided by the
+  rank count and only R's side is replicated (the broadcast relation);
+* self-join: the 128-row blocks of L in boustrophedon rounds -- block
   k*world + (rank if k even else world-1-rank) (pdb_join_opts
   shard_index/shard_count) -- which balances the triangular self-join and
   skewed clusters without a scheduler; pairs stay on the rank
@@ -27,6 +31,13 @@ BM = 128  # rows per block of L in the screen kernel (join.cu BM)
 
 def frame_range(rank: int, world: int, n_frames: int):
     return n_frames * rank // world, n_frames * (rank + 1) // world
+
+
+def left_rows(rank: int, world: int, n_left: int):
+    """Cross joins (config 3): rank's contiguous range [l0, l1) of L.  The
+    rank joins L[l0:l1] against all of R as a plain cross join (its band
+    plan covers only its own rows); its pairs' left indices shift by l0."""
+    return n_left * rank // world, n_left * (rank + 1) // world
 
 
 def row_blocks(rank: int, world: int, n_rows: int):

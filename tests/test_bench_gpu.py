@@ -64,3 +64,15 @@ def test_bench_join_workload_c1_and_two_ranks():
                 "--gpus", "2", "--workload", "c1", "--steps", "2", "--warmup", "3"],
                env={"PDB_DIST_BACKEND": "gloo"})
     assert two["n_gpus"] == 2 and two["pairs"] == one["pairs"]
+
+
+def test_bench_c3_two_ranks_row_sharded():
+    """--workload c3 under torchrun (2 ranks; gloo so both share this GPU):
+    L row-sharded, R broadcast; the ranks' pairs add up to config 3's 5399."""
+    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+                "2", "--master-addr", "127.0.0.1", "--master-port", "29535", "bench.py",
+                "--gpus", "2", "--workload", "c3", "--steps", "2", "--warmup", "3"],
+               env={"PDB_DIST_BACKEND": "gloo"})
+    assert two["n_gpus"] == 2 and two["pairs"] == 5399
+    assert two["config"]["nL_per_rank"] == 1048576 // 2
+    assert "R broadcast once" in two["config"]["parallelism"]

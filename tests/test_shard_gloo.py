@@ -83,3 +83,49 @@ def test_row_block_partition_and_balance():
     tiles = [shard.selfjoin_tiles(k, 8, n) for k in range(8)]
     assert max(tiles) / min(tiles) < 1.02   # cyclic blocks balance the triangle
     assert shard.frame_range(7, 8, 1000) == (875, 1000)
+
+
+def _cross_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_1812_07607_b200 import workloads
+        L, R, pl, pr = workloads.config3(n=6000)
+        # R travels from rank 0 (the broadcast relation); L rows are local
+        Rt = torch.from_numpy(R) if rank == 0 else torch.empty(R.shape, dtype=torch.float32)
+        dist.broadcast(Rt, src=0)
+        l0, l1 = shard.left_rows(rank, world, L.shape[0])
+        l, r, d = oracle.sim_join(L[l0:l1], Rt.numpy(), 0.02, threads=1)
+        got = shard.gather_pairs(torch.from_numpy(l.astype(np.int64) + l0).to(torch.int32),
+                                 torch.from_numpy(r), torch.from_numpy(d.astype(np.float32)), world)
+        if rank == 0:
+            q.put(tuple(t.numpy() for t in got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_row_sharded_cross_join():
+    """Config 3's multi-GPU layout (L row-sharded, R broadcast): the union of
+    the ranks' pairs, shifted to global rows, is the single-process join."""
+    from oracle import oracle
+    from paper_1812_07607_b200 import workloads
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cross_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    l, r, d = q.get(timeout=120)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    L, R, pl, pr = workloads.config3(n=6000)
+    ol, orr, od = oracle.sim_join(L, R, 0.02)
+    k = np.lexsort((r, l))
+    assert np.array_equal(l[k], ol) and np.array_equal(r[k], orr)
+    assert np.array_equal(d[k], od.astype(np.float32))
+    assert len(ol) >= len(pl) > 0
+    assert shard.left_rows(1, 2, 6000) == (3000, 6000)
