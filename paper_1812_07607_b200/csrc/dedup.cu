@@ -81,8 +81,10 @@ __global__ void k_dedup_round(const unsigned long long* __restrict__ keys,
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (status[i] != kUndecided) continue;
         bool any_rep = false, all_done = true;
+        PDB_DCHECK(off[i] <= off[i + 1]);
         for (int64_t e = off[i]; e < off[i + 1]; e++) {
             const int64_t j = static_cast<int64_t>(keys[e] & 0xffffffffull);
+            PDB_DCHECK(j >= 0 && j < i && static_cast<int64_t>(keys[e] >> 32) == i);
             // volatile: statuses decided earlier in this round may be seen
             const uint8_t sj = *reinterpret_cast<volatile uint8_t*>(status + j);
             if (sj == kRep) {
@@ -122,6 +124,7 @@ __global__ void k_dedup_attach(const unsigned long long* __restrict__ keys,
         double best_dist = __longlong_as_double(0x7ff0000000000000ll);  // +inf
         for (int64_t e = off[i]; e < off[i + 1]; e++) {
             const int64_t j = static_cast<int64_t>(keys[e] & 0xffffffffull);
+            PDB_DCHECK(j >= 0 && j < i);
             if (status[j] != kRep) continue;
             // euclidean(items[i], items[rep]) -- the reference's argument order
             const double dist = exact_dist(X + i * d, X + j * d, d, vec8);
@@ -130,6 +133,7 @@ __global__ void k_dedup_attach(const unsigned long long* __restrict__ keys,
                 best = j;
             }
         }
+        PDB_DCHECK(best >= 0 && best < i);  // every member has a representative neighbour
         rep_of[i] = best;
     }
 #pragma unroll

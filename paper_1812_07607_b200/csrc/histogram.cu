@@ -456,6 +456,16 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, const uint8_t* __re
                     ad[4 * g + 2] = pix_offset<LB>(__funnelshift_r(w1, w2, 16)) | lbase;
                     ad[4 * g + 3] = pix_offset<LB>(w2 >> 8) | lbase;
                 }
+#ifdef PDB_CHECKED
+                // every counter address inside this warp's 2 KB block and
+                // this lane's byte column; the stage read inside the ring
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const uint32_t rel = ad[k] - (s0 + cpad + warp * 2048u);
+                    PDB_DCHECK(rel < 2048u && ((rel >> 2) & 31u) == static_cast<uint32_t>(lane));
+                }
+                PDB_DCHECK(my_stage + s * stage_bytes + 48 <= stages + S * stage_bytes);
+#endif
                 if (G == 0) {
                     // (measurement only: the pipeline without the counting)
                     uint32_t x = 0;
@@ -549,6 +559,8 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, const uint8_t* __re
         __syncwarp();
         const int f = tr / nty, ty = tr - f * nty;
         const int64_t ofs = ((static_cast<int64_t>(f) * nty + ty) * ntx + warp) * NB;
+        PDB_DCHECK(mine0 <= static_cast<uint32_t>(th * tw) && mine1 <= static_cast<uint32_t>(th * tw));
+        PDB_DCHECK(ofs + NB <= static_cast<int64_t>(n_rows) * ntx * NB);
         const float v0 = normalise(mine0, npix), v1 = normalise(mine1, npix);
         // every output: the local features and, for a sharded step, each
         // peer's copy over NVLink (P2P stores overlapping the counting)

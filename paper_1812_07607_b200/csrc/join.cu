@@ -378,6 +378,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 for (int o = w.j0; o < w.j1; o++) {
                     const int J = J_next;
                     if (o + 1 < w.j1) J_next = tile_at(p, o + 1);
+                    PDB_DCHECK(J >= 0 && J < p.nt && stage < STAGES);
                     for (int kb = 0; kb < NKB; kb++) {
                         const bool with_g = AUG && kb == NKB - 1;
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -409,6 +410,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             for (;;) {
                 const Unit w = take_unit(false);
                 if (w.rb < 0) break;
+                PDB_DCHECK(static_cast<int64_t>(w.rb) * BM < p.nL && w.j0 <= w.j1);
                 const uint32_t slot = na % kASlots;
                 uint8_t* smAu = smA + slot * kASlot;
                 if (A_RES) {
@@ -1826,7 +1828,10 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
 #pragma unroll
     for (int i = 0; i < kScatterRows; i++) {
         const int64_t r = r0 + i * blockDim.x + threadIdx.x;
-        if (r < n) perm[base[k[i]] + local[i]] = static_cast<int32_t>(r);
+        if (r < n) {
+            PDB_DCHECK(k[i] < static_cast<uint32_t>(kBins) && base[k[i]] + local[i] < n);
+            perm[base[k[i]] + local[i]] = static_cast<int32_t>(r);
+        }
     }
 }
 
@@ -2197,7 +2202,9 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
                 const int k = __fns(s_mask, 0, c - s_excl + 1);  // that lane's (c - excl)-th set bit
                 j = s_j0 + k;
                 const int jp = j;  // column position (sorted under a band plan)
+                PDB_DCHECK(k >= 0 && k < 32 && jp >= 0 && jp < ldt);
                 if (permR) j = __ldg(permR + j);
+                PDB_DCHECK(j >= 0 && j < ldt && a >= 0);
                 // euclidean(L_i, R_j); bitwise symmetric, so a self-join pair
                 // can be reported as (min, max)
                 dist = GROUPED ? exact_dist_grouped(L + static_cast<int64_t>(a) * d,

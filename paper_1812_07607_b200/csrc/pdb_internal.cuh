@@ -11,6 +11,27 @@
 
 #define PDB_HIDDEN __attribute__((visibility("hidden")))
 
+// Device-side bounds checks of the checked build (libpdb_cuda_checked.so,
+// `make checked`, -DPDB_CHECKED): a violated check prints its site and traps,
+// failing the call with a CUDA error.  The product build compiles them out.
+// (compute-sanitizer is closed on this GPU pool; these checks plus the
+// oracle comparisons of tools/sanitize_cases.py stand in for memcheck.)
+#ifdef PDB_CHECKED
+#include <cstdio>
+#define PDB_DCHECK(c)                                                                  \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("PDB_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #c, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define PDB_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 namespace pdb {
 
 // Thread-local error state behind pdb_last_error().

@@ -1,9 +1,10 @@
-"""Small-shape runs of every kernel group for compute-sanitizer
-(tools/sanitize.sh): K1 (TMA-fed joint histogram, per-channel, f32 path),
+"""Small-shape runs of every kernel group, for the checked build
+(PDB_CUDA_LIB=paper_1812_07607_b200/libpdb_cuda_checked.so; tests/
+test_checked_gpu.py): K1 (TMA-fed joint histogram, per-channel, f32 path),
 K2 (1-SM screen, the cta_group::2 pair screen, tf32, the band plan), K3
 (row-major and grouped re-checks, cosine), dedup rounds, the sharded plan.
-Each case checks its result against the oracle so a sanitizer-clean run is
-also a correct one.  Usage: python tools/sanitize_cases.py [case ...]"""
+Each case checks its result against the oracle, so a clean run is also a
+correct one.  Usage: python tools/sanitize_cases.py [case ...]"""
 
 import os
 import sys
