@@ -64,6 +64,8 @@ __global__ void k_csr_offsets(const unsigned long long* __restrict__ keys, int64
 }
 
 constexpr uint8_t kUndecided = 0, kRep = 1, kMember = 2;
+// at most this many undecided items after a host check: the sequential tail
+constexpr unsigned int kTailSwitch = 65536;
 
 // One round of the greedy scan over the still undecided items.
 // Round counters are double-buffered: a round counts into cnt[r & 1] and
@@ -101,6 +103,118 @@ __global__ void k_dedup_round(const unsigned long long* __restrict__ keys,
     for (int o = 16; o > 0; o >>= 1) left += __shfl_xor_sync(0xffffffffu, left, o);
     if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
 }
+
+// The sequential tail of the greedy scan.  Once few items are undecided
+// (dependency chains: a chain of k items needs k rounds), one block decides
+// them in index order -- exactly the reference's sequential scan restricted
+// to them, since every lower neighbour of an item is final when its turn
+// comes.  The sorted undecided list is walked in chunks: the chunk's CSR
+// edges are staged in shared memory with each lower neighbour encoded as its
+// position in the chunk (>= 0) or its final status outside it (-1 rep, -2
+// not), then one thread decides the chunk item by item from shared memory.
+// An item with more edges than the stage holds is decided from global
+// memory.
+constexpr int kTailItems = 4096;
+
+__global__ void __launch_bounds__(1024)
+k_dedup_tail(const unsigned long long* __restrict__ keys, const int64_t* __restrict__ off,
+             const int32_t* __restrict__ list, int64_t U, uint8_t* status, int edge_cap) {
+    extern __shared__ int32_t tsm[];
+    int32_t* s_item = tsm;                      // [kTailItems]
+    int32_t* s_beg = s_item + kTailItems;       // [kTailItems + 1] edge offsets
+    int32_t* s_edge = s_beg + kTailItems + 1;   // [edge_cap] codes
+    uint8_t* s_stat = reinterpret_cast<uint8_t*>(s_edge + edge_cap);  // [kTailItems]
+    __shared__ int32_t s_c;
+    const int t = threadIdx.x;
+    for (int64_t u0 = 0; u0 < U;) {
+        // 1. the chunk: as many items as fit kTailItems and edge_cap edges
+        const int64_t navail = min(static_cast<int64_t>(kTailItems), U - u0);
+        for (int k = t; k < kTailItems; k += blockDim.x) {
+            if (k < navail) {
+                const int64_t i = list[u0 + k];
+                s_item[k] = static_cast<int32_t>(i);
+                s_beg[k + 1] = static_cast<int32_t>(min(off[i + 1] - off[i], static_cast<int64_t>(edge_cap) + 1));
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            // serial prefix (kTailItems values) and the cut
+            int32_t acc = 0, c = 0;
+            s_beg[0] = 0;
+            for (int k = 0; k < navail; k++) {
+                const int32_t dk = s_beg[k + 1];
+                if (acc + dk > edge_cap && c > 0) break;
+                acc += min(dk, edge_cap);
+                s_beg[k + 1] = acc;
+                c++;
+                if (dk > edge_cap) break;  // a huge item goes alone (global path)
+            }
+            s_c = c;
+        }
+        __syncthreads();
+        const int c = s_c;
+        const bool global_path = c == 1 && (off[s_item[0] + 1] - off[s_item[0]]) > edge_cap;
+        // 2. stage the edges' codes
+        if (!global_path) {
+            const int32_t ne = s_beg[c];
+            for (int e = t; e < ne; e += blockDim.x) {
+                int lo = 0, hi = c;  // item k with s_beg[k] <= e < s_beg[k + 1]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_beg[mid] <= e) lo = mid;
+                    else hi = mid;
+                }
+                const int64_t i = s_item[lo];
+                const int64_t j = static_cast<int64_t>(keys[off[i] + (e - s_beg[lo])] & 0xffffffffull);
+                PDB_DCHECK(j >= 0 && j < i);
+                int32_t code;
+                int a = 0, b = lo;  // is j an item of this chunk (before i)?
+                while (a < b) {
+                    const int mid = (a + b) >> 1;
+                    if (s_item[mid] < j) a = mid + 1;
+                    else b = mid;
+                }
+                if (a < lo && s_item[a] == j) code = a;
+                else code = status[j] == kRep ? -1 : -2;  // final: outside the chunk
+                s_edge[e] = code;
+            }
+        }
+        __syncthreads();
+        // 3. decide the chunk in order
+        if (t == 0) {
+            if (global_path) {
+                const int64_t i = s_item[0];
+                bool rep_nb = false;
+                for (int64_t e = off[i]; e < off[i + 1] && !rep_nb; e++)
+                    rep_nb = status[keys[e] & 0xffffffffull] == kRep;
+                s_stat[0] = rep_nb ? kMember : kRep;
+            } else {
+                for (int k = 0; k < c; k++) {
+                    bool rep_nb = false;
+                    for (int32_t e = s_beg[k]; e < s_beg[k + 1]; e++) {
+                        const int32_t code = s_edge[e];
+                        if (code == -1 || (code >= 0 && s_stat[code] == kRep)) {
+                            rep_nb = true;
+                            break;
+                        }
+                    }
+                    s_stat[k] = rep_nb ? kMember : kRep;
+                }
+            }
+        }
+        __syncthreads();
+        // 4. publish the chunk's statuses (later chunks read them as final)
+        for (int k = t; k < c; k += blockDim.x) status[s_item[k]] = s_stat[k];
+        __threadfence_block();
+        __syncthreads();
+        u0 += c;
+    }
+}
+
+struct IsUndecided {
+    const uint8_t* status;
+    __device__ bool operator()(int32_t i) const { return status[i] == kUndecided; }
+};
 
 // rep_of[i]: i for representatives, else the rep neighbour nearest in the
 // reference's fp64 distance (lowest index on ties; neighbours ascend).
@@ -201,7 +315,30 @@ void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStrea
         PDB_CUDA(cudaMemcpyAsync(hc, cnt.p + ((r - 1) & 1), sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, s));
         PDB_CUDA(cudaStreamSynchronize(s));
-        if (static_cast<unsigned int>(hc[0]) == 0) break;
+        const unsigned int und = static_cast<unsigned int>(hc[0]);
+        if (und == 0) break;
+        if (und <= kTailSwitch) {
+            // few undecided items left (dependency chains): the sequential
+            // tail in one block instead of one round per chain link
+            DevBuf<int32_t> list(und, s);
+            DevBuf<int> nsel(1, s);
+            cub::CountingInputIterator<int32_t> idx(0);
+            size_t tb = 0;
+            PDB_CUDA(cub::DeviceSelect::If(nullptr, tb, idx, list.p, nsel.p, n,
+                                           IsUndecided{status.p}, s));
+            DevBuf<uint8_t> tmp(tb, s);
+            PDB_CUDA(cub::DeviceSelect::If(tmp.p, tb, idx, list.p, nsel.p, n,
+                                           IsUndecided{status.p}, s));
+            const int edge_cap = 40000;
+            const size_t smem = static_cast<size_t>(kTailItems) * 4 + (kTailItems + 1) * 4 +
+                                static_cast<size_t>(edge_cap) * 4 + kTailItems;
+            set_max_smem(reinterpret_cast<const void*>(k_dedup_tail), static_cast<int>(smem));
+            k_dedup_tail<<<1, 1024, smem, s>>>(static_cast<const unsigned long long*>(keys.p),
+                                                static_cast<const int64_t*>(off.p), list.p,
+                                                static_cast<int64_t>(und), status.p, edge_cap);
+            PDB_CUDA(cudaGetLastError());
+            break;
+        }
         if (check > n) fail(PDB_ERR_CUDA, "dedup rounds did not converge");  // unreachable
     }
 

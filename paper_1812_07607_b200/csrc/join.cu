@@ -96,7 +96,11 @@ constexpr int kModeL2Bf16Pair = 4;  // kModeL2Bf16Aug on CTA pairs (k_screen_pai
 // Per-element perturbation bound U of the screen copies (round-to-nearest
 // to the MMA input type after an fp32 subtraction).
 constexpr double kU_tf32 = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
-constexpr double kU_bf16 = 1.953125e-3 + 9.5367431640625e-7;   // 2^-9 + 2^-20
+// bf16 keeps 8 significant bits (7 stored): round-to-nearest errs by up to
+// half an ulp, 2^-8 of the rounded value.  (r01 used 2^-9 here, half the
+// true bound: one-dimensional rows far from the centre, where the bound is
+// reached, lost pairs -- tests/test_join_gpu.py::test_bf16_rounding_bound.)
+constexpr double kU_bf16 = 3.90625e-3 + 9.5367431640625e-7;    // 2^-8 + 2^-20
 
 struct ScreenParams {
     int64_t nL, nR;
@@ -1401,7 +1405,10 @@ constexpr int kPcaMaxD = 128;
 constexpr int64_t kBandMinRows = 8192;
 constexpr int64_t kBandMinTiles = 16384;
 constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
-constexpr int kPcaIters = 4;   // subspace iterations for the top-2 principal plane
+#ifndef PDB_PCA_ITERS
+#define PDB_PCA_ITERS 4
+#endif
+constexpr int kPcaIters = PDB_PCA_ITERS;   // subspace iterations for the top-2 principal plane
 
 struct BandInfo {
     float u[2][kPcaMaxD];   // the two directions (zero past d)
@@ -1768,6 +1775,7 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
 constexpr int kBins = 1 << (2 * kMortonBits);
 
 constexpr int kScatterRows = 4;  // rows per thread (4096 per 1024-thread block)
+template <int RPT>
 __global__ void __launch_bounds__(1024)
 k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __restrict__ count,
               int32_t* __restrict__ fill, int32_t* __restrict__ perm) {
@@ -1811,11 +1819,11 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
         run += v[i];
     }
     __syncthreads();
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kScatterRows;
-    uint32_t k[kScatterRows];
-    int32_t local[kScatterRows];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * RPT;
+    uint32_t k[RPT];
+    int32_t local[RPT];
 #pragma unroll
-    for (int i = 0; i < kScatterRows; i++) {
+    for (int i = 0; i < RPT; i++) {
         const int64_t r = r0 + i * blockDim.x + threadIdx.x;
         k[i] = r < n ? __ldg(key + r) : 0xffffffffu;
         local[i] = r < n ? atomicAdd(&cnt[k[i]], 1) : 0;
@@ -1826,7 +1834,7 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
         if (cnt[b]) base[b] += atomicAdd(fill + b, cnt[b]);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kScatterRows; i++) {
+    for (int i = 0; i < RPT; i++) {
         const int64_t r = r0 + i * blockDim.x + threadIdx.x;
         if (r < n) {
             PDB_DCHECK(k[i] < static_cast<uint32_t>(kBins) && base[k[i]] + local[i] < n);
@@ -3087,8 +3095,15 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             const int nv = (d + 31) / 32;
             auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
                                                                                       : k_band_keys<4>;
+            // PDB_KEYS_BPS (A/B): blocks per SM of the keys pass (0: one
+            // block per 32 / 64 rows, capped at 16 per SM)
+            static const int keys_bps = [] {
+                const char* e = getenv("PDB_KEYS_BPS");
+                return e ? atoi(e) : 0;
+            }();
             const unsigned gk = static_cast<unsigned>(
-                std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
+                keys_bps > 0 ? std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * keys_bps)
+                             : std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
             launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
                        proj, k_in, v_in,
                        P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
@@ -3101,7 +3116,13 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                 launches += 5;
             } else {
                 int32_t* count = reinterpret_cast<int32_t*>(tmp);  // counted by k_band_keys
-                launch_pdl(k_bin_scatter, dim3(static_cast<unsigned>(ceil_div(n, 1024 * kScatterRows))),
+                // PDB_SCATTER_RPT (A/B): rows per scatter thread (1 or 4)
+                static const int rpt = [] {
+                    const char* e = getenv("PDB_SCATTER_RPT");
+                    return e && atoi(e) == 1 ? 1 : kScatterRows;
+                }();
+                launch_pdl(rpt == 1 ? k_bin_scatter<1> : k_bin_scatter<kScatterRows>,
+                           dim3(static_cast<unsigned>(ceil_div(n, 1024 * rpt))),
                            dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n,
                            static_cast<const int32_t*>(count), count + kBins, perm);
                 launches += 2;

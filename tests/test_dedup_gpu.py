@@ -62,7 +62,8 @@ def test_errors_and_degenerate():
         list(patchdb.dedup_stream([patchdb.Patch(3, np.zeros(0, np.float32), (0,))], 0.1))
 
 
-@pytest.mark.parametrize("case", ["config1_full", "config2_4000", "chain_1d", "nan_rows"])
+@pytest.mark.parametrize("case", ["config1_full", "config2_4000", "chain_1d", "nan_rows",
+                                  "chain_30k", "chain_branchy"])
 def test_against_restatement(case):
     if case == "config1_full":          # 20,000 rows, ~1e6 tau-graph edges
         X, tau = workloads.config1(), 0.05
@@ -71,6 +72,12 @@ def test_against_restatement(case):
         X, tau = oracle.featurize_tiles(fr, 60, 80, 4, 1)[:4000], 0.05
     elif case == "chain_1d":            # a long dependency chain: points 0.9 tau apart
         X, tau = (np.arange(3000, dtype=np.float32) * 0.09).reshape(-1, 1), 0.1
+    elif case == "chain_30k":           # decided by the sequential tail (k_dedup_tail) in chunks
+        X, tau = (np.arange(30000, dtype=np.float32) * 0.09).reshape(-1, 1), 0.1
+    elif case == "chain_branchy":       # chains with several lower neighbours per item
+        rng = np.random.default_rng(9)
+        X = np.cumsum(rng.random((12000, 2), dtype=np.float32) * 0.04, axis=0).astype(np.float32)
+        tau = 0.1
     else:
         rng = np.random.default_rng(3)
         X = rng.random((1500, 8), dtype=np.float32)

@@ -329,3 +329,28 @@ def test_release_caches():
     assert capi.lib().pdb_release_caches() == 0
     b = patchdb.sim_join(x, None, 0.01, self_join=True)
     assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)
+
+
+@pytest.mark.parametrize("variant", ["band", "dense", "nofold", "tf32", "pair"])
+@pytest.mark.parametrize("n,d", [(5000, 1), (9000, 1), (6000, 2), (4000, 8)])
+def test_bf16_rounding_bound(monkeypatch, variant, n, d):
+    """Rows on a line far from the screen copies' centre, neighbours 0.9 tau
+    apart: the bf16 copy's rounding error reaches its worst case (half an
+    ulp = 2^-8 of the rounded value) on every coordinate at once, so a margin
+    that underestimates it loses pairs (r01's 2^-9 did)."""
+    if variant == "nofold":
+        monkeypatch.setenv("PDB_NO_FOLD", "1")
+    if variant == "pair":
+        monkeypatch.setenv("PDB_SCREEN_PAIR", "1")
+    t = np.arange(n, dtype=np.float64) * 0.09
+    v = np.ones(d) / np.sqrt(d)
+    X = (t[:, None] * v[None, :] + 3.0).astype(np.float32)
+    tau = 0.1
+    ol, orr, od = oracle.sim_join(X, None, tau, self_join=True)
+    xt = torch.from_numpy(X).cuda()
+    r = patchdb.sim_join_device(xt, None, tau, self_join=True, sort=True,
+                                dense=variant == "dense", tf32=variant == "tf32")
+    l, rr, dd = (t_.cpu().numpy() for t_ in r.to_torch(xt.device))
+    assert len(ol) >= n - 2
+    assert np.array_equal(l, ol) and np.array_equal(rr, orr)
+    assert np.array_equal(dd, od.astype(np.float32))
