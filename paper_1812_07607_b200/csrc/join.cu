@@ -93,14 +93,16 @@ constexpr int kModeCosBf16 = 2;
 // parts of -g_j), so the epilogue tests raw accumulators (DP <= 128 only).
 constexpr int kModeL2Bf16Aug = 3;
 constexpr int kModeL2Bf16Pair = 4;  // kModeL2Bf16Aug on CTA pairs (k_screen_pair)
-// Per-element perturbation bound U of the screen copies (round-to-nearest
-// to the MMA input type after an fp32 subtraction).
-constexpr double kU_tf32 = 4.8828125e-4 + 9.5367431640625e-7;  // 2^-11 + 2^-20
-// bf16 keeps 8 significant bits (7 stored): round-to-nearest errs by up to
-// half an ulp, 2^-8 of the rounded value.  (r01 used 2^-9 here, half the
-// true bound: one-dimensional rows far from the centre, where the bound is
-// reached, lost pairs -- tests/test_join_gpu.py::test_bf16_rounding_bound.)
-constexpr double kU_bf16 = 3.90625e-3 + 9.5367431640625e-7;    // 2^-8 + 2^-20
+// The screen's perturbation term.  r01 bounded a row's rounding error by
+// U ||x~|| with a per-element relative bound U -- and used 2^-9 for bf16,
+// half the true bound (bf16 keeps 8 significant bits, so round-to-nearest
+// errs by up to 2^-8 of the rounded value): one-dimensional rows far from
+// the centre, where the bound is reached, lost pairs
+// (tests/test_join_gpu.py::test_bf16_rounding_bound).  Since r02 k_prep
+// stores each row's actual rounding-error norm (err_norm, an upper bound
+// computed from the exact per-coordinate errors) and the margin uses it
+// directly (u = 1): exact for any data, and tighter than any per-element
+// bound, since errors rarely all sit at half an ulp.
 
 struct ScreenParams {
     int64_t nL, nR;
@@ -113,7 +115,7 @@ struct ScreenParams {
     int64_t unit_step;  // 1, or S > 1 to screen only every S-th unit (output-size estimate)
     const int64_t* chunk_off;  // [n_chunks + 1]
     const float* hnL;   // L2: ||x~_i||^2;  COS: the row threshold h_i itself
-    const float* snL;   // L2: ||x~_i|| (rounded up) or a flag;  COS: unused
+    const float* snL;   // L2: ||x~_i - (x_i - mu)|| bound (err_norm) or a flag;  COS: unused
     const float* gR;    // L2: ||y~_j||^2 / 2 (+inf / -inf flags);  COS: 1/||y_j|| rounded up
                         // (0 for zero / non-finite rows); padded to nt*256
     const float* tmaxS; // per R tile
@@ -121,7 +123,7 @@ struct ScreenParams {
     const float* cmaxS; // per column chunk (max over its tiles)
     const float* cmaxN;
     double tau_p;       // tau (1 + 1e-9)
-    double u;           // perturbation bound U of the screen copies (L2 modes)
+    double u;           // scale of the error norms (1: snL / tmaxS / cmaxS hold them directly)
     double gam;         // DP 2^-23 + 2^-19
     int4* rec;                  // (row i, first column j0, hit mask, 0)
     unsigned long long cap;     // record capacity
@@ -1065,6 +1067,17 @@ __device__ __forceinline__ uint16_t to_bf16_bits(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
+// Bound on the norm of a row's total rounding error e = x~ - (x - mu): the
+// screen copy's rounding t - c (exact per coordinate, summed in eacc) plus
+// the fp32 centring c = fl(x - mu), |c - (x - mu)| <= 2^-24 |c| with
+// ||c|| <= ||t|| + ||t - c||.  Rounded up (fp64 roundings: 2^-40 slack).
+// |  ||x~_i - y~_j|| - ||x_i - y_j||  | <= e_i + e_j, so this replaces the
+// worst-case U ||x~|| per row in the screen's margin.
+__device__ __forceinline__ float err_norm(double acc, double eacc) {
+    const double et = sqrt(eacc), tn = sqrt(acc);
+    return __double2float_ru((et + 5.9604644775390625e-08 * (tn + et)) * (1.0 + 9.094947017729282e-13));
+}
+
 // Sum over the 32 lanes of eight per-row partials v[0..7] with 9 shuffles
 // (a transposing butterfly): afterwards lanes 4r .. 4r+3 hold row r's total.
 __device__ __forceinline__ double sum8_transpose(const double (&v)[8], int lane) {
@@ -1134,11 +1147,11 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
                 x[r][i] = (src >= 0 && lane * NV + i < d) ? __ldg(xr + i) : 0.0f;
         }
     }
-    double part[kRowsPerWarp];
+    double part[kRowsPerWarp], epart[kRowsPerWarp];
     uint32_t fin_mask = 0, big_mask = 0;
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; r++) {
-        double acc = 0.0;
+        double acc = 0.0, eacc = 0.0;
         bool finite = true, big = false;
         float t[NV];
 #pragma unroll
@@ -1151,10 +1164,14 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
                 t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
                             : round_tf32(c);
                 if (!(fabsf(t[i]) <= kBigLimit)) big = true;
+                // this coordinate's rounding error (exact in fp64)
+                const double e = static_cast<double>(t[i]) - static_cast<double>(c);
+                eacc += e * e;
             }
             acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
         }
         part[r] = acc;
+        epart[r] = eacc;
         finite = __all_sync(0xffffffffu, finite);
         big = __any_sync(0xffffffffu, big);
         fin_mask |= static_cast<uint32_t>(finite) << r;
@@ -1186,6 +1203,7 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
         }
     }
     const double acc = sum8_transpose(part, lane);
+    const double eacc = sum8_transpose(epart, lane);
     const int r = (lane >> 2) & 7;
     if ((lane & 3) != 0 || r0 + r >= n) return;
     const int64_t row = r0 + r;
@@ -1198,7 +1216,7 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
         sn[row] = kFlagBig;
     } else {
         hn[row] = static_cast<float>(acc);
-        sn[row] = __double2float_ru(sqrt(acc));
+        sn[row] = err_norm(acc, eacc);
     }
     if (gx) {
         // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
@@ -1236,7 +1254,7 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
     const float* x = X + row * d;
     float* xpf = static_cast<float*>(Xp_) + row * DP;
     uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
-    double acc = 0.0;
+    double acc = 0.0, eacc = 0.0;
     bool finite = true, big = false;
     for (int k = lane; k < DP; k += 32) {
         float t = 0.0f;
@@ -1247,13 +1265,18 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
             t = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
                      : round_tf32(c);
             if (!(fabsf(t) <= kBigLimit)) big = true;
+            const double e = static_cast<double>(t) - static_cast<double>(c);
+            eacc += e * e;
         }
         if (BF16) xpb[k] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
         else xpf[k] = t;
         acc += static_cast<double>(t) * static_cast<double>(t);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        eacc += __shfl_xor_sync(0xffffffffu, eacc, o);
+    }
     finite = __all_sync(0xffffffffu, finite);
     big = __any_sync(0xffffffffu, big);
     if (!finite || big) {
@@ -1271,7 +1294,7 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
             sn[row] = kFlagBig;
         } else {
             hn[row] = static_cast<float>(acc);
-            sn[row] = __double2float_ru(sqrt(acc));
+            sn[row] = err_norm(acc, eacc);
         }
     }
 }
@@ -3232,7 +3255,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                           static_cast<const float*>(tmaxN), cmaxS, cmaxN,
                           static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
                           unit_info, static_cast<const float*>(hnL), static_cast<const float*>(snL), nL,
-                          tau * (1.0 + 1e-9), tf32 ? kU_tf32 : kU_bf16,
+                          tau * (1.0 + 1e-9), 1.0,
                           (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow);
         launches++;
     } else {
@@ -3268,7 +3291,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.cmaxS = cmaxS;
     p.cmaxN = cmaxN;
     p.tau_p = tau * (1.0 + 1e-9);
-    p.u = tf32 ? kU_tf32 : kU_bf16;
+    p.u = 1.0;  // the error norms are stored directly (err_norm)
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
     if (band) {
         p.hrow = hrow;

@@ -148,8 +148,8 @@ def _pairs_of_rows(l, r, d, rows, n):
     sorted (row, other, dist) with other != row (both orientations)."""
     flag = torch.zeros(n, dtype=torch.bool, device=l.device)
     flag[torch.from_numpy(rows).to(l.device)] = True
-    a = flag[l.long()]
-    b = flag[r.long()]
+    a = flag[l]
+    b = flag[r]
     out = torch.cat([torch.stack([l[a], r[a]], 1), torch.stack([r[b], l[b]], 1)]).cpu().numpy()
     dist = torch.cat([d[a], d[b]]).cpu().numpy()
     o = np.lexsort((out[:, 1], out[:, 0]))
@@ -158,12 +158,16 @@ def _pairs_of_rows(l, r, d, rows, n):
 
 def _checksum(l, r, d):
     """Order-independent checksum of a pair set: count and two wrapping
-    int64 sums of mixed (left, right, dist bits)."""
-    l64, r64 = l.long(), r.long()
-    db = d.view(torch.int32).long()
-    h1 = (l64 * 0x9E3779B1 + r64 * 0x85EBCA77 + db * 0xC2B2AE3D) * 0x27D4EB2F
-    h2 = (l64 * 0x165667B1 ^ r64 * 0xD3A2646C) + db
-    return int(l.numel()), int(h1.sum()), int(h2.sum())
+    int64 sums of mixed (left, right, dist bits), in 2^27-pair slices."""
+    s1 = s2 = 0
+    for a in range(0, l.numel(), 1 << 27):
+        l64, r64 = l[a:a + (1 << 27)].long(), r[a:a + (1 << 27)].long()
+        db = d[a:a + (1 << 27)].view(torch.int32).long()
+        h1 = (l64 * 0x9E3779B1 + r64 * 0x85EBCA77 + db * 0xC2B2AE3D) * 0x27D4EB2F
+        h2 = (l64 * 0x165667B1 ^ r64 * 0xD3A2646C) + db
+        s1 = (s1 + int(h1.sum())) & ((1 << 64) - 1)
+        s2 = (s2 + int(h2.sum())) & ((1 << 64) - 1)
+    return int(l.numel()), s1, s2
 
 
 def test_config5_full_size_sampled_neighbourhoods(c5, monkeypatch):
@@ -173,7 +177,7 @@ def test_config5_full_size_sampled_neighbourhoods(c5, monkeypatch):
     res = patchdb.sim_join_device(dx, None, 0.01, self_join=True)
     l, r, d = res.to_torch(dx.device, copy=False)
     assert res.count > 5e8
-    deg = torch.bincount(l.long(), minlength=n) + torch.bincount(r.long(), minlength=n)
+    deg = torch.bincount(l, minlength=n) + torch.bincount(r, minlength=n)
     heavy = torch.topk(deg, 128).indices.cpu().numpy()
     rows = np.unique(np.concatenate([np.arange(0, n, n // 256), np.arange(2_000_000, 2_000_064),
                                      heavy]))
@@ -185,15 +189,21 @@ def test_config5_full_size_sampled_neighbourhoods(c5, monkeypatch):
     assert np.array_equal(gd, od.astype(np.float32))
     assert deg[torch.from_numpy(heavy).cuda()].min().item() > 1000   # cluster rows
     # grouped (default for this candidate-heavy join) vs row-major re-check:
-    # the same ~1e9 pairs
+    # the same ~1e9 pairs (the library's cached buffers are returned between
+    # the two joins: each holds a multi-GB candidate-record buffer)
+    from paper_1812_07607_b200 import _capi as capi
+    del deg
     c_default = _checksum(l, r, d)
     del l, r, d
     res.free()
+    torch.cuda.empty_cache()
+    assert capi.lib().pdb_release_caches() == 0
     monkeypatch.setenv("PDB_K3_GROUPED", "0")
     res2 = patchdb.sim_join_device(dx, None, 0.01, self_join=True)
     c_rowmajor = _checksum(*res2.to_torch(dx.device, copy=False))
     assert c_default == c_rowmajor
     res2.free()
+    assert capi.lib().pdb_release_caches() == 0
 
 
 # ---------------------------------------------------------------------------
