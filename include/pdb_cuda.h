@@ -283,6 +283,13 @@ int pdb_store_featurize(const pdb_store* s, int64_t lo, int64_t hi, int32_t tile
                         int32_t tile_w, int32_t bins, int32_t mode, float* d_features,
                         int64_t* n_frames, int32_t threads, void* stream);
 
+/* Creates the CUDA context and the library's memory pool and loads the
+ * kernels of the common paths (one tiny featurization and self-join), so that
+ * the first real call of a process does not pay the device start-up (~1.5 s
+ * on a fresh B200 process).  Optional; safe to call from a background thread
+ * at start-up.  No reference counterpart. */
+int pdb_warmup(void);
+
 /* Returns the device memory the library keeps between calls on the calling
  * thread (the grow-only candidate-record buffer of large joins) and trims the
  * library's own stream-ordered pool to zero.  Synchronises the device.  No

@@ -49,7 +49,7 @@ EXPORTS = (
     "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
     "pdb_store_open", "pdb_store_close", "pdb_store_describe", "pdb_store_read",
     "pdb_store_featurize", "pdb_rows_within", "pdb_featurize_tiles_dev_multi",
-    "pdb_release_caches",
+    "pdb_release_caches", "pdb_warmup",
 )
 
 
@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
         L.pdb_featurize_tiles_dev_multi.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, vp, i32,
                                                     vp]
         L.pdb_release_caches.argtypes = []
+        L.pdb_warmup.argtypes = []
         L.pdb_host_alloc.argtypes = [i64]
         L.pdb_host_alloc.restype = vp
         L.pdb_host_free.argtypes = [vp]

@@ -811,6 +811,8 @@ void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int
         auto pick = [&](auto g0, auto g1, auto g2, auto g4) {
             return grp == 4 ? g4 : grp == 2 ? g2 : grp == 0 ? g0 : g1;
         };
+#ifdef PDB_K1_VARIANTS
+        // (the A/B build: every measured variant; `make K1_VARIANTS=1`)
         auto kern = bulk ? (lb == 1 ? pick(k_hist_joint_rows8<1, 0, true>, k_hist_joint_rows8<1, 1, true>,
                                            k_hist_joint_rows8<1, 2, true>, k_hist_joint_rows8<1, 4, true>)
                                     : pick(k_hist_joint_rows8<2, 0, true>, k_hist_joint_rows8<2, 1, true>,
@@ -819,6 +821,13 @@ void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int
                                            k_hist_joint_rows8<1, 2, false>, k_hist_joint_rows8<1, 4, false>)
                                     : pick(k_hist_joint_rows8<2, 0, false>, k_hist_joint_rows8<2, 1, false>,
                                            k_hist_joint_rows8<2, 2, false>, k_hist_joint_rows8<2, 4, false>));
+#else
+        // the product build carries only the chosen variant (module load time
+        // grows with every instantiation)
+        (void)pick;
+        (void)bulk;
+        auto kern = lb == 1 ? k_hist_joint_rows8<1, 1, false> : k_hist_joint_rows8<2, 1, false>;
+#endif
         const int n_stages = kn.stages;
         const int skip_epi = kn.skip_epi;
         // (a bulk stage holds RB whole frame rows, edge columns included)
