@@ -1068,13 +1068,16 @@ __device__ __forceinline__ uint16_t to_bf16_bits(float x) {
 }
 
 // Bound on the norm of a row's total rounding error e = x~ - (x - mu): the
-// screen copy's rounding t - c (exact per coordinate, summed in eacc) plus
-// the fp32 centring c = fl(x - mu), |c - (x - mu)| <= 2^-24 |c| with
-// ||c|| <= ||t|| + ||t - c||.  Rounded up (fp64 roundings: 2^-40 slack).
+// screen copy's rounding t - c (exact per coordinate; squares summed with
+// fp32 FMAs -- non-negative terms, so the sum is at most (d + 2) 2^-23 low
+// relative to the exact one, at most d + 1 roundings of 2^-24 each, summed
+// per lane then exactly in fp64 across lanes), plus the fp32 centring
+// c = fl(x - mu), |c - (x - mu)| <= 2^-24 |c| with ||c|| <= ||t|| + ||t - c||.
+// Rounded up (fp64 roundings: 2^-40 slack).
 // |  ||x~_i - y~_j|| - ||x_i - y_j||  | <= e_i + e_j, so this replaces the
 // worst-case U ||x~|| per row in the screen's margin.
-__device__ __forceinline__ float err_norm(double acc, double eacc) {
-    const double et = sqrt(eacc), tn = sqrt(acc);
+__device__ __forceinline__ float err_norm(double acc, double eacc, int d) {
+    const double et = sqrt(eacc * (1.0 + (d + 2) * 1.1920928955078125e-07)), tn = sqrt(acc);
     return __double2float_ru((et + 5.9604644775390625e-08 * (tn + et)) * (1.0 + 9.094947017729282e-13));
 }
 
@@ -1151,7 +1154,8 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
     uint32_t fin_mask = 0, big_mask = 0;
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; r++) {
-        double acc = 0.0, eacc = 0.0;
+        double acc = 0.0;
+        float eacc = 0.0f;
         bool finite = true, big = false;
         float t[NV];
 #pragma unroll
@@ -1164,14 +1168,16 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
                 t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
                             : round_tf32(c);
                 if (!(fabsf(t[i]) <= kBigLimit)) big = true;
-                // this coordinate's rounding error (exact in fp64)
-                const double e = static_cast<double>(t[i]) - static_cast<double>(c);
-                eacc += e * e;
+                // this coordinate's rounding error: exact in fp32 (t is c
+                // rounded, so the two are within a factor 2); its square and
+                // the running sum round up to (d + 2) 2^-23 in all (err_norm)
+                const float e = __fsub_rn(t[i], c);
+                eacc = __fmaf_rn(e, e, eacc);
             }
             acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
         }
         part[r] = acc;
-        epart[r] = eacc;
+        epart[r] = static_cast<double>(eacc);
         finite = __all_sync(0xffffffffu, finite);
         big = __any_sync(0xffffffffu, big);
         fin_mask |= static_cast<uint32_t>(finite) << r;
@@ -1216,7 +1222,7 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
         sn[row] = kFlagBig;
     } else {
         hn[row] = static_cast<float>(acc);
-        sn[row] = err_norm(acc, eacc);
+        sn[row] = err_norm(acc, eacc, d);
     }
     if (gx) {
         // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
@@ -1254,7 +1260,8 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
     const float* x = X + row * d;
     float* xpf = static_cast<float*>(Xp_) + row * DP;
     uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP;
-    double acc = 0.0, eacc = 0.0;
+    double acc = 0.0;
+    float eaccf = 0.0f;
     bool finite = true, big = false;
     for (int k = lane; k < DP; k += 32) {
         float t = 0.0f;
@@ -1265,13 +1272,14 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
             t = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
                      : round_tf32(c);
             if (!(fabsf(t) <= kBigLimit)) big = true;
-            const double e = static_cast<double>(t) - static_cast<double>(c);
-            eacc += e * e;
+            const float e = __fsub_rn(t, c);  // exact (see k_prep)
+            eaccf = __fmaf_rn(e, e, eaccf);
         }
         if (BF16) xpb[k] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
         else xpf[k] = t;
         acc += static_cast<double>(t) * static_cast<double>(t);
     }
+    double eacc = static_cast<double>(eaccf);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1294,7 +1302,7 @@ k_prep_wide(const float* __restrict__ X, int64_t n, int d, int DP, const float* 
             sn[row] = kFlagBig;
         } else {
             hn[row] = static_cast<float>(acc);
-            sn[row] = err_norm(acc, eacc);
+            sn[row] = err_norm(acc, eacc, d);
         }
     }
 }
