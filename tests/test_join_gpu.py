@@ -332,7 +332,7 @@ def test_release_caches():
 
 
 @pytest.mark.parametrize("variant", ["band", "dense", "nofold", "tf32", "pair"])
-@pytest.mark.parametrize("n,d", [(5000, 1), (9000, 1), (6000, 2), (4000, 8)])
+@pytest.mark.parametrize("n,d", [(5000, 1), (9000, 1), (6000, 2), (4000, 8), (3000, 64)])
 def test_bf16_rounding_bound(monkeypatch, variant, n, d):
     """Rows on a line far from the screen copies' centre, neighbours 0.9 tau
     apart: the bf16 copy's rounding error reaches its worst case (half an
@@ -342,6 +342,8 @@ def test_bf16_rounding_bound(monkeypatch, variant, n, d):
         monkeypatch.setenv("PDB_NO_FOLD", "1")
     if variant == "pair":
         monkeypatch.setenv("PDB_SCREEN_PAIR", "1")
+    if variant == "band":
+        monkeypatch.setenv("PDB_JOIN_BAND", "1")   # the band plan at this size
     t = np.arange(n, dtype=np.float64) * 0.09
     v = np.ones(d) / np.sqrt(d)
     X = (t[:, None] * v[None, :] + 3.0).astype(np.float32)
@@ -354,3 +356,39 @@ def test_bf16_rounding_bound(monkeypatch, variant, n, d):
     assert len(ol) >= n - 2
     assert np.array_equal(l, ol) and np.array_equal(rr, orr)
     assert np.array_equal(dd, od.astype(np.float32))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_offsets_scales_dims(monkeypatch, seed):
+    """Random shapes, dimensions, offsets far from the data's spread, scales
+    and thresholds at distance quantiles, through a random screen variant:
+    the pair set and distances equal the oracle's."""
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([1, 2, 3, 5, 8, 13, 24, 31, 64, 100, 128, 200]))
+    nL, nR = int(rng.integers(50, 1500)), int(rng.integers(50, 1500))
+    scale = float(10.0 ** rng.uniform(-4, 3))
+    off = rng.normal(0, 1, d) * scale * float(10.0 ** rng.uniform(0, 3))
+    L = (rng.random((nL, d)) * scale + off).astype(np.float32)
+    near = L[rng.integers(0, nL, nR // 2)] + rng.normal(0, scale * 0.01, (nR // 2, d))
+    R = np.concatenate([near, rng.random((nR - nR // 2, d)) * scale + off]).astype(np.float32)
+    dd = np.sqrt(((L[:200, None, :].astype(np.float64) - R[None, :200]) ** 2).sum(-1))
+    tau = float(np.quantile(dd, rng.uniform(0.001, 0.05)))
+    if seed % 3 == 0:
+        # points on a line far from its centre, neighbours 0.9 tau apart: the
+        # copies' rounding errors line up along the line (worst case)
+        v = rng.normal(0, 1, d)
+        v /= np.linalg.norm(v)
+        tau = 0.1 * scale
+        t = np.arange(max(nL, nR), dtype=np.float64) * 0.09 * scale
+        L = (off + t[:nL, None] * v).astype(np.float32)
+        R = (off + t[:nR, None] * v + 0.05 * scale * v).astype(np.float32)
+    variant = rng.choice(["default", "dense", "band", "tf32", "nofold"])
+    if variant == "band":
+        monkeypatch.setenv("PDB_JOIN_BAND", "1")
+    if variant == "nofold":
+        monkeypatch.setenv("PDB_NO_FOLD", "1")
+    self_join = bool(rng.integers(0, 2))
+    res = patchdb.sim_join(L, None if self_join else R, tau, self_join=self_join,
+                           dense=variant == "dense", tf32=variant == "tf32")
+    ol, orr, od = oracle.sim_join(L, None if self_join else R, tau, self_join=self_join, threads=4)
+    _check(res, ol, orr, od)
