@@ -1801,8 +1801,8 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
 // the bins, each scatter block scans them and reserves its slots per bin
 // with one atomic (the order inside a bin is arbitrary -- harmless, since
 // the tile test is exact for any order).
-// Sharded joins need every rank to build the same order and use a stable
-// radix sort instead.
+// Sharded joins need every rank to build the same order and use the
+// deterministic stable counting sort below (k_rank_*) instead.
 constexpr int kBins = 1 << (2 * kMortonBits);
 
 constexpr int kScatterRows = 4;  // rows per thread (4096 per 1024-thread block)
@@ -1871,6 +1871,111 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
             PDB_DCHECK(k[i] < static_cast<uint32_t>(kBins) && base[k[i]] + local[i] < n);
             perm[base[k[i]] + local[i]] = static_cast<int32_t>(r);
         }
+    }
+}
+
+// Deterministic stable counting sort of the 12-bit keys (sharded joins:
+// every rank must build the same order).  k_rank_local: per block of
+// kRankRows consecutive rows, each row's rank among the block's earlier rows
+// with the same key -- the block's warps take turns (row order), each warp
+// ranking its 32 rows with __match_any_sync against a shared running count
+// per bin -- and the block's per-bin totals.
+constexpr int kRankRows = 4096;
+__global__ void __launch_bounds__(1024)
+k_rank_local(const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ rank,
+             int32_t* __restrict__ bcnt) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int32_t running[kBins];
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) running[b] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kRankRows;
+    for (int pass = 0; pass < kRankRows / 1024; pass++) {
+        const int64_t row = base + pass * 1024 + threadIdx.x;
+        const uint32_t k = row < n ? __ldg(key + row) : 0xffffffffu;  // sentinel past the end
+        const uint32_t same = __match_any_sync(0xffffffffu, k);
+        const int below = __popc(same & ((1u << lane) - 1u));
+        const bool last = (same >> lane) == 1u;  // highest lane of its key group
+        for (int turn = 0; turn < 32; turn++) {
+            if (turn == w && row < n) {
+                const int32_t b0 = running[k];
+                rank[row] = b0 + below;
+                __syncwarp(__activemask());
+                if (last) running[k] = b0 + __popc(same);
+            }
+            __syncthreads();
+        }
+    }
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+        bcnt[static_cast<int64_t>(blockIdx.x) * kBins + b] = running[b];
+}
+
+// In place: bcnt[blk][bin] -> the sorted position of the block's first row
+// of that bin: the bin's start (exclusive scan of the global counts) plus the
+// earlier blocks' counts of the bin.  One thread per bin.
+__global__ void __launch_bounds__(256)
+k_rank_offsets(const int32_t* __restrict__ count, int32_t* __restrict__ bcnt, int64_t nblk) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    __shared__ int32_t wsum[8];
+    __shared__ int32_t start_of_block;
+    const int bin = blockIdx.x * blockDim.x + threadIdx.x;
+    // this block's bins start after every lower bin: sum of count[0 .. first)
+    int32_t part = 0;
+    for (int b = threadIdx.x; b < blockIdx.x * blockDim.x; b += blockDim.x) part += count[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int q = 0; q < 8; q++) t += wsum[q];
+        start_of_block = t;
+    }
+    __syncthreads();
+    // exclusive scan of count over this block's 256 bins
+    const int32_t c = count[bin];
+    int32_t incl = c;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int32_t wpre = 0;
+    for (int q = 0; q < wid; q++) wpre += wsum[q];
+    int32_t run = start_of_block + wpre + incl - c;
+    // then down the blocks (independent loads issued ahead of the running sum)
+    for (int64_t b0 = 0; b0 < nblk; b0 += 8) {
+        int32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = b0 + q < nblk ? bcnt[(b0 + q) * kBins + bin] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (b0 + q < nblk) bcnt[(b0 + q) * kBins + bin] = run;
+            run += v[q];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+k_rank_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __restrict__ rank,
+               const int32_t* __restrict__ boff, int32_t* __restrict__ perm) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kRankRows;
+    for (int i = threadIdx.x; i < kRankRows; i += blockDim.x) {
+        const int64_t row = base + i;
+        if (row >= n) break;
+        const uint32_t k = __ldg(key + row);
+        const int64_t pos = static_cast<int64_t>(__ldg(boff + static_cast<int64_t>(blockIdx.x) * kBins + k)) +
+                            __ldg(rank + row);
+        PDB_DCHECK(k < static_cast<uint32_t>(kBins) && pos >= 0 && pos < n);
+        perm[pos] = static_cast<int32_t>(row);
     }
 }
 
@@ -3030,7 +3135,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         }
         // units <= total / ch + n_slots with ch = clamp(total / units_target, 1, 64)
         units_cap = 2 * static_cast<int64_t>(units_target) + list_cap / 64 + n_slots + 1;
-        // too little screen to save (sharded joins also pay a stable radix sort)
+        // too little screen to save (sharded joins also pay the stable sort)
         if (band_env != 1 && list_cap < kBandMinTiles * (P > 1 ? 2 : 1)) band = false;
         // tile-list positions travel as int32 (unit_info, Unit): beyond 2^31
         // dense tiles per shard (> ~11.8 M rows self-joined on one GPU) the
@@ -3038,13 +3143,12 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         if (list_cap >= (int64_t{1} << 31)) band = false;
     }
     if (band) {
-        if (P > 1)
-            PDB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint32_t*>(nullptr),
-                                                     static_cast<uint32_t*>(nullptr),
-                                                     static_cast<int32_t*>(nullptr),
-                                                     static_cast<int32_t*>(nullptr),
-                                                     std::max(nL, nR), 0, 2 * kMortonBits, s));
-        sort_tmp = std::max(sort_tmp, static_cast<size_t>(2 * kBins * 4));
+        sort_tmp = static_cast<size_t>(2 * kBins * 4);  // bin counts and fill cursors
+        if (P > 1) {
+            // ranks (n) + per-block bin counts / offsets of the stable sort
+            const int64_t nmax = std::max(nL, nR);
+            sort_tmp += Arena::need(nmax, 4) + Arena::need(ceil_div(nmax, kRankRows) * kBins, 4) + 512;
+        }
     }
     const size_t band_bytes =
         !band ? 0
@@ -3108,9 +3212,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         uint8_t* tmpL = ar.take<uint8_t>(sort_tmp);
         uint8_t* tmpR = self ? nullptr : ar.take<uint8_t>(sort_tmp);
         launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
-                   static_cast<const float*>(part), E, sum,
-                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpL),
-                   P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmpR));
+                   static_cast<const float*>(part), E, sum, reinterpret_cast<int32_t*>(tmpL),
+                   reinterpret_cast<int32_t*>(tmpR));
         const int eig_smem = d * d * 4;
         // (set_max_smem caches per function and device)
         set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
@@ -3126,34 +3229,31 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             const int nv = (d + 31) / 32;
             auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
                                                                                       : k_band_keys<4>;
-            // PDB_KEYS_BPS (A/B): blocks per SM of the keys pass (0: one
-            // block per 32 / 64 rows, capped at 16 per SM)
-            static const int keys_bps = [] {
-                const char* e = getenv("PDB_KEYS_BPS");
-                return e ? atoi(e) : 0;
-            }();
             const unsigned gk = static_cast<unsigned>(
-                keys_bps > 0 ? std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * keys_bps)
-                             : std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
+                std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
+            int32_t* count = reinterpret_cast<int32_t*>(tmp);  // bin counts, zeroed by k_pca_reduce
             launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
-                       proj, k_in, v_in,
-                       P > 1 ? nullptr : reinterpret_cast<int32_t*>(tmp));
+                       proj, k_in, v_in, count);
             if (P > 1) {
-                // every rank must build the same order: stable radix sort
-                uint32_t* k_out = ar.take<uint32_t>(n);
-                size_t tb = sort_tmp;
-                PDB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, perm, n, 0,
-                                                         2 * kMortonBits, s));
-                launches += 5;
+                // every rank must build the same order: a deterministic stable
+                // counting sort (block-local ranks in row order, per-bin block
+                // offsets, scatter) -- the single-GPU scatter below orders
+                // rows inside a bin by atomics
+                const int64_t nblk = ceil_div(n, kRankRows);
+                // (carved from this side's sort scratch, after the bin counts)
+                int32_t* rank = reinterpret_cast<int32_t*>(tmp + 2 * kBins * 4 + 256);
+                int32_t* bcnt = rank + ((n + 63) / 64) * 64;
+                launch_pdl(k_rank_local, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, s,
+                           static_cast<const uint32_t*>(k_in), n, rank, bcnt);
+                launch_pdl(k_rank_offsets, dim3(kBins / 256), dim3(256), 0, s,
+                           static_cast<const int32_t*>(count), bcnt, nblk);
+                launch_pdl(k_rank_scatter, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, s,
+                           static_cast<const uint32_t*>(k_in), n, static_cast<const int32_t*>(rank),
+                           static_cast<const int32_t*>(bcnt), perm);
+                launches += 4;
             } else {
-                int32_t* count = reinterpret_cast<int32_t*>(tmp);  // counted by k_band_keys
-                // PDB_SCATTER_RPT (A/B): rows per scatter thread (1 or 4)
-                static const int rpt = [] {
-                    const char* e = getenv("PDB_SCATTER_RPT");
-                    return e && atoi(e) == 1 ? 1 : kScatterRows;
-                }();
-                launch_pdl(rpt == 1 ? k_bin_scatter<1> : k_bin_scatter<kScatterRows>,
-                           dim3(static_cast<unsigned>(ceil_div(n, 1024 * rpt))),
+                launch_pdl(k_bin_scatter<kScatterRows>,
+                           dim3(static_cast<unsigned>(ceil_div(n, 1024 * kScatterRows))),
                            dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n,
                            static_cast<const int32_t*>(count), count + kBins, perm);
                 launches += 2;

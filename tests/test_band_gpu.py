@@ -142,3 +142,20 @@ def test_band_rule_keeps_small_joins_dense():
     r = patchdb.sim_join_device(x, None, 0.05, self_join=True)
     nb = -(-20_000 // 128)
     assert r.stats.tiles == sum(-(-20_000 // 256) - rb // 2 for rb in range(nb))
+
+
+def test_sharded_band_plan_deterministic_order(forced):
+    """Sharded self-joins need every rank to build the same row order: the
+    stable counting sort (k_rank_*) gives the shards an exact partition of the
+    pair set on clustered data with heavily shared sort keys, and identical
+    shard outputs on repeated calls."""
+    x = workloads.config5(60_000)
+    full = _pairs(patchdb.sim_join(x, None, 0.01, self_join=True))
+    for P in (2, 5):
+        parts = [patchdb.sim_join(x, None, 0.01, self_join=True, shard=(k, P)) for k in range(P)]
+        sets = [_pairs(p) for p in parts]
+        assert sum(len(s) for s in sets) == len(full)
+        assert set().union(*sets) == full
+    a = patchdb.sim_join(x, None, 0.01, self_join=True, shard=(1, 3))
+    b = patchdb.sim_join(x, None, 0.01, self_join=True, shard=(1, 3))
+    assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)
