@@ -70,4 +70,24 @@ __device__ __forceinline__ double exact_dist_grouped(const float* __restrict__ a
     return __dsqrt_rn(acc);
 }
 
+// Both rows from grouped copies (self-joins: the same copy, by row position).
+__device__ __forceinline__ double exact_dist_grouped2(const float* __restrict__ ag,
+                                                      const float* __restrict__ bg, int64_t gs,
+                                                      int d) {
+    double acc = 0.0;
+    for (int k = 0; k < d; k += 8) {
+        float x[8], y[8];
+        ldg256(ag + (k >> 3) * gs, x);
+        ldg256(bg + (k >> 3) * gs, y);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (k + q < d) {
+                const double t = __dsub_rn(static_cast<double>(x[q]), static_cast<double>(y[q]));
+                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            }
+        }
+    }
+    return __dsqrt_rn(acc);
+}
+
 }  // namespace pdb
