@@ -1112,7 +1112,7 @@ __device__ __forceinline__ double sum8_transpose(const double (&v)[8], int lane)
 // is input row perm[r] (band plan).
 constexpr int kRowsPerWarp = 8;
 template <bool BF16, int NV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)  // 4 resident blocks: the row loads need the warps
 k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
        void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn,
        uint16_t* __restrict__ gx, const int32_t* __restrict__ perm) {
