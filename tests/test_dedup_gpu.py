@@ -63,7 +63,7 @@ def test_errors_and_degenerate():
 
 
 @pytest.mark.parametrize("case", ["config1_full", "config2_4000", "chain_1d", "nan_rows",
-                                  "chain_30k", "chain_branchy"])
+                                  "chain_30k", "chain_branchy", "chain_then_clique"])
 def test_against_restatement(case):
     if case == "config1_full":          # 20,000 rows, ~1e6 tau-graph edges
         X, tau = workloads.config1(), 0.05
@@ -74,6 +74,11 @@ def test_against_restatement(case):
         X, tau = (np.arange(3000, dtype=np.float32) * 0.09).reshape(-1, 1), 0.1
     elif case == "chain_30k":           # decided by the sequential tail (k_dedup_tail) in chunks
         X, tau = (np.arange(30000, dtype=np.float32) * 0.09).reshape(-1, 1), 0.1
+    elif case == "chain_then_clique":   # tail items with more edges than the tail's stage holds
+        chain = (np.arange(200, dtype=np.float32) * 0.09).reshape(-1, 1)
+        rng = np.random.default_rng(4)
+        clique = (chain[-1, 0] + 0.09 + rng.random((42000, 1)) * 0.01).astype(np.float32)
+        X, tau = np.concatenate([chain, clique]).astype(np.float32), 0.1
     elif case == "chain_branchy":       # chains with several lower neighbours per item
         rng = np.random.default_rng(9)
         X = np.cumsum(rng.random((12000, 2), dtype=np.float32) * 0.04, axis=0).astype(np.float32)
