@@ -147,6 +147,9 @@ struct Unit {
     int32_t rb, j0, j1, chunk;
 };
 
+// Candidate-record slots an epilogue warp reserves per global atomic.
+constexpr unsigned kResChunk = 256;
+
 __device__ __forceinline__ int tile_at(const ScreenParams& p, int o) {
     return p.tile_list ? __ldg(p.tile_list + o) : o;
 }
@@ -485,14 +488,36 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         uint32_t nbuf = 0;                 // staged records (warp-uniform)
         unsigned long long ncand = 0;      // this lane's candidate pairs
         // write the staged records out: one atomic per flush, coalesced 16 B stores
+        // Records go to slots this warp reserves kResChunk at a time (one
+        // global atomic per chunk instead of per flush of <= 32; unused
+        // reserved slots are zeroed at the end -- the re-check skips a zero
+        // mask).
+        unsigned long long res_pos = 0, res_end = 0;
         auto flush = [&]() {
             __syncwarp();
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(nbuf));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (lane < static_cast<int>(nbuf) && base + lane < p.cap) p.rec[base + lane] = rbuf[lane];
+            const unsigned nb = nbuf;
+            const unsigned long long room = res_end - res_pos;
+            const unsigned first = room < nb ? static_cast<unsigned>(room) : nb;
+            if (static_cast<unsigned>(lane) < first && res_pos + lane < p.cap)
+                p.rec[res_pos + lane] = rbuf[lane];
+            res_pos += first;
+            if (first < nb) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunk));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                res_pos = base;
+                res_end = base + kResChunk;
+                if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
+                    res_pos + (lane - first) < p.cap)
+                    p.rec[res_pos + (lane - first)] = rbuf[lane];
+                res_pos += nb - first;
+            }
             __syncwarp();
             nbuf = 0;
+        };
+        auto zero_reserved = [&]() {
+            for (unsigned long long q = res_pos + lane; q < res_end; q += 32)
+                if (q < p.cap) p.rec[q] = make_int4(0, 0, 0, 0);
         };
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -629,6 +654,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             }
         }
         if (nbuf) flush();
+        zero_reserved();
         unsigned long long nc = ncand;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
@@ -909,14 +935,36 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         int4* rbuf = r_smem + ew * 32;
         uint32_t nbuf = 0;
         unsigned long long ncand = 0;
+        // Records go to slots this warp reserves kResChunk at a time (one
+        // global atomic per chunk instead of per flush of <= 32; unused
+        // reserved slots are zeroed at the end -- the re-check skips a zero
+        // mask).
+        unsigned long long res_pos = 0, res_end = 0;
         auto flush = [&]() {
             __syncwarp();
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(nbuf));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (lane < static_cast<int>(nbuf) && base + lane < p.cap) p.rec[base + lane] = rbuf[lane];
+            const unsigned nb = nbuf;
+            const unsigned long long room = res_end - res_pos;
+            const unsigned first = room < nb ? static_cast<unsigned>(room) : nb;
+            if (static_cast<unsigned>(lane) < first && res_pos + lane < p.cap)
+                p.rec[res_pos + lane] = rbuf[lane];
+            res_pos += first;
+            if (first < nb) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunk));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                res_pos = base;
+                res_end = base + kResChunk;
+                if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
+                    res_pos + (lane - first) < p.cap)
+                    p.rec[res_pos + (lane - first)] = rbuf[lane];
+                res_pos += nb - first;
+            }
             __syncwarp();
             nbuf = 0;
+        };
+        auto zero_reserved = [&]() {
+            for (unsigned long long q = res_pos + lane; q < res_end; q += 32)
+                if (q < p.cap) p.rec[q] = make_int4(0, 0, 0, 0);
         };
         const uint32_t t_empty_remote = leader ? 0u : leader_addr(&t_empty[0]);
         int acc = 0;
@@ -1007,6 +1055,7 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
         }
         if (nbuf) flush();
+        zero_reserved();
         unsigned long long nc = ncand;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
