@@ -90,4 +90,30 @@ __device__ __forceinline__ double exact_dist_grouped2(const float* __restrict__ 
     return __dsqrt_rn(acc);
 }
 
+// fp32 pre-filter of the grouped re-check: s = sum_k fl(a_k - b_k)^2 with
+// fp32 FMAs, on the same zero-padded 8-column groups (padding adds exact
+// zeros).  It only rejects: every fp32 step errs by at most 2^-24
+// relative (the subtraction's result is exact when subnormal, and
+// underflow in the sum can only make s smaller), so
+// s <= S (1 + 2^-24)^(d + 2) + d 2^-149 for the exact squared distance S,
+// and a candidate with s above the host's threshold (k_recheck) cannot
+// satisfy the reference's fp64 euclidean <= tau.  Overflow gives +inf
+// (every term is non-negative), which is rejected only when the threshold
+// is finite, i.e. when tau^2 is far below FLT_MAX.
+__device__ __forceinline__ float filter_dist2(const float* __restrict__ a, int64_t as,
+                                              const float* __restrict__ bg, int64_t gs, int d) {
+    float s = 0.0f;
+    for (int k = 0; k < d; k += 8) {
+        float x[8], y[8];
+        ldg256(a + (k >> 3) * as, x);
+        ldg256(bg + (k >> 3) * gs, y);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const float t = __fsub_rn(x[q], y[q]);
+            s = __fmaf_rn(t, t, s);
+        }
+    }
+    return s;
+}
+
 }  // namespace pdb

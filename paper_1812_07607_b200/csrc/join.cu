@@ -2432,6 +2432,134 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
     }
 }
 
+// K3 for candidate-heavy joins (the grouped copy XT of R; G = 1: L
+// row-major with d % 8 == 0 and 32-byte rows, G = 2: self-join, L from XT
+// by row position).  Two stages per warp: every candidate of the flattened
+// queue (as in k_recheck) first gets the fp32 pre-filter (filter_dist2,
+// FMA pipe); the survivors go to a per-warp shared-memory queue, and each
+// full batch of 32 survivors runs the reference's fp64 chain, so every
+// lane of the exact stage is busy.  The chain's float -> double
+// conversions run on the XU pipe at a quarter of the fp64 rate and bounded
+// the one-stage kernel (ncu, config 5: XU 75 % busy, 2.85e9 candidates for
+// 1.04e9 pairs); the filter skips them for candidates that cannot be
+// pairs.  Every emitted pair and distance still comes from the exact chain.
+template <int G>
+__global__ void __launch_bounds__(256)
+k_recheck_filtered(const int4* __restrict__ rec, const unsigned long long* __restrict__ n_rec,
+                   unsigned long long cap, const float* __restrict__ L, int d, double tau,
+                   float thr, int32_t* __restrict__ out_l, int32_t* __restrict__ out_r,
+                   float* __restrict__ out_d, unsigned long long out_cap,
+                   unsigned long long* __restrict__ out_count, const int32_t* __restrict__ permL,
+                   const int32_t* __restrict__ permR, int self_join, const float* __restrict__ XT,
+                   int64_t ldt) {
+    static_assert(G == 1 || G == 2, "grouped modes only");
+    __shared__ int2 queue[8][64];
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const unsigned long long n = min(*n_rec, cap);
+    const int lane = threadIdx.x & 31;
+    int2* q = queue[threadIdx.x >> 5];
+    int nq = 0;  // warp-uniform
+    const int64_t gs = ldt * 8;
+    // lanes < m re-check q[lane] exactly and emit the pairs
+    auto exact_batch = [&](int m) {
+        bool ok = false;
+        double dist = 0.0;
+        int a = 0, j = 0;
+        if (lane < m) {
+            const int2 e = q[lane];
+            a = permL ? __ldg(permL + e.x) : e.x;
+            j = permR ? __ldg(permR + e.y) : e.y;
+            PDB_DCHECK(a >= 0 && j >= 0 && j < ldt);
+            dist = G == 2 ? exact_dist_grouped2(XT + static_cast<int64_t>(e.x) * 8,
+                                                XT + static_cast<int64_t>(e.y) * 8, gs, d)
+                          : exact_dist_grouped(L + static_cast<int64_t>(a) * d,
+                                               XT + static_cast<int64_t>(e.y) * 8, gs, d, true);
+            ok = dist <= tau;
+            if (self_join && a > j) {
+                const int t = a;
+                a = j;
+                j = t;
+            }
+        }
+        const uint32_t ball = __ballot_sync(0xffffffffu, ok);
+        if (!ball) return;
+        unsigned long long w = 0;
+        if (lane == 0) w = atomicAdd(out_count, static_cast<unsigned long long>(__popc(ball)));
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (ok) {
+            const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
+            if (pos < out_cap) {
+                out_l[pos] = a;
+                out_r[pos] = j;
+                out_d[pos] = static_cast<float>(dist);
+            }
+        }
+    };
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                                   (threadIdx.x & ~31u);
+         base < n; base += stride) {
+        const unsigned long long idx = base + lane;
+        int4 rc = make_int4(0, 0, 0, 0);
+        if (idx < n) rc = rec[idx];
+        const uint32_t mask = static_cast<uint32_t>(rc.z);
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int c0 = 0; c0 < total; c0 += 32) {
+            const int c = c0 + lane;
+            int src = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int e = __shfl_sync(0xffffffffu, excl, src + step);
+                if (e <= c) src += step;
+            }
+            const int s_excl = __shfl_sync(0xffffffffu, excl, src);
+            const uint32_t s_mask = __shfl_sync(0xffffffffu, mask, src);
+            const int s_j0 = __shfl_sync(0xffffffffu, rc.y, src);
+            const int pa = __shfl_sync(0xffffffffu, rc.x, src);
+            bool pass = false;
+            int jp = 0;
+            if (c < total) {
+                jp = s_j0 + __fns(s_mask, 0, c - s_excl + 1);
+                PDB_DCHECK(jp >= 0 && jp < ldt && pa >= 0);
+                const float* ap;
+                int64_t as;
+                if (G == 2) {
+                    ap = XT + static_cast<int64_t>(pa) * 8;
+                    as = gs;
+                } else {
+                    ap = L + static_cast<int64_t>(permL ? __ldg(permL + pa) : pa) * d;
+                    as = 8;
+                }
+                pass = filter_dist2(ap, as, XT + static_cast<int64_t>(jp) * 8, gs, d) <= thr;
+            }
+            const uint32_t ball = __ballot_sync(0xffffffffu, pass);
+            if (pass) q[nq + __popc(ball & ((1u << lane) - 1u))] = make_int2(pa, jp);
+            nq += __popc(ball);
+            __syncwarp();
+            if (nq >= 32) {
+                exact_batch(32);
+                nq -= 32;
+                __syncwarp();
+                int2 t = make_int2(0, 0);
+                if (lane < nq) t = q[32 + lane];
+                __syncwarp();
+                if (lane < nq) q[lane] = t;
+                __syncwarp();
+            }
+        }
+    }
+    if (nq > 0) exact_batch(nq);
+}
+
 __global__ void k_pack_keys(const int32_t* __restrict__ l, const int32_t* __restrict__ r,
                             int64_t n, unsigned long long* __restrict__ keys) {
     for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
@@ -2882,6 +3010,23 @@ int grouped_mode() {
     const char* e = std::getenv("PDB_K3_GROUPED");
     if (!e || !e[0]) return 1;
     return std::clamp(atoi(e), 0, 2);
+}
+
+// Threshold of K3's fp32 pre-filter (filter_dist2): a reference pair has
+// exact squared distance S <= tau^2 (1 + 1e-9) (the fp64 chain errs far
+// below that), and the filter's sum is at most S (1 + 2^-24)^(d + 2) +
+// d 2^-149; the float threshold is rounded up.  +inf (no filtering) when
+// that bound is not far below FLT_MAX, or with PDB_K3_FILTER=0 (read on
+// every call).
+float recheck_filter_threshold(double tau, int d) {
+    const char* e = std::getenv("PDB_K3_FILTER");
+    if (e && e[0] && atoi(e) == 0) return INFINITY;
+    const double t2 = tau * tau * (1.0 + 1e-9) * (1.0 + (d + 3) * std::ldexp(1.0, -24) * 1.01) +
+                      d * std::ldexp(1.0, -149);
+    if (!(t2 < 1e37)) return INFINITY;
+    float f = static_cast<float>(t2);
+    if (static_cast<double>(f) < t2) f = std::nextafter(f, INFINITY);
+    return f;
 }
 
 // The shared back half of both joins: screen (with a sampled output-size
@@ -3467,6 +3612,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     DevBuf<float> XT;  // grouped copy of R for candidate-heavy re-checks
     bool xt_filled = false;
+    const float filter_thr = recheck_filter_threshold(tau, d);
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters, ready,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool& grouped) {
@@ -3490,6 +3636,20 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                            // a self-join reads both sides from the one grouped copy
                            // (rows by position): c5 re-check 145 -> 139 ms
                            const bool both = grouped && self;
+                           // the fp32 pre-filter (grouped copies only; L read
+                           // 32 bytes at a time in the cross-join variant)
+                           const bool vec8L = d % 8 == 0 && reinterpret_cast<uintptr_t>(d_L) % 32 == 0;
+                           if (grouped && filter_thr < INFINITY && (both || vec8L)) {
+                               launch_pdl_if(pdl, both ? k_recheck_filtered<2> : k_recheck_filtered<1>,
+                                   dim3(ctx.sm_count * 8), dim3(256), 0, s,
+                                   recs, counters, cap, d_L, d, tau, filter_thr, o2->left, o2->right,
+                                   o2->dist, static_cast<unsigned long long>(o2->capacity),
+                                   counters + 2, static_cast<const int32_t*>(permL),
+                                   static_cast<const int32_t*>(permR), static_cast<int>(self),
+                                   static_cast<const float*>(XT.p), nR);
+                               PDB_CUDA(cudaGetLastError());
+                               return;
+                           }
                            launch_pdl_if(pdl, both ? k_recheck<2> : grouped ? k_recheck<1> : k_recheck<0>,
                                dim3(ctx.sm_count * 8), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,

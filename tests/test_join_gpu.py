@@ -105,10 +105,13 @@ def test_value_scales_and_offsets(scale, tf32):
     _check(res, ol, orr, od)
 
 
-@pytest.mark.parametrize("tf32", [False, True])
-def test_boundary_pairs_exactly_at_tau(tf32):
+@pytest.mark.parametrize("tf32,grouped", [(False, False), (True, False), (False, True)])
+def test_boundary_pairs_exactly_at_tau(monkeypatch, tf32, grouped):
     # Pairs whose fp64 distance is EXACTLY tau must be kept (inclusive <=),
-    # and tau one ulp below must drop them.
+    # and tau one ulp below must drop them.  `grouped` forces the re-check
+    # through the grouped copy and its fp32 pre-filter (k_recheck_filtered).
+    if grouped:
+        monkeypatch.setenv("PDB_K3_GROUPED", "2")
     rng = np.random.default_rng(4)
     L = rng.random((513, 24), dtype=np.float32)
     R = L.copy()
@@ -126,8 +129,10 @@ def test_boundary_pairs_exactly_at_tau(tf32):
     assert len(ol2) < len(ol)
 
 
-@pytest.mark.parametrize("tf32", [False, True])
-def test_nonfinite_and_huge_rows(tf32):
+@pytest.mark.parametrize("tf32,grouped", [(False, False), (True, False), (False, True)])
+def test_nonfinite_and_huge_rows(monkeypatch, tf32, grouped):
+    if grouped:  # huge rows overflow the fp32 pre-filter's sums to +inf
+        monkeypatch.setenv("PDB_K3_GROUPED", "2")
     rng = np.random.default_rng(8)
     L = rng.random((300, 16), dtype=np.float32)
     R = L[::-1].copy()
@@ -279,7 +284,8 @@ def test_pair_overflow_rerun(monkeypatch):
 
 @pytest.mark.parametrize("case", ["config5_self", "band_cross_permR", "odd_d61"])
 def test_grouped_recheck_bit_identical(monkeypatch, case):
-    """The grouped re-check (k_group_copy + k_recheck<true>, forced with
+    """The grouped re-check (k_group_copy + k_recheck_filtered, or
+    k_recheck<1|2> without the fp32 pre-filter; forced with
     PDB_K3_GROUPED=2) and the row-major one (=0) return bit-identical sorted
     output, equal to the oracle: self join, a band-plan cross join (column
     permutation permR) and d % 8 != 0."""
@@ -296,12 +302,16 @@ def test_grouped_recheck_bit_identical(monkeypatch, case):
     Lt = torch.from_numpy(L).cuda()
     Rt = None if R is None else torch.from_numpy(R).cuda()
     outs = []
-    for mode in ("2", "0"):
+    # grouped with the fp32 pre-filter (k_recheck_filtered, the default),
+    # grouped without it (PDB_K3_FILTER=0: k_recheck<1|2>), and row-major
+    for mode, filt in (("2", "1"), ("2", "0"), ("0", "1")):
         monkeypatch.setenv("PDB_K3_GROUPED", mode)
+        monkeypatch.setenv("PDB_K3_FILTER", filt)
         r = patchdb.sim_join_device(Lt, Rt, tau, self_join=self_join, sort=True)
         outs.append([t.cpu().numpy() for t in r.to_torch(Lt.device)])
-    for a, b in zip(*outs):
-        assert np.array_equal(a, b)
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
     assert len(outs[0][0]) > 300
     rows = np.arange(0, L.shape[0], 97)
     ol, orr, od = oracle.sim_join_rows(L, R, tau, rows, self_join=self_join)
@@ -383,6 +393,8 @@ def test_fuzz_offsets_scales_dims(monkeypatch, seed):
         L = (off + t[:nL, None] * v).astype(np.float32)
         R = (off + t[:nR, None] * v + 0.05 * scale * v).astype(np.float32)
     variant = rng.choice(["default", "dense", "band", "tf32", "nofold"])
+    if seed % 2:  # the grouped re-check (with the fp32 pre-filter when it applies)
+        monkeypatch.setenv("PDB_K3_GROUPED", "2")
     if variant == "band":
         monkeypatch.setenv("PDB_JOIN_BAND", "1")
     if variant == "nofold":
