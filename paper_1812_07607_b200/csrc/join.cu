@@ -46,6 +46,7 @@
 #include <cub/cub.cuh>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -79,10 +80,35 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;        // warp 0 TMA, warp 1 MMA, 
 constexpr uint32_t kTmemCols = 512;   // two 256-column fp32 accumulators
 constexpr uint32_t kIdescTf32 = ptx::idesc_tf32(BM, BN);
 constexpr uint32_t kIdescBf16 = ptx::idesc_bf16(BM, BN);
+constexpr uint32_t kIdescF16 = ptx::idesc_f16(BM, BN);
 
 constexpr float kFlagNonFinite = -1.0f;
 constexpr float kFlagBig = -2.0f;
 constexpr float kBigLimit = 1.152921504606846976e18f;  // 2^60
+
+// fp16 screen copies (band plan, DP <= 128).  kind::f16 multiplies fp16 at
+// the bf16 rate, and fp16 keeps 11 significant bits to bf16's 8: the copies'
+// rounding errors -- the screen's margin (err_norm) -- shrink ~8x, and with
+// them the candidate band around tau (config 5: see DESIGN.md).  fp16's
+// range is covered by one power-of-two scale 2^s of the centred values,
+// chosen from their maximum xmax over both relations (k_band_keys; values
+// beyond 2^60 are the "big" rows, forced candidates in either format), so
+// that xmax 2^s < 2^14.  Distances scale by 2^s exactly; k_band_write
+// scales tau to match.  Values 2^24 below the maximum fall into fp16's
+// subnormals (absolute error 2^-25 after scaling): when that floor is not
+// far below tau the join keeps bf16 copies.  Every kernel that depends on
+// the format derives it from the same (xmax, tau, d), so they agree.
+// Returns the scale, or 0 for bf16.
+__device__ __forceinline__ float fp16_scale(const unsigned* xmax, double tau, int d) {
+    if (!xmax || !(tau > 0.0)) return 0.0f;
+    const float xm = __uint_as_float(*xmax);
+    if (!(xm > 0.0f)) return 1.0f;  // every centred value is zero
+    int e = 0;
+    frexpf(xm, &e);  // xm < 2^e
+    if (e < -100 || e > 100) return 0.0f;
+    if (!(sqrt(static_cast<double>(d)) * ldexp(1.0, e - 39) * 64.0 < tau)) return 0.0f;
+    return ldexpf(1.0f, 14 - e);
+}
 
 // Screen modes: L2 distance on tf32 or bf16 copies, or cosine on bf16 rows.
 constexpr int kModeL2Tf32 = 0;
@@ -141,6 +167,10 @@ struct ScreenParams {
     const int4* unit_info;         // decoded units (rb, first, end, slot), one load per unit
     int32_t n_slots;
     const float* hrow;             // banded: each row's screen threshold h_i (k_band_write)
+    // fp16 copies when fp16_scale(f16xmax, f16tau, f16d) > 0 (band plan only)
+    const unsigned* f16xmax;
+    double f16tau;
+    int32_t f16d;
 };
 
 struct Unit {
@@ -412,6 +442,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
+            const uint32_t idesc_data =
+                fp16_scale(p.f16xmax, p.f16tau, p.f16d) > 0.0f ? kIdescF16 : kIdescBf16;
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             uint32_t na = 0;  // units consumed
@@ -441,7 +473,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         for (int kk = 0; kk < 4; kk++) {  // 4 x 32 bytes of K per block
                             if (BF16)
                                 ptx::mma_f16(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
-                                             ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescBf16,
+                                             ptx::sdesc_k_sw128(b_addr + kk * 32), idesc_data,
                                              (kb | kk) != 0);
                             else
                                 ptx::mma_tf32(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
@@ -877,6 +909,8 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     } else if (warp == 1) {
         // ===================== MMA issuer (leader, one thread) =====================
         if (leader && lane == 0) {
+            const uint32_t idesc_data = fp16_scale(p.f16xmax, p.f16tau, p.f16d) > 0.0f
+                                            ? ptx::idesc_f16(2 * BM, BN) : kIdescPair;
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0, na = 0;
             unsigned long long ntiles = 0;
@@ -901,7 +935,7 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll
                         for (int kk = 0; kk < 4; kk++)
                             ptx::mma_f16_pair(d_tmem, ptx::sdesc_k_sw128(a_addr + kk * 32),
-                                              ptx::sdesc_k_sw128(b_addr + kk * 32), kIdescPair,
+                                              ptx::sdesc_k_sw128(b_addr + kk * 32), idesc_data,
                                               (kb | kk) != 0);
                     }
                     // the folded-g block: one K=16 step on 32-byte rows
@@ -1164,9 +1198,12 @@ template <bool BF16, int NV>
 __global__ void __launch_bounds__(256, 4)  // 4 resident blocks: the row loads need the warps
 k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
        void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn,
-       uint16_t* __restrict__ gx, const int32_t* __restrict__ perm) {
+       uint16_t* __restrict__ gx, const int32_t* __restrict__ perm,
+       const unsigned* __restrict__ f16xmax, double f16tau) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    // fp16 copies of the scaled centred rows, or bf16 / tf32 (fp16_scale)
+    const float sc = BF16 ? fp16_scale(f16xmax, f16tau, d) : 0.0f;
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t r0 = w * kRowsPerWarp;
@@ -1213,9 +1250,15 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
             t[i] = 0.0f;
             if (k < d) {
                 if (!isfinite(x[r][i])) finite = false;
-                const float c = __fsub_rn(x[r][i], m[i]);
-                t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
-                            : round_tf32(c);
+                float c = __fsub_rn(x[r][i], m[i]);
+                if (BF16 && sc > 0.0f) {
+                    c = __fmul_rn(c, sc);  // exact: a power of two (fp32 underflow
+                                           // below 2^-126 errs < 2^-150, inside the 1e-30 slack)
+                    t[i] = __half2float(__float2half_rn(c));
+                } else {
+                    t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
+                                : round_tf32(c);
+                }
                 if (!(fabsf(t[i]) <= kBigLimit)) big = true;
                 // this coordinate's rounding error: exact in fp32 (t is c
                 // rounded, so the two are within a factor 2); its square and
@@ -1239,7 +1282,9 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
                 uint16_t b[NV];
 #pragma unroll
                 for (int i = 0; i < NV; i++)
-                    b[i] = zero ? 0 : static_cast<uint16_t>(__float_as_uint(t[i]) >> 16);
+                    b[i] = zero ? 0
+                         : sc > 0.0f ? __half_as_ushort(__float2half_rn(t[i]))  // exact: t is fp16
+                                     : static_cast<uint16_t>(__float_as_uint(t[i]) >> 16);
                 if (NV == 4) {
                     *reinterpret_cast<uint2*>(xpb) =
                         make_uint2(b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16),
@@ -1495,6 +1540,7 @@ struct BandInfo {
     double lo[2], inv[2];   // key quantisation q = (p - lo) * inv, clamped to [0, 2^bits - 1]
     double s;               // sqrt(lambda_max(U^T U)), rounded up
     unsigned long long bmax;  // fp64 bits of max_rows sum_k |u_k x_k| (projection error scale)
+    unsigned xmax;            // fp32 bits of max |x_k - mu_k| <= 2^60 (fp16_scale)
 };
 
 // Partial sums over kPcaRows sample rows, centred by mu: the d x d products
@@ -1719,6 +1765,7 @@ k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
             info->inv[k] = sd > 0 ? static_cast<double>(1 << kMortonBits) / (6.0 * sd) : 0.0;
         }
         info->bmax = 0ull;
+        info->xmax = 0u;
     }
 }
 
@@ -1746,7 +1793,7 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
             int32_t* __restrict__ val, int32_t* __restrict__ bin_count) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    __shared__ float bred[8];
+    __shared__ float bred[8], xred[8];
     __shared__ float4 us[3][32 * NV / 4];  // u0, u1, mu
     for (int c = threadIdx.x; c < 32 * NV / 4; c += blockDim.x) {
         us[0][c] = reinterpret_cast<const float4*>(info->u[0])[c];
@@ -1767,7 +1814,7 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
     // eight rows per warp step (two per lane group), all loads issued first
     constexpr int RPG = NV >= 3 ? 2 : 1;
     const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4 * RPG;
-    float bm = 0.0f;
+    float bm = 0.0f, xm = 0.0f;
     for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * 4 * RPG; r0 < n;
          r0 += step) {
         float x[RPG][NV][4];
@@ -1804,6 +1851,7 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const float xc = x[h][i][j] - mc[j];
+                    if (fabsf(xc) <= kBigLimit) xm = fmaxf(xm, fabsf(xc));  // (NaN, inf: no)
                     p0 = fmaf(ua[j], xc, p0);
                     p1 = fmaf(ub[j], xc, p1);
                     b = fmaf(fabsf(ua[j]) + fabsf(ub[j]), fabsf(xc), b);
@@ -1836,13 +1884,23 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-    if (lane == 0) bred[wib] = bm;
+    for (int o = 16; o > 0; o >>= 1) {
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+    }
+    if (lane == 0) {
+        bred[wib] = bm;
+        xred[wib] = xm;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        float m = 0.0f;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) m = fmaxf(m, bred[w]);
+        float m = 0.0f, mx = 0.0f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) {
+            m = fmaxf(m, bred[w]);
+            mx = fmaxf(mx, xred[w]);
+        }
         if (m > 0) atomicMax(&info->bmax, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(m))));
+        if (mx > 0) atomicMax(&info->xmax, __float_as_uint(mx));
     }
 }
 
@@ -2249,9 +2307,13 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
              const int64_t* __restrict__ unit_off, const int32_t* __restrict__ dev_ch,
              int4* __restrict__ unit_info, const float* __restrict__ hnL,
              const float* __restrict__ snL, int64_t nL, double tau_p, double uu, double gam,
-             float* __restrict__ hrow) {
+             float* __restrict__ hrow, const unsigned* __restrict__ f16xmax) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    {  // fp16 copies measure distances in units of 2^-s (fp16_scale)
+        const float sc = fp16_scale(f16xmax, q.tau, q.d);
+        if (sc > 0.0f) tau_p *= static_cast<double>(sc);
+    }
     const int k = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (k >= q.n_slots) return;
@@ -3012,6 +3074,17 @@ int grouped_mode() {
     return std::clamp(atoi(e), 0, 2);
 }
 
+// PDB_SCREEN_FP16, read on every call: fp16 screen copies for band-plan
+// joins (fp16_scale) 0 never, 1 (default) when the sampled screen shows a
+// candidate-heavy output, 2 always.  (Measured: fp16 MMAs ran the screen
+// 2-5 % slower than bf16 on configs 3 and 5, so joins whose candidates are
+// already ~ their pairs keep bf16.)
+int screen_fp16_mode() {
+    const char* e = std::getenv("PDB_SCREEN_FP16");
+    if (!e || !e[0]) return 1;
+    return std::clamp(atoi(e), 0, 2);
+}
+
 // Threshold of K3's fp32 pre-filter (filter_dist2): a reference pair has
 // exact squared distance S <= tau^2 (1 + 1e-9) (the fp64 chain errs far
 // below that), and the filter's sum is at most S (1 + 2^-24)^(d + 2) +
@@ -3033,13 +3106,14 @@ float recheck_filter_threshold(double tau, int d) {
 // estimate for large problems), exact re-check, one counter read-back,
 // overflow handling, optional sort, stats.  `recheck(recs, cap, out)`
 // enqueues the mode's re-check kernel.
-template <class Recheck>
+template <class Recheck, class OnHeavy>
 void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
                         const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tG,
                         ScreenParams p,
                         int64_t nL, int64_t nR, const pdb_join_opts& o, pdb_dev_pairs* out,
                         pdb_join_stats* stats, PhaseTimer& tm, int launches,
-                        unsigned long long* counters_p, UnitsReady ready, Recheck&& recheck) {
+                        unsigned long long* counters_p, UnitsReady ready, Recheck&& recheck,
+                        OnHeavy&& on_heavy) {
     struct {
         unsigned long long* p;
     } counters{counters_p};  // [records, tiles, pairs, candidates, next unit]
@@ -3178,9 +3252,14 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     // records (config 1) gain nothing from it.  PDB_K3_GROUPED: see
     // grouped_mode().  The recheck callback may still fall back to the
     // row-major gather when the copy cannot be allocated.
+    const bool heavy = !small && h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR);
     const int gmode = grouped_mode();
-    bool grouped = gmode == 2 || (gmode == 1 && !small &&
-                                  h_cnt[3] * kSampleStep >= 4ull * static_cast<unsigned long long>(nR));
+    bool grouped = gmode == 2 || (gmode == 1 && heavy);
+    // a candidate-heavy join may re-make its screen copies in a finer format
+    // (L2: fp16, see fp16_scale); the callback returns the format's switch
+    if (heavy) {
+        if (const unsigned* f = on_heavy()) p.f16xmax = f;
+    }
     // Test hooks: PDB_TEST_REC_CAP / PDB_TEST_OUT_CAP cap the first pass's
     // record and pair buffers, forcing the overflow paths below.
     if (const char* e = std::getenv("PDB_TEST_REC_CAP"))
@@ -3376,14 +3455,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     PDB_CUDA(cudaGetLastError());
     launches++;
     auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out,
-                    const int32_t* perm) {
+                    const int32_t* perm, const unsigned* f16x) {
         if (DP <= 128) {  // g_out (the folded block) only exists for DP <= 128
             const unsigned g = static_cast<unsigned>(ceil_div(ceil_div(n, kRowsPerWarp) * 32, 256));
             auto pick = [&](auto k32, auto k64, auto k96, auto k128) {
                 const int nv = DP / 32;
                 auto k = nv == 1 ? k32 : nv == 2 ? k64 : nv == 3 ? k96 : k128;
                 launch_pdl(k, dim3(g), dim3(256), 0, s, X, n, d, DP, static_cast<const float*>(mu),
-                           static_cast<void*>(Xp), hn, sn, g_out, perm);
+                           static_cast<void*>(Xp), hn, sn, g_out, perm, f16x, tau);
             };
             if (tf32) pick(k_prep<false, 1>, k_prep<false, 2>, k_prep<false, 3>, k_prep<false, 4>);
             else pick(k_prep<true, 1>, k_prep<true, 2>, k_prep<true, 3>, k_prep<true, 4>);
@@ -3399,11 +3478,18 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     int32_t* permL = nullptr;
     int32_t* permR = nullptr;
     BandInfo* info = nullptr;
+    // fp16 screen copies (fp16_scale): band plans with DP <= 128 and bf16
+    // copies; PDB_SCREEN_FP16=2 from the start, 1 (default) when the sampled
+    // screen shows a candidate-heavy output, 0 never
+    const unsigned* f16x = nullptr;  // the copies' switch (nullptr: bf16)
+    const unsigned* f16_avail = nullptr;
     float2 *projL = nullptr, *projR = nullptr;
     if (band) {
         float* part = ar.take<float>(static_cast<size_t>(kPcaBlocks) * E);
         double* sum = ar.take<double>(E);
         info = ar.take<BandInfo>(1);
+        if (DP <= 128 && !tf32 && screen_fp16_mode() > 0) f16_avail = &info->xmax;
+        if (screen_fp16_mode() == 2) f16x = f16_avail;
         auto kp = d <= 16 ? k_pca_partial<1> : d <= 32 ? k_pca_partial<2> : d <= 64 ? k_pca_partial<4>
                                                                                   : k_pca_partial<8>;
         launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, s, d_L, nL, d, static_cast<const float*>(mu),
@@ -3537,14 +3623,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
     float* hnL = ar.take<float>(nL);
     float* snL = ar.take<float>(nL);
-    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL);
+    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x);
     const uint8_t* XpR = XpL;
     const float *hnR = hnL, *snR = snL;
     if (!self) {
         uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
         float* hr = ar.take<float>(nR);
         float* sr = ar.take<float>(nR);
-        prep(d_R, nR, xr, hr, sr, gx, permR);
+        prep(d_R, nR, xr, hr, sr, gx, permR, f16x);
         XpR = xr;
         hnR = hr;
         snR = sr;
@@ -3552,20 +3638,25 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
     float* tmaxS = ar.take<float>(nt);
     float* tmaxN = ar.take<float>(nt);
-    launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
-    if (band) {
-        if (aux) PDB_CUDA(cudaStreamWaitEvent(s, aux->join, 0));
-        if (n_slots > 0)
-            launch_pdl_if(!aux, k_band_write, dim3(static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256))),
+    // tile statistics and (band plan) each slot's tiles, maxima and row
+    // thresholds; re-run when the copies are re-made in fp16
+    auto tile_write = [&](bool first) {
+        launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
+        if (band && first && aux) PDB_CUDA(cudaStreamWaitEvent(s, aux->join, 0));
+        if (band && n_slots > 0)
+            launch_pdl_if(!(first && aux), k_band_write, dim3(static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256))),
                           dim3(256), 0, s, bp,
                           static_cast<const int64_t*>(list_off), list, static_cast<const float*>(tmaxS),
                           static_cast<const float*>(tmaxN), cmaxS, cmaxN,
                           static_cast<const int64_t*>(unit_off), static_cast<const int32_t*>(dev_ch),
                           unit_info, static_cast<const float*>(hnL), static_cast<const float*>(snL), nL,
                           tau * (1.0 + 1e-9), 1.0,
-                          (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow);
-        launches++;
-    } else {
+                          (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow,
+                          f16x);
+        launches += band ? 2 : 1;
+    };
+    tile_write(true);
+    if (!band) {
         cmaxS = ar.take<float>(nt + 1);
         cmaxN = ar.take<float>(nt + 1);
         launch_pdl(k_chunk_plan, dim3(1), dim3(1024), 0, s, static_cast<const float*>(tmaxS),
@@ -3575,6 +3666,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     PDB_CUDA(cudaGetLastError());
     launches++;
+    uint8_t* XpR_w = self ? XpL : const_cast<uint8_t*>(XpR);
+    float* hnR_w = const_cast<float*>(hnR);
+    float* snR_w = const_cast<float*>(snR);
 
     const CUtensorMap tA = make_tmap(ctx, XpL, nL, DP, BM, !tf32);
     const CUtensorMap tB = make_tmap(ctx, XpR, nR, DP, pair ? BN / 2 : BN, !tf32);
@@ -3600,6 +3694,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     p.tau_p = tau * (1.0 + 1e-9);
     p.u = 1.0;  // the error norms are stored directly (err_norm)
     p.gam = (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19);
+    p.f16xmax = f16x;
+    p.f16tau = tau;
+    p.f16d = d;
     if (band) {
         p.hrow = hrow;
         p.unit_info = unit_info;
@@ -3612,7 +3709,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     }
     DevBuf<float> XT;  // grouped copy of R for candidate-heavy re-checks
     bool xt_filled = false;
-    const float filter_thr = recheck_filter_threshold(tau, d);
+    // (the pre-filter pays off only against bf16's wide candidate band:
+    // config 5 re-check 141 -> 128 ms with bf16 copies, but 78 -> 86 ms
+    // with fp16 copies, whose candidates are 1.27x the pairs)
+    const float filter_thr_bf16 = recheck_filter_threshold(tau, d);
     screen_and_recheck(ctx, s, DP, pair ? kModeL2Bf16Pair : mode, tA, tB, tG, p, nL, nR, o, out, stats, tm, launches, counters, ready,
                        [&](const int4* recs, unsigned long long* counters,
                            unsigned long long cap, pdb_dev_pairs* o2, bool pdl, bool& grouped) {
@@ -3639,6 +3739,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                            // the fp32 pre-filter (grouped copies only; L read
                            // 32 bytes at a time in the cross-join variant)
                            const bool vec8L = d % 8 == 0 && reinterpret_cast<uintptr_t>(d_L) % 32 == 0;
+                           const float filter_thr = f16x ? INFINITY : filter_thr_bf16;
                            if (grouped && filter_thr < INFINITY && (both || vec8L)) {
                                launch_pdl_if(pdl, both ? k_recheck_filtered<2> : k_recheck_filtered<1>,
                                    dim3(ctx.sm_count * 8), dim3(256), 0, s,
@@ -3658,6 +3759,16 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                static_cast<const int32_t*>(permR), static_cast<int>(self),
                                static_cast<const float*>(grouped ? XT.p : nullptr), nR);
                            PDB_CUDA(cudaGetLastError());
+                       },
+                       [&]() -> const unsigned* {
+                           // candidate-heavy: re-make the copies in fp16
+                           // (the sampled pass screened bf16 copies)
+                           if (!f16_avail || f16x) return nullptr;
+                           f16x = f16_avail;
+                           prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x);
+                           if (!self) prep(d_R, nR, XpR_w, hnR_w, snR_w, gx, permR, f16x);
+                           tile_write(false);
+                           return f16x;
                        });
 }
 
@@ -3754,7 +3865,8 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2);
                            PDB_CUDA(cudaGetLastError());
-                       });
+                       },
+                       []() -> const unsigned* { return nullptr; });
 }
 
 }  // namespace pdb

@@ -159,3 +159,91 @@ def test_sharded_band_plan_deterministic_order(forced):
     a = patchdb.sim_join(x, None, 0.01, self_join=True, shard=(1, 3))
     b = patchdb.sim_join(x, None, 0.01, self_join=True, shard=(1, 3))
     assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)
+
+
+def _device_join(x, R, tau, self_join):
+    import torch
+    xt = torch.from_numpy(x).cuda()
+    rt = None if R is None else torch.from_numpy(R).cuda()
+    r = patchdb.sim_join_device(xt, rt, tau, self_join=self_join, sort=True)
+    out = [t.cpu().numpy() for t in r.to_torch(xt.device)]
+    return out, r.stats.candidates
+
+
+@pytest.mark.parametrize("case", ["config5", "config3", "forced_d17"])
+def test_fp16_copies_same_pairs_fewer_candidates(monkeypatch, case):
+    """Band-plan joins can screen fp16 copies of the scaled centred rows
+    (fp16_scale; forced here with PDB_SCREEN_FP16=2): the same pairs and
+    distances as the bf16 copies (PDB_SCREEN_FP16=0) and the oracle, with a
+    narrower candidate band."""
+    if case == "config5":
+        L, R, tau, self_join = workloads.config5(131_072), None, 0.01, True
+    elif case == "config3":
+        L, R, _, _ = workloads.config3(n=65_536)
+        tau, self_join = 0.02, False
+    else:
+        monkeypatch.setenv("PDB_JOIN_BAND", "1")
+        L = workloads.clusters(9000, 17, 80, 0.02, True, 17) * np.float32(300.0) - np.float32(7.0)
+        R, tau, self_join = None, 0.05 * 300.0, True
+    outs, cands = [], []
+    for f16 in ("2", "0"):  # forced fp16 copies, bf16 copies
+        monkeypatch.setenv("PDB_SCREEN_FP16", f16)
+        o, c = _device_join(L, R, tau, self_join)
+        outs.append(o)
+        cands.append(c)
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert len(outs[0][0]) > 100
+    assert cands[0] <= cands[1]
+    if case == "config5":
+        assert cands[0] < 0.7 * cands[1]  # the band around tau narrows
+    rows = np.arange(0, L.shape[0], 131)
+    ol, orr, od = oracle.sim_join_rows(L, R, tau, rows, self_join=self_join)
+    m = np.isin(outs[0][0], rows)
+    assert np.array_equal(outs[0][0][m], ol) and np.array_equal(outs[0][1][m], orr)
+    assert np.array_equal(outs[0][2][m], od.astype(np.float32))
+
+
+def test_fp16_copies_fall_back_for_wide_ranges(monkeypatch):
+    """One row 1e15 away sets the fp16 scale so low that the other rows
+    would land in fp16's subnormals; the join keeps bf16 copies (same
+    candidates as PDB_SCREEN_FP16=0) and stays exact."""
+    monkeypatch.setenv("PDB_JOIN_BAND", "1")
+    x = workloads.clusters(6000, 64, 70, 0.02, True, 5)
+    x[17] = 1e15
+    cands = []
+    for f16 in ("2", "0"):
+        monkeypatch.setenv("PDB_SCREEN_FP16", f16)
+        got = patchdb.sim_join(x, None, 0.05, self_join=True)
+        cands.append(got)
+    ol, orr, od = oracle.sim_join(x, None, 0.05, self_join=True)
+    for got in cands:
+        assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
+        assert np.array_equal(got.dist, od.astype(np.float32))
+    _, c1 = _device_join(x, None, 0.05, True)
+    monkeypatch.setenv("PDB_SCREEN_FP16", "2")
+    _, c2 = _device_join(x, None, 0.05, True)
+    assert c1 == c2
+
+
+def test_fp16_copies_chosen_for_candidate_heavy_joins(monkeypatch):
+    """By default a band-plan join re-makes its copies in fp16 when the
+    sampled screen shows >= 4 candidates per column row (config 5's
+    distribution at 1M rows): identical output to bf16 copies throughout,
+    far fewer candidates, exact on sampled rows."""
+    x = workloads.config5(1 << 20)
+    outs, cands = [], []
+    for f16 in ("1", "0"):
+        monkeypatch.setenv("PDB_SCREEN_FP16", f16)
+        o, c = _device_join(x, None, 0.01, True)
+        outs.append(o)
+        cands.append(c)
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert len(outs[0][0]) > 10_000_000
+    assert cands[0] < 0.6 * cands[1]
+    rows = np.arange(0, x.shape[0], 16_411)
+    ol, orr, od = oracle.sim_join_rows(x, None, 0.01, rows, self_join=True)
+    m = np.isin(outs[0][0], rows)
+    assert np.array_equal(outs[0][0][m], ol) and np.array_equal(outs[0][1][m], orr)
+    assert np.array_equal(outs[0][2][m], od.astype(np.float32))

@@ -302,11 +302,13 @@ def test_grouped_recheck_bit_identical(monkeypatch, case):
     Lt = torch.from_numpy(L).cuda()
     Rt = None if R is None else torch.from_numpy(R).cuda()
     outs = []
-    # grouped with the fp32 pre-filter (k_recheck_filtered, the default),
-    # grouped without it (PDB_K3_FILTER=0: k_recheck<1|2>), and row-major
-    for mode, filt in (("2", "1"), ("2", "0"), ("0", "1")):
+    # grouped with the fp32 pre-filter (k_recheck_filtered: bf16 screen
+    # copies), grouped without it (PDB_K3_FILTER=0: k_recheck<1|2>),
+    # grouped after an fp16 screen (band plans), and row-major
+    for mode, filt, f16 in (("2", "1", "0"), ("2", "0", "0"), ("2", "1", "1"), ("0", "1", "1")):
         monkeypatch.setenv("PDB_K3_GROUPED", mode)
         monkeypatch.setenv("PDB_K3_FILTER", filt)
+        monkeypatch.setenv("PDB_SCREEN_FP16", f16)
         r = patchdb.sim_join_device(Lt, Rt, tau, self_join=self_join, sort=True)
         outs.append([t.cpu().numpy() for t in r.to_torch(Lt.device)])
     for o in outs[1:]:
@@ -395,6 +397,8 @@ def test_fuzz_offsets_scales_dims(monkeypatch, seed):
     variant = rng.choice(["default", "dense", "band", "tf32", "nofold"])
     if seed % 2:  # the grouped re-check (with the fp32 pre-filter when it applies)
         monkeypatch.setenv("PDB_K3_GROUPED", "2")
+    if seed % 4 == 1:  # bf16 copies for band plans too
+        monkeypatch.setenv("PDB_SCREEN_FP16", "0")
     if variant == "band":
         monkeypatch.setenv("PDB_JOIN_BAND", "1")
     if variant == "nofold":
