@@ -29,12 +29,25 @@ __device__ __forceinline__ double exact_dist(const float* __restrict__ a,
         acc = __dadd_rn(acc, __dmul_rn(t, t));
     };
     if (vec8) {
+        // the next group's loads are issued before this group's chain: a
+        // lane's candidate is a dependent sequence of d/8 gathers, and the
+        // short joins (configs 1-3) are bound by their latency
+        float x[8], y[8];
+        ldg256(a, x);
+        ldg256(b, y);
         for (int k = 0; k < d; k += 8) {
-            float x[8], y[8];
-            ldg256(a + k, x);
-            ldg256(b + k, y);
+            float cx[8], cy[8];
 #pragma unroll
-            for (int q = 0; q < 8; q++) step(x[q], y[q]);
+            for (int q = 0; q < 8; q++) {
+                cx[q] = x[q];
+                cy[q] = y[q];
+            }
+            if (k + 8 < d) {
+                ldg256(a + k + 8, x);
+                ldg256(b + k + 8, y);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) step(cx[q], cy[q]);
         }
     } else {
         for (int k = 0; k < d; k++) step(__ldg(a + k), __ldg(b + k));

@@ -2419,13 +2419,29 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
     const int lane = threadIdx.x & 31;
     const bool vec8 =
         (d % 8 == 0) && ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(R)) % 32 == 0);
-    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
-                                   (threadIdx.x & ~31u);
+    // k records per warp step: 32, or fewer when the records are too few to
+    // give every warp a step of 32, and no more than ~32 candidates per step
+    // (n_rec[3] counts them).  Dense records of a sorted small join carry
+    // ~30 candidates each: 32 consecutive ones on one warp left most warps
+    // idle (config 1 with the band plan's order: re-check 0.124 -> 0.097 ms);
+    // sparse buffers -- mostly the zeroed tails of reserved slots -- keep one
+    // step per warp, and buffers long enough for >= 4 full steps per warp
+    // keep 32.
+    const unsigned long long warps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
+    const unsigned long long ncand = n_rec[3];
+    unsigned long long kk = min(32ull, (n + warps - 1) / warps);
+    if (n < 128 * warps) {  // (long buffers: 32, config 5 re-check 77 vs 102 ms at ~6)
+        if (ncand > 32 * n) kk = 1;
+        else if (ncand > 0) kk = min(kk, 32 * n / ncand);
+    }
+    const unsigned k = static_cast<unsigned>(max(1ull, kk));
+    const unsigned long long stride = warps * k;
+    for (unsigned long long base = (static_cast<unsigned long long>(blockIdx.x) * (blockDim.x >> 5) +
+                                    (threadIdx.x >> 5)) * k;
          base < n; base += stride) {
         const unsigned long long idx = base + lane;
         int4 rc = make_int4(0, 0, 0, 0);
-        if (idx < n) rc = rec[idx];
+        if (static_cast<unsigned>(lane) < k && idx < n) rc = rec[idx];
         const uint32_t mask = static_cast<uint32_t>(rc.z);
         // banded plans screen row-sorted copies: map back to input rows
         const int my_i = (permL && mask) ? __ldg(permL + rc.x) : rc.x;
@@ -2558,13 +2574,29 @@ k_recheck_filtered(const int4* __restrict__ rec, const unsigned long long* __res
             }
         }
     };
-    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
-                                   (threadIdx.x & ~31u);
+    // k records per warp step: 32, or fewer when the records are too few to
+    // give every warp a step of 32, and no more than ~32 candidates per step
+    // (n_rec[3] counts them).  Dense records of a sorted small join carry
+    // ~30 candidates each: 32 consecutive ones on one warp left most warps
+    // idle (config 1 with the band plan's order: re-check 0.124 -> 0.097 ms);
+    // sparse buffers -- mostly the zeroed tails of reserved slots -- keep one
+    // step per warp, and buffers long enough for >= 4 full steps per warp
+    // keep 32.
+    const unsigned long long warps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
+    const unsigned long long ncand = n_rec[3];
+    unsigned long long kk = min(32ull, (n + warps - 1) / warps);
+    if (n < 128 * warps) {  // (long buffers: 32, config 5 re-check 77 vs 102 ms at ~6)
+        if (ncand > 32 * n) kk = 1;
+        else if (ncand > 0) kk = min(kk, 32 * n / ncand);
+    }
+    const unsigned k = static_cast<unsigned>(max(1ull, kk));
+    const unsigned long long stride = warps * k;
+    for (unsigned long long base = (static_cast<unsigned long long>(blockIdx.x) * (blockDim.x >> 5) +
+                                    (threadIdx.x >> 5)) * k;
          base < n; base += stride) {
         const unsigned long long idx = base + lane;
         int4 rc = make_int4(0, 0, 0, 0);
-        if (idx < n) rc = rec[idx];
+        if (static_cast<unsigned>(lane) < k && idx < n) rc = rec[idx];
         const uint32_t mask = static_cast<uint32_t>(rc.z);
         const int cnt = __popc(mask);
         int incl = cnt;
