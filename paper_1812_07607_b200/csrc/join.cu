@@ -1531,9 +1531,13 @@ constexpr int64_t kBandMinRows = 8192;
 constexpr int64_t kBandMinTiles = 16384;
 constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
 #ifndef PDB_PCA_ITERS
-#define PDB_PCA_ITERS 4
+#define PDB_PCA_ITERS 2
 #endif
-constexpr int kPcaIters = PDB_PCA_ITERS;   // subspace iterations for the top-2 principal plane
+// Subspace iterations for the leading plane.  Any plane prunes correctly;
+// measured screened tiles for 1 / 2 / 3 / 4 iterations (r02): config 2
+// 21,967 / 19,540 / 19,797 / 19,595, config 3 2.59 M / 318 k / 330 k / 337 k,
+// config 5 51.1 M / 34.0 M / 34.9 M / 34.1 M.
+constexpr int kPcaIters = PDB_PCA_ITERS;
 
 struct BandInfo {
     float u[2][kPcaMaxD];   // the two directions (zero past d)
@@ -1811,8 +1815,8 @@ k_band_keys(const float* __restrict__ X, int64_t n, int d, const float* __restri
     const float lo0 = static_cast<float>(info->lo[0]), lo1 = static_cast<float>(info->lo[1]);
     const float inv0 = static_cast<float>(info->inv[0]), inv1 = static_cast<float>(info->inv[1]);
     const bool vec = d == 32 * NV && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-    // eight rows per warp step (two per lane group), all loads issued first
-    constexpr int RPG = NV >= 3 ? 2 : 1;
+    // 8 or 16 rows per warp step (RPG per lane group), all loads issued first
+    constexpr int RPG = NV >= 3 ? 2 : 4;  // rows per lane group in flight
     const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4 * RPG;
     float bm = 0.0f, xm = 0.0f;
     for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * 4 * RPG; r0 < n;
@@ -3276,7 +3280,10 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
             while (v < x) v *= 1.189207115002721;  // 2^(1/4)
             return static_cast<unsigned long long>(v);
         };
-        cap = std::max(cap, snap(h_cnt[0] * kSampleStep * 2.0));
+        // (records: 3x the sample -- at 2x a 262k-row config-5 join still
+        // overflowed once its clusters fell between the sampled units, and
+        // a miss costs a whole second screen; 16 B per record)
+        cap = std::max(cap, snap(h_cnt[0] * kSampleStep * 3.0));
         out_need = std::max(out_need, snap(h_cnt[3] * kSampleStep * 1.5));
     }
     // Re-check over a grouped copy of R when the sampled output is
@@ -3303,7 +3310,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
     // Screen and re-check run back to back and the host reads the counters
     // once.  A record overflow re-runs the screen with the exact record
     // count; an output overflow re-runs only the re-check.
-    for (int attempt = 0; attempt < 2; attempt++) {
+    bool switched = false;
+    for (int attempt = 0; attempt < 3; attempt++) {
         recs_reset(cap);
         ensure_out(out_need);
         arm();
@@ -3320,6 +3328,13 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         if (h_cnt[0] <= cap) break;
         cap = h_cnt[0] + h_cnt[0] / 8 + 1024;
         out_need = std::max(out_need, h_cnt[3]);
+        // a short join (no sampled pass) that turns out candidate-heavy: the
+        // re-screen runs on the finer copies (their records are fewer; a
+        // third pass, with the exact count, covers the rare exception)
+        if (small && !switched && h_cnt[3] >= 4ull * static_cast<unsigned long long>(nR)) {
+            switched = true;
+            if (const unsigned* f = on_heavy()) p.f16xmax = f;
+        }
     }
     if (h_cnt[2] > static_cast<unsigned long long>(out->capacity)) {
         ensure_out(h_cnt[2]);

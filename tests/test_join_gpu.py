@@ -255,21 +255,40 @@ def test_record_overflow_rescreen(monkeypatch):
     l_, r_, d_ = (t.cpu().numpy() for t in r.to_torch(xt.device))
     assert np.array_equal(l_, ol) and np.array_equal(r_, orr)
     assert np.array_equal(d_, od.astype(np.float32))
-    big = workloads.config5(262_144)
+    big = workloads.config5(1 << 20)
     bt = torch.from_numpy(big).cuda()
     monkeypatch.delenv("PDB_TEST_REC_CAP")
     ref = patchdb.sim_join_device(bt, None, 0.01, self_join=True, sort=True)
     want = [t.cpu().numpy() for t in ref.to_torch(bt.device)]
     assert ref.stats.screen_passes == 1
+    ref.free()
     monkeypatch.setenv("PDB_TEST_REC_CAP", "4096")
     got = patchdb.sim_join_device(bt, None, 0.01, self_join=True, sort=True)
     assert got.stats.screen_passes == 2
     for a, b in zip(want, (t.cpu().numpy() for t in got.to_torch(bt.device))):
         assert np.array_equal(a, b)
-    rows = np.arange(0, big.shape[0], 4096)
+    rows = np.arange(0, big.shape[0], 16_411)
     ol, orr, od = oracle.sim_join_rows(big, None, 0.01, rows, self_join=True)
     m = np.isin(want[0], rows)
     assert np.array_equal(want[0][m], ol) and np.array_equal(want[1][m], orr)
+
+
+def test_short_heavy_join_rescreens_on_fp16_copies():
+    """A band-plan join too short for the sampled sizing pass whose first
+    screen overflows the default record buffer with a candidate-heavy output
+    (config 5's distribution at 262k rows) re-screens on fp16 copies: two
+    passes, far fewer candidates than the bf16 copies give, exact pairs."""
+    big = workloads.config5(262_144)
+    bt = torch.from_numpy(big).cuda()
+    r = patchdb.sim_join_device(bt, None, 0.01, self_join=True, sort=True)
+    assert r.stats.screen_passes == 2
+    assert r.stats.candidates < 0.7 * 10_900_000  # bf16 copies: ~10.9 M
+    got = [t.cpu().numpy() for t in r.to_torch(bt.device)]
+    rows = np.arange(0, big.shape[0], 2049)
+    ol, orr, od = oracle.sim_join_rows(big, None, 0.01, rows, self_join=True)
+    m = np.isin(got[0], rows)
+    assert np.array_equal(got[0][m], ol) and np.array_equal(got[1][m], orr)
+    assert np.array_equal(got[2][m], od.astype(np.float32))
 
 
 def test_pair_overflow_rerun(monkeypatch):

@@ -5,3 +5,4 @@ line default
 PDB_JOIN_BAND=1 line band
 PDB_JOIN_BAND=1 PDB_K3_GROUPED=2 line band_grouped
 PDB_K3_GROUPED=2 line dense_grouped
+PDB_JOIN_BAND=1 PDB_K3_GROUPED=2 PDB_K3_FILTER=0 line band_grouped_nofilter
