@@ -1671,10 +1671,23 @@ k_pca_eig(const double* __restrict__ sum, int d, const float* __restrict__ mu,
         v[1][c] = c < d ? ((c & 1) ? 1.0f : -1.0f) * (1.0f + 0.002f * c) : 0.0f;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int e = t; e < d * d; e += blockDim.x) {
-        const int a = e / d, b = e - a * d;
-        Cs[e] = static_cast<float>(m > 0 ? sum[d + e] * im - mean[a] * mean[b] : (a == b ? 1.0 : 0.0));
+    // all of a thread's loads of the sums in flight before their use (the
+    // dependent load-per-element loop was two thirds of this kernel's time)
+    for (int e0 = 0; e0 < d * d; e0 += 16 * static_cast<int>(blockDim.x)) {
+        double sv[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int e = e0 + t + i * static_cast<int>(blockDim.x);
+            sv[i] = e < d * d ? sum[d + e] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int e = e0 + t + i * static_cast<int>(blockDim.x);
+            if (e < d * d) {
+                const int a = e / d, b = e - a * d;
+                Cs[e] = static_cast<float>(m > 0 ? sv[i] * im - mean[a] * mean[b] : (a == b ? 1.0 : 0.0));
+            }
+        }
     }
     __syncthreads();
     const int np = min(8, max(1, static_cast<int>(blockDim.x) / d));  // column groups
@@ -2322,6 +2335,15 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     const int lane = threadIdx.x & 31;
     if (k >= q.n_slots) return;
     const int rb = slot_rb(q, k);
+    // the slot's row norms, loaded during the walk (the row thresholds below)
+    const int64_t i_end = min(nL, static_cast<int64_t>(rb + 1) * BM);
+    float hnv[BM / 32], snv[BM / 32];
+#pragma unroll
+    for (int q = 0; q < BM / 32; q++) {
+        const int64_t i = static_cast<int64_t>(rb) * BM + lane + 32 * q;
+        hnv[q] = i < i_end ? hnL[i] : 0.0f;
+        snv[q] = i < i_end ? snL[i] : 0.0f;
+    }
     const double thr2 = band_thr2(q);
     const double4 a = q.boxL[rb];
     int64_t w = list_off[k];
@@ -2346,9 +2368,11 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
     }
     // each row's screen threshold, exactly as k_screen's epilogue would
     // compute it from the slot maxima (one load per unit there instead)
-    for (int64_t i = static_cast<int64_t>(rb) * BM + lane; i < min(nL, static_cast<int64_t>(rb + 1) * BM);
-         i += 32) {
-        const float hn = hnL[i], sn = snL[i];
+#pragma unroll
+    for (int q = 0; q < BM / 32; q++) {
+        const int64_t i = static_cast<int64_t>(rb) * BM + lane + 32 * q;
+        if (i >= i_end) break;
+        const float hn = hnv[q], sn = snv[q];
         float h;
         if (sn == kFlagNonFinite) {
             h = __int_as_float(0x7f800000);
