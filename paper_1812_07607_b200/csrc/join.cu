@@ -1635,14 +1635,13 @@ k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum,
         if (bins1) bins1[b] = 0;
     }
     if (e >= E) return;
+    // every partial's load in flight at once, then the fixed-order sum
+    float v[kPcaBlocks];
+#pragma unroll
+    for (int b = 0; b < kPcaBlocks; b++) v[b] = part[static_cast<size_t>(b) * E + e];
     double acc = 0.0;
-    for (int b = 0; b < kPcaBlocks; b += 8) {
-        float v[8];
 #pragma unroll
-        for (int q = 0; q < 8; q++) v[q] = part[static_cast<size_t>(b + q) * E + e];
-#pragma unroll
-        for (int q = 0; q < 8; q++) acc += static_cast<double>(v[q]);
-    }
+    for (int b = 0; b < kPcaBlocks; b++) acc += static_cast<double>(v[b]);
     sum[e] = acc;
 }
 
@@ -1942,6 +1941,14 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
     // offsets need no kernel of their own
     constexpr int per = kBins / 1024;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    // this block's keys load while the counts are scanned
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * RPT;
+    uint32_t k[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; i++) {
+        const int64_t r = r0 + i * blockDim.x + threadIdx.x;
+        k[i] = r < n ? __ldg(key + r) : 0xffffffffu;
+    }
     int32_t v[per], lsum = 0;
 #pragma unroll
     for (int i = 0; i < per; i++) {
@@ -1974,13 +1981,10 @@ k_bin_scatter(const uint32_t* __restrict__ key, int64_t n, const int32_t* __rest
         run += v[i];
     }
     __syncthreads();
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * RPT;
-    uint32_t k[RPT];
     int32_t local[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; i++) {
         const int64_t r = r0 + i * blockDim.x + threadIdx.x;
-        k[i] = r < n ? __ldg(key + r) : 0xffffffffu;
         local[i] = r < n ? atomicAdd(&cnt[k[i]], 1) : 0;
     }
     __syncthreads();
