@@ -1115,9 +1115,21 @@ constexpr int kMeanRows = 256;
 // y, y+32, ... of column 32*blockIdx.x + x; the 32 partial sums are then
 // added in a fixed order, so mu is deterministic.
 __global__ void __launch_bounds__(1024)
-k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restrict__ mu) {
+k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restrict__ mu,
+           float* __restrict__ tmaxS, float* __restrict__ tmaxN, int nt, float* __restrict__ g,
+           int64_t nR) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    if (tmaxS) {  // k_prep max-reduces the R tiles' statistics into these
+        const int tid = (blockIdx.x * blockDim.y + threadIdx.y) * blockDim.x + threadIdx.x;
+        const int nth = gridDim.x * blockDim.x * blockDim.y;
+        for (int j = tid; j < nt; j += nth) {
+            tmaxS[j] = 0.0f;
+            tmaxN[j] = 0.0f;
+        }
+        for (int64_t j = nR + tid; j < static_cast<int64_t>(nt) * BN; j += nth)
+            g[j] = __int_as_float(0x7f800000);  // padding columns never match
+    }
     __shared__ double part[32][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
     double s = 0.0;
@@ -1199,7 +1211,8 @@ __global__ void __launch_bounds__(256, 4)  // 4 resident blocks: the row loads n
 k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __restrict__ mu,
        void* __restrict__ Xp_, float* __restrict__ hn, float* __restrict__ sn,
        uint16_t* __restrict__ gx, const int32_t* __restrict__ perm,
-       const unsigned* __restrict__ f16xmax, double f16tau) {
+       const unsigned* __restrict__ f16xmax, double f16tau, float* __restrict__ g,
+       float* __restrict__ tmaxS, float* __restrict__ tmaxN) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     // fp16 copies of the scaled centred rows, or bf16 / tf32 (fp16_scale)
@@ -1305,9 +1318,29 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
     const double acc = sum8_transpose(part, lane);
     const double eacc = sum8_transpose(epart, lane);
     const int r = (lane >> 2) & 7;
-    if ((lane & 3) != 0 || r0 + r >= n) return;
-    const int64_t row = r0 + r;
+    const bool mine = (lane & 3) == 0 && r0 + r < n;
     const bool finite = (fin_mask >> r) & 1, big = (big_mask >> r) & 1;
+    const bool normal = mine && finite && !big;
+    const float hv = normal ? static_cast<float>(acc) : 0.0f;
+    const float sv = normal ? err_norm(acc, eacc, d) : 0.0f;
+    if (tmaxS) {
+        // the R tile's statistics (was k_tile_stats): the warp's eight rows
+        // lie in one 256-row tile; maxima of non-negative floats order as
+        // their bit patterns (zeroed by k_col_mean)
+        float ms = sv, mn = hv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+            mn = fmaxf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (lane == 0) {
+            atomicMax(reinterpret_cast<int*>(tmaxS + (r0 / BN)), __float_as_int(ms));
+            atomicMax(reinterpret_cast<int*>(tmaxN + (r0 / BN)), __float_as_int(mn));
+        }
+    }
+    if (!mine) return;
+    const int64_t row = r0 + r;
+    if (g) g[row] = !finite ? __int_as_float(0x7f800000) : big ? -__int_as_float(0x7f800000) : hv * 0.5f;
     if (!finite) {
         hn[row] = 0.0f;
         sn[row] = kFlagNonFinite;
@@ -1315,8 +1348,8 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
         hn[row] = 0.0f;
         sn[row] = kFlagBig;
     } else {
-        hn[row] = static_cast<float>(acc);
-        sn[row] = err_norm(acc, eacc, d);
+        hn[row] = hv;
+        sn[row] = sv;
     }
     if (gx) {
         // folded-g block of this row: -||x~||^2/2 as the sum of three bf16
@@ -2266,22 +2299,33 @@ k_band_scan(const int32_t* __restrict__ cnt, int n_slots, int units_target, int6
             unsigned long long* __restrict__ counters, unsigned long long* host_units) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    __shared__ int64_t part[1024];
+    __shared__ int64_t part[32];
     __shared__ int ch_s;
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     if (t < 5) counters[t] = 0;
     const int per = (n_slots + 1023) / 1024;
     const int k0 = min(t * per, n_slots), k1 = min((t + 1) * per, n_slots);
     auto scan = [&](int64_t local) -> int64_t {  // exclusive prefix of this thread's range
-        part[t] = local;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const int64_t v = t >= o ? part[t - o] : 0;
-            __syncthreads();
-            part[t] += v;
-            __syncthreads();
+        int64_t incl = local;  // warp shuffles, then one warp over the 32 warp totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
-        const int64_t r = part[t] - local;
+        if (lane == 31) part[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int64_t x = part[lane];
+            int64_t xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t v = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += v;
+            }
+            part[lane] = xi - x;
+        }
+        __syncthreads();
+        const int64_t r = part[wid] + incl - local;
         __syncthreads();
         return r;
     };
@@ -3078,7 +3122,7 @@ PinSlot pinned_slot() {
 // count reaches the host while the main stream still writes the tile lists.
 struct PlanAux {
     cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, scan = nullptr;
 };
 PlanAux* plan_aux() {
     thread_local PlanAux cache[64];
@@ -3089,7 +3133,8 @@ PlanAux* plan_aux() {
     if (!made[dev & 63]) {
         if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.scan, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;
         }
@@ -3523,27 +3568,38 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                s);
     float* mu = ar.take<float>(DP);
     uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * kGCols) : nullptr;
+    // R tile statistics: written by k_prep (DP <= 128, zeroed by k_col_mean)
+    // or k_tile_stats (wider rows)
+    const int nt_tiles = static_cast<int>(nt_);
+    float* gR = ar.take<float>(static_cast<size_t>(nt_) * BN);
+    float* tmaxS = ar.take<float>(nt_);
+    float* tmaxN = ar.take<float>(nt_);
+    const bool fused_stats = DP <= 128;
 
     // ---- preparation ----------------------------------------------------
     launch_pdl(k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
-               nL, d, DP, mu);
+               nL, d, DP, mu, fused_stats ? tmaxS : nullptr, fused_stats ? tmaxN : nullptr, nt_tiles,
+               gR, nR);
     PDB_CUDA(cudaGetLastError());
     launches++;
     auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out,
-                    const int32_t* perm, const unsigned* f16x) {
+                    const int32_t* perm, const unsigned* f16x, bool r_side, cudaStream_t sp = nullptr,
+                    bool pdl = true) {
+        if (!sp) sp = s;
         if (DP <= 128) {  // g_out (the folded block) only exists for DP <= 128
             const unsigned g = static_cast<unsigned>(ceil_div(ceil_div(n, kRowsPerWarp) * 32, 256));
             auto pick = [&](auto k32, auto k64, auto k96, auto k128) {
                 const int nv = DP / 32;
                 auto k = nv == 1 ? k32 : nv == 2 ? k64 : nv == 3 ? k96 : k128;
-                launch_pdl(k, dim3(g), dim3(256), 0, s, X, n, d, DP, static_cast<const float*>(mu),
-                           static_cast<void*>(Xp), hn, sn, g_out, perm, f16x, tau);
+                launch_pdl_if(pdl, k, dim3(g), dim3(256), 0, sp, X, n, d, DP, static_cast<const float*>(mu),
+                           static_cast<void*>(Xp), hn, sn, g_out, perm, f16x, tau,
+                           r_side ? gR : nullptr, r_side ? tmaxS : nullptr, r_side ? tmaxN : nullptr);
             };
             if (tf32) pick(k_prep<false, 1>, k_prep<false, 2>, k_prep<false, 3>, k_prep<false, 4>);
             else pick(k_prep<true, 1>, k_prep<true, 2>, k_prep<true, 3>, k_prep<true, 4>);
         } else {
             const unsigned g = static_cast<unsigned>(ceil_div(n * 32, 256));
-            launch_pdl(tf32 ? k_prep_wide<false> : k_prep_wide<true>, dim3(g), dim3(256), 0, s, X,
+            launch_pdl_if(pdl, tf32 ? k_prep_wide<false> : k_prep_wide<true>, dim3(g), dim3(256), 0, sp, X,
                        n, d, DP, static_cast<const float*>(mu), static_cast<void*>(Xp), hn, sn);
         }
         PDB_CUDA(cudaGetLastError());
@@ -3651,6 +3707,35 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         return !(e && e[0] == '0');
     }();
     PlanAux* aux = band && use_aux ? plan_aux() : nullptr;
+    // The screen copies go to the aux stream (band plans): the tile walk
+    // below (boxes, groups, counts, scan) is the longer chain and stays on
+    // the PDL-chained main stream, so the cross-stream start-up gap (~6 us)
+    // lands off the critical path (config-2 join: see DESIGN.md).
+    cudaStream_t sp = s;
+    if (aux) {
+        PDB_CUDA(cudaEventRecord(aux->fork, s));
+        PDB_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+        sp = aux->s;
+    }
+    uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
+    float* hnL = ar.take<float>(nL);
+    float* snL = ar.take<float>(nL);
+    // (the first kernel after a cross-stream wait launches without PDL)
+    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x, self, sp, !aux);
+    const uint8_t* XpR = XpL;
+    const float *hnR = hnL, *snR = snL;
+    if (!self) {
+        uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
+        float* hr = ar.take<float>(nR);
+        float* sr = ar.take<float>(nR);
+        prep(d_R, nR, xr, hr, sr, gx, permR, f16x, true, sp, true);
+        XpR = xr;
+        hnR = hr;
+        snR = sr;
+    }
+    if (aux && !fused_stats)
+        launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, sp, hnR, snR, nR, gR, tmaxS, tmaxN);
+    if (aux) PDB_CUDA(cudaEventRecord(aux->join, sp));
     if (band) {
         double4* boxL = ar.take<double4>(nbl);
         double4* boxR = ar.take<double4>(nt);
@@ -3668,13 +3753,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         cudaStream_t sa = s;
         const PinSlot pin = pinned_slot();
         if (pin.h) *reinterpret_cast<volatile unsigned long long*>(pin.h + 4) = kUnitsUnset;
-        if (aux) {
-            PDB_CUDA(cudaEventRecord(aux->fork, s));
-            PDB_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
-            sa = aux->s;
-        }
-        // (the first kernel after a cross-stream wait launches without PDL)
-        launch_pdl_if(!aux, k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))),
+        launch_pdl(k_band_boxes, dim3(static_cast<unsigned>(ceil_div(nbl * 32, 256))),
                       dim3(256), 0, sa, static_cast<const float2*>(projL),
                       static_cast<const int32_t*>(permL), nL, BM, nbl, boxL);
         if (!self)
@@ -3691,33 +3770,17 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                    units_target, list_off, unit_off, dev_n_units, dev_ch, counters,
                    pin.d ? pin.d + 4 : nullptr);
         launches += 4 + (self ? 0 : 1);
-        if (aux) PDB_CUDA(cudaEventRecord(aux->join, sa));
-        if (pin.h) ready = UnitsReady{aux ? aux->join : nullptr, pin.h + 4};
+        if (aux) PDB_CUDA(cudaEventRecord(aux->scan, sa));
+        if (pin.h) ready = UnitsReady{aux ? aux->scan : nullptr, pin.h + 4};
     }
 
-    uint8_t* XpL = ar.take<uint8_t>(static_cast<size_t>(nL) * DP * es);
-    float* hnL = ar.take<float>(nL);
-    float* snL = ar.take<float>(nL);
-    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x);
-    const uint8_t* XpR = XpL;
-    const float *hnR = hnL, *snR = snL;
-    if (!self) {
-        uint8_t* xr = ar.take<uint8_t>(static_cast<size_t>(nR) * DP * es);
-        float* hr = ar.take<float>(nR);
-        float* sr = ar.take<float>(nR);
-        prep(d_R, nR, xr, hr, sr, gx, permR, f16x);
-        XpR = xr;
-        hnR = hr;
-        snR = sr;
-    }
-    float* gR = ar.take<float>(static_cast<size_t>(nt) * BN);
-    float* tmaxS = ar.take<float>(nt);
-    float* tmaxN = ar.take<float>(nt);
-    // tile statistics and (band plan) each slot's tiles, maxima and row
-    // thresholds; re-run when the copies are re-made in fp16
+    // tile statistics (wide rows; k_prep wrote them otherwise) and (band
+    // plan) each slot's tiles, maxima and row thresholds; re-run when the
+    // copies are re-made in fp16
     auto tile_write = [&](bool first) {
-        launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
-        if (band && first && aux) PDB_CUDA(cudaStreamWaitEvent(s, aux->join, 0));
+        if (!fused_stats && !(first && aux))
+            launch_pdl(k_tile_stats, dim3(nt), dim3(BN), 0, s, hnR, snR, nR, gR, tmaxS, tmaxN);
+        if (first && aux) PDB_CUDA(cudaStreamWaitEvent(s, aux->join, 0));
         if (band && n_slots > 0)
             launch_pdl_if(!(first && aux), k_band_write, dim3(static_cast<unsigned>(ceil_div(int64_t{n_slots} * 32, 256))),
                           dim3(256), 0, s, bp,
@@ -3728,8 +3791,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                           tau * (1.0 + 1e-9), 1.0,
                           (DP + (fold ? 64 : 0)) * std::ldexp(1.0, -23) + std::ldexp(1.0, -19), hrow,
                           f16x);
-        launches += band ? 2 : 1;
+        launches += (fused_stats ? 0 : 1) + (band && n_slots > 0 ? 1 : 0);
     };
+    // (the copies on the aux stream are joined above; a dense plan has no aux)
     tile_write(true);
     if (!band) {
         cmaxS = ar.take<float>(nt + 1);
@@ -3840,8 +3904,12 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                            // (the sampled pass screened bf16 copies)
                            if (!f16_avail || f16x) return nullptr;
                            f16x = f16_avail;
-                           prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x);
-                           if (!self) prep(d_R, nR, XpR_w, hnR_w, snR_w, gx, permR, f16x);
+                           if (fused_stats) {  // re-zeroed: k_prep max-reduces into them
+                               PDB_CUDA(cudaMemsetAsync(tmaxS, 0, nt_ * sizeof(float), s));
+                               PDB_CUDA(cudaMemsetAsync(tmaxN, 0, nt_ * sizeof(float), s));
+                           }
+                           prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x, self);
+                           if (!self) prep(d_R, nR, XpR_w, hnR_w, snR_w, gx, permR, f16x, true);
                            tile_write(false);
                            return f16x;
                        });

@@ -45,7 +45,10 @@ for _ in range(2):
 torch.cuda.synchronize()
 if plain:
     sys.exit(0)
+head = "--headstart" in sys.argv  # a ~0.5 ms spin first, so the host enqueues ahead of the device
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    if head:
+        torch.cuda._sleep(1_000_000)
     call()
     torch.cuda.synchronize()
 evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
