@@ -248,6 +248,18 @@ __device__ __forceinline__ Unit decode_unit(const ScreenParams& p, int64_t u) {
 // Shared-memory plan of k_screen, shared by the kernel and its launcher.
 // Resident A is double-buffered when it fits, so the next work unit's rows
 // load while the current unit's tiles are still multiplying.
+// Epilogue warps of the 1-SM screen: 16 for DP <= 64 (a tile's epilogue is
+// as long as its MMAs there; config 1 screen 0.100 -> 0.088 ms, config 2
+// 0.090 -> 0.088, config 5 167 -> 164 ms), 8 above (config 3: 16 was 6 %
+// slower).
+template <int DP>
+struct Epi {
+    static constexpr int W = DP <= 64 ? 16 : 8;
+    static constexpr int kColsPerWarp = BN / (W / 4);
+    static constexpr int kChunks = kColsPerWarp / 32;
+    static constexpr int kThreads = 64 + 32 * W;
+};
+
 template <int DP, bool A_RES, int STAGES, int MODE>
 struct ScreenSmem {
     static constexpr bool AUG = MODE == kModeL2Bf16Aug;
@@ -258,7 +270,7 @@ struct ScreenSmem {
     static constexpr int kStage = (A_RES ? kBBytes : (kABytes + kBBytes)) + (AUG ? kGBytes : 0);
     // one A slot: NKB 128B-swizzled K-blocks (+ the 32B-swizzled folded-g block)
     static constexpr int kASlot = A_RES ? (NKB * kABytes + (AUG ? BM * kGCols * 2 : 0) + 1023) / 1024 * 1024 : 0;
-    static constexpr int kTail = 256 + kEpiWarps * kColsPerWarp * 4 + kEpiWarps * 32 * 16 + 128;
+    static constexpr int kTail = 256 + Epi<DP>::W * Epi<DP>::kColsPerWarp * 4 + Epi<DP>::W * 32 * 16 + 128;
     static constexpr size_t bytes(int slots) {
         return 1024 + static_cast<size_t>(slots) * kASlot + static_cast<size_t>(STAGES) * kStage + kTail;
     }
@@ -267,7 +279,7 @@ struct ScreenSmem {
 };
 
 template <int DP, bool A_RES, int STAGES, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Epi<DP>::kThreads, 1)
 k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const __grid_constant__ CUtensorMap tmG, const ScreenParams p) {
     constexpr bool COS = MODE == kModeCosBf16;
@@ -277,6 +289,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     constexpr int KE = BF16 ? 64 : 32;  // elements per 128-byte K-block
     constexpr int NKB = DP / KE;
     using SM = ScreenSmem<DP, A_RES, STAGES, MODE>;
+    constexpr int kEpiWarpsL = Epi<DP>::W;
+    constexpr int kColsPerWarpL = Epi<DP>::kColsPerWarp;
+    constexpr int kChunksL = Epi<DP>::kChunks;
+    // (the same slots per CTA: a warp's unused reserved tail is zeroed and skipped by K3)
+    constexpr unsigned kResChunkL = kResChunk * 8 / kEpiWarpsL;
     constexpr int kStageBytes = SM::kStage;
     constexpr int kASlot = SM::kASlot;
     constexpr int kASlots = SM::kASlots;
@@ -295,11 +312,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
     uint64_t* t_full = a_full + 4;          // [2]
     uint64_t* t_empty = a_full + 6;         // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 8);
-    float* g_smem = reinterpret_cast<float*>(a_full + 10);  // [epilogue warps][kColsPerWarp]
-    int4* r_smem = reinterpret_cast<int4*>(g_smem + kEpiWarps * kColsPerWarp);  // [warps][32] records
+    float* g_smem = reinterpret_cast<float*>(a_full + 10);  // [epilogue warps][kColsPerWarpL]
+    int4* r_smem = reinterpret_cast<int4*>(g_smem + kEpiWarpsL * kColsPerWarpL);  // [warps][32] records
     // dynamic scheduler: the producer claims work units with one global
     // atomic and hands them to the MMA and epilogue warps through a 4-slot ring
-    uint64_t* u_full = reinterpret_cast<uint64_t*>(r_smem + kEpiWarps * 32);
+    uint64_t* u_full = reinterpret_cast<uint64_t*>(r_smem + kEpiWarpsL * 32);
     uint64_t* u_empty = u_full + 4;
     // the producer publishes decoded units {rb, first tile, end, chunk}; rb < 0 ends
     volatile int4* u_dec = reinterpret_cast<volatile int4*>(u_full + 8);
@@ -317,11 +334,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         }
         for (int a = 0; a < 2; a++) {
             ptx::mbar_init(&t_full[a], 1);
-            ptx::mbar_init(&t_empty[a], kEpiWarps);
+            ptx::mbar_init(&t_empty[a], kEpiWarpsL);
         }
         for (int k = 0; k < 4; k++) {
             ptx::mbar_init(&u_full[k], 1);
-            ptx::mbar_init(&u_empty[k], 1 + kEpiWarps);
+            ptx::mbar_init(&u_empty[k], 1 + kEpiWarpsL);
         }
         ptx::fence_mbar_init();
     }
@@ -512,10 +529,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         // so the next tcgen05.ld overlaps the current chunk's arithmetic.
         const int ew = warp - 2;
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int half = ew >> 2;  // which kColsPerWarp-wide column slice
+        const int half = ew >> 2;  // which kColsPerWarpL-wide column slice
         const int row = q * 32 + lane;
         const uint32_t t_lane = static_cast<uint32_t>(q * 32) << 16;
-        float* gs = g_smem + ew * kColsPerWarp;
+        float* gs = g_smem + ew * kColsPerWarpL;
         int4* rbuf = r_smem + ew * 32;
         uint32_t nbuf = 0;                 // staged records (warp-uniform)
         unsigned long long ncand = 0;      // this lane's candidate pairs
@@ -535,10 +552,10 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             res_pos += first;
             if (first < nb) {
                 unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunk));
+                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunkL));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 res_pos = base;
-                res_end = base + kResChunk;
+                res_end = base + kResChunkL;
                 if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
                     res_pos + (lane - first) < p.cap)
                     p.rec[res_pos + (lane - first)] = rbuf[lane];
@@ -560,11 +577,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             const bool row_ok = i < p.nL;
             const float hn = (row_ok && !p.hrow) ? __ldg(p.hnL + i) : 0.0f;
             const float sn = (row_ok && !p.hrow) ? __ldg(p.snL + i) : kFlagNonFinite;
-            using GV = typename std::conditional<kColsPerWarp == 128, float4, float2>::type;
+            using GV = typename std::conditional<kColsPerWarpL == 128, float4, float2>::type;
             GV gnext{};
             if (!AUG)
                 gnext = __ldg(reinterpret_cast<const GV*>(
-                    p.gR + static_cast<int64_t>(tile_at(p, w.j0)) * BN + half * kColsPerWarp) + lane);
+                    p.gR + static_cast<int64_t>(tile_at(p, w.j0)) * BN + half * kColsPerWarpL) + lane);
             // Threshold h_i for the whole unit, from the largest R norms over
             // its tiles (conservative; fp64 once per unit, not per tile).
             float h;
@@ -593,13 +610,13 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 // force a wait at the register move (none needed when g is folded)
                 if (!AUG)
                 gnext = __ldg(reinterpret_cast<const GV*>(
-                    p.gR + static_cast<int64_t>(tile_at(p, min(o + 1, w.j1 - 1))) * BN + half * kColsPerWarp) + lane);
+                    p.gR + static_cast<int64_t>(tile_at(p, min(o + 1, w.j1 - 1))) * BN + half * kColsPerWarpL) + lane);
                 __syncwarp();
                 ptx::mbar_wait(&t_full[acc], acc_phase);
                 ptx::tc_fence_after();
-                const int64_t colw = static_cast<int64_t>(J) * BN + half * kColsPerWarp;
+                const int64_t colw = static_cast<int64_t>(J) * BN + half * kColsPerWarpL;
                 const uint32_t t_acc =
-                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * kColsPerWarp);
+                    tmem_base + t_lane + static_cast<uint32_t>(acc * BN + half * kColsPerWarpL);
 
                 auto process = [&](const uint32_t(&v)[32], int c) {
                     // e_k = dot_k - g_k (L2) or dot_k * g_k (cosine), two
@@ -665,8 +682,8 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 ptx::tmem_ld_wait();
                 ptx::reg_fence(vbuf[0]);
 #pragma unroll
-                for (int c = 0; c < kChunks; c++) {
-                    if (c + 1 < kChunks) {
+                for (int c = 0; c < kChunksL; c++) {
+                    if (c + 1 < kChunksL) {
                         ptx::tmem_ld32(t_acc + (c + 1) * 32, vbuf[(c + 1) & 1]);
                     } else {
                         ptx::tc_fence_before();
@@ -674,7 +691,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                         if (lane == 0) ptx::mbar_arrive(&t_empty[acc]);  // TMEM reads done
                     }
                     process(vbuf[c & 1], c);
-                    if (c + 1 < kChunks) {
+                    if (c + 1 < kChunksL) {
                         ptx::tmem_ld_wait();
                         ptx::reg_fence(vbuf[(c + 1) & 1]);
                     }
@@ -2419,7 +2436,7 @@ k_band_write(const BandPlan q, const int64_t* __restrict__ list_off, int32_t* __
 #pragma unroll
     for (int q = 0; q < BM / 32; q++) {
         const int64_t i = static_cast<int64_t>(rb) * BM + lane + 32 * q;
-        if (i >= i_end) break;
+        if (i >= i_end) continue;  // (not break: the arrays stay in registers)
         const float hn = hnv[q], sn = snv[q];
         float h;
         if (sn == kFlagNonFinite) {
@@ -2938,7 +2955,7 @@ void launch_screen(const DeviceCtx& ctx, const CUtensorMap& tA, const CUtensorMa
     auto k = k_screen<DP, A_RES, STAGES, MODE>;
     set_max_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
     const int64_t grid = std::min<int64_t>(ctx.sm_count, std::max<int64_t>(p.n_units, 1));
-    launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kThreads), smem, s, tA, tB, tG, p);
+    launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(Epi<DP>::kThreads), smem, s, tA, tB, tG, p);
     PDB_CUDA(cudaGetLastError());
 }
 
