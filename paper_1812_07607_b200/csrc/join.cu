@@ -542,6 +542,9 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
         // reserved slots are zeroed at the end -- the re-check skips a zero
         // mask).
         unsigned long long res_pos = 0, res_end = 0;
+        // reservations grow 32, 64, ... up to the full chunk: a sparse
+        // output leaves short zeroed tails for the re-check to skip
+        unsigned res_chunk = 32;
         auto flush = [&]() {
             __syncwarp();
             const unsigned nb = nbuf;
@@ -552,10 +555,11 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             res_pos += first;
             if (first < nb) {
                 unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunkL));
+                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(res_chunk));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 res_pos = base;
-                res_end = base + kResChunkL;
+                res_end = base + res_chunk;
+                res_chunk = min(2 * res_chunk, kResChunkL);
                 if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
                     res_pos + (lane - first) < p.cap)
                     p.rec[res_pos + (lane - first)] = rbuf[lane];
@@ -991,6 +995,9 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // reserved slots are zeroed at the end -- the re-check skips a zero
         // mask).
         unsigned long long res_pos = 0, res_end = 0;
+        // reservations grow 32, 64, ... up to the full chunk: a sparse
+        // output leaves short zeroed tails for the re-check to skip
+        unsigned res_chunk = 32;
         auto flush = [&]() {
             __syncwarp();
             const unsigned nb = nbuf;
@@ -1001,10 +1008,11 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             res_pos += first;
             if (first < nb) {
                 unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(kResChunk));
+                if (lane == 0) base = atomicAdd(p.counter, static_cast<unsigned long long>(res_chunk));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 res_pos = base;
-                res_end = base + kResChunk;
+                res_end = base + res_chunk;
+                res_chunk = min(2 * res_chunk, kResChunk);
                 if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
                     res_pos + (lane - first) < p.cap)
                     p.rec[res_pos + (lane - first)] = rbuf[lane];
