@@ -467,7 +467,8 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
             "metric": metric, "value": cand / (ms * 1e-3) / 1e9, "unit": "Gpairs/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16 screen / f64 exact" if not cos else "bf16 screen / f64 exact (cosine)",
+            "dtype": ("fp16 screen / f64 exact" if int(pairs.stats.screen_format) == 2 else
+                      "bf16 screen / f64 exact") if not cos else "bf16 screen / f64 exact (cosine)",
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "nL": nL_all, "nL_per_rank": nL, "nR": nR, "d": d,
                        "threshold": cfg["tau"], "candidate_pairs": cand,
@@ -479,7 +480,9 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
             "pairs": n_pairs, "candidates": n_cand,
             "phase_ms": {"prep": ms_prep, "screen": ms_screen, "recheck": ms_recheck},
             "setup_ms": {"broadcast": setup_ms},
-            "roofline": {"kernel": "k_screen (K2, tcgen05 kind::f16 on bf16 screen copies)",
+            "roofline": {"kernel": "k_screen (K2, tcgen05 kind::f16 on %s screen copies)"
+                                   % {0: "tf32", 1: "bf16", 2: "fp16", 3: "bf16 (cosine)"}.get(
+                                       int(pairs.stats.screen_format), "bf16"),
                          "bound": "tensor", "achieved": screen_tf, "peak": bpeak,
                          "unit": "TFLOP/s", "frac": screen_tf / bpeak,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",

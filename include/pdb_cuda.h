@@ -186,6 +186,10 @@ typedef struct pdb_join_stats {
     float screen_ms;         /* K2, the tcgen05 screen */
     float recheck_ms;        /* K3, exact re-check + compaction */
     float sort_ms;           /* optional canonical ordering */
+    int32_t screen_format;   /* screen copies: 0 tf32, 1 bf16, 2 fp16 (chosen for candidate-heavy
+                                band-plan joins; the device keeps bf16 when the data's range
+                                would push rows into fp16's subnormals), 3 cosine bf16 */
+    int32_t reserved1;
 } pdb_join_stats;
 
 /* Host pointers: L [nL, d] and R [nR, d] fp32 row-major. */

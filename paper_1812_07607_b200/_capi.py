@@ -79,7 +79,8 @@ class JoinStats(C.Structure):
     _fields_ = [("candidates", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64),
                 ("candidate_capacity", C.c_int64), ("launches", C.c_int32),
                 ("screen_passes", C.c_int32), ("prep_ms", C.c_float), ("screen_ms", C.c_float),
-                ("recheck_ms", C.c_float), ("sort_ms", C.c_float)]
+                ("recheck_ms", C.c_float), ("sort_ms", C.c_float),
+                ("screen_format", C.c_int32), ("reserved1", C.c_int32)]
 
 
 _lib: Optional[C.CDLL] = None

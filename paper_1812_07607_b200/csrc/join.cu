@@ -3475,6 +3475,8 @@ void screen_and_recheck(const DeviceCtx& ctx, cudaStream_t s, int DP, int mode,
         stats->recheck_ms = tm.ms(2, 3);
         if (tm.on && (o.flags & PDB_JOIN_SORTED)) PDB_CUDA(cudaEventSynchronize(tm.ev[4]));
         stats->sort_ms = (o.flags & PDB_JOIN_SORTED) ? tm.ms(3, 4) : 0.0f;
+        stats->screen_format = mode == kModeCosBf16 ? 3 : mode == kModeL2Tf32 ? 0 : (p.f16xmax ? 2 : 1);
+        stats->reserved1 = 0;
     }
 }
 
