@@ -345,7 +345,17 @@ def run_ours(args, rank, world, local_rank):
            "prep": []}
     launches = 0
 
-    def step(timed: bool, phases: bool = False):
+    # one GPU: the step is one pdb_featurize_join_dev call (the band plan's
+    # directions computed beside K1); sharded: featurize, exchange, join
+    use_fused = world == 1 and not args.no_fused
+
+    def fused():
+        rc = lib.pdb_featurize_join_dev(d_frames.data_ptr(), nf, H, W, th, tw, B, mode, tau,
+                                        C.byref(opts), feats.data_ptr(), C.byref(pairs._p),
+                                        C.byref(pairs.stats))
+        assert rc == 0, capi.last_error()
+
+    def step(timed: bool, phases: bool = False, split: bool = False):
         nonlocal launches
         if world > 1:
             dist.barrier()
@@ -355,19 +365,24 @@ def run_ours(args, rank, world, local_rank):
         # (not the host's launch latency on an idle device)
         l2_flush()
         ev[0].record(stream)
-        featurize()
-        ev[1].record(stream)
-        gather()
-        ev[2].record(stream)
-        join(phases)
+        if use_fused and not (phases or split):
+            fused()
+        else:
+            featurize()
+            ev[1].record(stream)
+            gather()
+            ev[2].record(stream)
+            join(phases)
         ev[3].record(stream)
         torch.cuda.synchronize()
-        if timed and not phases:
+        if timed and not (phases or split):
             rec["step"].append(ev[0].elapsed_time(ev[3]))
+            launches += pairs.stats.launches + (0 if use_fused else 1)
+        if timed and (split or (not phases and not use_fused)):
+            # the featurize / join split (separate calls, no join phase events)
             rec["feat"].append(ev[0].elapsed_time(ev[1]))
             rec["gather"].append(ev[1].elapsed_time(ev[2]))
             rec["join"].append(ev[2].elapsed_time(ev[3]))
-            launches += 1 + pairs.stats.launches
         if timed and phases:
             st = pairs.stats
             rec["screen"].append(st.screen_ms)
@@ -382,6 +397,9 @@ def run_ours(args, rank, world, local_rank):
     sampler.__enter__()
     for _ in range(args.steps):
         step(True)
+    if use_fused:
+        for _ in range(args.steps):
+            step(True, split=True)
     # the per-phase split (roofline of the screen kernel) comes from separate
     # steps with CUDA events between the join's phases; those events break
     # the programmatic-dependent-launch chain, so they stay out of `value`
@@ -542,7 +560,11 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"frames sharded x{world}, "
                        + ("features P2P-stored by K1 into every rank's matrix (fused all-gather)"
                           if p2p is not None else "features all-gathered")
-                       + f", join row-blocks cyclic x{world}"},
+                       + f", join row-blocks cyclic x{world}",
+                       "step_api": ("pdb_featurize_join_dev (the band plan's directions computed "
+                                    "beside K1); phase_ms from separate featurize / join calls"
+                                    if use_fused else
+                                    "pdb_featurize_tiles_dev + exchange + pdb_sim_join_dev")},
             "join_gpairs_per_s": pairs_cand / (ms_join * 1e-3) / 1e9,
             "featurize_frames_per_s": F / (ms_feat * 1e-3),
             "phase_ms": {"featurize": ms_feat, "gather": ms_gather,
@@ -578,6 +600,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="time the config-2 step as separate featurize and join calls instead of "
+                         "pdb_featurize_join_dev")
     ap.add_argument("--no-config3", action="store_true",
                     help="skip the config-3 (1M x 1M x 128) sub-record of the default line")
     ap.add_argument("--ref-threads", type=int, default=0,

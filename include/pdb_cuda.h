@@ -235,6 +235,17 @@ int pdb_featurize_join(const uint8_t* frames, int64_t n_frames, int32_t height, 
                        double tau, const pdb_join_opts* opts, float* features,
                        pdb_pairs* out);
 
+/* The same pipeline on the device: d_frames [n_frames, H, W, 3] u8 in,
+ * d_features [tiles, D] and device pairs (PDB_JOIN_SELF semantics) out, on
+ * opts->stream.  The band plan's directions are computed on the first
+ * frames' tiles while K1 featurizes the rest (the pair set is the same as
+ * pdb_featurize_tiles_dev + pdb_sim_join_dev; only the screened tiles
+ * differ).  No sharding. */
+int pdb_featurize_join_dev(const uint8_t* d_frames, int64_t n_frames, int32_t height, int32_t width,
+                           int32_t tile_h, int32_t tile_w, int32_t bins, int32_t mode, double tau,
+                           const pdb_join_opts* opts, float* d_features, pdb_dev_pairs* out,
+                           pdb_join_stats* stats);
+
 /* Near-duplicate grouping -- replaces run_dedup (src/query.cpp:535-566),
  * the grouping of PlanNode::dedup (include/patchdb/query.hpp:142) and the
  * kept set of dedup_stream (query.hpp:203-204, src/query.cpp:1063-1092).

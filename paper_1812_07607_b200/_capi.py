@@ -49,7 +49,7 @@ EXPORTS = (
     "pdb_cosine_join_bf16", "pdb_cosine_join_bf16_dev", "pdb_dedup", "pdb_dedup_dev",
     "pdb_store_open", "pdb_store_close", "pdb_store_describe", "pdb_store_read",
     "pdb_store_featurize", "pdb_rows_within", "pdb_featurize_tiles_dev_multi",
-    "pdb_release_caches", "pdb_warmup",
+    "pdb_release_caches", "pdb_warmup", "pdb_featurize_join_dev",
 )
 
 
@@ -119,6 +119,9 @@ def lib() -> C.CDLL:
         L.pdb_dev_pairs_free.restype = None
         L.pdb_featurize_join.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, f64,
                                          C.POINTER(JoinOpts), vp, C.POINTER(Pairs)]
+        L.pdb_featurize_join_dev.argtypes = [vp, i64, i32, i32, i32, i32, i32, i32, f64,
+                                             C.POINTER(JoinOpts), vp, C.POINTER(DevPairs),
+                                             C.POINTER(JoinStats)]
         L.pdb_cosine_join_bf16.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(JoinOpts),
                                            C.POINTER(Pairs)]
         L.pdb_cosine_join_bf16_dev.argtypes = [vp, i64, vp, i64, i32, f64, C.POINTER(JoinOpts),

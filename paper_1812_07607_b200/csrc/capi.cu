@@ -263,6 +263,7 @@ PDB_API int pdb_featurize_tiles_dev_multi(const uint8_t* d_frames, int64_t n, in
         check_featurize_args(d_frames, n, H, W, th, tw, bins, mode, d_outs[0]);
         device_ctx();
         FeatOuts o{};
+        o.done = nullptr;
         for (int k = 0; k < n_outs; k++) o.p[k] = d_outs[k];
         o.n = n_outs;
         launch_featurize_tiles_multi(d_frames, n, H, W, th, tw, bins, mode, o, stream_of(stream));
@@ -339,6 +340,25 @@ PDB_API int pdb_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int
         pdb_join_opts o = opts ? *opts : pdb_join_opts{};
         o.stream = stream_of(o.stream);
         run_sim_join_dev(d_L, nL, d_R, nR, d, tau, o, out, stats);
+    });
+}
+
+PDB_API int pdb_featurize_join_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W,
+                                   int32_t th, int32_t tw, int32_t bins, int32_t mode, double tau,
+                                   const pdb_join_opts* opts, float* d_features, pdb_dev_pairs* out,
+                                   pdb_join_stats* stats) {
+    return guarded([&] {
+        if (!out) fail(PDB_ERR_INVALID_ARGUMENT, "null output");
+        check_featurize_args(d_frames, n, H, W, th, tw, bins, mode, d_features);
+        if (tau < 0.0) fail(PDB_ERR_CONFIG, "similarity join needs tau >= 0");
+        if (opts && opts->shard_count > 1)
+            fail(PDB_ERR_INVALID_ARGUMENT, "pdb_featurize_join_dev does not shard");
+        const int64_t nt = n_tiles_of(n, H, W, th, tw);
+        if (nt > INT32_MAX) fail(PDB_ERR_INVALID_ARGUMENT, "too many tiles");
+        device_ctx();
+        pdb_join_opts o = opts ? *opts : pdb_join_opts{};
+        o.stream = stream_of(o.stream);
+        run_featurize_join_dev(d_frames, n, H, W, th, tw, bins, mode, d_features, tau, o, out, stats);
     });
 }
 

@@ -524,7 +524,10 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, const uint8_t* __re
         __syncwarp();
         // (measurement only: 1 skips the epilogue, 2 skips the lane reduction,
         // 3 skips the feature stores)
-        if (skip_epi == 1) continue;
+        if (skip_epi == 1) {
+            if (outs.done && tr == static_cast<int>(blockIdx.x) && lane == 0) atomicAdd(outs.done, 1u);
+            continue;
+        }
         // sum bytes 0,2 and 1,3 of every counter word over lanes in 16-bit
         // halves; lane l keeps the totals of bins l and l+32.
         // Lane 0 parks the two half-sums of word wd in the warp's park area
@@ -570,6 +573,13 @@ k_hist_joint_rows8(const __grid_constant__ CUtensorMap tmap, const uint8_t* __re
             float* o = outs.p[k] + ofs;
             if (lane < NB) __stcs(o + lane, v0);
             if (NB > 32) __stcs(o + lane + 32, v1);
+        }
+        if (outs.done && tr == static_cast<int>(blockIdx.x)) {
+            // this tile's features are stored: publish (a consumer on another
+            // stream spins on the count, then reads the first round's tiles)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(outs.done, 1u);
         }
     }
     // peer stores become visible before anything the host orders after us
@@ -723,16 +733,19 @@ int hist_dim(int32_t bins, int32_t mode) {
 
 void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H, int32_t W,
                             int32_t th, int32_t tw, int32_t bins, int32_t mode, float* d_out,
-                            cudaStream_t s) {
+                            cudaStream_t s, int sm_reserve) {
     FeatOuts one{};
     one.p[0] = d_out;
     one.n = 1;
-    launch_featurize_tiles_multi(d_frames, n_frames, H, W, th, tw, bins, mode, one, s);
+    one.done = nullptr;
+    launch_featurize_tiles_multi(d_frames, n_frames, H, W, th, tw, bins, mode, one, s, sm_reserve);
 }
 
 void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int32_t H, int32_t W,
                                   int32_t th, int32_t tw, int32_t bins, int32_t mode,
-                                  const FeatOuts& outs, cudaStream_t s) {
+                                  const FeatOuts& outs, cudaStream_t s, int sm_reserve,
+                                  int64_t* first_round) {
+    if (first_round) *first_round = -1;
     float* d_out = outs.p[0];
     const int D = hist_dim(bins, mode);
     const int ntx = W / tw, nty = H / th;
@@ -859,8 +872,11 @@ void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int
             }
         }
         if (kn.ctas > 0) per_sm = std::min(per_sm, kn.ctas);
-        const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * ctx.sm_count;
+        // (sm_reserve: SMs' worth of CTAs left free for concurrent work)
+        const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) *
+                            std::max(1, ctx.sm_count - std::max(0, sm_reserve));
         const dim3 g(static_cast<unsigned>(std::min(n_rows, cap)));
+        if (first_round) *first_round = static_cast<int64_t>(g.x) * ntx;
         kern<<<g, threads, smem, s>>>(m, d_frames, static_cast<int>(n_rows), nty, H, W * 3, th, tw,
                                       ntx, static_cast<uint32_t>(stage_b), n_stages, pf, skip_epi,
                                       npix_h, outs);

@@ -1142,7 +1142,7 @@ constexpr int kMeanRows = 256;
 __global__ void __launch_bounds__(1024)
 k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restrict__ mu,
            float* __restrict__ tmaxS, float* __restrict__ tmaxN, int nt, float* __restrict__ g,
-           int64_t nR) {
+           int64_t nR, const float* __restrict__ mu_src) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     if (tmaxS) {  // k_prep max-reduces the R tiles' statistics into these
@@ -1158,21 +1158,23 @@ k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restr
     __shared__ double part[32][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
     double s = 0.0;
-    if (col < d) {
-#pragma unroll
-        for (int k = 0; k < kMeanRows / 32; k++) {
-            const int64_t r = threadIdx.y + 32 * k;
+    if (col < d) {  // (blockDim.y 32, or 8 beside a running K1: same rows)
+        for (int r = threadIdx.y; r < kMeanRows; r += blockDim.y) {
             if (r < n) {
-                const float v = X[r * d + col];
+                const float v = X[static_cast<int64_t>(r) * d + col];
                 if (isfinite(v)) s += static_cast<double>(v);
             }
         }
     }
     part[threadIdx.y][threadIdx.x] = s;
     __syncthreads();
+    if (mu_src) {  // the centre was computed ahead (run_featurize_join_dev)
+        if (threadIdx.y == 0 && col < DP) mu[col] = mu_src[col];
+        return;
+    }
     if (threadIdx.y == 0 && col < DP) {
         double t = 0.0;
-        for (int k = 0; k < 32; k++) t += part[k][threadIdx.x];
+        for (int k = 0; k < static_cast<int>(blockDim.y); k++) t += part[k][threadIdx.x];
         const int64_t m = n < kMeanRows ? n : kMeanRows;
         const float v = (col < d && m > 0) ? static_cast<float>(t / static_cast<double>(m)) : 0.0f;
         mu[col] = isfinite(v) ? v : 0.0f;
@@ -1701,6 +1703,16 @@ k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum,
 #pragma unroll
     for (int b = 0; b < kPcaBlocks; b++) acc += static_cast<double>(v[b]);
     sum[e] = acc;
+}
+
+// The counting sorts' bin counts and fill cursors, when the directions were
+// computed ahead (k_pca_reduce zeroes them otherwise).
+__global__ void k_zero_bins(int32_t* __restrict__ bins0, int32_t* __restrict__ bins1) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < 2 * (1 << (2 * kMortonBits))) {
+        if (bins0) bins0[b] = 0;
+        if (bins1) bins1[b] = 0;
+    }
 }
 
 // One block: the covariance (fp32, symmetric, read by columns so lanes hit
@@ -3491,7 +3503,7 @@ void release_join_caches() {
 
 void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR, int32_t d,
                       double tau, const pdb_join_opts& o, pdb_dev_pairs* out,
-                      pdb_join_stats* stats) {
+                      pdb_join_stats* stats, const JoinPre* pre) {
     const DeviceCtx& ctx = device_ctx();
     cudaStream_t s = static_cast<cudaStream_t>(o.stream);
     const bool self = (o.flags & PDB_JOIN_SELF) != 0;
@@ -3604,9 +3616,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     const bool fused_stats = DP <= 128;
 
     // ---- preparation ----------------------------------------------------
-    launch_pdl(k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
+    // (after a cross-stream wait on the precomputed centre: no PDL)
+    launch_pdl_if(!pre, k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
                nL, d, DP, mu, fused_stats ? tmaxS : nullptr, fused_stats ? tmaxN : nullptr, nt_tiles,
-               gR, nR);
+               gR, nR, pre ? pre->mu : static_cast<const float*>(nullptr));
     PDB_CUDA(cudaGetLastError());
     launches++;
     auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out,
@@ -3645,24 +3658,32 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     if (band) {
         float* part = ar.take<float>(static_cast<size_t>(kPcaBlocks) * E);
         double* sum = ar.take<double>(E);
-        info = ar.take<BandInfo>(1);
+        info = pre && P == 1 ? static_cast<BandInfo*>(const_cast<void*>(pre->info)) : ar.take<BandInfo>(1);
         if (DP <= 128 && !tf32 && screen_fp16_mode() > 0) f16_avail = &info->xmax;
         if (screen_fp16_mode() == 2) f16x = f16_avail;
-        auto kp = d <= 16 ? k_pca_partial<1> : d <= 32 ? k_pca_partial<2> : d <= 64 ? k_pca_partial<4>
-                                                                                  : k_pca_partial<8>;
-        launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, s, d_L, nL, d, static_cast<const float*>(mu),
-                   part);
         uint8_t* tmpL = ar.take<uint8_t>(sort_tmp);
         uint8_t* tmpR = self ? nullptr : ar.take<uint8_t>(sort_tmp);
-        launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
-                   static_cast<const float*>(part), E, sum, reinterpret_cast<int32_t*>(tmpL),
-                   reinterpret_cast<int32_t*>(tmpR));
-        const int eig_smem = d * d * 4;
-        // (set_max_smem caches per function and device)
-        set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
-        launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
-                   static_cast<const float*>(mu), info);
-        launches += 3;
+        if (pre && P == 1) {
+            // directions computed ahead on a prefix sample (run_featurize_join_dev):
+            // only the counting sorts' bins need zeroing (k_pca_reduce's job)
+            k_zero_bins<<<2 * kBins / 256, 256, 0, s>>>(reinterpret_cast<int32_t*>(tmpL),
+                                                         reinterpret_cast<int32_t*>(tmpR));
+            launches++;
+        } else {
+            auto kp = d <= 16 ? k_pca_partial<1> : d <= 32 ? k_pca_partial<2> : d <= 64 ? k_pca_partial<4>
+                                                                                      : k_pca_partial<8>;
+            launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, s, d_L, nL, d, static_cast<const float*>(mu),
+                       part);
+            launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
+                       static_cast<const float*>(part), E, sum, reinterpret_cast<int32_t*>(tmpL),
+                       reinterpret_cast<int32_t*>(tmpR));
+            const int eig_smem = d * d * 4;
+            // (set_max_smem caches per function and device)
+            set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
+            launch_pdl(k_pca_eig, dim3(1), dim3(256), eig_smem, s, static_cast<const double*>(sum), d,
+                       static_cast<const float*>(mu), info);
+            launches += 3;
+        }
         auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm,
                                  uint8_t* tmp) {
             proj = ar.take<float2>(n);
@@ -4037,6 +4058,121 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
                            PDB_CUDA(cudaGetLastError());
                        },
                        []() -> const unsigned* { return nullptr; });
+}
+
+
+// Spins until the first K1 round has stored its tiles (FeatOuts::done).
+__global__ void k_wait_count(const unsigned* __restrict__ done, unsigned target) {
+    if (threadIdx.x == 0) {
+        unsigned v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+            if (v >= target) break;
+            __nanosleep(256);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Featurize then self-join in one call, with the band plan's centre and
+// directions computed while K1 is still running.  K1 (persistent, rows in
+// grid-stride order) leaves a few SMs' worth of CTA slots free and counts
+// the tiles of its first round as their features are stored; on a
+// high-priority stream a one-thread kernel waits for that count, then
+// k_col_mean and the PCA (partials over the first round's tiles, reduce,
+// eig) run beside the rest of K1, and the join starts from them (JoinPre).
+// Any plane prunes correctly, so the prefix sample only changes which tiles
+// are screened, never the pairs.  Falls back to featurize + join when the
+// join would not use a band plan.
+void run_featurize_join_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W, int32_t th,
+                            int32_t tw, int32_t bins, int32_t mode, float* d_feats, double tau,
+                            const pdb_join_opts& o0, pdb_dev_pairs* out, pdb_join_stats* stats) {
+    device_ctx();
+    pdb_join_opts o = o0;
+    o.flags |= PDB_JOIN_SELF;
+    cudaStream_t s = static_cast<cudaStream_t>(o.stream);
+    const int64_t tpf = static_cast<int64_t>(W / tw) * (H / th);
+    const int64_t nt = n * tpf;
+    const int D = hist_dim(bins, mode);
+    const bool tf32 = (o.flags & PDB_JOIN_TF32) != 0;
+    const int DP = tf32 ? padded_dim(D) : padded_dim_bf16(D);
+    const char* be = getenv("PDB_JOIN_BAND");
+    const int band_env = be ? atoi(be) : -1;
+    const char* pe = getenv("PDB_SCREEN_PAIR");
+    const char* fe = getenv("PDB_FUSED_PCA");  // 0: plain featurize + join (A/B)
+    const bool band = DP <= 128 && D <= kPcaMaxD && (o.flags & PDB_JOIN_DENSE) == 0 && band_env != 0 &&
+                      o.shard_count <= 1 && (band_env == 1 || nt >= kBandMinRows) &&
+                      !(pe && pe[0] == '1') && !(fe && fe[0] == '0');
+    if (!band || tau != tau || nt == 0) {
+        launch_featurize_tiles(d_frames, n, H, W, th, tw, bins, mode, d_feats, s);
+        run_sim_join_dev(d_feats, nt, d_feats, nt, D, tau, o, out, stats);
+        return;
+    }
+    struct Aux {
+        cudaStream_t s = nullptr;
+        cudaEvent_t pre = nullptr, k1 = nullptr, pca = nullptr;
+    };
+    thread_local Aux auxs[64];
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    Aux& a = auxs[dev & 63];
+    if (!a.s) {
+        int lo = 0, hi = 0;
+        PDB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        PDB_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, hi));
+        PDB_CUDA(cudaEventCreateWithFlags(&a.pre, cudaEventDisableTiming));
+        PDB_CUDA(cudaEventCreateWithFlags(&a.k1, cudaEventDisableTiming));
+        PDB_CUDA(cudaEventCreateWithFlags(&a.pca, cudaEventDisableTiming));
+    }
+    const int E = D + D * D + 1;
+    DevBuf<float> mu(static_cast<size_t>(DP), s);
+    DevBuf<float> part(static_cast<size_t>(kPcaBlocks) * E, s);
+    DevBuf<double> sum(static_cast<size_t>(E), s);
+    DevBuf<BandInfo> info(1, s);
+    DevBuf<unsigned> done(1, s);
+    PDB_CUDA(cudaMemsetAsync(done.p, 0, sizeof(unsigned), s));
+    PDB_CUDA(cudaEventRecord(a.pre, s));
+    // (SMs' worth of K1 CTA slots left to the PCA: config-2 step 0.350 ms
+    // unfused; fused 0.345 / 0.344 / 0.349 ms with 0 / 1 / 2 reserved)
+    static const int reserve = [] {
+        const char* e = getenv("PDB_FJ_RESERVE");
+        return e ? atoi(e) : 1;
+    }();
+    FeatOuts fo{};
+    fo.p[0] = d_feats;
+    fo.n = 1;
+    fo.done = done.p;
+    int64_t first = -1;
+    launch_featurize_tiles_multi(d_frames, n, H, W, th, tw, bins, mode, fo, s, reserve, &first);
+    int64_t n_rows = first;
+    if (first > 0) {  // K1 signals its first round: the PCA starts beside it
+        PDB_CUDA(cudaStreamWaitEvent(a.s, a.pre, 0));
+        k_wait_count<<<1, 32, 0, a.s>>>(done.p, static_cast<unsigned>(first));
+    } else {  // (other K1 variants: after K1, on its whole output)
+        PDB_CUDA(cudaEventRecord(a.k1, s));
+        PDB_CUDA(cudaStreamWaitEvent(a.s, a.k1, 0));
+        n_rows = nt;
+    }
+    n_rows = std::min<int64_t>(n_rows, nt);
+    k_col_mean<<<static_cast<unsigned>(ceil_div(DP, 32)), dim3(32, 8), 0, a.s>>>(
+        d_feats, n_rows, D, DP, mu.p, nullptr, nullptr, 0, nullptr, 0, nullptr);
+    auto kp = D <= 16 ? k_pca_partial<1> : D <= 32 ? k_pca_partial<2> : D <= 64 ? k_pca_partial<4>
+                                                                              : k_pca_partial<8>;
+    launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, a.s, static_cast<const float*>(d_feats), n_rows, D,
+               static_cast<const float*>(mu.p), part.p);
+    launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, a.s,
+               static_cast<const float*>(part.p), E, sum.p, static_cast<int32_t*>(nullptr),
+               static_cast<int32_t*>(nullptr));
+    set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
+    launch_pdl(k_pca_eig, dim3(1), dim3(256), D * D * 4, a.s, static_cast<const double*>(sum.p), D,
+               static_cast<const float*>(mu.p), info.p);
+    PDB_CUDA(cudaGetLastError());
+    PDB_CUDA(cudaEventRecord(a.pca, a.s));
+    PDB_CUDA(cudaStreamWaitEvent(s, a.pca, 0));
+    const JoinPre pre{mu.p, info.p};
+    run_sim_join_dev(d_feats, nt, d_feats, nt, D, tau, o, out, stats, &pre);
+    if (stats) stats->launches += 6;  // K1, the wait, col_mean, the PCA's three
 }
 
 }  // namespace pdb

@@ -156,21 +156,40 @@ constexpr int kMaxFeatOuts = 8;
 struct FeatOuts {
     float* p[kMaxFeatOuts];
     int n;
+    // optional: each consumer warp of the joint-rows K1 adds 1 here once its
+    // first tile row's features are stored (run_featurize_join_dev)
+    unsigned* done;
 };
+// *first_round (optional): tiles [0, *first_round) are the ones whose
+// completion outs.done counts (one count per tile), or -1 when the kernel
+// taken does not signal.
 PDB_HIDDEN void launch_featurize_tiles_multi(const uint8_t* d_frames, int64_t n_frames, int32_t H,
                                              int32_t W, int32_t th, int32_t tw, int32_t bins,
-                                             int32_t mode, const FeatOuts& outs, cudaStream_t s);
+                                             int32_t mode, const FeatOuts& outs, cudaStream_t s,
+                                             int sm_reserve = 0, int64_t* first_round = nullptr);
 PDB_HIDDEN int hist_dim(int32_t bins, int32_t mode);
 PDB_HIDDEN void launch_featurize_tiles(const uint8_t* d_frames, int64_t n_frames, int32_t H,
                                        int32_t W, int32_t th, int32_t tw, int32_t bins,
-                                       int32_t mode, float* d_out, cudaStream_t s);
+                                       int32_t mode, float* d_out, cudaStream_t s,
+                                       int sm_reserve = 0);
 PDB_HIDDEN void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t w,
                                 int32_t bins, int32_t mode, float* d_out, cudaStream_t s);
 
 // ---- K2/K3 (join.cu) -------------------------------------------------------
+// The band plan's centre and directions computed ahead of the join
+// (run_featurize_join_dev: on a prefix sample, beside the rest of K1).
+struct JoinPre {
+    const float* mu;   // [DP] centre
+    const void* info;  // BandInfo (join.cu)
+};
 PDB_HIDDEN void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
                                  int32_t d, double tau, const pdb_join_opts& o,
-                                 pdb_dev_pairs* out, pdb_join_stats* stats);
+                                 pdb_dev_pairs* out, pdb_join_stats* stats,
+                                 const JoinPre* pre = nullptr);
+PDB_HIDDEN void run_featurize_join_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32_t W,
+                                       int32_t th, int32_t tw, int32_t bins, int32_t mode,
+                                       float* d_feats, double tau, const pdb_join_opts& o,
+                                       pdb_dev_pairs* out, pdb_join_stats* stats);
 PDB_HIDDEN void run_dedup_dev(const float* d_X, int64_t n, int32_t d, double tau, cudaStream_t s,
                               int64_t* d_rep_of, int64_t* n_reps);
 // out[k] = euclidean(A[k], B[k]) <= radius (rows.cu)
