@@ -56,9 +56,10 @@ def test_fused_matches_separate_calls(monkeypatch, frames, reserve):
 
 
 def test_fused_against_oracle_and_fallbacks(monkeypatch):
-    """The oracle's pairs on a 120-frame set; the dense and no-overlap
-    fallbacks (PDB_JOIN_BAND=0, PDB_FUSED_PCA=0) give the same."""
-    fr, _ = workloads.frames(120, 480, 640, seed=7)
+    """The oracle's pairs on a 150-frame set (9,600 tiles: above the band
+    plan's size threshold); the dense and no-overlap fallbacks
+    (PDB_JOIN_BAND=0, PDB_FUSED_PCA=0) give the same."""
+    fr, _ = workloads.frames(150, 480, 640, seed=7)
     feats, l, r, dd, st = _run(fr, 60, 80, 4, 1, 0.05, True)
     ol, orr, od = oracle.sim_join(feats, None, 0.05, self_join=True)
     assert np.array_equal(l, ol) and np.array_equal(r, orr)
@@ -81,3 +82,16 @@ def test_fused_rejects_sharding():
     rc = lib.pdb_featurize_join_dev(d.data_ptr(), 4, 480, 640, 60, 80, 4, 1, 0.05, C.byref(o),
                                     feats.data_ptr(), C.byref(p._p), C.byref(p.stats))
     assert rc != 0
+
+
+@pytest.mark.parametrize("B,mode", [(2, 1), (4, 0)])
+def test_fused_other_histograms(B, mode):
+    """K1 variants without the first-round signal (per-channel histograms) and
+    the 8-bin joint one: the PCA then waits for K1, same pairs either way."""
+    fr, _ = workloads.frames(200, 480, 640, seed=9)
+    tau = 0.05 if mode == 1 else 0.03
+    a = _run(fr, 60, 80, B, mode, tau, True)
+    b = _run(fr, 60, 80, B, mode, tau, False)
+    assert np.array_equal(a[0], b[0])
+    for x, y in zip(a[1:4], b[1:4]):
+        assert np.array_equal(x, y)
