@@ -1619,7 +1619,7 @@ k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __rest
     __shared__ float xs[kPcaRows][16 * T];
     __shared__ int ok[kPcaRows];
     __shared__ int64_t rows[kPcaRows];
-    const int64_t S = static_cast<int64_t>(kPcaBlocks) * kPcaRows;
+    const int64_t S = static_cast<int64_t>(gridDim.x) * kPcaRows;  // (kPcaBlocks, or fewer)
     if (threadIdx.x < kPcaRows) {
         rows[threadIdx.x] = (static_cast<int64_t>(blockIdx.x * kPcaRows + threadIdx.x) * n) / S;
         ok[threadIdx.x] = 1;
@@ -1685,7 +1685,7 @@ k_pca_partial(const float* __restrict__ X, int64_t n, int d, const float* __rest
 // Fixed-order fp64 reduction of the partials (deterministic).
 __global__ void __launch_bounds__(128)
 k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum,
-             int32_t* __restrict__ bins0, int32_t* __restrict__ bins1) {
+             int32_t* __restrict__ bins0, int32_t* __restrict__ bins1, int nparts) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1698,7 +1698,7 @@ k_pca_reduce(const float* __restrict__ part, int E, double* __restrict__ sum,
     // every partial's load in flight at once, then the fixed-order sum
     float v[kPcaBlocks];
 #pragma unroll
-    for (int b = 0; b < kPcaBlocks; b++) v[b] = part[static_cast<size_t>(b) * E + e];
+    for (int b = 0; b < kPcaBlocks; b++) v[b] = b < nparts ? part[static_cast<size_t>(b) * E + e] : 0.0f;
     double acc = 0.0;
 #pragma unroll
     for (int b = 0; b < kPcaBlocks; b++) acc += static_cast<double>(v[b]);
@@ -3676,7 +3676,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                        part);
             launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, s,
                        static_cast<const float*>(part), E, sum, reinterpret_cast<int32_t*>(tmpL),
-                       reinterpret_cast<int32_t*>(tmpR));
+                       reinterpret_cast<int32_t*>(tmpR), kPcaBlocks);
             const int eig_smem = d * d * 4;
             // (set_max_smem caches per function and device)
             set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
@@ -4159,11 +4159,18 @@ void run_featurize_join_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32
         d_feats, n_rows, D, DP, mu.p, nullptr, nullptr, 0, nullptr, 0, nullptr);
     auto kp = D <= 16 ? k_pca_partial<1> : D <= 32 ? k_pca_partial<2> : D <= 64 ? k_pca_partial<4>
                                                                               : k_pca_partial<8>;
-    launch_pdl(kp, dim3(kPcaBlocks), dim3(256), 0, a.s, static_cast<const float*>(d_feats), n_rows, D,
+    // (PDB_FJ_PCA_BLOCKS: a smaller sample finishes sooner beside K1 but
+    // prunes worse -- 16 blocks: 19,990 tiles vs 19,460 and a 3 us slower
+    // step -- so the full 4,096-row sample stays)
+    static const int pca_blocks = [] {
+        const char* e = getenv("PDB_FJ_PCA_BLOCKS");
+        return std::clamp(e ? atoi(e) : kPcaBlocks, 1, kPcaBlocks);
+    }();
+    launch_pdl(kp, dim3(pca_blocks), dim3(256), 0, a.s, static_cast<const float*>(d_feats), n_rows, D,
                static_cast<const float*>(mu.p), part.p);
     launch_pdl(k_pca_reduce, dim3(static_cast<unsigned>(ceil_div(E, 128))), dim3(128), 0, a.s,
                static_cast<const float*>(part.p), E, sum.p, static_cast<int32_t*>(nullptr),
-               static_cast<int32_t*>(nullptr));
+               static_cast<int32_t*>(nullptr), pca_blocks);
     set_max_smem(reinterpret_cast<const void*>(k_pca_eig), kPcaMaxD * kPcaMaxD * 4);
     launch_pdl(k_pca_eig, dim3(1), dim3(256), D * D * 4, a.s, static_cast<const double*>(sum.p), D,
                static_cast<const float*>(mu.p), info.p);
