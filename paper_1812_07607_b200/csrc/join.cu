@@ -3694,7 +3694,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             auto kk = nv == 1 ? k_band_keys<1> : nv == 2 ? k_band_keys<2> : nv == 3 ? k_band_keys<3>
                                                                                       : k_band_keys<4>;
             const unsigned gk = static_cast<unsigned>(
-                std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 32), int64_t{ctx.sm_count} * 16));
+                // (8 warps x 4 lane groups x RPG rows per block step)
+                std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 128), int64_t{ctx.sm_count} * 16));
             int32_t* count = reinterpret_cast<int32_t*>(tmp);  // bin counts, zeroed by k_pca_reduce
             launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
                        proj, k_in, v_in, count);
