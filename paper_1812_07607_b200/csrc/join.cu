@@ -3717,8 +3717,11 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                            static_cast<const int32_t*>(bcnt), perm);
                 launches += 4;
             } else {
-                launch_pdl(k_bin_scatter<kScatterRows>,
-                           dim3(static_cast<unsigned>(ceil_div(n, 1024 * kScatterRows))),
+                // 4 rows per thread, or 1 when that leaves SMs idle (config 2:
+                // 16 blocks of 4,096 rows vs 63 of 1,024)
+                const int rpt = ceil_div(n, int64_t{1024} * kScatterRows) < ctx.sm_count ? 1 : kScatterRows;
+                launch_pdl(rpt == 1 ? k_bin_scatter<1> : k_bin_scatter<kScatterRows>,
+                           dim3(static_cast<unsigned>(ceil_div(n, int64_t{1024} * rpt))),
                            dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n,
                            static_cast<const int32_t*>(count), count + kBins, perm);
                 launches += 2;
