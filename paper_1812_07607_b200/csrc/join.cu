@@ -4066,13 +4066,17 @@ void run_cos_join_dev(const uint16_t* d_L, int64_t nL, const uint16_t* d_R, int6
 
 
 // Spins until the first K1 round has stored its tiles (FeatOuts::done).
+// Bounded: a count that never arrives (K1 gone wrong) traps after ~10 s
+// instead of hanging the stream.
 __global__ void k_wait_count(const unsigned* __restrict__ done, unsigned target) {
     if (threadIdx.x == 0) {
+        const long long t0 = clock64();
         unsigned v;
         for (;;) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
             if (v >= target) break;
             __nanosleep(256);
+            if (clock64() - t0 > (1ll << 34)) __trap();
         }
         __threadfence();
     }
