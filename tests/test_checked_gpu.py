@@ -20,7 +20,7 @@ pytestmark = [pytest.mark.gpu,
 
 
 @pytest.mark.parametrize("case", ["k1", "k2_dense", "k2_pair", "band", "k3_grouped", "cosine",
-                                  "dedup"])
+                                  "dedup", "fp16_filter", "fused"])
 def test_checked_build_case(case):
     env = dict(os.environ, PDB_CUDA_LIB=LIB)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py"), case],

@@ -98,8 +98,49 @@ def dedup():
     assert np.array_equal(g.rep_of, rep_of) and len(g.reps) == nr
 
 
+def fp16_filter():
+    """fp16 screen copies (forced) and the K3 fp32 pre-filter (bf16 copies,
+    grouped), against the oracle."""
+    for env in ({"PDB_JOIN_BAND": "1", "PDB_SCREEN_FP16": "2"},
+                {"PDB_JOIN_BAND": "1", "PDB_SCREEN_FP16": "0", "PDB_K3_GROUPED": "2"}):
+        os.environ.update(env)
+        try:
+            x = workloads.config5(8192)
+            _eq_join(patchdb.sim_join(x, None, 0.01, self_join=True), x, None, 0.01, True)
+            L, R, _, _ = workloads.config3(n=6000)
+            _eq_join(patchdb.sim_join(L, R, 0.02), L, R, 0.02, False)
+        finally:
+            for k in env:
+                del os.environ[k]
+
+
+def fused():
+    """pdb_featurize_join_dev (K1's first-round count, the PCA beside it)."""
+    import ctypes as C
+    import torch
+    from paper_1812_07607_b200 import _capi as capi
+    lib = capi.lib()
+    fr, _ = workloads.frames(150, 480, 640, seed=7)
+    d = torch.from_numpy(fr).cuda()
+    feats = torch.empty(150 * 64, 64, device="cuda")
+    o = capi.JoinOpts()
+    o.flags = capi.PDB_JOIN_SELF
+    p = patchdb.DevicePairs()
+    assert lib.pdb_featurize_join_dev(d.data_ptr(), 150, 480, 640, 60, 80, 4, 1, 0.05, C.byref(o),
+                                      feats.data_ptr(), C.byref(p._p), C.byref(p.stats)) == 0
+    torch.cuda.synchronize()
+    f = feats.cpu().numpy()
+    assert np.array_equal(f.view(np.uint32), oracle.featurize_tiles(fr, 60, 80, 4, 1).view(np.uint32))
+    l, r, dd = (t.cpu().numpy() for t in p.to_torch(d.device))
+    k = np.lexsort((r, l))
+    ol, orr, od = oracle.sim_join(f, None, 0.05, self_join=True)
+    assert np.array_equal(l[k], ol) and np.array_equal(r[k], orr)
+    assert np.array_equal(dd[k], od.astype(np.float32))
+
+
 CASES = {"k1": k1, "k2_dense": k2_dense, "k2_pair": k2_pair, "band": band,
-         "k3_grouped": k3_grouped, "cosine": cosine, "dedup": dedup}
+         "k3_grouped": k3_grouped, "cosine": cosine, "dedup": dedup,
+         "fp16_filter": fp16_filter, "fused": fused}
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or list(CASES):
