@@ -1278,69 +1278,85 @@ k_prep(const float* __restrict__ X, int64_t n, int d, int DP, const float* __res
     }
     double part[kRowsPerWarp], epart[kRowsPerWarp];
     uint32_t fin_mask = 0, big_mask = 0;
+    // the copy format (fp16 / bf16 / tf32) and whether every lane column is
+    // in range are uniform: the row loop is instantiated per case, so the
+    // per-value work carries no branches (config-3 prep: 186 warp
+    // instructions per row with them, issue-bound)
+    auto rows = [&](auto f16_tag, auto full_tag) {
+        constexpr bool F16 = decltype(f16_tag)::value;
+        constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int r = 0; r < kRowsPerWarp; r++) {
-        double acc = 0.0;
-        float eacc = 0.0f;
-        bool finite = true, big = false;
-        float t[NV];
+        for (int r = 0; r < kRowsPerWarp; r++) {
+            double acc = 0.0;
+            float eacc = 0.0f;
+            bool finite = true, big = false;
+            float t[NV];
 #pragma unroll
-        for (int i = 0; i < NV; i++) {
-            const int k = lane * NV + i;
-            t[i] = 0.0f;
-            if (k < d) {
-                if (!isfinite(x[r][i])) finite = false;
-                float c = __fsub_rn(x[r][i], m[i]);
-                if (BF16 && sc > 0.0f) {
-                    c = __fmul_rn(c, sc);  // exact: a power of two (fp32 underflow
-                                           // below 2^-126 errs < 2^-150, inside the 1e-30 slack)
-                    t[i] = __half2float(__float2half_rn(c));
-                } else {
-                    t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
-                                : round_tf32(c);
+            for (int i = 0; i < NV; i++) {
+                const int k = lane * NV + i;
+                t[i] = 0.0f;
+                if (FULL || k < d) {
+                    if (!isfinite(x[r][i])) finite = false;
+                    float c = __fsub_rn(x[r][i], m[i]);
+                    if constexpr (F16) {
+                        c = __fmul_rn(c, sc);  // exact: a power of two (fp32 underflow
+                                               // below 2^-126 errs < 2^-150, inside the 1e-30 slack)
+                        t[i] = __half2float(__float2half_rn(c));
+                    } else {
+                        t[i] = BF16 ? __uint_as_float(static_cast<uint32_t>(to_bf16_bits(c)) << 16)
+                                    : round_tf32(c);
+                    }
+                    if (!(fabsf(t[i]) <= kBigLimit)) big = true;
+                    // this coordinate's rounding error: exact in fp32 (t is c
+                    // rounded, so the two are within a factor 2); its square and
+                    // the running sum round up to (d + 2) 2^-23 in all (err_norm)
+                    const float e = __fsub_rn(t[i], c);
+                    eacc = __fmaf_rn(e, e, eacc);
                 }
-                if (!(fabsf(t[i]) <= kBigLimit)) big = true;
-                // this coordinate's rounding error: exact in fp32 (t is c
-                // rounded, so the two are within a factor 2); its square and
-                // the running sum round up to (d + 2) 2^-23 in all (err_norm)
-                const float e = __fsub_rn(t[i], c);
-                eacc = __fmaf_rn(e, e, eacc);
+                acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
             }
-            acc += static_cast<double>(t[i]) * static_cast<double>(t[i]);
-        }
-        part[r] = acc;
-        epart[r] = static_cast<double>(eacc);
-        finite = __all_sync(0xffffffffu, finite);
-        big = __any_sync(0xffffffffu, big);
-        fin_mask |= static_cast<uint32_t>(finite) << r;
-        big_mask |= static_cast<uint32_t>(big) << r;
-        if (r0 + r < n) {
-            const bool zero = !finite || big;
-            const int64_t row = r0 + r;
-            if (BF16) {
-                uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP + lane * NV;
-                uint16_t b[NV];
+            part[r] = acc;
+            epart[r] = static_cast<double>(eacc);
+            finite = __all_sync(0xffffffffu, finite);
+            big = __any_sync(0xffffffffu, big);
+            fin_mask |= static_cast<uint32_t>(finite) << r;
+            big_mask |= static_cast<uint32_t>(big) << r;
+            if (r0 + r < n) {
+                const bool zero = !finite || big;
+                const int64_t row = r0 + r;
+                if (BF16) {
+                    uint16_t* xpb = static_cast<uint16_t*>(Xp_) + row * DP + lane * NV;
+                    uint16_t b[NV];
 #pragma unroll
-                for (int i = 0; i < NV; i++)
-                    b[i] = zero ? 0
-                         : sc > 0.0f ? __half_as_ushort(__float2half_rn(t[i]))  // exact: t is fp16
-                                     : static_cast<uint16_t>(__float_as_uint(t[i]) >> 16);
-                if (NV == 4) {
-                    *reinterpret_cast<uint2*>(xpb) =
-                        make_uint2(b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16),
-                                   b[2 % NV] | (static_cast<uint32_t>(b[3 % NV]) << 16));
-                } else if (NV == 2) {
-                    *reinterpret_cast<uint32_t*>(xpb) = b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16);
+                    for (int i = 0; i < NV; i++)
+                        b[i] = zero ? 0
+                             : F16 ? __half_as_ushort(__float2half_rn(t[i]))  // exact: t is fp16
+                                   : static_cast<uint16_t>(__float_as_uint(t[i]) >> 16);
+                    if (NV == 4) {
+                        *reinterpret_cast<uint2*>(xpb) =
+                            make_uint2(b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16),
+                                       b[2 % NV] | (static_cast<uint32_t>(b[3 % NV]) << 16));
+                    } else if (NV == 2) {
+                        *reinterpret_cast<uint32_t*>(xpb) = b[0] | (static_cast<uint32_t>(b[1 % NV]) << 16);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NV; i++) xpb[i] = b[i];
+                    }
                 } else {
+                    float* xpf = static_cast<float*>(Xp_) + row * DP + lane * NV;
 #pragma unroll
-                    for (int i = 0; i < NV; i++) xpb[i] = b[i];
+                    for (int i = 0; i < NV; i++) xpf[i] = zero ? 0.0f : t[i];
                 }
-            } else {
-                float* xpf = static_cast<float*>(Xp_) + row * DP + lane * NV;
-#pragma unroll
-                for (int i = 0; i < NV; i++) xpf[i] = zero ? 0.0f : t[i];
             }
         }
+    };
+    const bool full = d == DP;
+    if (BF16 && sc > 0.0f) {
+        if (full) rows(std::true_type{}, std::true_type{});
+        else rows(std::true_type{}, std::false_type{});
+    } else {
+        if (full) rows(std::false_type{}, std::true_type{});
+        else rows(std::false_type{}, std::false_type{});
     }
     const double acc = sum8_transpose(part, lane);
     const double eacc = sum8_transpose(epart, lane);
