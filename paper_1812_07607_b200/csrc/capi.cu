@@ -190,7 +190,7 @@ void check_join_args(const void* L, int64_t nL, const void* R, int64_t nR, int32
 // 12.5 GB -- costs millions of first-touch page faults inside the copy).
 void* host_pairs_alloc(size_t bytes) {
     constexpr size_t kHuge = size_t{2} << 20;
-    if (bytes < (size_t{64} << 20)) return std::malloc(bytes);
+    if (bytes < kHuge) return std::malloc(bytes);
     void* p = nullptr;
     if (posix_memalign(&p, kHuge, (bytes + kHuge - 1) / kHuge * kHuge) != 0) return nullptr;
 #ifdef MADV_HUGEPAGE
@@ -233,8 +233,8 @@ void d2h_large(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         ring.dev = dev;
     }
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    // (one host thread per ~4 MB, at most 16)
-    const int nthr = static_cast<int>(std::min<size_t>(std::min(16u, hw), std::max<size_t>(1, bytes >> 22)));
+    // (one host thread per MB, at most 16)
+    const int nthr = static_cast<int>(std::min<size_t>(std::min(16u, hw), std::max<size_t>(1, bytes >> 20)));
     auto host_copy = [&](char* d, const char* src_h, size_t len) {
         const size_t part = (len / nthr + 4095) / 4096 * 4096;
         std::vector<std::thread> th;
@@ -262,6 +262,17 @@ void d2h_large(void* dst, const void* src, size_t bytes, cudaStream_t s) {
                       len_of(i - 1));
         }
     }
+}
+
+// The library's own device pairs, returned to the stream-ordered pool (the
+// public pdb_dev_pairs_free uses cudaFree, which synchronises the device).
+void dev_pairs_release(pdb_dev_pairs* p, cudaStream_t s) {
+    dev_free(p->left, s);
+    dev_free(p->right, s);
+    dev_free(p->dist, s);
+    p->left = p->right = nullptr;
+    p->dist = nullptr;
+    p->count = p->capacity = 0;
 }
 
 void pairs_to_host(const pdb_dev_pairs& dp, pdb_pairs* out, cudaStream_t s) {
@@ -477,10 +488,10 @@ PDB_API int pdb_sim_join(const float* L, int64_t nL, const float* R, int64_t nR,
             run_sim_join_dev(dL.p, nL, self ? dL.p : dR.p, self ? nL : nR, d, tau, o, &dp, nullptr);
             pairs_to_host(dp, out, s);
         } catch (...) {
-            pdb_dev_pairs_free(&dp);
+            dev_pairs_release(&dp, s);
             throw;
         }
-        pdb_dev_pairs_free(&dp);
+        dev_pairs_release(&dp, s);
     });
 }
 
@@ -532,10 +543,10 @@ PDB_API int pdb_cosine_join_bf16(const uint16_t* L, int64_t nL, const uint16_t* 
                              nullptr);
             pairs_to_host(dp, out, s);
         } catch (...) {
-            pdb_dev_pairs_free(&dp);
+            dev_pairs_release(&dp, s);
             throw;
         }
-        pdb_dev_pairs_free(&dp);
+        dev_pairs_release(&dp, s);
     });
 }
 
@@ -610,10 +621,10 @@ PDB_API int pdb_featurize_join(const uint8_t* frames, int64_t n, int32_t H, int3
                                          cudaMemcpyDeviceToHost, s));
             pairs_to_host(dp, out, s);
         } catch (...) {
-            pdb_dev_pairs_free(&dp);
+            dev_pairs_release(&dp, s);
             throw;
         }
-        pdb_dev_pairs_free(&dp);
+        dev_pairs_release(&dp, s);
     });
 }
 
@@ -703,10 +714,10 @@ PDB_API int pdb_warmup(void) {
         try {
             run_sim_join_dev(X.p, 256, X.p, 256, 64, 0.05, o, &dp, nullptr);
         } catch (...) {
-            pdb_dev_pairs_free(&dp);
+            dev_pairs_release(&dp, s);
             throw;
         }
-        pdb_dev_pairs_free(&dp);
+        dev_pairs_release(&dp, s);
         PDB_CUDA(cudaStreamSynchronize(s));
     });
 }
