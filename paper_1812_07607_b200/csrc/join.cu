@@ -3175,8 +3175,17 @@ PinSlot pinned_slot() {
 // count reaches the host while the main stream still writes the tile lists.
 struct PlanAux {
     cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr, scan = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, scan = nullptr, kfork = nullptr, kjoin = nullptr;
 };
+// (PDB_PLAN_AUX=0: one PDL-chained stream)
+bool use_plan_aux() {
+    static const bool on = [] {
+        const char* e = std::getenv("PDB_PLAN_AUX");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 PlanAux* plan_aux() {
     thread_local PlanAux cache[64];
     thread_local bool made[64] = {};
@@ -3187,7 +3196,9 @@ PlanAux* plan_aux() {
         if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&a.scan, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&a.scan, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.kfork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.kjoin, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;
         }
@@ -3701,7 +3712,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
             launches += 3;
         }
         auto keys_and_sort = [&](const float* X, int64_t n, float2*& proj, int32_t*& perm,
-                                 uint8_t* tmp) {
+                                 uint8_t* tmp, cudaStream_t ks, bool pdl_first) {
             proj = ar.take<float2>(n);
             uint32_t* k_in = ar.take<uint32_t>(n);
             int32_t* v_in = ar.take<int32_t>(n);
@@ -3713,8 +3724,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                 // (8 warps x 4 lane groups x RPG rows per block step)
                 std::min<int64_t>(ceil_div(n, d > 64 ? 64 : 128), int64_t{ctx.sm_count} * 16));
             int32_t* count = reinterpret_cast<int32_t*>(tmp);  // bin counts, zeroed by k_pca_reduce
-            launch_pdl(kk, dim3(gk), dim3(256), 0, s, X, n, d, static_cast<const float*>(mu), info,
-                       proj, k_in, v_in, count);
+            launch_pdl_if(pdl_first, kk, dim3(gk), dim3(256), 0, ks, X, n, d, static_cast<const float*>(mu),
+                          info, proj, k_in, v_in, count);
             if (P > 1) {
                 // every rank must build the same order: a deterministic stable
                 // counting sort (block-local ranks in row order, per-bin block
@@ -3724,11 +3735,11 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                 // (carved from this side's sort scratch, after the bin counts)
                 int32_t* rank = reinterpret_cast<int32_t*>(tmp + 2 * kBins * 4 + 256);
                 int32_t* bcnt = rank + ((n + 63) / 64) * 64;
-                launch_pdl(k_rank_local, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, s,
+                launch_pdl(k_rank_local, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, ks,
                            static_cast<const uint32_t*>(k_in), n, rank, bcnt);
-                launch_pdl(k_rank_offsets, dim3(kBins / 256), dim3(256), 0, s,
+                launch_pdl(k_rank_offsets, dim3(kBins / 256), dim3(256), 0, ks,
                            static_cast<const int32_t*>(count), bcnt, nblk);
-                launch_pdl(k_rank_scatter, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, s,
+                launch_pdl(k_rank_scatter, dim3(static_cast<unsigned>(nblk)), dim3(1024), 0, ks,
                            static_cast<const uint32_t*>(k_in), n, static_cast<const int32_t*>(rank),
                            static_cast<const int32_t*>(bcnt), perm);
                 launches += 4;
@@ -3738,17 +3749,29 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                 const int rpt = ceil_div(n, int64_t{1024} * kScatterRows) < ctx.sm_count ? 1 : kScatterRows;
                 launch_pdl(rpt == 1 ? k_bin_scatter<1> : k_bin_scatter<kScatterRows>,
                            dim3(static_cast<unsigned>(ceil_div(n, int64_t{1024} * rpt))),
-                           dim3(1024), 0, s, static_cast<const uint32_t*>(k_in), n,
+                           dim3(1024), 0, ks, static_cast<const uint32_t*>(k_in), n,
                            static_cast<const int32_t*>(count), count + kBins, perm);
                 launches += 2;
             }
         };
-        keys_and_sort(d_L, nL, projL, permL, tmpL);
+        // a cross join's two sides are independent: R's keys and sort run on
+        // the aux stream beside L's (each alone keeps HBM ~45 % busy)
+        PlanAux* kaux = !self && use_plan_aux() ? plan_aux() : nullptr;
+        if (kaux) {
+            PDB_CUDA(cudaEventRecord(kaux->kfork, s));
+            PDB_CUDA(cudaStreamWaitEvent(kaux->s, kaux->kfork, 0));
+        }
+        keys_and_sort(d_L, nL, projL, permL, tmpL, s, true);
         if (self) {
             permR = permL;
             projR = projL;
+        } else if (kaux) {
+            // (the first kernel after a cross-stream wait launches without PDL)
+            keys_and_sort(d_R, nR, projR, permR, tmpR, kaux->s, false);
+            PDB_CUDA(cudaEventRecord(kaux->kjoin, kaux->s));
+            PDB_CUDA(cudaStreamWaitEvent(s, kaux->kjoin, 0));
         } else {
-            keys_and_sort(d_R, nR, projR, permR, tmpR);
+            keys_and_sort(d_R, nR, projR, permR, tmpR, s, true);
         }
     }
 
@@ -3770,11 +3793,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     UnitsReady ready;
     // (PDB_PLAN_AUX=0: one PDL-chained stream, the host spinning on the
     // mapped unit count instead -- ~2 us slower on config 2)
-    static const bool use_aux = [] {
-        const char* e = std::getenv("PDB_PLAN_AUX");
-        return !(e && e[0] == '0');
-    }();
-    PlanAux* aux = band && use_aux ? plan_aux() : nullptr;
+    PlanAux* aux = band && use_plan_aux() ? plan_aux() : nullptr;
     // The screen copies go to the aux stream (band plans): the tile walk
     // below (boxes, groups, counts, scan) is the longer chain and stays on
     // the PDL-chained main stream, so the cross-stream start-up gap (~6 us)
