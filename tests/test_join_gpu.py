@@ -427,3 +427,19 @@ def test_fuzz_offsets_scales_dims(monkeypatch, seed):
                            dense=variant == "dense", tf32=variant == "tf32")
     ol, orr, od = oracle.sim_join(L, None if self_join else R, tau, self_join=self_join, threads=4)
     _check(res, ol, orr, od)
+
+
+def test_host_output_path_large():
+    """The host API's pair output above 64 MB per array (config 5's
+    distribution at 600k rows, ~22 M pairs): staged through the pinned ring
+    in several chunks with threaded host copies (capi.cu d2h_large); equal
+    to the device path's pairs."""
+    x = workloads.config5(600_000)
+    res = patchdb.sim_join(x, None, 0.01, self_join=True, sort=True)
+    assert len(res.left) * 4 > (64 << 20)
+    xt = torch.from_numpy(x).cuda()
+    r = patchdb.sim_join_device(xt, None, 0.01, self_join=True, sort=True)
+    want = [t.cpu().numpy() for t in r.to_torch(xt.device)]
+    r.free()
+    assert np.array_equal(res.left, want[0]) and np.array_equal(res.right, want[1])
+    assert np.array_equal(res.dist, want[2])
