@@ -1158,7 +1158,7 @@ k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restr
     __shared__ double part[32][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
     double s = 0.0;
-    if (col < d) {  // (blockDim.y 32, or 8 beside a running K1: same rows)
+    if (mu && col < d) {  // (blockDim.y 32, or 8 beside a running K1: same rows)
         for (int r = threadIdx.y; r < kMeanRows; r += blockDim.y) {
             if (r < n) {
                 const float v = X[static_cast<int64_t>(r) * d + col];
@@ -1168,7 +1168,8 @@ k_col_mean(const float* __restrict__ X, int64_t n, int d, int DP, float* __restr
     }
     part[threadIdx.y][threadIdx.x] = s;
     __syncthreads();
-    if (mu_src) {  // the centre was computed ahead (run_featurize_join_dev)
+    if (!mu) return;  // the centre was computed ahead (run_featurize_join_dev)
+    if (mu_src) {
         if (threadIdx.y == 0 && col < DP) mu[col] = mu_src[col];
         return;
     }
@@ -3633,6 +3634,18 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                    (fold ? Arena::need(static_cast<size_t>(nR) * kGCols, 2) : 0) + band_bytes,
                s);
     float* mu = ar.take<float>(DP);
+    // a precomputed centre and directions (run_featurize_join_dev): the join's
+    // first kernels (tile-statistic zeroing, bin zeroing) start right after
+    // K1, and the stream waits for the PCA only before the first kernel that
+    // reads them
+    bool pre_waited = false;
+    auto wait_pre = [&]() -> bool {
+        if (!pre || pre_waited) return false;
+        pre_waited = true;
+        if (pre->ready) PDB_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(pre->ready), 0));
+        return pre->ready != nullptr;
+    };
+    if (pre) mu = const_cast<float*>(pre->mu);
     uint16_t* gx = fold ? ar.take<uint16_t>(static_cast<size_t>(nR) * kGCols) : nullptr;
     // R tile statistics: written by k_prep (DP <= 128, zeroed by k_col_mean)
     // or k_tile_stats (wider rows)
@@ -3643,10 +3656,9 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     const bool fused_stats = DP <= 128;
 
     // ---- preparation ----------------------------------------------------
-    // (after a cross-stream wait on the precomputed centre: no PDL)
-    launch_pdl_if(!pre, k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
-               nL, d, DP, mu, fused_stats ? tmaxS : nullptr, fused_stats ? tmaxN : nullptr, nt_tiles,
-               gR, nR, pre ? pre->mu : static_cast<const float*>(nullptr));
+    launch_pdl(k_col_mean, dim3(static_cast<unsigned>(ceil_div(DP, 32))), dim3(32, 32), 0, s, d_L,
+               nL, d, DP, pre ? static_cast<float*>(nullptr) : mu, fused_stats ? tmaxS : nullptr,
+               fused_stats ? tmaxN : nullptr, nt_tiles, gR, nR, static_cast<const float*>(nullptr));
     PDB_CUDA(cudaGetLastError());
     launches++;
     auto prep = [&](const float* X, int64_t n, uint8_t* Xp, float* hn, float* sn, uint16_t* g_out,
@@ -3756,12 +3768,14 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         };
         // a cross join's two sides are independent: R's keys and sort run on
         // the aux stream beside L's (each alone keeps HBM ~45 % busy)
+        // (after a cross-stream wait on the precomputed directions: no PDL)
+        const bool waited = wait_pre();
         PlanAux* kaux = !self && use_plan_aux() ? plan_aux() : nullptr;
         if (kaux) {
             PDB_CUDA(cudaEventRecord(kaux->kfork, s));
             PDB_CUDA(cudaStreamWaitEvent(kaux->s, kaux->kfork, 0));
         }
-        keys_and_sort(d_L, nL, projL, permL, tmpL, s, true);
+        keys_and_sort(d_L, nL, projL, permL, tmpL, s, !waited);
         if (self) {
             permR = permL;
             projR = projL;
@@ -3798,6 +3812,8 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     // below (boxes, groups, counts, scan) is the longer chain and stays on
     // the PDL-chained main stream, so the cross-stream start-up gap (~6 us)
     // lands off the critical path (config-2 join: see DESIGN.md).
+    // (a dense plan with a precomputed centre waits for it here)
+    const bool waited_dense = wait_pre();
     cudaStream_t sp = s;
     if (aux) {
         PDB_CUDA(cudaEventRecord(aux->fork, s));
@@ -3808,7 +3824,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
     float* hnL = ar.take<float>(nL);
     float* snL = ar.take<float>(nL);
     // (the first kernel after a cross-stream wait launches without PDL)
-    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x, self, sp, !aux);
+    prep(d_L, nL, XpL, hnL, snL, self ? gx : nullptr, permL, f16x, self, sp, !aux && !waited_dense);
     const uint8_t* XpR = XpL;
     const float *hnR = hnL, *snR = snL;
     if (!self) {
@@ -4218,9 +4234,8 @@ void run_featurize_join_dev(const uint8_t* d_frames, int64_t n, int32_t H, int32
     launch_pdl(k_pca_eig, dim3(1), dim3(256), D * D * 4, a.s, static_cast<const double*>(sum.p), D,
                static_cast<const float*>(mu.p), info.p);
     PDB_CUDA(cudaGetLastError());
-    PDB_CUDA(cudaEventRecord(a.pca, a.s));
-    PDB_CUDA(cudaStreamWaitEvent(s, a.pca, 0));
-    const JoinPre pre{mu.p, info.p};
+    PDB_CUDA(cudaEventRecord(a.pca, a.s));  // (the join waits for it, JoinPre::ready)
+    const JoinPre pre{mu.p, info.p, a.pca};
     run_sim_join_dev(d_feats, nt, d_feats, nt, D, tau, o, out, stats, &pre);
     if (stats) stats->launches += 6;  // K1, the wait, col_mean, the PCA's three
 }

@@ -181,6 +181,8 @@ PDB_HIDDEN void launch_hist_f32(const float* d_px, int64_t n, int32_t h, int32_t
 struct JoinPre {
     const float* mu;   // [DP] centre
     const void* info;  // BandInfo (join.cu)
+    void* ready;       // cudaEvent_t after which mu and info are valid (the join's
+                       // stream waits for it before their first reader), or null
 };
 PDB_HIDDEN void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR,
                                  int32_t d, double tau, const pdb_join_opts& o,
