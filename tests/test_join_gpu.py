@@ -443,3 +443,35 @@ def test_host_output_path_large():
     r.free()
     assert np.array_equal(res.left, want[0]) and np.array_equal(res.right, want[1])
     assert np.array_equal(res.dist, want[2])
+
+
+def test_concurrent_host_threads():
+    """Joins and featurization from four host threads at once (ctypes drops
+    the GIL; each thread has its own stream, record cache and pinned
+    read-back slot): every result equals the single-threaded one."""
+    import threading
+    xs = [workloads.config1(6000, seed=s) for s in range(4)]
+    fr, _ = workloads.frames(40, 480, 640, seed=3)
+    want = [patchdb.sim_join(x, None, 0.05, self_join=True, sort=True) for x in xs]
+    want_f = patchdb.featurize_tiles(fr, 60, 80, 4, "joint")
+    got, errs = [None] * 4, []
+
+    def work(k):
+        try:
+            for _ in range(5):
+                r = patchdb.sim_join(xs[k], None, 0.05, self_join=True, sort=True)
+                f = patchdb.featurize_tiles(fr, 60, 80, 4, "joint")
+                assert np.array_equal(f, want_f)
+            got[k] = r
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for w, g in zip(want, got):
+        assert np.array_equal(w.left, g.left) and np.array_equal(w.right, g.right)
+        assert np.array_equal(w.dist, g.dist)
