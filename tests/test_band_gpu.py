@@ -61,7 +61,11 @@ def test_forced_band_degenerate_data(forced):
     assert len(got) == 2500 * 2499 // 2
 
 
-def test_forced_band_nonfinite_and_huge_rows(forced):
+@pytest.mark.parametrize("f16", ["1", "2"])
+def test_forced_band_nonfinite_and_huge_rows(forced, monkeypatch, f16):
+    # f16 = "2": the same on fp16 copies (NaN / inf rows excluded, 3e30 rows
+    # beyond the scale's range forced candidates)
+    monkeypatch.setenv("PDB_SCREEN_FP16", f16)
     rng = np.random.default_rng(7)
     x = rng.random((4000, 64), dtype=np.float32)
     x[10] = np.nan
