@@ -211,26 +211,22 @@ void d2h_large(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         PDB_CUDA(cudaStreamSynchronize(s));
         return;
     }
+    // one process-wide ring (192 MB of pinned memory, portable across
+    // devices; events per device), held for the whole copy: concurrent
+    // copies share PCIe anyway
     struct Ring {
         void* buf[kRing] = {};
-        cudaEvent_t ev[kRing] = {};
-        int dev = -1;
+        cudaEvent_t ev[64][kRing] = {};
     };
-    thread_local Ring ring;
+    static Ring ring;
+    static std::mutex ring_mu;
+    std::lock_guard<std::mutex> lk(ring_mu);
     int dev = 0;
     PDB_CUDA(cudaGetDevice(&dev));
-    if (ring.dev != dev) {
-        for (int k = 0; k < kRing; k++) {
-            if (ring.buf[k]) cudaFreeHost(ring.buf[k]);
-            if (ring.ev[k]) cudaEventDestroy(ring.ev[k]);
-            ring.buf[k] = nullptr;
-            ring.ev[k] = nullptr;
-        }
-        for (int k = 0; k < kRing; k++) {
-            PDB_CUDA(cudaMallocHost(&ring.buf[k], kChunk));
-            PDB_CUDA(cudaEventCreateWithFlags(&ring.ev[k], cudaEventDisableTiming));
-        }
-        ring.dev = dev;
+    cudaEvent_t* evs = ring.ev[dev & 63];
+    for (int k = 0; k < kRing; k++) {
+        if (!ring.buf[k]) PDB_CUDA(cudaHostAlloc(&ring.buf[k], kChunk, cudaHostAllocPortable));
+        if (!evs[k]) PDB_CUDA(cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming));
     }
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     // (one host thread per MB, at most 16)
@@ -253,11 +249,11 @@ void d2h_large(void* dst, const void* src, size_t bytes, cudaStream_t s) {
             const int k = static_cast<int>(i % kRing);
             PDB_CUDA(cudaMemcpyAsync(ring.buf[k], static_cast<const char*>(src) + i * kChunk, len_of(i),
                                      cudaMemcpyDeviceToHost, s));
-            PDB_CUDA(cudaEventRecord(ring.ev[k], s));
+            PDB_CUDA(cudaEventRecord(evs[k], s));
         }
         if (i >= 1) {  // the previous chunk: on the host while this one crosses PCIe
             const int k = static_cast<int>((i - 1) % kRing);
-            PDB_CUDA(cudaEventSynchronize(ring.ev[k]));
+            PDB_CUDA(cudaEventSynchronize(evs[k]));
             host_copy(static_cast<char*>(dst) + (i - 1) * kChunk, static_cast<const char*>(ring.buf[k]),
                       len_of(i - 1));
         }
