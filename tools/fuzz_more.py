@@ -12,9 +12,13 @@ class MP:
         self.saved = {}
 import test_join_gpu as t
 lo, hi = int(sys.argv[1]), int(sys.argv[2])
+# extra KEY=VALUE arguments are set for every seed (e.g. PDB_SCREEN_FP16=2 PDB_JOIN_BAND=1)
+extra = dict(a.split("=", 1) for a in sys.argv[3:])
 bad = []
 for seed in range(lo, hi):
     mp = MP()
+    for k, v in extra.items():
+        mp.setenv(k, v)
     try:
         t.test_fuzz_offsets_scales_dims(mp, seed)
     except Exception as e:
