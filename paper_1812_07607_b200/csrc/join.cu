@@ -551,7 +551,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
             const unsigned long long room = res_end - res_pos;
             const unsigned first = room < nb ? static_cast<unsigned>(room) : nb;
             if (static_cast<unsigned>(lane) < first && res_pos + lane < p.cap)
-                p.rec[res_pos + lane] = rbuf[lane];
+                __stcs(p.rec + res_pos + lane, rbuf[lane]);  // (read once, by K3: no L2 residency)
             res_pos += first;
             if (first < nb) {
                 unsigned long long base = 0;
@@ -562,7 +562,7 @@ k_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtens
                 res_chunk = min(2 * res_chunk, kResChunkL);
                 if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
                     res_pos + (lane - first) < p.cap)
-                    p.rec[res_pos + (lane - first)] = rbuf[lane];
+                    __stcs(p.rec + res_pos + (lane - first), rbuf[lane]);
                 res_pos += nb - first;
             }
             __syncwarp();
@@ -1004,7 +1004,7 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const unsigned long long room = res_end - res_pos;
             const unsigned first = room < nb ? static_cast<unsigned>(room) : nb;
             if (static_cast<unsigned>(lane) < first && res_pos + lane < p.cap)
-                p.rec[res_pos + lane] = rbuf[lane];
+                __stcs(p.rec + res_pos + lane, rbuf[lane]);  // (read once, by K3: no L2 residency)
             res_pos += first;
             if (first < nb) {
                 unsigned long long base = 0;
@@ -1015,7 +1015,7 @@ k_screen_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 res_chunk = min(2 * res_chunk, kResChunk);
                 if (static_cast<unsigned>(lane) >= first && static_cast<unsigned>(lane) < nb &&
                     res_pos + (lane - first) < p.cap)
-                    p.rec[res_pos + (lane - first)] = rbuf[lane];
+                    __stcs(p.rec + res_pos + (lane - first), rbuf[lane]);
                 res_pos += nb - first;
             }
             __syncwarp();
@@ -2571,7 +2571,7 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
          base < n; base += stride) {
         const unsigned long long idx = base + lane;
         int4 rc = make_int4(0, 0, 0, 0);
-        if (static_cast<unsigned>(lane) < k && idx < n) rc = rec[idx];
+        if (static_cast<unsigned>(lane) < k && idx < n) rc = __ldcs(rec + idx);  // (read once: evict first)
         const uint32_t mask = static_cast<uint32_t>(rc.z);
         // banded plans screen row-sorted copies: map back to input rows
         const int my_i = (permL && mask) ? __ldg(permL + rc.x) : rc.x;
@@ -2631,9 +2631,11 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
             if (ok) {
                 const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
                 if (pos < out_cap) {
-                    out_l[pos] = a;
-                    out_r[pos] = j;
-                    out_d[pos] = static_cast<float>(dist);
+                    // streaming stores: the pairs must not evict the rows
+                    // the re-check is still reading from L2
+                    __stcs(out_l + pos, a);
+                    __stcs(out_r + pos, j);
+                    __stcs(out_d + pos, static_cast<float>(dist));
                 }
             }
         }
@@ -2698,9 +2700,9 @@ k_recheck_filtered(const int4* __restrict__ rec, const unsigned long long* __res
         if (ok) {
             const unsigned long long pos = w + __popc(ball & ((1u << lane) - 1u));
             if (pos < out_cap) {
-                out_l[pos] = a;
-                out_r[pos] = j;
-                out_d[pos] = static_cast<float>(dist);
+                __stcs(out_l + pos, a);
+                __stcs(out_r + pos, j);
+                __stcs(out_d + pos, static_cast<float>(dist));
             }
         }
     };
@@ -2726,7 +2728,7 @@ k_recheck_filtered(const int4* __restrict__ rec, const unsigned long long* __res
          base < n; base += stride) {
         const unsigned long long idx = base + lane;
         int4 rc = make_int4(0, 0, 0, 0);
-        if (static_cast<unsigned>(lane) < k && idx < n) rc = rec[idx];
+        if (static_cast<unsigned>(lane) < k && idx < n) rc = __ldcs(rec + idx);  // (read once: evict first)
         const uint32_t mask = static_cast<uint32_t>(rc.z);
         const int cnt = __popc(mask);
         int incl = cnt;
