@@ -1601,11 +1601,18 @@ __global__ void k_export_counters(const unsigned long long* __restrict__ c,
 constexpr int kPcaRows = 64;    // sample rows per partial block
 constexpr int kPcaBlocks = 64;  // 4096 sample rows
 constexpr int kPcaMaxD = 128;
-// The plan costs ~60-90 us (config-2 size) whatever the shard count; it pays
-// when this shard's dense screen would visit at least kBandMinTiles tiles
-// (~60 us of dense screen at d = 64) and both sides have kBandMinRows rows.
+// The plan costs ~40-90 us whatever the shard count; it pays when this
+// shard's dense screen would visit at least kBandMinTiles tiles and both
+// sides have kBandMinRows rows.  Single-GPU joins take it from 4,096 tiles:
+// besides pruning, its row order makes a clustered output's candidate
+// records dense (config 1, 6,319 tiles: 0.246 -> 0.210 ms; a 40k-row
+// clustered self-join 0.518 -> 0.364 ms), at ~20-27 us more for small
+// outputs-free joins (uniform 20k x 64: 0.083 -> 0.110 ms;
+// tools/small_band_ab.py).  Sharded joins also pay the stable sort and keep
+// the r01 threshold (16,384 per shard, doubled).
 constexpr int64_t kBandMinRows = 8192;
-constexpr int64_t kBandMinTiles = 16384;
+constexpr int64_t kBandMinTiles = 4096;
+constexpr int64_t kBandMinTilesSharded = 2 * 16384;
 constexpr int kMortonBits = 6;  // per projection: 12-bit sort keys (one counting pass)
 #ifndef PDB_PCA_ITERS
 #define PDB_PCA_ITERS 2
@@ -3603,7 +3610,7 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
         // units <= total / ch + n_slots with ch = clamp(total / units_target, 1, 64)
         units_cap = 2 * static_cast<int64_t>(units_target) + list_cap / 64 + n_slots + 1;
         // too little screen to save (sharded joins also pay the stable sort)
-        if (band_env != 1 && list_cap < kBandMinTiles * (P > 1 ? 2 : 1)) band = false;
+        if (band_env != 1 && list_cap < (P > 1 ? kBandMinTilesSharded : kBandMinTiles)) band = false;
         // tile-list positions travel as int32 (unit_info, Unit): beyond 2^31
         // dense tiles per shard (> ~11.8 M rows self-joined on one GPU) the
         // join keeps the dense plan

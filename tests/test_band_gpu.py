@@ -140,12 +140,29 @@ def test_forced_band_tf32_copies(forced):
     assert np.array_equal(got.left, ol) and np.array_equal(got.right, orr)
 
 
-def test_band_rule_keeps_small_joins_dense():
+def test_band_rule_small_joins(monkeypatch):
+    """Single-GPU self-joins take the band plan from 4,096 dense tiles
+    (config 1's 20,000 rows: 6,319), smaller ones (12,000 rows: 2,303
+    tiles) stay dense; both give the oracle's pairs."""
     import torch
-    x = torch.from_numpy(workloads.config1(20_000, seed=1)).cuda()
-    r = patchdb.sim_join_device(x, None, 0.05, self_join=True)
-    nb = -(-20_000 // 128)
-    assert r.stats.tiles == sum(-(-20_000 // 256) - rb // 2 for rb in range(nb))
+    for n, band in ((12_000, False), (20_000, True)):
+        xh = workloads.config1(n, seed=1)
+        x = torch.from_numpy(xh).cuda()
+        monkeypatch.delenv("PDB_JOIN_BAND", raising=False)
+        r = patchdb.sim_join_device(x, None, 0.05, self_join=True, sort=True)
+        monkeypatch.setenv("PDB_JOIN_BAND", "0")
+        d = patchdb.sim_join_device(x, None, 0.05, self_join=True, sort=True)
+        nb = -(-n // 128)
+        assert d.stats.tiles == sum(-(-n // 256) - rb // 2 for rb in range(nb))
+        assert (r.stats.launches > d.stats.launches) == band, n
+        got = [t.cpu().numpy() for t in r.to_torch(x.device)]
+        want = [t.cpu().numpy() for t in d.to_torch(x.device)]
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+        if n == 12_000:
+            ol, orr, od = oracle.sim_join(xh, None, 0.05, self_join=True, threads=8)
+            assert np.array_equal(got[0], ol) and np.array_equal(got[1], orr)
+            assert np.array_equal(got[2], od.astype(np.float32))
 
 
 def test_sharded_band_plan_deterministic_order(forced):
