@@ -473,7 +473,8 @@ def measure(args, rank, world, local_rank, which, metric, peaks, clock_sampler, 
             "config": {"workload": cfg["workload"], "nL": nL_all, "nL_per_rank": nL, "nR": nR, "d": d,
                        "threshold": cfg["tau"], "candidate_pairs": cand,
                        "l2": "flushed (256 MB read) before each step",
-                       "parallelism": (f"L rows sharded contiguously x{world} (each rank's band plan "
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"L rows sharded contiguously x{world} (each rank's band plan "
                                        f"covers its own L rows), R broadcast once over NCCL"
                                        if cross_shard else
                                        f"L row blocks boustrophedon x{world}, X broadcast once")},
