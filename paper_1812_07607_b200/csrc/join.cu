@@ -2564,8 +2564,18 @@ k_recheck(const int4* __restrict__ rec, const unsigned long long* __restrict__ n
     // sparse buffers -- mostly the zeroed tails of reserved slots -- keep one
     // step per warp, and buffers long enough for >= 4 full steps per warp
     // keep 32.
-    const unsigned long long warps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
     const unsigned long long ncand = n_rec[3];
+    // blocks that take part: all of them for candidate-heavy buffers, a
+    // quarter (one resident wave) when the candidates are few -- a sparse
+    // buffer is mostly zeroed slot tails, and the extra blocks' start-up
+    // then outweighs their share (r02h: config 1 re-check 0.087 -> 0.082 ms
+    // with 16 blocks per SM, configs 2 / 3 0.014 -> 0.011 / 0.025 -> 0.017 ms
+    // with 4)
+    unsigned active = gridDim.x;
+    if (ncand < static_cast<unsigned long long>(gridDim.x) * 256)
+        active = max(gridDim.x / 4, static_cast<unsigned>((ncand + 255) / 256));
+    if (blockIdx.x >= active) return;
+    const unsigned long long warps = static_cast<unsigned long long>(active) * (blockDim.x >> 5);
     unsigned long long kk = min(32ull, (n + warps - 1) / warps);
     if (n < 128 * warps) {  // (long buffers: 32, config 5 re-check 77 vs 102 ms at ~6)
         if (ncand > 32 * n) kk = 1;
@@ -4002,8 +4012,10 @@ void run_sim_join_dev(const float* d_L, int64_t nL, const float* d_R, int64_t nR
                                PDB_CUDA(cudaGetLastError());
                                return;
                            }
+                           // (16 blocks per SM; the kernel keeps a quarter of
+                           // them when the candidates are few)
                            launch_pdl_if(pdl, both ? k_recheck<2> : grouped ? k_recheck<1> : k_recheck<0>,
-                               dim3(ctx.sm_count * 8), dim3(256), 0, s,
+                               dim3(ctx.sm_count * 16), dim3(256), 0, s,
                                recs, counters, cap, d_L, d_R, d, tau, o2->left, o2->right,
                                o2->dist, static_cast<unsigned long long>(o2->capacity),
                                counters + 2, static_cast<const int32_t*>(permL),
